@@ -1,0 +1,196 @@
+/* include/wbx.h — C ABI of the B200-native waveblur hot path (libwbx.so).
+ *
+ * This is the drop-in boundary. The reference (waveblur, C++20, CPU/OpenMP) exposes
+ * its hot path as a C++ header API only; every entry point below replaces one of
+ * those functions (file:line citations are relative to /root/reference/proj) and
+ * keeps its argument meaning and error behaviour. Plain pointers and sizes only.
+ *
+ *   * Host-pointer entry points take/return the reference's fp64 vectors
+ *     (std::vector<double> in the reference) and synchronise before returning.
+ *   * `_dev` entry points take device pointers and are asynchronous on the
+ *     context's stream (wbx_ctx_stream).
+ *   * Every function returns a wbx_status; the message of the last failure on the
+ *     calling thread is available from wbx_last_error(). Status codes map 1:1 onto
+ *     the reference's exception types (`include/waveblur/image.hpp:10-36`), which the
+ *     C++ facade (include/waveblur/*.hpp) re-throws.
+ *   * A context binds one CUDA device and one stream; calls on one context must be
+ *     serialised by the caller (the reference's functions are pure and re-entrant;
+ *     use one context per host thread for the same property).
+ */
+#ifndef WBX_H
+#define WBX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WBX_ABI_VERSION 1
+
+typedef enum {
+    WBX_OK = 0,
+    WBX_SHAPE_MISMATCH = 1,     /* ShapeMismatch      (image.hpp:10)  */
+    WBX_UNSUPPORTED_FILTER = 2, /* UnsupportedFilter  (image.hpp:13)  */
+    WBX_BAND_NOT_FOUND = 3,     /* BandNotFound       (image.hpp:16)  */
+    WBX_BAD_SPEC = 4,           /* BadSpec            (image.hpp:19)  */
+    WBX_TOO_LARGE = 5,          /* TooLarge           (image.hpp:22)  */
+    WBX_BAD_EPSILON = 6,        /* BadEpsilon         (image.hpp:25)  */
+    WBX_MEMORY_GUARD = 7,       /* MemoryGuard        (image.hpp:28)  */
+    WBX_NONFINITE_ENERGY = 8,   /* NonFiniteEnergy    (image.hpp:31)  */
+    WBX_IO_ERROR = 9,           /* IoError            (image.hpp:34)  */
+    WBX_CUDA_ERROR = 10,        /* device failure (no reference equivalent) */
+    WBX_INVALID_ARGUMENT = 11   /* null handle / pointer                    */
+} wbx_status;
+
+typedef enum { WBX_HAAR = 0, WBX_DAUBECHIES = 1, WBX_SYMMLET = 2 } wbx_family; /* FilterFamily, wavelet.hpp:12 */
+typedef enum { WBX_FP32 = 32, WBX_FP64 = 64 } wbx_precision;
+
+typedef struct wbx_ctx wbx_ctx;     /* device + stream + scratch                        */
+typedef struct wbx_basis wbx_basis; /* WaveletBasis (wavelet.hpp:68-74) resident on device */
+typedef struct wbx_op wbx_op;       /* SparseThetaOp (solver.hpp:25-38): Theta_K + cached transpose */
+typedef struct wbx_solver wbx_solver; /* a prepared preconditioned-FISTA solve (op, P, w, lambda, tau) */
+
+typedef struct {
+    uint32_t level, orientation; /* Band (wavelet.hpp:39-52) */
+    uint64_t shape[2];           /* shape[1] == 1 for 1-D layouts */
+    uint64_t offset;
+} wbx_band;
+
+/* SolverConfig (solver.hpp:66-74) + device knobs */
+typedef struct {
+    uint64_t max_iters;      /* default 500 */
+    double rel_energy_tol;   /* default 1e-3 */
+    double step_safety;      /* default 1.01 */
+    double ref_energy;       /* NaN disables the energy stopping rule */
+    int32_t zero_momentum;   /* test hook: beta = 0 */
+    int32_t track_support;   /* fill report.support_sizes */
+    int32_t track_energy;    /* fill report.energies (forced on when ref_energy is finite) */
+    int32_t precision;       /* WBX_FP32 (hot path) or WBX_FP64 (bitwise reference mode) */
+    double tau;              /* > 0: use this step instead of estimate_step (e.g. cached) */
+} wbx_solver_cfg;
+
+/* SolveReport (solver.hpp:76-84). energies / support_sizes are caller-allocated
+ * (length >= max_iters) or NULL. */
+typedef struct {
+    uint64_t iters_used;
+    double initial_energy;
+    double wall_time_s;         /* device time of the solve incl. tau, CUDA events */
+    double tau;                 /* the step actually used */
+    uint32_t tau_iters;         /* power iterations spent (0 when tau was given) */
+    double ops_per_pixel_per_iter;
+    double* energies;
+    uint64_t* support_sizes;
+} wbx_report;
+
+typedef struct {
+    uint64_t n, nnz;
+    uint64_t nonempty_rows, nonempty_cols; /* |R| and |C| of the compacted layouts */
+    uint64_t sell_rows_padded, sell_cols_padded;
+    uint64_t device_bytes;
+    uint64_t bytes_per_iter_fp32;          /* algorithmic HBM bytes of one FISTA iteration */
+} wbx_op_info;
+
+/* ---------------------------------------------------------------- context */
+const char* wbx_last_error(void);
+int wbx_abi_version(void);
+int wbx_ctx_create(int device, wbx_ctx** out);
+int wbx_ctx_destroy(wbx_ctx* ctx);
+void* wbx_ctx_stream(wbx_ctx* ctx); /* cudaStream_t */
+int wbx_ctx_synchronize(wbx_ctx* ctx);
+/* number of kernels this library launched on ctx since creation (launch accounting) */
+uint64_t wbx_ctx_launch_count(const wbx_ctx* ctx);
+
+/* ---------------------------------------------------------------- wavelets */
+/* make_filters (wavelet_filters.cpp:110-144); lo/hi must hold 20 doubles */
+int wbx_make_filters(uint32_t family, uint32_t order, double* lo, double* hi, uint32_t* length);
+/* make_filters(name) (wavelet_filters.cpp:146-161): "haar", "db4", "sym6", "symmlet6" */
+int wbx_parse_filter(const char* name, uint32_t* family, uint32_t* order);
+/* make_layout (wavelet.cpp:32-70); bands must hold 1 + 3*J entries; returns count */
+int wbx_make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, wbx_band* bands,
+                    uint32_t* nbands);
+int wbx_basis_create(wbx_ctx* ctx, uint32_t family, uint32_t order, uint32_t ndim,
+                     const uint64_t* dims, uint32_t J, wbx_basis** out);
+int wbx_basis_destroy(wbx_basis* basis);
+/* analyze (wavelet.cpp:254-256): x = Psi^* u; fp64, bitwise equal to the reference */
+int wbx_analyze(wbx_ctx* ctx, const wbx_basis* basis, const double* u, double* x);
+/* synthesize (wavelet.cpp:258-260): u = Psi x; fp64, bitwise equal to the reference */
+int wbx_synthesize(wbx_ctx* ctx, const wbx_basis* basis, const double* x, double* u);
+int wbx_analyze_dev(wbx_ctx* ctx, const wbx_basis* basis, const double* u_dev, double* x_dev);
+int wbx_synthesize_dev(wbx_ctx* ctx, const wbx_basis* basis, const double* x_dev, double* u_dev);
+/* single_wavelet (wavelet.cpp:262-269) */
+int wbx_single_wavelet(wbx_ctx* ctx, const wbx_basis* basis, uint32_t level, uint32_t orientation,
+                       double* u);
+
+/* ---------------------------------------------------------------- Theta_K */
+/* Upload a CSR Theta_K (SparseOperator, theta.hpp:50-60) and build the device layouts
+ * (compacted sliced-ELL of Theta and of its transpose, fp32 + fp64 values). Validates
+ * like read_operator (theta.cpp:479-488): WBX_SHAPE_MISMATCH on bad offsets/columns. */
+int wbx_op_create(wbx_ctx* ctx, uint64_t n, const uint64_t* row_offsets,
+                  const uint32_t* col_indices, const double* values, wbx_op** out);
+int wbx_op_destroy(wbx_op* op);
+int wbx_op_get_info(const wbx_op* op, wbx_op_info* info);
+/* spmv / SparseThetaOp::apply (theta.cpp:300-311, solver.cpp:11-13) when transpose == 0;
+ * SparseThetaOp::apply_adjoint / spmv_t (solver.cpp:15-17, theta.cpp:344-356) when 1.
+ * fp64 with the reference's in-row order: bitwise equal to the reference. */
+int wbx_spmv(wbx_ctx* ctx, const wbx_op* op, int transpose, const double* x, double* y);
+int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, const void* x_dev,
+                 void* y_dev);
+/* approx_gradient (theta.cpp:358-365): Theta^T (Theta x - x0) */
+int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0,
+                        double* g);
+/* Expand a thresholded circulant operator given as kept generator groups (the
+ * reference's top-K walk, theta.cpp:236-275, + assemble :180-201) into CSR.
+ * gens: n_gens records {block = out*nbands + in, gen_index, count, value}.
+ * Call with row_offsets/col_indices/values == NULL to query nnz first. */
+int wbx_theta_expand(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
+                     const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
+                     const double* values, uint64_t* nnz, uint64_t* row_offsets,
+                     uint32_t* col_indices, double* out_values);
+
+/* ---------------------------------------------------------------- preconditioners */
+/* gram_diagonals (precond.cpp:16-67), spai (:79-87), jacobi (:69-77); fp64, bitwise */
+int wbx_gram_diagonals(wbx_ctx* ctx, const wbx_op* op, uint64_t nnz_cap_factor, double* diagM,
+                       double* diagM2);
+int wbx_spai(wbx_ctx* ctx, const wbx_op* op, double* p);
+int wbx_jacobi(wbx_ctx* ctx, const wbx_op* op, double eps, double* p);
+
+/* ---------------------------------------------------------------- solver */
+/* scale_weights (solver.cpp:33-42) */
+int wbx_scale_weights(uint32_t ndim, const uint64_t* dims, uint32_t J, double* w);
+/* prox_weighted_l1_P (solver.cpp:57-67), on device, fp64 */
+int wbx_prox_l1w(wbx_ctx* ctx, uint64_t n, const double* z0, double tau, const double* w,
+                 double lambda, const double* p, double* z);
+/* energy (solver.cpp:44-55) */
+int wbx_energy(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0,
+               const double* w, double lambda, double* e);
+/* estimate_step (solver.cpp:69-99): fp64 power iteration on the device */
+int wbx_estimate_step(wbx_ctx* ctx, const wbx_op* op, const double* p, double step_safety,
+                      double* tau, uint32_t* iters);
+void wbx_solver_cfg_default(wbx_solver_cfg* cfg);
+/* ista / fista (solver.cpp:161-169 -> run_pgd :103-157). x_final: n doubles. */
+int wbx_pgd(wbx_ctx* ctx, const wbx_op* op, const double* x0, const double* w, double lambda,
+            const double* p, const wbx_solver_cfg* cfg, int accelerate, double* x_final,
+            wbx_report* report);
+
+/* ---------------------------------------------------------------- prepared deblur (hot path)
+ * The unit the bench times: u0 (observed image) -> analyze -> [estimate_step] ->
+ * preconditioned FISTA -> synthesize -> restored image (pre-clamp; clamp=1 applies the
+ * CLI's [0,1] clamp, waveblur.cpp:296-297). Mirrors cmd_deblur's solve
+ * (waveblur.cpp:286-297) with the operator, P, w, lambda bound once. */
+int wbx_solver_create(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* basis, const double* p,
+                      const double* w, double lambda, const wbx_solver_cfg* cfg,
+                      wbx_solver** out);
+int wbx_solver_destroy(wbx_solver* s);
+/* device pointers (fp64 images, n doubles), async on the ctx stream */
+int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp);
+/* host pointers: H2D copy, deblur, D2H copy, synchronise */
+int wbx_deblur(wbx_solver* s, const double* u0, double* u, int clamp, wbx_report* report);
+/* launches of the last deblur, and the solver kernel's device time (ms) */
+int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

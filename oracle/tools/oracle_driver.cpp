@@ -197,7 +197,7 @@ std::string json_array(const std::vector<double>& v) {
 }  // namespace
 
 int main(int argc, char** argv) {
-    std::string out, family = "daubechies", mode = "dyadic", precond = "spai", u0_path;
+    std::string out, family = "daubechies", mode = "dyadic", precond = "spai", u0_path, method = "fista";
     std::vector<std::size_t> dims = {256, 256};
     unsigned order = 4, J = 4;
     double sigma = 5.0, noise = 5e-3, lambda = 1e-4, kfactor = 3.0;
@@ -230,6 +230,7 @@ int main(int argc, char** argv) {
         else if (a == "--u0") u0_path = next();
         else if (a == "--bench-reps") bench_reps = std::stoull(next());
         else if (a == "--no-solve") solve = false;
+        else if (a == "--method") method = next();
         else throw std::runtime_error("unknown flag " + a);
     }
     if (out.empty()) throw std::runtime_error("--out required");
@@ -286,7 +287,7 @@ int main(int argc, char** argv) {
     meta << "],\n  \"family\": \"" << family << "\", \"order\": " << order << ", \"J\": " << J
          << ",\n  \"psf\": \"gaussian\", \"sigma\": " << fmt(sigma) << ", \"K\": " << K
          << ", \"mode\": \"" << mode << "\", \"noise\": " << fmt(noise) << ", \"seed\": " << seed
-         << ", \"lambda\": " << fmt(lambda) << ", \"iters\": " << iters << ", \"precond\": \""
+         << ", \"lambda\": " << fmt(lambda) << ", \"method\": \"" << method << "\", \"iters\": " << iters << ", \"precond\": \""
          << precond << "\",\n  \"nnz\": " << sp.nnz() << ", \"n_gens\": " << gens.size()
          << ", \"expand_ok\": " << (expand_ok ? "true" : "false") << ", \"u0_from_file\": "
          << (u0_path.empty() ? "false" : "true")
@@ -320,7 +321,7 @@ int main(int argc, char** argv) {
         cfg.max_iters = iters;
         const double tau = estimate_step(op, P, cfg.step_safety);
         auto s3 = clk::now();
-        SolveReport rep = fista(prob, P, cfg);
+        SolveReport rep = method == "ista" ? ista(prob, P, cfg) : fista(prob, P, cfg);
         auto s4 = clk::now();
         Image restored = synthesize(WaveletCoeffs{&basis.layout, rep.x_final}, basis);
         auto s5 = clk::now();

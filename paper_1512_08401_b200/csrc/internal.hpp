@@ -1,0 +1,148 @@
+// Internal declarations of libwbx (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "wbx.h"
+
+namespace wbx {
+
+// Exception carrying a wbx_status; converted to a status code at the C-ABI edge.
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(WBX_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define WBX_CUDA(call) ::wbx::cuda_check((call), #call)
+
+// Device buffer owned by RAII.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) WBX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        if (count) WBX_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void upload(const std::vector<T>& h, cudaStream_t s) {
+        if (n < h.size()) alloc(h.size());
+        upload(h.data(), h.size(), s);
+    }
+};
+
+}  // namespace wbx
+
+struct wbx_ctx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+};
+
+// Wavelet layout + filters (WaveletBasis, wavelet.hpp:68-74).
+struct wbx_basis {
+    wbx_ctx* ctx = nullptr;
+    uint32_t family = 0, order = 0, ndim = 2, J = 1;
+    uint64_t dims[2] = {1, 1};
+    std::vector<wbx_band> bands;
+    double lo[20] = {0}, hi[20] = {0};
+    uint32_t len = 0;
+    uint64_t n = 0;
+    wbx::DevBuf<double> work_a, work_b, io;  // ping-pong scratch + staging
+};
+
+// Compacted sliced-ELL (SELL-32) operator. Rows of the slice structure are the
+// NONEMPTY rows of the matrix, sorted by descending length; columns are remapped to
+// positions in the compacted column space of the consuming vector.
+struct wbx_sell {
+    uint64_t rows = 0;           // real rows
+    uint64_t slices = 0;         // ceil(rows / 32)
+    uint64_t pairs = 0;          // total element pairs (padded)
+    wbx::DevBuf<uint64_t> slice_ptr;  // pair offset of each slice (slices + 1)
+    wbx::DevBuf<uint32_t> slice_len;  // elements per row in the slice (padded to even)
+    wbx::DevBuf<uint4> pk;            // {val0,col0,val1,col1} fp32 pairs
+    wbx::DevBuf<double> val64;        // element-major fp64 values (index 2*pair_base + j*32 + lane)
+    wbx::DevBuf<uint32_t> col;        // element-major columns (same index)
+    wbx::DevBuf<uint32_t> row_len;    // true length of each (sorted) row
+};
+
+struct wbx_op {
+    wbx_ctx* ctx = nullptr;
+    uint64_t n = 0, nnz = 0;
+    uint64_t nR = 0, nC = 0;      // nonempty rows / nonempty columns
+    wbx_sell A;                   // Theta   : rows = R (sorted), cols -> C positions
+    wbx_sell T;                   // Theta^T : rows = C (sorted), cols -> R positions
+    wbx::DevBuf<uint32_t> R_glob; // R position -> original row
+    wbx::DevBuf<uint32_t> C_glob; // C position -> original column
+    wbx::DevBuf<uint32_t> isC;    // bitmask over n: column nonempty
+    wbx::DevBuf<uint32_t> isR;    // bitmask over n: row nonempty
+    std::vector<uint32_t> h_R_glob, h_C_glob;
+    // host copy of the CSR (for the exact host-side setup routines: Gram diagonals)
+    std::vector<uint64_t> h_rowptr;
+    std::vector<uint32_t> h_col;
+    std::vector<double> h_val;
+    uint64_t device_bytes = 0;
+};
+
+namespace wbx {
+
+// Kernel-launch accounting (gpu_launches in bench.py).
+inline void count_launch(wbx_ctx* ctx, uint64_t k = 1) { ctx->launches += k; }
+
+// dwt.cu
+void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s);
+void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s);
+void make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, std::vector<wbx_band>& bands);
+void make_filters(uint32_t family, uint32_t order, double* lo, double* hi, uint32_t* len);
+
+// spmv.cu
+template <typename T>
+void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s);
+void spmv_full_fp64(wbx_op* op, int transpose, const double* x_dev, double* y_dev, cudaStream_t s);
+void spmv_full_fp32(wbx_op* op, int transpose, const float* x_dev, float* y_dev, cudaStream_t s);
+
+// op_build.cu
+struct SellView;
+SellView view_of(const wbx_sell& m);
+
+void build_op(wbx_op* op, uint64_t n, const uint64_t* rowptr, const uint32_t* col,
+              const double* val);
+
+}  // namespace wbx

@@ -1,0 +1,790 @@
+"""Python mirror of the reference's C++ hot-path API (waveblur, /root/reference/proj).
+
+Same names, argument meaning and error behaviour as the reference headers
+(`include/waveblur/{wavelet,theta,precond,solver}.hpp`); every compute call goes
+through the C ABI of libwbx.so (include/wbx.h) onto the B200. Host-side bookkeeping
+that the reference also does on the host (layouts, CSR transposition, WTHETA01 file
+I/O) is plain numpy here. Nothing in this module falls back to a CPU computation of a
+device operation: if libwbx.so (or a GPU) is missing, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import struct
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from . import _native as N
+
+lib = N.lib
+
+
+# ----------------------------------------------------------------------------- errors
+# image.hpp:10-36; the status codes of include/wbx.h map 1:1 onto these.
+class WaveblurError(Exception):
+    pass
+
+
+class ShapeMismatch(WaveblurError, ValueError):
+    pass
+
+
+class UnsupportedFilter(WaveblurError, ValueError):
+    pass
+
+
+class BandNotFound(WaveblurError, ValueError):
+    pass
+
+
+class BadSpec(WaveblurError, ValueError):
+    pass
+
+
+class TooLarge(WaveblurError, ValueError):
+    pass
+
+
+class BadEpsilon(WaveblurError, ValueError):
+    pass
+
+
+class MemoryGuard(WaveblurError, RuntimeError):
+    pass
+
+
+class NonFiniteEnergy(WaveblurError, RuntimeError):
+    pass
+
+
+class IoError(WaveblurError, RuntimeError):
+    pass
+
+
+class CudaError(WaveblurError, RuntimeError):
+    pass
+
+
+_STATUS = {1: ShapeMismatch, 2: UnsupportedFilter, 3: BandNotFound, 4: BadSpec, 5: TooLarge,
+           6: BadEpsilon, 7: MemoryGuard, 8: NonFiniteEnergy, 9: IoError, 10: CudaError,
+           11: ValueError}
+
+
+def _check(status: int) -> None:
+    if status != N.WBX_OK:
+        raise _STATUS.get(status, WaveblurError)(N.last_error())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _u64ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def _u32ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _f64(x, n: Optional[int] = None, what: str = "vector") -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if n is not None and a.size != n:
+        raise ShapeMismatch(f"{what}: length {a.size} != {n}")
+    return a
+
+
+# ----------------------------------------------------------------------------- device context
+class Context:
+    """One CUDA device + stream (wbx_ctx). Calls on one context are serialised."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.wbx_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        return lib.wbx_ctx_stream(self.handle) or 0
+
+    def synchronize(self) -> None:
+        _check(lib.wbx_ctx_synchronize(self.handle))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.wbx_ctx_launch_count(self.handle))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.wbx_ctx_destroy(self.handle)
+            self.handle = None
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ----------------------------------------------------------------------------- wavelets
+class FilterFamily(enum.IntEnum):  # wavelet.hpp:12
+    Haar = 0
+    Daubechies = 1
+    Symmlet = 2
+
+
+def family_name(f: FilterFamily) -> str:
+    return {0: "haar", 1: "daubechies", 2: "symmlet"}[int(f)]
+
+
+@dataclass
+class FilterPair:  # wavelet.hpp:18-28
+    family: FilterFamily
+    order: int
+    lowpass: np.ndarray
+    highpass: np.ndarray
+
+    def length(self) -> int:
+        return len(self.lowpass)
+
+
+def make_filters(family: Union[FilterFamily, str], order: Optional[int] = None) -> FilterPair:
+    """make_filters (wavelet_filters.cpp:110-161)."""
+    if isinstance(family, str):
+        f, o = C.c_uint32(), C.c_uint32()
+        _check(lib.wbx_parse_filter(family.encode(), C.byref(f), C.byref(o)))
+        family, order = FilterFamily(f.value), o.value
+    lo = np.zeros(20)
+    hi = np.zeros(20)
+    ln = C.c_uint32()
+    _check(lib.wbx_make_filters(int(family), int(order), _dptr(lo), _dptr(hi), C.byref(ln)))
+    return FilterPair(FilterFamily(family), int(order), lo[: ln.value].copy(), hi[: ln.value].copy())
+
+
+@dataclass
+class Band:  # wavelet.hpp:39-52
+    level: int
+    orientation: int
+    shape: tuple
+    offset: int
+
+    def count(self) -> int:
+        return int(np.prod(self.shape))
+
+
+@dataclass
+class SubbandLayout:  # wavelet.hpp:58-64
+    dims: tuple
+    J: int
+    bands: list
+
+    def total(self) -> int:
+        return int(np.prod(self.dims))
+
+    def find(self, level: int, orientation: int) -> Band:
+        for b in self.bands:
+            if b.level == level and b.orientation == orientation:
+                return b
+        raise BandNotFound(f"no band (level={level}, e={orientation})")
+
+    def band_of_flat(self, flat: int) -> int:
+        for i in range(len(self.bands) - 1, -1, -1):
+            if flat >= self.bands[i].offset:
+                return i
+        raise BandNotFound("flat index out of range")
+
+
+def make_layout(dims: Sequence[int], J: int) -> SubbandLayout:
+    """make_layout (wavelet.cpp:32-70)."""
+    dims = tuple(int(d) for d in dims)
+    if len(dims) < 1 or len(dims) > 2:
+        raise ShapeMismatch("layout needs 1 or 2 dims")
+    d = np.array(dims, dtype=np.uint64)
+    out = (N.wbx_band * (1 + 3 * max(int(J), 1)))()
+    nb = C.c_uint32()
+    _check(lib.wbx_make_layout(len(dims), _u64ptr(d), int(J), out, C.byref(nb)))
+    bands = []
+    for i in range(nb.value):
+        b = out[i]
+        shape = (int(b.shape[0]), int(b.shape[1])) if len(dims) == 2 else (int(b.shape[0]),)
+        bands.append(Band(int(b.level), int(b.orientation), shape, int(b.offset)))
+    return SubbandLayout(dims, int(J), bands)
+
+
+class WaveletBasis:  # wavelet.hpp:68-74, plus its device residency (wbx_basis)
+    def __init__(self, filters: FilterPair, layout: SubbandLayout, ctx: Optional[Context] = None):
+        self.filters = filters
+        self.layout = layout
+        self._ctx = ctx
+        self._handle = None
+
+    def dims(self):
+        return self.layout.dims
+
+    def levels(self) -> int:
+        return self.layout.J
+
+    def device(self, ctx: Optional[Context] = None):
+        ctx = ctx or self._ctx or default_context()
+        if self._handle is None or self._ctx is not ctx:
+            d = np.array(self.layout.dims, dtype=np.uint64)
+            h = C.c_void_p()
+            _check(lib.wbx_basis_create(ctx.handle, int(self.filters.family), self.filters.order,
+                                        len(self.layout.dims), _u64ptr(d), self.layout.J, C.byref(h)))
+            self._release()
+            self._handle, self._ctx = h, ctx
+        return self._handle
+
+    def _release(self):
+        if self._handle is not None:
+            lib.wbx_basis_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        self._release()
+
+
+def make_basis(family_or_name, *args) -> WaveletBasis:
+    """make_basis (wavelet.cpp:72-80): (family, order, dims, J) or (name, dims, J)."""
+    if isinstance(family_or_name, str):
+        dims, J = args
+        return WaveletBasis(make_filters(family_or_name), make_layout(dims, J))
+    order, dims, J = args
+    return WaveletBasis(make_filters(family_or_name, order), make_layout(dims, J))
+
+
+@dataclass
+class WaveletCoeffs:  # wavelet.hpp:81-84
+    layout: SubbandLayout
+    values: np.ndarray
+
+
+def analyze(signal: np.ndarray, basis: WaveletBasis, ctx: Optional[Context] = None) -> WaveletCoeffs:
+    """x = Psi^* u (wavelet.cpp:254-256), on the device, bitwise equal to the reference."""
+    u = np.asarray(signal, dtype=np.float64)
+    if tuple(u.shape) != tuple(basis.layout.dims):
+        raise ShapeMismatch("signal dims do not match basis")
+    ctx = ctx or basis._ctx or default_context()
+    u = np.ascontiguousarray(u).ravel()
+    x = np.empty(u.size)
+    _check(lib.wbx_analyze(ctx.handle, basis.device(ctx), _dptr(u), _dptr(x)))
+    return WaveletCoeffs(basis.layout, x)
+
+
+def synthesize(coeffs: Union[WaveletCoeffs, np.ndarray], basis: WaveletBasis,
+               ctx: Optional[Context] = None) -> np.ndarray:
+    """u = Psi x (wavelet.cpp:258-260), on the device, bitwise equal to the reference."""
+    vals = coeffs.values if isinstance(coeffs, WaveletCoeffs) else coeffs
+    x = _f64(vals)
+    if x.size != basis.layout.total():
+        raise ShapeMismatch("coefficient length does not match basis")
+    ctx = ctx or basis._ctx or default_context()
+    u = np.empty(x.size)
+    _check(lib.wbx_synthesize(ctx.handle, basis.device(ctx), _dptr(x), _dptr(u)))
+    return u.reshape(basis.layout.dims)
+
+
+def single_wavelet(basis: WaveletBasis, level: int, orientation: int,
+                   ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or basis._ctx or default_context()
+    u = np.empty(basis.layout.total())
+    _check(lib.wbx_single_wavelet(ctx.handle, basis.device(ctx), level, orientation, _dptr(u)))
+    return u.reshape(basis.layout.dims)
+
+
+# ----------------------------------------------------------------------------- Theta_K
+class SparseOperator:
+    """K-sparse CSR operator (theta.hpp:50-60): u64 row offsets, u32 strictly increasing
+    columns per row, f64 values, plus subband metadata. Device layouts are built lazily
+    on first use (wbx_op_create) and cached per context."""
+
+    def __init__(self, n: int, row_offsets, col_indices, values, layout: Optional[SubbandLayout] = None,
+                 family: FilterFamily = FilterFamily.Haar, order: int = 1):
+        self.n = int(n)
+        self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        self.col_indices = np.ascontiguousarray(col_indices, dtype=np.uint32)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        self.layout = layout
+        self.family = FilterFamily(family)
+        self.order = int(order)
+        self._dev = None
+        self._ctx = None
+
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    def device(self, ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        if self._dev is None or self._ctx is not ctx:
+            if self.row_offsets.size != self.n + 1:
+                raise ShapeMismatch("row_offsets must have n+1 entries")
+            h = C.c_void_p()
+            _check(lib.wbx_op_create(ctx.handle, self.n, _u64ptr(self.row_offsets),
+                                     _u32ptr(self.col_indices), _dptr(self.values), C.byref(h)))
+            self._release()
+            self._dev, self._ctx = h, ctx
+        return self._dev
+
+    def info(self, ctx: Optional[Context] = None) -> N.wbx_op_info:
+        inf = N.wbx_op_info()
+        _check(lib.wbx_op_get_info(self.device(ctx), C.byref(inf)))
+        return inf
+
+    def _release(self):
+        if self._dev is not None:
+            lib.wbx_op_destroy(self._dev)
+            self._dev = None
+
+    def __del__(self):
+        self._release()
+
+
+def _ctx_of(op: SparseOperator, ctx):
+    return ctx or op._ctx or default_context()
+
+
+def spmv(op: SparseOperator, x, ctx: Optional[Context] = None) -> np.ndarray:
+    """y = Theta_K x (theta.cpp:300-311); fp64, bitwise equal to the reference."""
+    xv = _f64(x)
+    if xv.size != op.n:
+        raise ShapeMismatch("spmv: vector length mismatch")
+    ctx = _ctx_of(op, ctx)
+    y = np.empty(op.n)
+    _check(lib.wbx_spmv(ctx.handle, op.device(ctx), 0, _dptr(xv), _dptr(y)))
+    return y
+
+
+def spmv_t(op: SparseOperator, x, ctx: Optional[Context] = None) -> np.ndarray:
+    """y = Theta_K^T x (theta.cpp:344-356)."""
+    xv = _f64(x)
+    if xv.size != op.n:
+        raise ShapeMismatch("spmv_t: vector length mismatch")
+    ctx = _ctx_of(op, ctx)
+    y = np.empty(op.n)
+    _check(lib.wbx_spmv(ctx.handle, op.device(ctx), 1, _dptr(xv), _dptr(y)))
+    return y
+
+
+def approx_gradient(op: SparseOperator, x, x0, ctx: Optional[Context] = None) -> np.ndarray:
+    """Theta^T (Theta x - x0) (theta.cpp:358-365)."""
+    xv, x0v = _f64(x), _f64(x0)
+    if xv.size != op.n or x0v.size != op.n:
+        raise ShapeMismatch("approx_gradient: vector length mismatch")
+    ctx = _ctx_of(op, ctx)
+    g = np.empty(op.n)
+    _check(lib.wbx_approx_gradient(ctx.handle, op.device(ctx), _dptr(xv), _dptr(x0v), _dptr(g)))
+    return g
+
+
+def ops_per_pixel(op: SparseOperator) -> float:
+    return 2.0 * op.nnz() / op.n
+
+
+def transpose(op: SparseOperator) -> SparseOperator:
+    """Theta_K^T as CSR (theta.cpp:371-382; make_transpose order :324-340). Host-side setup."""
+    n = op.n
+    cols = op.col_indices.astype(np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(op.row_offsets.astype(np.int64)))
+    order = np.lexsort((rows, cols))  # by column, then ascending row (stable CSR scan)
+    counts = np.bincount(cols, minlength=n)
+    off = np.zeros(n + 1, dtype=np.uint64)
+    off[1:] = np.cumsum(counts)
+    return SparseOperator(n, off, rows[order].astype(np.uint32), op.values[order], op.layout,
+                          op.family, op.order)
+
+
+_MAGIC = b"WTHETA01"
+
+
+def write_operator(op: SparseOperator, path: str) -> None:
+    """Bit-exact WTHETA01 file (theta.cpp:428-443)."""
+    if op.layout is None:
+        raise IoError("operator has no layout")
+    try:
+        with open(path, "wb") as f:
+            f.write(_MAGIC)
+            dims = op.layout.dims
+            f.write(struct.pack("<I", len(dims)))
+            for s in dims:
+                f.write(struct.pack("<I", s))
+            f.write(struct.pack("<IIII", op.layout.J, int(op.family), op.order, op.nnz()))
+            f.write(op.row_offsets.astype("<u8").tobytes())
+            f.write(op.col_indices.astype("<u4").tobytes())
+            f.write(op.values.astype("<f8").tobytes())
+    except OSError as e:
+        raise IoError(f"cannot write operator file {path}: {e}") from e
+
+
+def read_operator(path: str) -> SparseOperator:
+    """WTHETA01 reader with the reference's validation (theta.cpp:445-490)."""
+    try:
+        data = open(path, "rb").read()
+    except OSError as e:
+        raise IoError(f"cannot open operator file {path}") from e
+    if len(data) < 8:
+        raise IoError("operator file truncated")
+    if data[:8] != _MAGIC:
+        raise IoError(f"{path}: not a WTHETA01 operator file")
+    pos = 8
+
+    def u32():
+        nonlocal pos
+        if pos + 4 > len(data):
+            raise IoError("operator file truncated")
+        v = struct.unpack_from("<I", data, pos)[0]
+        pos += 4
+        return v
+
+    d = u32()
+    if d < 1 or d > 2:
+        raise IoError(f"{path}: bad dimension count")
+    dims = [u32() for _ in range(d)]
+    J, family, order, nnz = u32(), u32(), u32(), u32()
+    if family > 2:
+        raise IoError(f"{path}: bad filter family id")
+    layout = make_layout(dims, J)
+    n = layout.total()
+    need = 8 * (n + 1) + 4 * nnz + 8 * nnz
+    if pos + need > len(data):
+        raise IoError("operator file truncated")
+    ro = np.frombuffer(data, "<u8", n + 1, pos).astype(np.uint64)
+    pos += 8 * (n + 1)
+    ci = np.frombuffer(data, "<u4", nnz, pos).astype(np.uint32)
+    pos += 4 * nnz
+    va = np.frombuffer(data, "<f8", nnz, pos).astype(np.float64)
+    if ro[0] != 0 or ro[n] != nnz:
+        raise IoError(f"{path}: inconsistent row offsets")
+    if np.any(np.diff(ro.astype(np.int64)) < 0):
+        raise IoError(f"{path}: row offsets not nondecreasing")
+    if nnz and np.any(ci >= n):
+        raise IoError(f"{path}: column index out of range")
+    if nnz > 1:
+        rows = np.repeat(np.arange(n), np.diff(ro.astype(np.int64)))
+        same = rows[1:] == rows[:-1]
+        if np.any(same & (ci[1:].astype(np.int64) <= ci[:-1].astype(np.int64))):
+            raise IoError(f"{path}: columns not strictly increasing in a row")
+    return SparseOperator(n, ro, ci, va, layout, FilterFamily(family), order)
+
+
+@dataclass
+class GeneratorList:
+    """A thresholded circulant Theta_K in compressed form: the kept (block, generator
+    index, count, value) groups of the reference's global top-K walk
+    (theta.cpp:206-276). block = out_band * nbands + in_band."""
+    dims: tuple
+    J: int
+    family: FilterFamily
+    order: int
+    blocks: np.ndarray
+    gen_index: np.ndarray
+    counts: np.ndarray
+    values: np.ndarray
+
+    @staticmethod
+    def from_bytes(raw: bytes, dims, J, family, order) -> "GeneratorList":
+        rec = np.frombuffer(raw, dtype=np.dtype([("b", "<u4"), ("g", "<u4"), ("c", "<u8"), ("v", "<f8")]))
+        return GeneratorList(tuple(dims), int(J), FilterFamily(family), int(order),
+                             rec["b"].astype(np.uint32), rec["g"].astype(np.uint32),
+                             rec["c"].astype(np.uint64), rec["v"].astype(np.float64))
+
+    def to_bytes(self) -> bytes:
+        rec = np.zeros(self.blocks.size, dtype=np.dtype([("b", "<u4"), ("g", "<u4"), ("c", "<u8"), ("v", "<f8")]))
+        rec["b"], rec["g"], rec["c"], rec["v"] = self.blocks, self.gen_index, self.counts, self.values
+        return rec.tobytes()
+
+
+def theta_from_generators(gl: GeneratorList) -> SparseOperator:
+    """Expand a GeneratorList into the CSR the reference's threshold_* would assemble
+    (walk theta.cpp:236-275 + assemble :180-201), via wbx_theta_expand."""
+    dims = np.array(gl.dims, dtype=np.uint64)
+    nnz = C.c_uint64()
+    args = (len(gl.dims), _u64ptr(dims), gl.J, gl.blocks.size, _u32ptr(gl.blocks), _u32ptr(gl.gen_index),
+            _u64ptr(gl.counts), _dptr(gl.values), C.byref(nnz))
+    _check(lib.wbx_theta_expand(*args, None, None, None))
+    layout = make_layout(gl.dims, gl.J)
+    n = layout.total()
+    ro = np.zeros(n + 1, dtype=np.uint64)
+    ci = np.zeros(max(nnz.value, 1), dtype=np.uint32)
+    va = np.zeros(max(nnz.value, 1), dtype=np.float64)
+    _check(lib.wbx_theta_expand(*args, _u64ptr(ro), _u32ptr(ci), _dptr(va)))
+    return SparseOperator(n, ro, ci[: nnz.value], va[: nnz.value], layout, gl.family, gl.order)
+
+
+# ----------------------------------------------------------------------------- weights
+@dataclass
+class WeightVector:
+    sigma: np.ndarray
+
+
+def uniform_weights(layout: SubbandLayout) -> WeightVector:
+    return WeightVector(np.ones(layout.total()))
+
+
+def dyadic_weights(layout: SubbandLayout) -> WeightVector:
+    """sigma = 2^(t-J) of the coefficient's band (theta.cpp:153-165)."""
+    s = np.empty(layout.total())
+    for b in layout.bands:
+        s[b.offset:b.offset + b.count()] = 2.0 ** (b.level - layout.J)
+    return WeightVector(s)
+
+
+def scale_weights(layout: SubbandLayout) -> np.ndarray:
+    """w = level t on detail bands, J on the approximation (solver.cpp:33-42)."""
+    d = np.array(layout.dims, dtype=np.uint64)
+    w = np.empty(layout.total())
+    _check(lib.wbx_scale_weights(len(layout.dims), _u64ptr(d), layout.J, _dptr(w)))
+    return w
+
+
+# ----------------------------------------------------------------------------- preconditioners
+class PrecondKind(enum.IntEnum):
+    Identity = 0
+    Jacobi = 1
+    Spai = 2
+
+
+@dataclass
+class DiagonalPreconditioner:  # precond.hpp:11-14
+    p: np.ndarray
+    kind: PrecondKind = PrecondKind.Identity
+
+
+def identity_precond(n: int) -> DiagonalPreconditioner:
+    return DiagonalPreconditioner(np.ones(n), PrecondKind.Identity)
+
+
+@dataclass
+class GramDiagonals:
+    diagM: np.ndarray
+    diagM2: np.ndarray
+
+
+def gram_diagonals(op: SparseOperator, nnz_cap_factor: int = 50, ctx=None) -> GramDiagonals:
+    """precond.cpp:16-67 (exact fp64, same accumulation order)."""
+    ctx = _ctx_of(op, ctx)
+    m = np.empty(op.n)
+    m2 = np.empty(op.n)
+    _check(lib.wbx_gram_diagonals(ctx.handle, op.device(ctx), nnz_cap_factor, _dptr(m), _dptr(m2)))
+    return GramDiagonals(m, m2)
+
+
+def spai(op: SparseOperator, ctx=None) -> DiagonalPreconditioner:
+    ctx = _ctx_of(op, ctx)
+    p = np.empty(op.n)
+    _check(lib.wbx_spai(ctx.handle, op.device(ctx), _dptr(p)))
+    return DiagonalPreconditioner(p, PrecondKind.Spai)
+
+
+def jacobi(op: SparseOperator, eps: float, ctx=None) -> DiagonalPreconditioner:
+    if eps <= 0.0:
+        raise BadEpsilon("jacobi: epsilon must be positive")
+    ctx = _ctx_of(op, ctx)
+    p = np.empty(op.n)
+    _check(lib.wbx_jacobi(ctx.handle, op.device(ctx), float(eps), _dptr(p)))
+    return DiagonalPreconditioner(p, PrecondKind.Jacobi)
+
+
+# ----------------------------------------------------------------------------- solver
+class SparseThetaOp:
+    """ThetaOp over a SparseOperator (solver.hpp:25-38)."""
+
+    def __init__(self, op: SparseOperator, ctx: Optional[Context] = None):
+        self._op = op
+        self._ctx = ctx
+
+    def apply(self, x) -> np.ndarray:
+        return spmv(self._op, x, self._ctx)
+
+    def apply_adjoint(self, x) -> np.ndarray:
+        return spmv_t(self._op, x, self._ctx)
+
+    def dim(self) -> int:
+        return self._op.n
+
+    def ops_per_pixel(self) -> float:
+        return ops_per_pixel(self._op)
+
+    def sparse(self) -> SparseOperator:
+        return self._op
+
+
+@dataclass
+class DeblurProblem:  # solver.hpp:55-61
+    op: SparseThetaOp = None
+    x0: np.ndarray = None
+    weights: np.ndarray = None
+    lambda_: float = 1e-4
+
+
+@dataclass
+class SolverConfig:  # solver.hpp:66-74 (+ device knobs)
+    max_iters: int = 500
+    rel_energy_tol: float = 1e-3
+    step_safety: float = 1.01
+    track_support: bool = False
+    ref_energy: float = math.nan
+    zero_momentum: bool = False
+    track_energy: bool = True   # the reference always records energies
+    precision: int = N.WBX_FP32
+    tau: float = 0.0            # > 0: given step (skips estimate_step)
+
+    def to_c(self) -> N.wbx_solver_cfg:
+        c = N.wbx_solver_cfg()
+        c.max_iters = int(self.max_iters)
+        c.rel_energy_tol = float(self.rel_energy_tol)
+        c.step_safety = float(self.step_safety)
+        c.ref_energy = float(self.ref_energy)
+        c.zero_momentum = int(bool(self.zero_momentum))
+        c.track_support = int(bool(self.track_support))
+        c.track_energy = int(bool(self.track_energy))
+        c.precision = int(self.precision)
+        c.tau = float(self.tau or 0.0)
+        return c
+
+
+@dataclass
+class SolveReport:  # solver.hpp:76-84
+    x_final: np.ndarray = None
+    energies: list = field(default_factory=list)
+    iters_used: int = 0
+    support_sizes: list = field(default_factory=list)
+    wall_time_s: float = 0.0
+    ops_per_pixel_per_iter: float = 0.0
+    initial_energy: float = 0.0
+    tau: float = 0.0
+    tau_iters: int = 0
+
+
+def energy(x, problem: DeblurProblem, ctx=None) -> float:
+    """½‖Θx − x0‖² + λ Σ w|x| (solver.cpp:44-55)."""
+    op = problem.op.sparse()
+    xv = _f64(x)
+    if xv.size != len(problem.x0):
+        raise ShapeMismatch("energy: vector length mismatch")
+    ctx = _ctx_of(op, ctx)
+    e = C.c_double()
+    _check(lib.wbx_energy(ctx.handle, op.device(ctx), _dptr(xv), _dptr(_f64(problem.x0)),
+                          _dptr(_f64(problem.weights)), float(problem.lambda_), C.byref(e)))
+    return e.value
+
+
+def prox_weighted_l1_P(z0, tau: float, weights, lambda_: float, P: DiagonalPreconditioner,
+                       ctx=None) -> np.ndarray:
+    """z = sign(z0) max(|z0| − τλw/p, 0) (solver.cpp:57-67), on the device."""
+    z0v = _f64(z0)
+    n = z0v.size
+    w = _f64(weights, n, "weights")
+    p = _f64(P.p, n, "preconditioner")
+    ctx = ctx or default_context()
+    z = np.empty(n)
+    _check(lib.wbx_prox_l1w(ctx.handle, n, _dptr(z0v), float(tau), _dptr(w), float(lambda_), _dptr(p),
+                            _dptr(z)))
+    return z
+
+
+def estimate_step(op: SparseThetaOp, P: DiagonalPreconditioner, step_safety: float = 1.0,
+                  ctx=None, return_iters: bool = False):
+    """τ = 1/(step_safety ‖P^-½ΘᵀΘP^-½‖) by the reference's power iteration (solver.cpp:69-99)."""
+    sp = op.sparse()
+    ctx = _ctx_of(sp, ctx)
+    p = _f64(P.p, sp.n, "preconditioner")
+    tau = C.c_double()
+    it = C.c_uint32()
+    _check(lib.wbx_estimate_step(ctx.handle, sp.device(ctx), _dptr(p), float(step_safety), C.byref(tau),
+                                 C.byref(it)))
+    return (tau.value, it.value) if return_iters else tau.value
+
+
+def _run_pgd(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig, accelerate: int,
+             ctx=None) -> SolveReport:
+    sp = problem.op.sparse()
+    n = sp.n
+    x0 = _f64(problem.x0)
+    w = _f64(problem.weights)
+    p = _f64(P.p)
+    if x0.size != n or w.size != n or p.size != n:
+        raise ShapeMismatch("solver: inconsistent problem dimensions")
+    ctx = _ctx_of(sp, ctx)
+    cfg = config.to_c()
+    K = int(config.max_iters)
+    energies = np.zeros(max(K, 1))
+    supports = np.zeros(max(K, 1), dtype=np.uint64)
+    rep = N.wbx_report()
+    rep.energies = _dptr(energies)
+    rep.support_sizes = _u64ptr(supports)
+    xf = np.empty(n)
+    _check(lib.wbx_pgd(ctx.handle, sp.device(ctx), _dptr(x0), _dptr(w), float(problem.lambda_), _dptr(p),
+                       C.byref(cfg), accelerate, _dptr(xf), C.byref(rep)))
+    used = int(rep.iters_used)
+    track = config.track_energy or config.track_support or math.isfinite(config.ref_energy)
+    return SolveReport(
+        x_final=xf,
+        energies=list(energies[:used]) if track else [],
+        iters_used=used,
+        support_sizes=[int(s) for s in supports[:used]] if (track and config.track_support) else [],
+        wall_time_s=rep.wall_time_s,
+        ops_per_pixel_per_iter=rep.ops_per_pixel_per_iter,
+        initial_energy=rep.initial_energy,
+        tau=rep.tau,
+        tau_iters=int(rep.tau_iters))
+
+
+def ista(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig, ctx=None) -> SolveReport:
+    """solver.cpp:161-164."""
+    return _run_pgd(problem, P, config, 0, ctx)
+
+
+def fista(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig, ctx=None) -> SolveReport:
+    """Preconditioned accelerated proximal gradient, momentum (k−1)/(k+2) (solver.cpp:166-169)."""
+    return _run_pgd(problem, P, config, 1, ctx)
+
+
+# ----------------------------------------------------------------------------- prepared deblur
+class Deblurrer:
+    """The deblur unit of the reference CLI (waveblur.cpp:286-297) with the operator,
+    preconditioner, weights and λ bound once: u0 → analyze → [estimate_step] → FISTA →
+    synthesize (→ clamp). `deblur` takes host arrays; `deblur_dev` device pointers."""
+
+    def __init__(self, op: SparseOperator, basis: WaveletBasis, P: DiagonalPreconditioner, weights,
+                 lambda_: float, config: SolverConfig, ctx: Optional[Context] = None):
+        self.ctx = ctx or op._ctx or default_context()
+        self.op, self.basis, self.config = op, basis, config
+        self.n = op.n
+        p = _f64(P.p, op.n, "preconditioner")
+        w = _f64(weights, op.n, "weights")
+        cfg = config.to_c()
+        h = C.c_void_p()
+        _check(lib.wbx_solver_create(self.ctx.handle, op.device(self.ctx), basis.device(self.ctx), _dptr(p),
+                                     _dptr(w), float(lambda_), C.byref(cfg), C.byref(h)))
+        self.handle = h
+
+    def deblur(self, u0: np.ndarray, clamp: bool = True, out: Optional[np.ndarray] = None):
+        u = _f64(u0, self.n, "u0")
+        res = out if out is not None else np.empty(self.n)
+        rep = N.wbx_report()
+        _check(lib.wbx_deblur(self.handle, _dptr(u), res.ctypes.data_as(C.POINTER(C.c_double)), int(clamp),
+                              C.byref(rep)))
+        return res.reshape(self.basis.layout.dims), rep
+
+    def deblur_dev(self, u0_ptr: int, u_ptr: int, clamp: bool = True) -> None:
+        _check(lib.wbx_deblur_dev(self.handle, C.c_void_p(u0_ptr), C.c_void_p(u_ptr), int(clamp)))
+
+    def last_stats(self):
+        launches = C.c_uint64()
+        ms = C.c_float()
+        _check(lib.wbx_solver_last_stats(self.handle, C.byref(launches), C.byref(ms)))
+        return int(launches.value), float(ms.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.wbx_solver_destroy(self.handle)
+            self.handle = None
