@@ -9,23 +9,32 @@ namespace wbx {
 
 constexpr int kWarp = 32;
 
-// Streaming loads of read-only operator data: bypass L1 allocation so the L1 keeps
-// the gathered vector entries (which ARE reused across lanes and rows).
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+// Loads of the read-only operator streams: bypass L1 allocation (each element is read
+// once per SM per iteration, the L1 is kept for the gathered vector entries, which ARE
+// reused across lanes and rows) and mark the lines EVICT_LAST in L2 so the operator
+// (tens of MB) stays resident in the 126 MB L2 across solver iterations. A plain
+// `.nc.L1::no_allocate` load is treated as evict-first by L2 and re-streams from HBM
+// every iteration (ncu: 72 % L2 miss on those sectors).
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ double ld_stream(const double* p) {
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
     double r;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
     uint32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 

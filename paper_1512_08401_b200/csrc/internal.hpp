@@ -92,15 +92,22 @@ struct wbx_basis {
 // NONEMPTY rows of the matrix, sorted by descending length; columns are remapped to
 // positions in the compacted column space of the consuming vector.
 struct wbx_sell {
-    uint64_t rows = 0;           // real rows
-    uint64_t slices = 0;         // ceil(rows / 32)
-    uint64_t pairs = 0;          // total element pairs (padded)
-    wbx::DevBuf<uint64_t> slice_ptr;  // pair offset of each slice (slices + 1)
-    wbx::DevBuf<uint32_t> slice_len;  // elements per row in the slice (padded to even)
+    uint64_t rows = 0;     // real rows
+    // exact fp64 layout (one lane per row, element-major): slice s, element j, lane l at
+    // xslice_ptr[s] + 32*j + l
+    uint64_t xslices = 0;
+    wbx::DevBuf<uint64_t> xslice_ptr;
+    wbx::DevBuf<uint32_t> xslice_len;
+    wbx::DevBuf<double> val64;
+    wbx::DevBuf<uint32_t> col;
+    wbx::DevBuf<uint32_t> row_len;
+    // segmented fp32 layout (rows split into <= 16-element segments, one lane each)
+    uint64_t slices = 0;
+    uint64_t pairs = 0;               // uint4 element pairs incl. padding
+    wbx::DevBuf<uint64_t> slice_ptr;  // pair offset of each slice
+    wbx::DevBuf<uint32_t> slice_np;   // pairs per lane in the slice (<= 8)
     wbx::DevBuf<uint4> pk;            // {val0,col0,val1,col1} fp32 pairs
-    wbx::DevBuf<double> val64;        // element-major fp64 values (index 2*pair_base + j*32 + lane)
-    wbx::DevBuf<uint32_t> col;        // element-major columns (same index)
-    wbx::DevBuf<uint32_t> row_len;    // true length of each (sorted) row
+    wbx::DevBuf<uint32_t> lane_info;  // head lane: row | nseg << 27; else 0xffffffff
 };
 
 struct wbx_op {
@@ -122,6 +129,9 @@ struct wbx_op {
 };
 
 namespace wbx {
+
+constexpr uint64_t kSegElems = 16;  // max elements per lane segment (8 uint4 pairs)
+constexpr uint32_t kInfoShift = 27;
 
 // Kernel-launch accounting (gpu_launches in bench.py).
 inline void count_launch(wbx_ctx* ctx, uint64_t k = 1) { ctx->launches += k; }

@@ -18,6 +18,7 @@
 //   * fp32 values packed with their column as {val0, col0, val1, col1} (one 16-byte
 //     load per two nonzeros per lane); fp64 values + u32 columns element-major.
 #include <algorithm>
+#include <array>
 #include <numeric>
 
 #include <cstring>
@@ -30,12 +31,18 @@ namespace wbx {
 namespace {
 
 struct HostSell {
-    std::vector<uint64_t> slice_ptr;
-    std::vector<uint32_t> slice_len;
-    std::vector<uint4> pk;
+    // exact (fp64) layout: one lane per row, element-major, unpadded rows
+    std::vector<uint64_t> xslice_ptr;
+    std::vector<uint32_t> xslice_len;
     std::vector<double> v64;
     std::vector<uint32_t> col;
     std::vector<uint32_t> row_len;
+    // segmented fp32 layout: rows split into <= kSegElems-element segments, one lane per
+    // segment, a row's segments in consecutive lanes of one slice
+    std::vector<uint64_t> slice_ptr;
+    std::vector<uint32_t> slice_np;
+    std::vector<uint4> pk;
+    std::vector<uint32_t> lane_info;
 };
 
 // rows: list of row ids (in slice order); each row r has [beg[r], end[r]) in (cols, vals),
@@ -43,9 +50,10 @@ struct HostSell {
 template <typename RowRange>
 HostSell make_sell(uint64_t nrows, RowRange range) {
     HostSell h;
+    // ---- exact layout
     const uint64_t slices = (nrows + 31) / 32;
-    h.slice_ptr.assign(slices + 1, 0);
-    h.slice_len.assign(slices, 0);
+    h.xslice_ptr.assign(slices + 1, 0);
+    h.xslice_len.assign(slices, 0);
     h.row_len.assign(nrows, 0);
     for (uint64_t r = 0; r < nrows; ++r) h.row_len[r] = static_cast<uint32_t>(range.len(r));
     for (uint64_t s = 0; s < slices; ++s) {
@@ -54,26 +62,76 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
             const uint64_t r = s * 32 + lane;
             if (r < nrows) L = std::max<uint64_t>(L, range.len(r));
         }
-        L = (L + 1) & ~uint64_t{1};
-        h.slice_len[s] = static_cast<uint32_t>(L);
-        h.slice_ptr[s + 1] = h.slice_ptr[s] + (L / 2) * 32;
+        h.xslice_len[s] = static_cast<uint32_t>(L);
+        h.xslice_ptr[s + 1] = h.xslice_ptr[s] + L * 32;
     }
-    const uint64_t pairs = h.slice_ptr[slices];
-    h.pk.assign(pairs, make_uint4(0, 0, 0, 0));
-    h.v64.assign(2 * pairs, 0.0);
-    h.col.assign(2 * pairs, 0);
-    for (uint64_t s = 0; s < slices; ++s) {
-        const uint64_t L = h.slice_len[s];
+    h.v64.assign(h.xslice_ptr[slices], 0.0);
+    h.col.assign(h.xslice_ptr[slices], 0);
+    for (uint64_t s = 0; s < slices; ++s)
         for (uint64_t lane = 0; lane < 32; ++lane) {
             const uint64_t r = s * 32 + lane;
             const uint64_t len = r < nrows ? range.len(r) : 0;
-            for (uint64_t j = 0; j < L; ++j) {
-                double v = 0.0;
-                uint32_t c = 0;
-                if (j < len) range.get(r, j, c, v);
-                const uint64_t e = 2 * h.slice_ptr[s] + j * 32 + lane;
-                h.v64[e] = v;
-                h.col[e] = c;
+            for (uint64_t j = 0; j < len; ++j) {
+                const uint64_t e = h.xslice_ptr[s] + j * 32 + lane;
+                range.get(r, j, h.col[e], h.v64[e]);
+            }
+        }
+    // ---- segmented fp32 layout
+    struct Seg {
+        uint64_t row, beg, len;
+        uint32_t info;
+    };
+    // Segment-major placement: a slice holds m rows that all have q segments
+    // (m = floor(32 / q)); segment t of the slice's i-th row sits in lane t*m + i. Lanes
+    // 0..m-1 (and each further group of m) therefore hold consecutive rows, so a warp's
+    // gather instruction touches consecutive rows of one band: for a circulant block,
+    // consecutive columns — coalesced. Segments split a row evenly.
+    std::vector<std::array<Seg, 32>> sl;
+    std::vector<uint32_t> stride;
+    uint64_t r = 0;
+    while (r < nrows) {
+        const uint64_t len0 = range.len(r);
+        const uint64_t q = std::max<uint64_t>(1, (len0 + kSegElems - 1) / kSegElems);
+        if (q > 31) fail(WBX_TOO_LARGE, "row longer than 31 segments");
+        const uint64_t m = 32 / q;
+        std::array<Seg, 32> a;
+        for (auto& g : a) g = Seg{0, 0, 0, 0xffffffffu};
+        uint64_t i = 0;
+        for (; i < m && r < nrows; ++i, ++r) {
+            const uint64_t len = range.len(r);
+            const uint64_t qr = std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems);
+            if (qr != q) break;  // next run of rows (rows are sorted by length)
+            for (uint64_t t = 0; t < q; ++t) {
+                const uint64_t beg = t * len / q, end = (t + 1) * len / q;
+                a[t * m + i] = Seg{r, beg, end - beg,
+                                   t == 0 ? static_cast<uint32_t>(r | (q << kInfoShift)) : 0xffffffffu};
+            }
+        }
+        sl.push_back(a);
+        stride.push_back(static_cast<uint32_t>(m));
+    }
+    if (nrows >= (1ull << kInfoShift)) fail(WBX_TOO_LARGE, "too many rows for the segment layout");
+    const uint64_t ns = sl.size();
+    h.slice_ptr.assign(ns + 1, 0);
+    h.slice_np.assign(ns, 0);
+    h.lane_info.assign(ns * 32, 0xffffffffu);
+    for (uint64_t s = 0; s < ns; ++s) {
+        uint64_t np = 0;
+        for (const auto& g : sl[s]) np = std::max<uint64_t>(np, (g.len + 1) / 2);
+        if (np > kSegElems / 2) fail(WBX_TOO_LARGE, "segment longer than kSegElems");
+        // slice metadata word: pairs per lane (bits 0-7) | lane stride between segments (8-15)
+        h.slice_np[s] = static_cast<uint32_t>(np) | (stride[s] << 8);
+        h.slice_ptr[s + 1] = h.slice_ptr[s] + np * 32;
+    }
+    h.pk.assign(h.slice_ptr[ns], make_uint4(0, 0, 0, 0));
+    for (uint64_t s = 0; s < ns; ++s)
+        for (uint64_t lane = 0; lane < 32; ++lane) {
+            const Seg& g = sl[s][lane];
+            h.lane_info[s * 32 + lane] = g.info;
+            for (uint64_t j = 0; j < g.len; ++j) {
+                double v;
+                uint32_t c;
+                range.get(g.row, g.beg + j, c, v);
                 uint4& p = h.pk[h.slice_ptr[s] + (j / 2) * 32 + lane];
                 const float vf = static_cast<float>(v);
                 uint32_t bits;
@@ -87,34 +145,43 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
                 }
             }
         }
-    }
     return h;
 }
 
 void upload_sell(wbx_sell& d, const HostSell& h, uint64_t rows, cudaStream_t s, uint64_t& bytes) {
     d.rows = rows;
-    d.slices = h.slice_len.size();
+    d.xslices = h.xslice_len.size();
+    d.slices = h.slice_np.size();
     d.pairs = h.pk.size();
-    d.slice_ptr.upload(h.slice_ptr, s);
-    d.slice_len.upload(h.slice_len, s);
-    d.pk.upload(h.pk, s);
+    d.xslice_ptr.upload(h.xslice_ptr, s);
+    d.xslice_len.upload(h.xslice_len, s);
     d.val64.upload(h.v64, s);
     d.col.upload(h.col, s);
     d.row_len.upload(h.row_len, s);
-    bytes += d.row_len.bytes() + d.slice_ptr.bytes() + d.slice_len.bytes() + d.pk.bytes() + d.val64.bytes() + d.col.bytes();
+    d.slice_ptr.upload(h.slice_ptr, s);
+    d.slice_np.upload(h.slice_np, s);
+    d.pk.upload(h.pk, s);
+    d.lane_info.upload(h.lane_info, s);
+    bytes += d.xslice_ptr.bytes() + d.xslice_len.bytes() + d.val64.bytes() + d.col.bytes() +
+             d.row_len.bytes() + d.slice_ptr.bytes() + d.slice_np.bytes() + d.pk.bytes() +
+             d.lane_info.bytes();
 }
 
 }  // namespace
 
 SellView view_of(const wbx_sell& m) {
     SellView v;
-    v.slice_ptr = m.slice_ptr.p;
-    v.slice_len = m.slice_len.p;
-    v.pk = m.pk.p;
+    v.xslice_ptr = m.xslice_ptr.p;
+    v.xslice_len = m.xslice_len.p;
     v.v64 = m.val64.p;
     v.col = m.col.p;
     v.row_len = m.row_len.p;
+    v.slice_ptr = m.slice_ptr.p;
+    v.slice_np = m.slice_np.p;
+    v.pk = m.pk.p;
+    v.lane_info = m.lane_info.p;
     v.rows = static_cast<uint32_t>(m.rows);
+    v.xslices = static_cast<uint32_t>(m.xslices);
     v.slices = static_cast<uint32_t>(m.slices);
     return v;
 }

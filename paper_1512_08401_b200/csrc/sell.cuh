@@ -1,8 +1,15 @@
-// SELL-32 row dot products: one warp per slice, one lane per row.
+// Sliced-ELL row dot products over the two device layouts of an operator.
 //
-// The lane's row is summed SEQUENTIALLY in element order — the reference's in-row
-// order (theta.cpp:306-308) — so the exact fp64 variant reproduces the reference's
-// spmv bit for bit; the fp32 variants use FMA and differ only by rounding.
+// * Segmented fp32 layout (the hot path): every row is cut into segments of at most
+//   kSegElems = 16 nonzeros; one lane owns one segment and a row's segments sit in
+//   consecutive lanes of one 32-lane slice. A lane issues all of its (<= 8) 16-byte
+//   {val,col,val,col} loads back to back, then the (<= 16) gathers, so a warp's
+//   dependency chain is two memory round trips regardless of row length (rows reach 99
+//   nonzeros in Theta and 137 in Theta^T at 1024^2). Segment partials are combined by
+//   warp shuffles into the row's head lane in a fixed order (deterministic).
+// * Exact fp64 layout: one lane per row, the row summed SEQUENTIALLY in element order —
+//   the reference's in-row order (theta.cpp:306-308) with no FMA contraction — so it
+//   reproduces the reference's spmv bit for bit.
 #pragma once
 
 #include "device_util.cuh"
@@ -10,88 +17,88 @@
 namespace wbx {
 
 struct SellView {
-    const uint64_t* slice_ptr;  // pair offset per slice
-    const uint32_t* slice_len;  // padded (even) row length of the slice
-    const uint4* pk;            // fp32 {v0,c0,v1,c1}
-    const double* v64;          // fp64 values, element-major
-    const uint32_t* col;        // columns, element-major
-    const uint32_t* row_len;    // true row length (fp64 exact path)
-    uint32_t rows, slices;
+    // exact fp64
+    const uint64_t* xslice_ptr;
+    const uint32_t* xslice_len;
+    const double* v64;
+    const uint32_t* col;
+    const uint32_t* row_len;
+    // segmented fp32
+    const uint64_t* slice_ptr;
+    const uint32_t* slice_np;
+    const uint4* pk;
+    const uint32_t* lane_info;
+    uint32_t rows, xslices, slices;
 };
 
-// fp32 values, fp32 vector, fp32 FMA accumulation.
-__device__ __forceinline__ float sell_dot_f32(const SellView& M, uint32_t s, int lane,
-                                              const float* __restrict__ x) {
+constexpr uint32_t kNoRow = 0xffffffffu;
+constexpr uint32_t kRowMask = (1u << 27) - 1;
+
+// Segment partial of this lane, accumulated in ACC with gathers from X.
+template <typename ACC, typename X>
+__device__ __forceinline__ ACC seg_partial(const SellView& M, uint32_t s, int lane, const X* __restrict__ x) {
     const uint4* p = M.pk + M.slice_ptr[s] + lane;
-    const uint32_t np = M.slice_len[s] >> 1;
-    float acc = 0.f;
-    uint32_t j = 0;
-    for (; j + 4 <= np; j += 4) {
-        const uint4 e0 = ld_stream(p + (j + 0) * kWarp);
-        const uint4 e1 = ld_stream(p + (j + 1) * kWarp);
-        const uint4 e2 = ld_stream(p + (j + 2) * kWarp);
-        const uint4 e3 = ld_stream(p + (j + 3) * kWarp);
-        const float g0 = x[e0.y], g1 = x[e0.w], g2 = x[e1.y], g3 = x[e1.w];
-        const float g4 = x[e2.y], g5 = x[e2.w], g6 = x[e3.y], g7 = x[e3.w];
-        acc = fmaf(__uint_as_float(e0.x), g0, acc);
-        acc = fmaf(__uint_as_float(e0.z), g1, acc);
-        acc = fmaf(__uint_as_float(e1.x), g2, acc);
-        acc = fmaf(__uint_as_float(e1.z), g3, acc);
-        acc = fmaf(__uint_as_float(e2.x), g4, acc);
-        acc = fmaf(__uint_as_float(e2.z), g5, acc);
-        acc = fmaf(__uint_as_float(e3.x), g6, acc);
-        acc = fmaf(__uint_as_float(e3.z), g7, acc);
+    const uint32_t np = M.slice_np[s] & 0xffu;
+    const uint64_t pol = l2_keep_policy();
+    uint4 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = j < static_cast<int>(np) ? ld_stream(p + j * kWarp, pol) : make_uint4(0, 0, 0, 0);
+    X g[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j < static_cast<int>(np)) {
+            g[2 * j] = x[e[j].y];
+            g[2 * j + 1] = x[e[j].w];
+        } else {
+            g[2 * j] = X(0);
+            g[2 * j + 1] = X(0);
+        }
     }
-    for (; j < np; ++j) {
-        const uint4 e = ld_stream(p + j * kWarp);
-        acc = fmaf(__uint_as_float(e.x), x[e.y], acc);
-        acc = fmaf(__uint_as_float(e.z), x[e.w], acc);
+    ACC acc = ACC(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j < static_cast<int>(np)) {
+            acc = fma(static_cast<ACC>(__uint_as_float(e[j].x)), static_cast<ACC>(g[2 * j]), acc);
+            acc = fma(static_cast<ACC>(__uint_as_float(e[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
+        }
     }
     return acc;
 }
 
-// fp32 values, fp64 vector and accumulation (power iteration in the fp32 hot path).
-__device__ __forceinline__ double sell_dot_f32v_f64(const SellView& M, uint32_t s, int lane,
-                                                    const double* __restrict__ x) {
-    const uint4* p = M.pk + M.slice_ptr[s] + lane;
-    const uint32_t np = M.slice_len[s] >> 1;
-    double acc = 0.0;
-    uint32_t j = 0;
-    for (; j + 2 <= np; j += 2) {
-        const uint4 e0 = ld_stream(p + (j + 0) * kWarp);
-        const uint4 e1 = ld_stream(p + (j + 1) * kWarp);
-        const double g0 = x[e0.y], g1 = x[e0.w], g2 = x[e1.y], g3 = x[e1.w];
-        acc = fma(static_cast<double>(__uint_as_float(e0.x)), g0, acc);
-        acc = fma(static_cast<double>(__uint_as_float(e0.z)), g1, acc);
-        acc = fma(static_cast<double>(__uint_as_float(e1.x)), g2, acc);
-        acc = fma(static_cast<double>(__uint_as_float(e1.z)), g3, acc);
+// Combine segment partials into the head lane; returns the row index (kNoRow for
+// non-head lanes) and leaves the row sum in `acc` of the head lane.
+template <typename ACC>
+__device__ __forceinline__ uint32_t seg_combine(const SellView& M, uint32_t s, int lane, ACC& acc) {
+    const uint32_t info = M.lane_info[static_cast<uint64_t>(s) * kWarp + lane];
+    const uint32_t m = M.slice_np[s] >> 8;  // lane stride between a row's segments
+    const uint32_t nseg = info == kNoRow ? 1u : (info >> 27);
+    const uint32_t maxseg = __reduce_max_sync(0xffffffffu, nseg);
+    for (uint32_t j = 1; j < maxseg; ++j) {
+        const ACC t = __shfl_down_sync(0xffffffffu, acc, j * m);
+        if (j < nseg) acc += t;
     }
-    for (; j < np; ++j) {
-        const uint4 e = ld_stream(p + j * kWarp);
-        acc = fma(static_cast<double>(__uint_as_float(e.x)), x[e.y], acc);
-        acc = fma(static_cast<double>(__uint_as_float(e.z)), x[e.w], acc);
-    }
-    return acc;
+    return info == kNoRow ? kNoRow : (info & kRowMask);
 }
 
 // fp64 values, fp64 vector, reference arithmetic: s = s + v*x, no contraction,
-// exactly the row's own elements (no padding terms).
+// exactly the row's own elements.
 __device__ __forceinline__ double sell_dot_f64_exact(const SellView& M, uint32_t s, int lane,
                                                      const double* __restrict__ x) {
-    const uint64_t base = 2 * M.slice_ptr[s] + lane;
+    const uint64_t base = M.xslice_ptr[s] + lane;
     const uint32_t r = s * kWarp + lane;
     const uint32_t len = r < M.rows ? M.row_len[r] : 0;
+    const uint64_t pol = l2_keep_policy();
     double acc = 0.0;
     uint32_t j = 0;
     for (; j + 4 <= len; j += 4) {
-        const double v0 = ld_stream(M.v64 + base + (j + 0) * kWarp);
-        const double v1 = ld_stream(M.v64 + base + (j + 1) * kWarp);
-        const double v2 = ld_stream(M.v64 + base + (j + 2) * kWarp);
-        const double v3 = ld_stream(M.v64 + base + (j + 3) * kWarp);
-        const uint32_t c0 = ld_stream(M.col + base + (j + 0) * kWarp);
-        const uint32_t c1 = ld_stream(M.col + base + (j + 1) * kWarp);
-        const uint32_t c2 = ld_stream(M.col + base + (j + 2) * kWarp);
-        const uint32_t c3 = ld_stream(M.col + base + (j + 3) * kWarp);
+        const double v0 = ld_stream(M.v64 + base + (j + 0) * kWarp, pol);
+        const double v1 = ld_stream(M.v64 + base + (j + 1) * kWarp, pol);
+        const double v2 = ld_stream(M.v64 + base + (j + 2) * kWarp, pol);
+        const double v3 = ld_stream(M.v64 + base + (j + 3) * kWarp, pol);
+        const uint32_t c0 = ld_stream(M.col + base + (j + 0) * kWarp, pol);
+        const uint32_t c1 = ld_stream(M.col + base + (j + 1) * kWarp, pol);
+        const uint32_t c2 = ld_stream(M.col + base + (j + 2) * kWarp, pol);
+        const uint32_t c3 = ld_stream(M.col + base + (j + 3) * kWarp, pol);
         const double g0 = x[c0], g1 = x[c1], g2 = x[c2], g3 = x[c3];
         acc = __dadd_rn(acc, __dmul_rn(v0, g0));
         acc = __dadd_rn(acc, __dmul_rn(v1, g1));
@@ -99,8 +106,8 @@ __device__ __forceinline__ double sell_dot_f64_exact(const SellView& M, uint32_t
         acc = __dadd_rn(acc, __dmul_rn(v3, g3));
     }
     for (; j < len; ++j) {
-        const double v = ld_stream(M.v64 + base + j * kWarp);
-        const uint32_t c = ld_stream(M.col + base + j * kWarp);
+        const double v = ld_stream(M.v64 + base + j * kWarp, pol);
+        const uint32_t c = ld_stream(M.col + base + j * kWarp, pol);
         acc = __dadd_rn(acc, __dmul_rn(v, x[c]));
     }
     return acc;

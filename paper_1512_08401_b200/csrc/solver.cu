@@ -1,28 +1,37 @@
-// Preconditioned FISTA / ISTA on the device: ONE persistent cooperative kernel per solve.
+// Preconditioned FISTA / ISTA on the device: persistent cooperative kernels.
 //
 // Replaces run_pgd (`proj/src/solver.cpp:103-157`), estimate_step (:69-99) and
 // prox_weighted_l1_P (:57-67). Per iteration the reference does 3 CSR SpMVs and ~6
-// serial O(n) passes with fresh allocations; here one iteration is two grid-wide
-// phases of one resident kernel:
-//   phase A (rows R of Theta):      res[r] = (Theta y)[r] - x0[r]
-//   ---- grid barrier ----
-//   phase T (rows C of Theta^T):    g = (Theta^T res)[c]; z0 = y - tau g / p;
-//                                   x' = prox(z0); y = x' + beta_k (x' - x_prev)
-//   ---- grid barrier ----
-// fused: gradient + residual + preconditioner + weighted soft threshold + momentum.
+// serial O(n) passes with fresh allocations; here a solve is TWO resident kernels:
+//
+//   tau_kernel   (estimate_step): per power iteration
+//       phase A  t = Theta u / |w_prev|         (rows R)      -- grid barrier --
+//       phase T  w = P^-1/2 Theta^T t; <v,w>, <w,w>  (rows C of Theta^T) -- barrier+reduction --
+//   fista_kernel (run_pgd loop): per iteration
+//       phase A  res[r] = (Theta y)[r] - x0[r]                           -- grid barrier --
+//       phase T  g = (Theta^T res)[c]; z0 = y - tau g / p; x' = prox(z0);
+//                y = x' + beta_k (x' - x_prev)                             -- grid barrier --
+//     i.e. gradient + residual + preconditioner + weighted soft threshold + momentum
+//     fused into the Theta^T SpMV epilogue.
+//
 // Vectors live in COMPACTED coordinates (R = nonempty rows, C = nonempty columns);
 // every other coordinate has gradient exactly 0 (empty column of Theta), so its
 // trajectory is the 1-D recurrence x' = prox(y), y = x' + beta (x' - x_prev): those are
 // iterated to completion in registers in one pass (loop interchange; per-coordinate
 // arithmetic identical to the reference's).
 //
+// Each warp owns a fixed set of SELL slices for the whole solve; their metadata is
+// loaded once into registers, so an iteration's dependency chain per slice is the
+// operator load + the gather. The grid barrier is a flag barrier (one arrival word per
+// block, no atomics) whose master block also performs the deterministic grid reduction.
+//
 // Precision: WBX_FP32 is the hot path (fp32 values/vectors, FMA); WBX_FP64 reproduces
 // the reference arithmetic exactly (sequential in-row sums, no contraction, the
 // reference's expression order) and, given the same tau, its iterates BITWISE.
-// The step tau is estimated in fp64 accumulation by the reference's power iteration
-// (same CounterRng(0x5eed) start vector, 200-iteration cap, 1e-6 relative rule).
+// tau uses fp64 vectors and accumulation in both modes (fp32 or fp64 operator values)
+// with the reference's CounterRng(0x5eed) start, 200-iteration cap and 1e-6 rule.
 #include <cmath>
-#include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "internal.hpp"
 #include "sell.cuh"
@@ -35,6 +44,14 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarpsPerBlock = kBlock / 32;
+constexpr int kMaxK = 8;        // slices per warp kept in registers
+constexpr int kRedSlots = 4;    // values per grid reduction
+#ifndef WBX_FISTA_MINB
+#define WBX_FISTA_MINB 2
+#endif
+#ifndef WBX_TAU_MINB
+#define WBX_TAU_MINB 2
+#endif
 
 // output scalars (SolveArgs::out)
 enum : int {
@@ -45,6 +62,17 @@ enum : int {
     OUT_STATUS = 4,  // 0 ok, 8 nonfinite energy
     OUT_LAMBDA_MAX = 5,
     OUT_COUNT = 8
+};
+
+// Grid barrier state (device memory, zeroed once per solver).
+struct Sync {
+    unsigned* gen;     // released epoch
+    unsigned* arrive;  // [grid] arrived epoch per block
+    double* part;      // [kRedSlots][grid] block partials
+    double* red;       // [kRedSlots] grid totals of the last reduction
+    unsigned long long* trace;  // optional [trace_cap][grid][2] globaltimer stamps
+    unsigned trace_cap;
+    int mode;  // 0: master block releases (default), 1: every block polls all arrivals
 };
 
 struct SolveArgs {
@@ -65,7 +93,7 @@ struct SolveArgs {
     const double* beta64;  // beta_k, k = 1..max_iters (index k-1)
     const float* beta32;
     double lambda, tau_given, step_safety, ref_energy, rel_tol;
-    int have_tau, tau_from_device, max_iters, track, stop_on_ref, decoupled_inline;
+    int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline;
     // T-typed state
     void* yC;
     void* xpC;
@@ -74,17 +102,15 @@ struct SolveArgs {
     void* tpC;
     void* thrC;
     // power iteration (fp64)
-    double* vC;
     double* wv;
     double* uC;
     double* t64;
-    double* part;       // [16][grid] rotating partial sums
-    const double* dec_reg;  // [max_iters] decoupled sum w|x_k| (tracking)
-    const double* dec_supp; // [max_iters] decoupled support count (tracking)
+    const double* dec_reg;   // [max_iters] decoupled sum w|x_k| (tracking)
+    const double* dec_supp;  // [max_iters] decoupled support count (tracking)
     double* out;
     double* energies;
     unsigned long long* supports;
-    unsigned* bar;
+    Sync sync;
 };
 
 __device__ __forceinline__ bool bit_set(const uint32_t* mask, uint64_t i) {
@@ -110,18 +136,255 @@ __device__ __forceinline__ double rng_normal(uint64_t seed, uint64_t i) {
     return (i & 1) ? r * sin(a) : r * cos(a);
 }
 
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Master warp: poll all arrival words, every lane its strided subset with independent
+// loads per round (one memory round trip per round, not one per block), then acquire.
+__device__ __forceinline__ void wait_arrivals(const Sync& s, unsigned epoch, unsigned G) {
+    constexpr int kMaxPoll = 40;  // grids up to 1280 blocks
+    bool ok;
+    do {
+        unsigned v[kMaxPoll];
+#pragma unroll
+        for (int j = 0; j < kMaxPoll; ++j) {
+            const unsigned i = threadIdx.x + 32u * j;
+            v[j] = i < G ? ld_relaxed(s.arrive + i) : epoch;
+        }
+        ok = true;
+#pragma unroll
+        for (int j = 0; j < kMaxPoll; ++j) ok &= static_cast<int>(v[j] - epoch) >= 0;
+    } while (!__all_sync(0xffffffffu, ok));
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- grid barrier + reduction
+// Arrival: each block publishes its partials and then its epoch in its own word (no
+// atomics). Block 0's first warp waits for every word, reduces the partials in a fixed
+// order, publishes the totals and releases the epoch; the other blocks spin on it.
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Barrier epoch of this block; `start` is the released epoch seen at kernel entry.
+struct Epoch {
+    unsigned cur, start;
+};
+
+// Optional phase trace (WBX_TRACE_FILE): per barrier and block, the time the block
+// arrived and the time it saw the release.
+__device__ __forceinline__ void trace_point(const Sync& s, const Epoch& e, int which) {
+    if (s.trace != nullptr && threadIdx.x == 0) {
+        const unsigned idx = e.cur - e.start - 1;
+        if (idx < s.trace_cap) s.trace[(static_cast<uint64_t>(idx) * gridDim.x + blockIdx.x) * 2 + which] = globaltimer();
+    }
+}
+
+// All-poll barrier: a block arrives by publishing (partials, then) its epoch in its own
+// word; the first warp of EVERY block polls all arrival words (one batched round trip
+// per poll round) — no master hop, no atomics. Reductions: every block sums the
+// published block partials itself in the same fixed order, so all blocks obtain
+// bit-identical totals. Partials are double-buffered by epoch parity (a block cannot
+// run two barriers ahead of any other block).
+template <int NV>
+__device__ __forceinline__ void grid_sync_reduce(const Sync& s, Epoch& epoch, double (&v)[NV],
+                                                 double* smem) {
+    const unsigned G = gridDim.x;
+    ++epoch.cur;
+    double* part = s.part + static_cast<uint64_t>(epoch.cur & 1u) * kRedSlots * G;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const double b = block_sum<kBlock>(v[k], smem);
+        if (threadIdx.x == 0) part[k * G + blockIdx.x] = b;
+    }
+    trace_point(s, epoch, 0);
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        st_release(s.arrive + blockIdx.x, epoch.cur);
+    }
+    if (s.mode == 1) {  // all-poll: every block reduces
+        if (threadIdx.x < 32) {
+            wait_arrivals(s, epoch.cur, G);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                double t = 0.0;
+                for (unsigned i = threadIdx.x; i < G; i += 32) t += part[k * G + i];
+                t = warp_sum(t);
+                if (threadIdx.x == 0) smem[k] = t;
+            }
+        }
+    } else {  // master: block 0 reduces, publishes, releases
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            wait_arrivals(s, epoch.cur, G);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                double t = 0.0;
+                for (unsigned i = threadIdx.x; i < G; i += 32) t += part[k * G + i];
+                t = warp_sum(t);
+                if (threadIdx.x == 0) s.red[k] = t;
+            }
+            __syncwarp();
+            if (threadIdx.x == 0) st_release(s.gen, epoch.cur);
+        }
+        if (threadIdx.x == 0) {
+            while (static_cast<int>(ld_acquire(s.gen) - epoch.cur) < 0) {
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) smem[k] = s.red[k];
+        }
+    }
+    trace_point(s, epoch, 1);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = smem[k];
+    __syncthreads();
+}
+
+__device__ __forceinline__ void grid_sync(const Sync& s, Epoch& epoch, double* smem) {
+    const unsigned G = gridDim.x;
+    ++epoch.cur;
+    __syncthreads();
+    trace_point(s, epoch, 0);
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        st_release(s.arrive + blockIdx.x, epoch.cur);
+    }
+    if (s.mode == 1) {
+        if (threadIdx.x < 32) wait_arrivals(s, epoch.cur, G);
+    } else {
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            wait_arrivals(s, epoch.cur, G);
+            if (threadIdx.x == 0) st_release(s.gen, epoch.cur);
+        }
+        if (threadIdx.x == 0)
+            while (static_cast<int>(ld_acquire(s.gen) - epoch.cur) < 0) {
+            }
+    }
+    trace_point(s, epoch, 1);
+    (void)smem;
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- per-warp slice plan
+// The slices a warp owns (s = gwarp + k * nwarps) with their metadata in registers:
+// lane k holds slice k's pair offset and pair count, every lane its own lane_info word
+// for each slice. Falls back to per-slice metadata loads beyond kMaxK slices.
+struct Plan {
+    uint32_t nk;
+    uint32_t np;
+    uint64_t ptr;
+    uint32_t info[kMaxK];
+    bool fallback;
+};
+
+__device__ __forceinline__ Plan make_plan(const SellView& M, uint32_t gwarp, uint32_t nwarps, int lane) {
+    Plan p;
+    p.nk = M.slices > gwarp ? (M.slices - gwarp + nwarps - 1) / nwarps : 0;
+    p.fallback = p.nk > kMaxK;
+    p.np = 0;
+    p.ptr = 0;
+    if (!p.fallback && static_cast<uint32_t>(lane) < p.nk) {
+        const uint32_t s = gwarp + lane * nwarps;
+        p.ptr = M.slice_ptr[s];
+        p.np = M.slice_np[s];
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k)
+        p.info[k] = (!p.fallback && static_cast<uint32_t>(k) < p.nk)
+                        ? M.lane_info[static_cast<uint64_t>(gwarp + k * nwarps) * kWarp + lane]
+                        : kNoRow;
+    return p;
+}
+
+// Segment partial with explicit slice base / pair count (see seg_partial in sell.cuh).
+template <typename ACC, typename X>
+__device__ __forceinline__ ACC seg_partial_at(const uint4* __restrict__ p, uint32_t np,
+                                              const X* __restrict__ x, uint64_t pol) {
+    uint4 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = j < static_cast<int>(np) ? ld_stream(p + j * kWarp, pol) : make_uint4(0, 0, 0, 0);
+    X g[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        g[2 * j] = j < static_cast<int>(np) ? x[e[j].y] : X(0);
+        g[2 * j + 1] = j < static_cast<int>(np) ? x[e[j].w] : X(0);
+    }
+    ACC acc = ACC(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j < static_cast<int>(np)) {
+            acc = fma(static_cast<ACC>(__uint_as_float(e[j].x)), static_cast<ACC>(g[2 * j]), acc);
+            acc = fma(static_cast<ACC>(__uint_as_float(e[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
+        }
+    }
+    return acc;
+}
+
+// meta = slice_np word: pairs per lane (bits 0-7) | lane stride m of a row's segments
+template <typename ACC>
+__device__ __forceinline__ uint32_t combine_info(uint32_t info, uint32_t meta, ACC& acc) {
+    const uint32_t m = meta >> 8;
+    const uint32_t nseg = info == kNoRow ? 1u : (info >> 27);
+    const uint32_t maxseg = __reduce_max_sync(0xffffffffu, nseg);
+    for (uint32_t j = 1; j < maxseg; ++j) {
+        const ACC t = __shfl_down_sync(0xffffffffu, acc, j * m);
+        if (j < nseg) acc += t;
+    }
+    return info == kNoRow ? kNoRow : (info & kRowMask);
+}
+
+// Apply `epi(row, value)` to every row of the warp's slices: value = sum_j M[row,j] x[j]
+// accumulated in ACC over the segmented fp32 layout.
+template <typename ACC, typename X, typename Epi>
+__device__ __forceinline__ void for_rows_seg(const SellView& M, const Plan& plan, uint32_t gwarp, uint32_t nwarps,
+                                             int lane, const X* __restrict__ x, Epi epi) {
+    const uint64_t pol = l2_keep_policy();
+    if (!plan.fallback) {
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) {
+            if (static_cast<uint32_t>(k) >= plan.nk) break;
+            const uint64_t ptr = __shfl_sync(0xffffffffu, plan.ptr, k);
+            const uint32_t meta = __shfl_sync(0xffffffffu, plan.np, k);
+            ACC acc = seg_partial_at<ACC, X>(M.pk + ptr + lane, meta & 0xffu, x, pol);
+            const uint32_t row = combine_info(plan.info[k], meta, acc);
+            if (row != kNoRow) epi(row, acc);
+        }
+    } else {
+        for (uint32_t s = gwarp; s < M.slices; s += nwarps) {
+            const uint32_t meta = M.slice_np[s];
+            ACC acc = seg_partial_at<ACC, X>(M.pk + M.slice_ptr[s] + lane, meta & 0xffu, x, pol);
+            const uint32_t row = combine_info(M.lane_info[static_cast<uint64_t>(s) * kWarp + lane], meta, acc);
+            if (row != kNoRow) epi(row, acc);
+        }
+    }
+}
+
+// Same over the exact fp64 layout (one lane per row, reference order).
+template <typename Epi>
+__device__ __forceinline__ void for_rows_exact(const SellView& M, uint32_t gwarp, uint32_t nwarps, int lane,
+                                               const double* __restrict__ x, Epi epi) {
+    for (uint32_t s = gwarp; s < M.xslices; s += nwarps) {
+        const double v = sell_dot_f64_exact(M, s, lane, x);
+        const uint32_t r = s * kWarp + lane;
+        if (r < M.rows) epi(r, v);
+    }
+}
+
 // ---------------------------------------------------------------- precision traits
 template <typename T>
 struct Prec;
 
 template <>
 struct Prec<float> {
-    __device__ static float dot(const SellView& M, uint32_t s, int lane, const float* x) {
-        return sell_dot_f32(M, s, lane, x);
-    }
-    __device__ static double dot_pw(const SellView& M, uint32_t s, int lane, const double* x) {
-        return sell_dot_f32v_f64(M, s, lane, x);
-    }
     __device__ static float sub(float a, float b) { return a - b; }
     // z0 = y - (tau/p) g   (tp = tau/p precomputed in fp64, rounded once)
     __device__ static float z0(float y, float g, float tp, double, double) { return fmaf(-tp, g, y); }
@@ -129,20 +392,12 @@ struct Prec<float> {
         const float a = fabsf(z0) - thr;
         return a > 0.f ? (z0 > 0.f ? a : -a) : 0.f;
     }
-    __device__ static float momentum(float xn, float xp, float beta) {
-        return fmaf(beta, xn - xp, xn);
-    }
+    __device__ static float momentum(float xn, float xp, float beta) { return fmaf(beta, xn - xp, xn); }
     __device__ static float beta(const SolveArgs& a, int k) { return a.beta32[k - 1]; }
 };
 
 template <>
 struct Prec<double> {
-    __device__ static double dot(const SellView& M, uint32_t s, int lane, const double* x) {
-        return sell_dot_f64_exact(M, s, lane, x);
-    }
-    __device__ static double dot_pw(const SellView& M, uint32_t s, int lane, const double* x) {
-        return sell_dot_f64_exact(M, s, lane, x);
-    }
     __device__ static double sub(double a, double b) { return __dsub_rn(a, b); }
     // solver.cpp:126: y - tau * grad / p  ==  y - ((tau*grad)/p)
     __device__ static double z0(double y, double g, double, double tau, double p) {
@@ -165,22 +420,33 @@ __device__ __forceinline__ double thr_exact(double tau, double lambda, double w,
     return __ddiv_rn(__dmul_rn(__dmul_rn(tau, lambda), w), p);
 }
 
+// Row loop dispatch: T = float -> segmented fp32 values (ACC/X as given);
+// T = double -> exact fp64 layout.
+template <typename T, typename ACC, typename X, typename Epi>
+__device__ __forceinline__ void for_rows(const SellView& M, const Plan& plan, uint32_t gwarp, uint32_t nwarps,
+                                         int lane, const X* x, Epi epi) {
+    if constexpr (sizeof(T) == 4) {
+        for_rows_seg<ACC, X>(M, plan, gwarp, nwarps, lane, x, epi);
+    } else {
+        for_rows_exact(M, gwarp, nwarps, lane, reinterpret_cast<const double*>(x), epi);
+    }
+}
+
 // ---------------------------------------------------------------- decoupled coordinates
 // Coordinates with an empty Theta column: g == 0 exactly, so z0 == y and the iterate
 // is prox + momentum only. Runs K iterations per coordinate in registers and stops as
 // soon as x' == x_prev == 0 (then y == 0 forever: a fixed point).
 // mode 0: write x_K into x_full.  mode 1: per-iteration warp sums of w|x_k| and
-// [x_k != 0] into wsum[(k-1) * nwarps + gwarp] (deterministic, no atomics).
+// [x_k != 0] into w*[(k-1) * nwarps + gwarp] (deterministic, no atomics).
 template <typename T>
 __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, uint64_t gthread,
                                uint64_t nthreads, double* wreg, double* wsup, uint64_t nwarps) {
     const int lane = threadIdx.x & 31;
     const uint64_t gwarp = gthread >> 5;
-    // warp-uniform trip count so warp sums stay well-defined in mode 1
-    const uint64_t trips = (a.n + nthreads - 1) / nthreads;
+    const uint64_t trips = (a.n + nthreads - 1) / nthreads;  // warp-uniform
     for (uint64_t t = 0; t < trips; ++t) {
         const uint64_t i = t * nthreads + gthread;
-        bool active = i < a.n && !bit_set(a.isC, i);
+        const bool active = i < a.n && !bit_set(a.isC, i);
         T x = T(0), xp = T(0), y = T(0);
         T thr = T(0);
         double w = 0.0;
@@ -227,220 +493,170 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
     }
 }
 
-// ---------------------------------------------------------------- the persistent kernel
+// ---------------------------------------------------------------- estimate_step kernel
+// Power iteration on P^-1/2 Theta^T Theta P^-1/2 (solver.cpp:69-99). The reference's
+// v_k = w_k / |w_k| followed by u = P^-1/2 v is folded into the next product:
+// Theta (P^-1/2 v_k) = (Theta (P^-1/2 w_k)) / |w_k|, so an iteration is two phases.
 template <typename T>
-__global__ void __launch_bounds__(kBlock) solve_kernel(SolveArgs a) {
-    __shared__ double red[kWarpsPerBlock + 1];
-    const unsigned G = gridDim.x;
+__global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
     const int lane = threadIdx.x & 31;
     const uint32_t gwarp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const uint32_t nwarps = G * kWarpsPerBlock;
+    const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const uint64_t nthreads = static_cast<uint64_t>(G) * kBlock;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    const Plan pA = sizeof(T) == 4 ? make_plan(a.A, gwarp, nwarps, lane) : Plan{};
+    const Plan pT = sizeof(T) == 4 ? make_plan(a.T, gwarp, nwarps, lane) : Plan{};
+
+    // v0 = CounterRng(0x5eed) normals over ALL n, normalised by the full norm; only the
+    // C part ever meets Theta (Theta^T output is zero outside C).
+    double s2[1] = {0.0};
+    for (uint64_t i = gthread; i < a.n; i += nthreads) {
+        const double v = rng_normal(0x5eedull, i);
+        s2[0] += v * v;
+    }
+    for (uint64_t c = gthread; c < a.nC; c += nthreads) {
+        const double v = rng_normal(0x5eedull, a.C_glob[c]);
+        a.wv[c] = v;               // "w_prev" = raw v0, |w_prev| = |v0|
+        a.uC[c] = a.ispC[c] * v;   // P^-1/2 w_prev
+    }
+    grid_sync_reduce<1>(a.sync, epoch, s2, smem);
+    double nw_prev = sqrt(s2[0]);
+    double lambda_prev = 0.0;
+    int it = 0;
+    bool zero_op = false;
+    for (; it < 200; ++it) {
+        // t = Theta (P^-1/2 v) = Theta (P^-1/2 w_prev) / |w_prev|
+        const double inv = nw_prev;
+        for_rows<T, double, double>(a.A, pA, gwarp, nwarps, lane, a.uC,
+                                    [&](uint32_t r, double t) { a.t64[r] = t / inv; });
+        grid_sync(a.sync, epoch, smem);
+        // w = P^-1/2 Theta^T t ; <v, w>, <w, w> with v = w_prev / |w_prev|
+        double acc[2] = {0.0, 0.0};
+        for_rows<T, double, double>(a.T, pT, gwarp, nwarps, lane, a.t64, [&](uint32_t c, double g) {
+            const double w = g * a.ispC[c];
+            const double v = a.wv[c] / inv;
+            acc[0] += v * w;
+            acc[1] += w * w;
+            a.wv[c] = w;
+            a.uC[c] = a.ispC[c] * w;
+        });
+        grid_sync_reduce<2>(a.sync, epoch, acc, smem);
+        const double lambda = acc[0];
+        const double nw = sqrt(acc[1]);
+        if (nw == 0.0) {  // zero operator sentinel (solver.cpp:89)
+            zero_op = true;
+            ++it;
+            break;
+        }
+        if (it > 0 && fabs(lambda - lambda_prev) <= 1e-6 * fabs(lambda)) {
+            lambda_prev = lambda;
+            ++it;
+            break;
+        }
+        lambda_prev = lambda;
+        nw_prev = nw;
+    }
+    if (gthread == 0) {
+        a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
+        a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
+        a.out[OUT_LAMBDA_MAX] = lambda_prev;
+    }
+}
+
+// ---------------------------------------------------------------- FISTA kernel
+template <typename T>
+__global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
+    const int lane = threadIdx.x & 31;
+    const uint32_t gwarp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
     T* yC = static_cast<T*>(a.yC);
     T* xpC = static_cast<T*>(a.xpC);
     T* res = static_cast<T*>(a.res);
     T* x0R = static_cast<T*>(a.x0R);
     T* tpC = static_cast<T*>(a.tpC);
     T* thrC = static_cast<T*>(a.thrC);
-    unsigned slot = 0;  // rotating partials slot
-    auto part = [&](int which) { return a.part + static_cast<uint64_t>((slot * 4 + which) % 16) * G; };
+    const Plan pA = sizeof(T) == 4 ? make_plan(a.A, gwarp, nwarps, lane) : Plan{};
+    const Plan pT = sizeof(T) == 4 ? make_plan(a.T, gwarp, nwarps, lane) : Plan{};
+    const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
 
-    // ---- init: compacted copies of x0; warm start x = x_prev = y = x0 (solver.cpp:115-117)
+    // ---- init: compacted copies of x0; warm start x = x_prev = y = x0 (solver.cpp:115-117);
+    // per-coordinate tau/p and tau*lambda*w/p on C
     for (uint64_t c = gthread; c < a.nC; c += nthreads) {
         const T v = static_cast<T>(a.x0_full[a.C_glob[c]]);
         yC[c] = v;
         xpC[c] = v;
-    }
-    for (uint64_t r = gthread; r < a.nR; r += nthreads) x0R[r] = static_cast<T>(a.x0_full[a.R_glob[r]]);
-
-    // ---- step size: estimate_step (solver.cpp:69-99)
-    double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
-    if (!a.have_tau && !a.tau_from_device) {
-        // v = CounterRng(0x5eed) normals over ALL n, normalised by the full norm; only the
-        // C part of v ever meets Theta (v is zero outside C after the first product).
-        double s2 = 0.0;
-        for (uint64_t i = gthread; i < a.n; i += nthreads) {
-            const double v = rng_normal(0x5eedull, i);
-            s2 += v * v;
-        }
-        s2 = block_sum<kBlock>(s2, red);
-        if (threadIdx.x == 0) part(0)[blockIdx.x] = s2;
-        grid_sync(a.bar, G);
-        const double nv = sqrt(reduce_partials(part(0), G, red));
-        ++slot;
-        for (uint64_t c = gthread; c < a.nC; c += nthreads) {
-            const double v = rng_normal(0x5eedull, a.C_glob[c]) / nv;
-            a.vC[c] = v;
-            a.uC[c] = a.ispC[c] * v;
-        }
-        grid_sync(a.bar, G);
-        double lambda_prev = 0.0;
-        int it = 0;
-        bool zero_op = false;
-        for (; it < 200; ++it) {
-            // t = Theta (isp .* v)
-            for (uint32_t s = gwarp; s < a.A.slices; s += nwarps) {
-                const double t = Prec<T>::dot_pw(a.A, s, lane, a.uC);
-                const uint32_t r = s * kWarp + lane;
-                if (r < a.A.rows) a.t64[r] = t;
-            }
-            grid_sync(a.bar, G);
-            // w = isp .* (Theta^T t); partial <v,w>, <w,w>
-            double pl = 0.0, pn = 0.0;
-            for (uint32_t s = gwarp; s < a.T.slices; s += nwarps) {
-                const double g = Prec<T>::dot_pw(a.T, s, lane, a.t64);
-                const uint32_t c = s * kWarp + lane;
-                if (c < a.T.rows) {
-                    const double w = g * a.ispC[c];
-                    a.wv[c] = w;
-                    pl += a.vC[c] * w;
-                    pn += w * w;
-                }
-            }
-            pl = block_sum<kBlock>(pl, red);
-            pn = block_sum<kBlock>(pn, red);
-            if (threadIdx.x == 0) {
-                part(0)[blockIdx.x] = pl;
-                part(1)[blockIdx.x] = pn;
-            }
-            grid_sync(a.bar, G);
-            const double lambda = reduce_partials(part(0), G, red);
-            const double nw = sqrt(reduce_partials(part(1), G, red));
-            ++slot;
-            if (nw == 0.0) {
-                zero_op = true;
-                ++it;
-                break;
-            }
-            for (uint64_t c = gthread; c < a.nC; c += nthreads) {
-                const double v = a.wv[c] / nw;
-                a.vC[c] = v;
-                a.uC[c] = a.ispC[c] * v;
-            }
-            if (it > 0 && fabs(lambda - lambda_prev) <= 1e-6 * fabs(lambda)) {
-                lambda_prev = lambda;
-                ++it;
-                break;
-            }
-            lambda_prev = lambda;
-            grid_sync(a.bar, G);
-        }
-        tau = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
-        if (gthread == 0) {
-            a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
-            a.out[OUT_LAMBDA_MAX] = lambda_prev;
-        }
-    }
-    if (gthread == 0 && !a.tau_from_device) {
-        a.out[OUT_TAU] = tau;
-        if (a.have_tau) a.out[OUT_TAU_ITERS] = 0;
-    }
-
-    // ---- per-coordinate constants on C: tau/p and tau*lambda*w/p
-    for (uint64_t c = gthread; c < a.nC; c += nthreads) {
         tpC[c] = static_cast<T>(tau / a.pC[c]);
         thrC[c] = static_cast<T>(thr_exact(tau, a.lambda, a.wC[c], a.pC[c]));
     }
-
-    // ---- tracking: initial energy E(x0) (solver.cpp:118)
-    double stop_gap = 0.0, quad_nonR = 0.0;
-    if (a.track) {
-        double qn = 0.0, rg = 0.0;
-        for (uint64_t i = gthread; i < a.n; i += nthreads) {
-            const double x0 = a.x0_full[i];
-            if (!bit_set(a.isR, i)) qn += x0 * x0;
-            rg += a.w_full[i] * fabs(x0);
-        }
-        double qr = 0.0;
-        for (uint32_t s = gwarp; s < a.A.slices; s += nwarps) {
-            const uint32_t r = s * kWarp + lane;
-            const double t = static_cast<double>(Prec<T>::dot(a.A, s, lane, yC));
-            if (r < a.A.rows) {
-                const double d = t - static_cast<double>(x0R[r]);
-                qr += d * d;
-            }
-        }
-        qn = block_sum<kBlock>(qn, red);
-        rg = block_sum<kBlock>(rg, red);
-        qr = block_sum<kBlock>(qr, red);
-        if (threadIdx.x == 0) {
-            part(0)[blockIdx.x] = qn;
-            part(1)[blockIdx.x] = rg;
-            part(2)[blockIdx.x] = qr;
-        }
-        grid_sync(a.bar, G);
-        quad_nonR = reduce_partials(part(0), G, red);
-        const double reg0 = reduce_partials(part(1), G, red);
-        const double quadR0 = reduce_partials(part(2), G, red);
-        ++slot;
-        const double e0 = 0.5 * (quadR0 + quad_nonR) + a.lambda * reg0;
-        stop_gap = a.rel_tol * e0;
-        if (gthread == 0) a.out[OUT_INITIAL_ENERGY] = e0;
-    }
+    for (uint64_t r = gthread; r < a.nR; r += nthreads) x0R[r] = static_cast<T>(a.x0_full[a.R_glob[r]]);
 
     // ---- decoupled coordinates (independent of everything else)
     if (a.decoupled_inline) decoupled_pass<T>(a, tau, a.max_iters, 0, gthread, nthreads, nullptr, nullptr, 0);
 
-    grid_sync(a.bar, G);
+    // ---- tracking: initial energy E(x0) (solver.cpp:118)
+    double stop_gap = 0.0, quad_nonR = 0.0;
+    if (a.track) {
+        grid_sync(a.sync, epoch, smem);  // yC / x0R complete
+        double e[3] = {0.0, 0.0, 0.0};
+        for (uint64_t i = gthread; i < a.n; i += nthreads) {
+            const double x0 = a.x0_full[i];
+            if (!bit_set(a.isR, i)) e[0] += x0 * x0;
+            e[1] += a.w_full[i] * fabs(x0);
+        }
+        for_rows<T, T, T>(a.A, pA, gwarp, nwarps, lane, yC, [&](uint32_t r, T t) {
+            const double d = static_cast<double>(t) - static_cast<double>(x0R[r]);
+            e[2] += d * d;
+        });
+        grid_sync_reduce<3>(a.sync, epoch, e, smem);
+        quad_nonR = e[0];
+        const double e0 = 0.5 * (e[2] + quad_nonR) + a.lambda * e[1];
+        stop_gap = a.rel_tol * e0;
+        if (gthread == 0) a.out[OUT_INITIAL_ENERGY] = e0;
+    } else {
+        grid_sync(a.sync, epoch, smem);
+    }
 
     // ---- the FISTA / ISTA loop (solver.cpp:121-151)
     int k = 1;
     for (; k <= a.max_iters; ++k) {
         // phase A: res = Theta y - x0 on nonempty rows
-        for (uint32_t s = gwarp; s < a.A.slices; s += nwarps) {
-            const T acc = Prec<T>::dot(a.A, s, lane, yC);
-            const uint32_t r = s * kWarp + lane;
-            if (r < a.A.rows) res[r] = Prec<T>::sub(acc, x0R[r]);
-        }
-        grid_sync(a.bar, G);
+        for_rows<T, T, T>(a.A, pA, gwarp, nwarps, lane, yC,
+                          [&](uint32_t r, T acc) { res[r] = Prec<T>::sub(acc, x0R[r]); });
+        grid_sync(a.sync, epoch, smem);
         // phase T: gradient on nonempty columns + fused step / prox / momentum
         const T beta = Prec<T>::beta(a, k);
-        double reg = 0.0, sup = 0.0;
-        for (uint32_t s = gwarp; s < a.T.slices; s += nwarps) {
-            const T g = Prec<T>::dot(a.T, s, lane, res);
-            const uint32_t c = s * kWarp + lane;
-            if (c < a.T.rows) {
-                const T y = yC[c], xp = xpC[c];
-                const T z0 = Prec<T>::z0(y, g, tpC[c], tau, a.pC[c]);
-                const T xn = Prec<T>::prox(z0, thrC[c]);
-                yC[c] = Prec<T>::momentum(xn, xp, beta);
-                xpC[c] = xn;
-                if (a.track) {
-                    reg += a.wC[c] * fabs(static_cast<double>(xn));
-                    sup += xn != T(0) ? 1.0 : 0.0;
-                }
+        double tr[3] = {0.0, 0.0, 0.0};
+        for_rows<T, T, T>(a.T, pT, gwarp, nwarps, lane, res, [&](uint32_t c, T g) {
+            const T y = yC[c], xp = xpC[c];
+            const T z0 = Prec<T>::z0(y, g, tpC[c], tau, a.pC[c]);
+            const T xn = Prec<T>::prox(z0, thrC[c]);
+            yC[c] = Prec<T>::momentum(xn, xp, beta);
+            xpC[c] = xn;
+            if (a.track) {
+                tr[1] += a.wC[c] * fabs(static_cast<double>(xn));
+                tr[2] += xn != T(0) ? 1.0 : 0.0;
             }
-        }
-        grid_sync(a.bar, G);
+        });
+        grid_sync(a.sync, epoch, smem);
         if (a.track) {
             // energy(x') (solver.cpp:130, :44-55): Theta x' on rows R
-            double qr = 0.0;
-            for (uint32_t s = gwarp; s < a.A.slices; s += nwarps) {
-                const uint32_t r = s * kWarp + lane;
-                const double t = static_cast<double>(Prec<T>::dot(a.A, s, lane, xpC));
-                if (r < a.A.rows) {
-                    const double d = t - static_cast<double>(x0R[r]);
-                    qr += d * d;
-                }
-            }
-            qr = block_sum<kBlock>(qr, red);
-            reg = block_sum<kBlock>(reg, red);
-            sup = block_sum<kBlock>(sup, red);
-            if (threadIdx.x == 0) {
-                part(0)[blockIdx.x] = qr;
-                part(1)[blockIdx.x] = reg;
-                part(2)[blockIdx.x] = sup;
-            }
-            grid_sync(a.bar, G);
-            const double quadR = reduce_partials(part(0), G, red);
-            const double regC = reduce_partials(part(1), G, red);
-            const double supC = reduce_partials(part(2), G, red);
-            ++slot;
-            const double e = 0.5 * (quadR + quad_nonR) + a.lambda * (regC + a.dec_reg[k - 1]);
+            for_rows<T, T, T>(a.A, pA, gwarp, nwarps, lane, xpC, [&](uint32_t r, T t) {
+                const double d = static_cast<double>(t) - static_cast<double>(x0R[r]);
+                tr[0] += d * d;
+            });
+            grid_sync_reduce<3>(a.sync, epoch, tr, smem);
+            const double e = 0.5 * (tr[0] + quad_nonR) + a.lambda * (tr[1] + a.dec_reg[k - 1]);
             if (gthread == 0) {
                 a.energies[k - 1] = e;
-                a.supports[k - 1] = static_cast<unsigned long long>(supC + a.dec_supp[k - 1]);
+                a.supports[k - 1] = static_cast<unsigned long long>(tr[2] + a.dec_supp[k - 1]);
             }
             if (!isfinite(e)) {
                 if (gthread == 0) a.out[OUT_STATUS] = 8.0;
@@ -479,6 +695,11 @@ __global__ void reduce_rows_kernel(const double* w, uint64_t nwarps, int K, doub
     outp[k] = s;
 }
 
+__global__ void set_tau_kernel(double* out, double tau) {
+    out[OUT_TAU] = tau;
+    out[OUT_TAU_ITERS] = 0;
+}
+
 __global__ void clamp_kernel(double* u, uint64_t n) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) u[i] = fmin(fmax(u[i], 0.0), 1.0);  // std::clamp(v, 0, 1), waveblur.cpp:297
@@ -499,11 +720,13 @@ struct wbx_solver {
     wbx::DevBuf<double> pC, wC, ispC, w_full, p_full, beta64;
     wbx::DevBuf<float> beta32;
     wbx::DevBuf<unsigned char> state;  // yC, xpC, res, x0R, tpC, thrC (T-typed)
-    wbx::DevBuf<double> vC, wv, uC, t64, part, out, energies, dec_reg, dec_supp, wreg, wsup;
+    wbx::DevBuf<double> wv, uC, t64, out, energies, dec_reg, dec_supp, wreg, wsup, part, red;
     wbx::DevBuf<unsigned long long> supports;
-    wbx::DevBuf<unsigned> bar;
+    wbx::DevBuf<unsigned> gen, arrive;
+    wbx::DevBuf<unsigned long long> trace;  // WBX_TRACE_FILE diagnostics
+    uint64_t trace_cap = 0;
     wbx::DevBuf<double> u0, x0full, xfull, uout;
-    int grid = 0;
+    int grid_fista = 0, grid_tau = 0;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     uint64_t last_launches = 0;
@@ -514,12 +737,16 @@ namespace wbx {
 
 namespace {
 
-template <typename T>
-int occupancy_grid(wbx_ctx* ctx) {
+int blocks_per_sm(const void* kernel) {
     int per_sm = 0;
-    WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<T>, kBlock, 0));
+    WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
     if (per_sm < 1) fail(WBX_CUDA_ERROR, "solver kernel cannot be resident");
-    return per_sm * ctx->num_sms;
+    // tuning override: WBX_SOLVER_BLOCKS_PER_SM (clamped to what is co-resident)
+    if (const char* e = std::getenv("WBX_SOLVER_BLOCKS_PER_SM")) {
+        const int want = std::atoi(e);
+        if (want >= 1 && want < per_sm) per_sm = want;
+    }
+    return per_sm;
 }
 
 template <typename T>
@@ -546,7 +773,7 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.beta32 = s->beta32.p;
     a.lambda = s->lambda;
     a.tau_given = s->cfg.tau;
-    a.have_tau = s->cfg.tau > 0.0;
+    a.tau_from_device = 1;
     a.step_safety = s->cfg.step_safety;
     a.ref_energy = s->cfg.ref_energy;
     a.rel_tol = s->cfg.rel_energy_tol;
@@ -567,18 +794,31 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.x0R = carve(nR);
     a.tpC = carve(nC);
     a.thrC = carve(nC);
-    a.vC = s->vC.p;
     a.wv = s->wv.p;
     a.uC = s->uC.p;
     a.t64 = s->t64.p;
-    a.part = s->part.p;
     a.dec_reg = s->dec_reg.p;
     a.dec_supp = s->dec_supp.p;
     a.out = s->out.p;
     a.energies = s->energies.p;
     a.supports = s->supports.p;
-    a.bar = s->bar.p;
+    a.sync.gen = s->gen.p;
+    a.sync.arrive = s->arrive.p;
+    a.sync.part = s->part.p;
+    a.sync.red = s->red.p;
+    a.sync.trace = s->trace.p;
+    a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
+    {
+        const char* e = std::getenv("WBX_BARRIER");
+        a.sync.mode = (e && std::string(e) == "allpoll") ? 1 : 0;
+    }
     return a;
+}
+
+template <typename T>
+void launch_coop(const void* kernel, int grid, SolveArgs& a, cudaStream_t st) {
+    void* params[] = {&a};
+    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, 0, st));
 }
 
 template <typename T>
@@ -586,24 +826,22 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
     WBX_CUDA(cudaMemsetAsync(s->out.p, 0, s->out.bytes(), st));
-    void* params[] = {&a};
+    // step: estimate_step on the device, or the given one
+    if (s->cfg.tau > 0.0) {
+        set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
+    } else {
+        launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
+    }
+    count_launch(ctx);
     if (!a.track) {
-        WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_kernel<T>), dim3(s->grid),
-                                             dim3(kBlock), params, 0, st));
+        launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
         count_launch(ctx);
+        WBX_CUDA(cudaGetLastError());
         return;
     }
     // Tracking (energies / supports / ref_energy stopping rule, solver.cpp:130-150):
-    // (1) tau-only pass; (2) decoupled per-iteration sums with that tau; (3) reduce them;
-    // (4) tracked solve; (5) decoupled final write at the iteration count used.
-    SolveArgs pre = a;
-    pre.max_iters = 0;
-    pre.track = 0;
-    pre.decoupled_inline = 0;
-    pre.stop_on_ref = 0;
-    void* pparams[] = {&pre};
-    WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_kernel<T>), dim3(s->grid),
-                                         dim3(kBlock), pparams, 0, st));
+    // decoupled per-iteration sums with the tau on device, reduced; tracked solve;
+    // decoupled final write at the iteration count used.
     const uint64_t nthreads = static_cast<uint64_t>(s->dec_grid) * kBlock;
     const uint64_t nwarps = nthreads / 32;
     const int K = a.max_iters;
@@ -615,11 +853,9 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         reduce_rows_kernel<<<(K + 127) / 128, 128, 0, st>>>(s->wsup.p, nwarps, K, s->dec_supp.p);
         count_launch(ctx, 3);
     }
-    a.tau_from_device = 1;
-    WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_kernel<T>), dim3(s->grid),
-                                         dim3(kBlock), params, 0, st));
+    launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
     decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, 0, nullptr, nullptr, s->out.p);
-    count_launch(ctx, 3);
+    count_launch(ctx, 2);
     WBX_CUDA(cudaGetLastError());
 }
 
@@ -628,6 +864,8 @@ void alloc_state(wbx_solver* s) {
     const wbx_op* op = s->op;
     auto rnd = [](uint64_t count) { return ((count * sizeof(T) + 255) / 256) * 256; };
     s->state.alloc(4 * rnd(op->nC) + 2 * rnd(op->nR) + 256);
+    s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_kernel<T>)) * s->ctx->num_sms;
+    s->grid_tau = blocks_per_sm(reinterpret_cast<const void*>(tau_kernel<T>)) * s->ctx->num_sms;
 }
 
 }  // namespace
@@ -666,22 +904,22 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     }
     s->beta64.upload(b64, st);
     s->beta32.upload(b32, st);
-    if (s->cfg.precision == WBX_FP64) {
+    if (s->cfg.precision == WBX_FP64)
         alloc_state<double>(s);
-        s->grid = occupancy_grid<double>(s->ctx);
-    } else {
+    else
         alloc_state<float>(s);
-        s->grid = occupancy_grid<float>(s->ctx);
-    }
     s->dec_grid = 4 * s->ctx->num_sms;
-    s->vC.alloc(nC ? nC : 1);
     s->wv.alloc(nC ? nC : 1);
     s->uC.alloc(nC ? nC : 1);
     s->t64.alloc(op->nR ? op->nR : 1);
-    s->part.alloc(16 * static_cast<uint64_t>(s->grid));
     s->out.alloc(OUT_COUNT);
-    s->bar.alloc(2);
-    WBX_CUDA(cudaMemsetAsync(s->bar.p, 0, s->bar.bytes(), st));
+    const uint64_t gmax = static_cast<uint64_t>(std::max(s->grid_fista, s->grid_tau));
+    s->gen.alloc(32);
+    s->arrive.alloc(gmax);
+    s->part.alloc(2 * kRedSlots * gmax);
+    s->red.alloc(kRedSlots);
+    WBX_CUDA(cudaMemsetAsync(s->gen.p, 0, s->gen.bytes(), st));
+    WBX_CUDA(cudaMemsetAsync(s->arrive.p, 0, s->arrive.bytes(), st));
     const bool track = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
     if (track && K > 0) {
         const uint64_t nwarps = static_cast<uint64_t>(s->dec_grid) * kBlock / 32;
@@ -691,6 +929,11 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
         s->dec_supp.alloc(K);
         s->wreg.alloc(K * nwarps);
         s->wsup.alloc(K * nwarps);
+    }
+    if (std::getenv("WBX_TRACE_FILE")) {
+        s->trace_cap = 1024;
+        s->trace.alloc(s->trace_cap * gmax * 2);
+        WBX_CUDA(cudaMemsetAsync(s->trace.p, 0, s->trace.bytes(), st));
     }
     WBX_CUDA(cudaEventCreate(&s->ev0));
     WBX_CUDA(cudaEventCreate(&s->ev1));
@@ -715,6 +958,16 @@ void solver_report(wbx_solver* s, wbx_report* rep) {
     float ms = 0.f;
     WBX_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
     s->last_solve_ms = ms;
+    if (s->trace.p) {
+        if (FILE* f = std::fopen(std::getenv("WBX_TRACE_FILE"), "ab")) {
+            std::vector<unsigned long long> h(s->trace.n);
+            WBX_CUDA(cudaMemcpy(h.data(), s->trace.p, s->trace.bytes(), cudaMemcpyDeviceToHost));
+            const unsigned long long hdr[2] = {static_cast<unsigned long long>(s->grid_fista), s->trace_cap};
+            std::fwrite(hdr, sizeof hdr, 1, f);
+            std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+            std::fclose(f);
+        }
+    }
     if (out[OUT_STATUS] == 8.0) fail(WBX_NONFINITE_ENERGY, "solver diverged (non-finite energy)");
     if (rep == nullptr) return;
     rep->iters_used = static_cast<uint64_t>(out[OUT_ITERS_USED]);
@@ -734,10 +987,6 @@ void launch_clamp(wbx_ctx* ctx, double* u, uint64_t n, cudaStream_t st) {
     clamp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(u, n);
     count_launch(ctx);
 }
-
-}  // namespace wbx
-
-namespace wbx {
 
 wbx_solver* solver_new(wbx_ctx* ctx, const wbx_op* op, wbx_basis* basis, double lambda,
                        const wbx_solver_cfg& cfg, int accelerate) {

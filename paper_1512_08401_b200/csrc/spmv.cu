@@ -31,7 +31,7 @@ __global__ void scatter_kernel(const T* __restrict__ in, const uint32_t* __restr
 __global__ void sell_f64_kernel(SellView M, const double* __restrict__ x, double* __restrict__ y) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (warp >= M.slices) return;
+    if (warp >= M.xslices) return;
     const double v = sell_dot_f64_exact(M, warp, lane, x);
     const uint32_t r = warp * kWarp + lane;
     if (r < M.rows) y[r] = v;
@@ -41,9 +41,9 @@ __global__ void sell_f32_kernel(SellView M, const float* __restrict__ x, float* 
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= M.slices) return;
-    const float v = sell_dot_f32(M, warp, lane, x);
-    const uint32_t r = warp * kWarp + lane;
-    if (r < M.rows) y[r] = v;
+    float v = seg_partial<float, float>(M, warp, lane, x);
+    const uint32_t r = seg_combine(M, warp, lane, v);
+    if (r != kNoRow) y[r] = v;
 }
 
 inline unsigned blocks_for(uint64_t threads) {
@@ -63,7 +63,7 @@ void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
         gather_kernel<T><<<blocks_for(m_in), kBlock, 0, s>>>(x, in_idx, m_in, xin.p);
         const SellView v = view_of(M);
         if constexpr (sizeof(T) == 8)
-            sell_f64_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
+            sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
         else
             sell_f32_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
         scatter_kernel<T><<<blocks_for(m_out), kBlock, 0, s>>>(yout.p, out_idx, m_out, y);
@@ -87,10 +87,10 @@ void spmv_full_fp32(wbx_op* op, int transpose, const float* x_dev, float* y_dev,
 // y[R] = A x[C] with both vectors already compacted.
 template <typename T>
 void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s) {
-    if (M.slices == 0) return;
+    if (M.rows == 0) return;
     const SellView v = view_of(M);
     if constexpr (sizeof(T) == 8)
-        sell_f64_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, x, y);
+        sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, x, y);
     else
         sell_f32_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, x, y);
     count_launch(ctx);
