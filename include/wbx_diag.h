@@ -9,6 +9,15 @@ extern "C" {
  * kernels, measured over `iters` back-to-back barriers with blocks_per_sm resident CTAs
  * per SM (256 threads each). */
 int wbx_diag_barrier_us(int device, int iters, int blocks_per_sm, double* us);
+/* Streaming read bandwidth (GB/s) of a `bytes`-sized buffer read `reps` times by a
+ * persistent grid: mode 0 = per-warp 1-D bulk copies (TMA) of `chunk` bytes into shared
+ * memory with `inflight` copies in flight; mode 1 = 16-byte LDG per lane (8 in flight). */
+int wbx_diag_stream_gbs(int device, int mode, uint64_t bytes, int reps, int chunk, int inflight,
+                        int blocks_per_sm, double* gbs);
+/* Per-slice cycle accounting of the last solves run with WBX_DEBUG_MODE=2: average cycles
+ * per slice in [TMA wait, load+gather+FMA, combine+issue+epilogue] and the slice count;
+ * resets the counters. */
+int wbx_diag_slice_profile(double* out4);
 #ifdef __cplusplus
 }
 #endif

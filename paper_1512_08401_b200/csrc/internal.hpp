@@ -108,6 +108,9 @@ struct wbx_sell {
     wbx::DevBuf<uint32_t> slice_np;   // pairs per lane in the slice (<= 8)
     wbx::DevBuf<uint4> pk;            // {val0,col0,val1,col1} fp32 pairs
     wbx::DevBuf<uint32_t> lane_info;  // head lane: row | nseg << 27; else 0xffffffff
+    // the same slices as contiguous records for TMA staging: [lane_info x32][pairs]
+    wbx::DevBuf<uint64_t> rec_off;    // uint4 offset of each record
+    wbx::DevBuf<uint4> rec;
 };
 
 struct wbx_op {

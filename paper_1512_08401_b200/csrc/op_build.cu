@@ -43,6 +43,8 @@ struct HostSell {
     std::vector<uint32_t> slice_np;
     std::vector<uint4> pk;
     std::vector<uint32_t> lane_info;
+    std::vector<uint64_t> rec_off;  // uint4 offset of each slice record (+ total)
+    std::vector<uint4> rec;
 };
 
 // rows: list of row ids (in slice order); each row r has [beg[r], end[r]) in (cols, vals),
@@ -123,6 +125,9 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
         h.slice_np[s] = static_cast<uint32_t>(np) | (stride[s] << 8);
         h.slice_ptr[s + 1] = h.slice_ptr[s] + np * 32;
     }
+    // slice records for the TMA-staged solver: [lane_info: 32 x u32][pairs: np x 32 x uint4]
+    h.rec_off.assign(ns + 1, 0);
+    for (uint64_t s = 0; s < ns; ++s) h.rec_off[s + 1] = h.rec_off[s] + 8 + (h.slice_np[s] & 0xffu) * 32;
     h.pk.assign(h.slice_ptr[ns], make_uint4(0, 0, 0, 0));
     for (uint64_t s = 0; s < ns; ++s)
         for (uint64_t lane = 0; lane < 32; ++lane) {
@@ -145,6 +150,14 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
                 }
             }
         }
+    h.rec.assign(h.rec_off[ns], make_uint4(0, 0, 0, 0));
+    for (uint64_t s = 0; s < ns; ++s) {
+        uint32_t* info = reinterpret_cast<uint32_t*>(&h.rec[h.rec_off[s]]);
+        for (uint64_t lane = 0; lane < 32; ++lane) info[lane] = h.lane_info[s * 32 + lane];
+        const uint64_t np = h.slice_np[s] & 0xffu;
+        std::copy(h.pk.begin() + static_cast<long>(h.slice_ptr[s]),
+                  h.pk.begin() + static_cast<long>(h.slice_ptr[s] + np * 32), h.rec.begin() + static_cast<long>(h.rec_off[s] + 8));
+    }
     return h;
 }
 
@@ -162,6 +175,9 @@ void upload_sell(wbx_sell& d, const HostSell& h, uint64_t rows, cudaStream_t s, 
     d.slice_np.upload(h.slice_np, s);
     d.pk.upload(h.pk, s);
     d.lane_info.upload(h.lane_info, s);
+    d.rec_off.upload(h.rec_off, s);
+    d.rec.upload(h.rec, s);
+    bytes += d.rec_off.bytes() + d.rec.bytes();
     bytes += d.xslice_ptr.bytes() + d.xslice_len.bytes() + d.val64.bytes() + d.col.bytes() +
              d.row_len.bytes() + d.slice_ptr.bytes() + d.slice_np.bytes() + d.pk.bytes() +
              d.lane_info.bytes();
@@ -180,6 +196,8 @@ SellView view_of(const wbx_sell& m) {
     v.slice_np = m.slice_np.p;
     v.pk = m.pk.p;
     v.lane_info = m.lane_info.p;
+    v.rec = m.rec.p;
+    v.rec_off = m.rec_off.p;
     v.rows = static_cast<uint32_t>(m.rows);
     v.xslices = static_cast<uint32_t>(m.xslices);
     v.slices = static_cast<uint32_t>(m.slices);

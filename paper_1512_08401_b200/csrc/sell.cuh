@@ -28,6 +28,8 @@ struct SellView {
     const uint32_t* slice_np;
     const uint4* pk;
     const uint32_t* lane_info;
+    const uint4* rec;          // slice records [lane_info x32][pairs] (TMA staging)
+    const uint64_t* rec_off;   // uint4 offset of each record
     uint32_t rows, xslices, slices;
 };
 

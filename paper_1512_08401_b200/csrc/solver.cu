@@ -35,6 +35,7 @@
 
 #include "internal.hpp"
 #include "sell.cuh"
+#include "stream.cuh"
 
 extern "C" void wbx_set_last_error(const char* msg);
 
@@ -93,7 +94,7 @@ struct SolveArgs {
     const double* beta64;  // beta_k, k = 1..max_iters (index k-1)
     const float* beta32;
     double lambda, tau_given, step_safety, ref_energy, rel_tol;
-    int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline;
+    int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline, nslots;
     // T-typed state
     void* yC;
     void* xpC;
@@ -493,6 +494,186 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
     }
 }
 
+// Diagnostics switch (WBX_DEBUG_MODE, timing experiments only; results are wrong when set):
+// 1 = gather x[0] instead of x[col] (removes the gather dependency).
+__device__ int g_debug_mode = 0;
+// 2 = per-slice cycle accounting: [tma wait, load+gather+fma, combine+issue+epilogue, slices]
+__device__ unsigned long long g_prof[6];
+
+}  // namespace
+}  // namespace wbx
+
+extern "C" int wbx_diag_slice_profile(double* out4) {
+    unsigned long long h[6];
+    if (cudaMemcpyFromSymbol(h, wbx::g_prof, sizeof h) != cudaSuccess) return WBX_CUDA_ERROR;
+    for (int i = 0; i < 5; ++i) out4[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
+    out4[5] = static_cast<double>(h[5]);
+    const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(wbx::g_prof, z, sizeof z);
+    return WBX_OK;
+}
+
+namespace wbx {
+namespace {
+
+// ---------------------------------------------------------------- TMA-staged operator stream
+// Per-warp ring of kSlots slice records in shared memory filled by 1-D bulk copies
+// (stream.cuh). Entry e of the warp's periodic sequence (period P = nA + nT [+ nA when
+// the energy pass is on]) is slice k of Theta (A) or Theta^T (T).
+constexpr unsigned kRecU4 = (kSlotBytes + 128u) / 16u;  // slot stride in uint4 (max record)
+constexpr int kMaxSlots = 8;
+// per-warp shared memory: [mbarriers x8][meta x8][pad to 128][ns x record slot]
+__host__ __device__ constexpr unsigned warp_smem_bytes(int ns) { return 128u + static_cast<unsigned>(ns) * kRecU4 * 16u; }
+
+struct Streamer {
+    uint4* slots;
+    uint64_t* bars;
+    uint32_t* meta;
+    uint32_t ns;  // slots in flight (<= kMaxSlots)
+    uint32_t nA, nT, P;
+    uint64_t issued, consumed, limit;
+    uint64_t pol;
+    // lane j holds the metadata of period entry j (P <= 32), so issuing never waits on
+    // a global load
+    uint32_t reg_meta;
+    uint64_t reg_off;
+    unsigned long long prof[6];  // WBX_DEBUG_MODE=2 cycle accounting
+};
+
+__device__ __forceinline__ uint32_t count_slices(const SellView& M, uint32_t gwarp, uint32_t nwarps) {
+    return M.slices > gwarp ? (M.slices - gwarp + nwarps - 1) / nwarps : 0;
+}
+
+// entry r of the period -> (operator, slice)
+__device__ __forceinline__ uint32_t entry_slice(const Streamer& st, uint32_t r, uint32_t gwarp, uint32_t nwarps,
+                                                bool& isT) {
+    isT = r >= st.nA && r < st.nA + st.nT;
+    const uint32_t k = r < st.nA ? r : (isT ? r - st.nA : r - st.nA - st.nT);
+    return gwarp + k * nwarps;
+}
+
+__device__ __forceinline__ void st_issue(Streamer& st, const SellView& A, const SellView& T, uint32_t gwarp,
+                                         uint32_t nwarps, int lane) {
+    const uint64_t e = st.issued++;
+    const uint32_t r = static_cast<uint32_t>(e % st.P);
+    bool isT;
+    const uint32_t s = entry_slice(st, r, gwarp, nwarps, isT);
+    const SellView& M = isT ? T : A;
+    uint32_t meta;
+    uint64_t off;
+    if (st.P <= 32) {
+        meta = __shfl_sync(0xffffffffu, st.reg_meta, r);
+        off = __shfl_sync(0xffffffffu, st.reg_off, r);
+    } else {
+        meta = M.slice_np[s];
+        off = M.rec_off[s];
+    }
+    if (lane != 0) return;
+    const unsigned bytes = 128u + (meta & 0xffu) * 512u;
+    const unsigned slot = static_cast<unsigned>(e % st.ns);
+    st.meta[slot] = meta;
+    mbar_expect_tx(st.bars + slot, bytes);
+    bulk_g2s(st.slots + slot * kRecU4, M.rec + off, bytes, st.bars + slot, st.pol);
+}
+
+__device__ __forceinline__ void st_init(Streamer& st, unsigned char* warp_smem, const SellView& A,
+                                        const SellView& T, uint32_t gwarp, uint32_t nwarps, int lane,
+                                        uint64_t iters, bool energy_pass, int nslots) {
+    st.bars = reinterpret_cast<uint64_t*>(warp_smem);
+    st.meta = reinterpret_cast<uint32_t*>(warp_smem + 8u * kMaxSlots);
+    st.slots = reinterpret_cast<uint4*>(warp_smem + 128u);
+    st.ns = static_cast<uint32_t>(nslots);
+    st.nA = count_slices(A, gwarp, nwarps);
+    st.nT = count_slices(T, gwarp, nwarps);
+    st.P = st.nA + st.nT + (energy_pass ? st.nA : 0);
+    st.issued = st.consumed = 0;
+    st.limit = st.P == 0 ? 0 : iters * st.P;
+    st.pol = l2_keep_policy();
+    st.reg_meta = 0;
+    st.reg_off = 0;
+    if (st.P <= 32 && static_cast<uint32_t>(lane) < st.P) {
+        bool isT;
+        const uint32_t s = entry_slice(st, static_cast<uint32_t>(lane), gwarp, nwarps, isT);
+        const SellView& M = isT ? T : A;
+        st.reg_meta = M.slice_np[s];
+        st.reg_off = M.rec_off[s];
+    }
+    if (lane == 0)
+        for (uint32_t i = 0; i < st.ns; ++i) mbar_init(st.bars + i, 1);
+    mbar_fence_init();
+    __syncwarp();
+    while (st.issued < st.limit && st.issued < st.ns) st_issue(st, A, T, gwarp, nwarps, lane);
+}
+
+// Consume the next `count` entries: value = sum over the row of val * x[col] (ACC
+// accumulation), combined over the row's segments. pre(row) issues the epilogue's own
+// loads BEFORE the gathers (same round trip); post(row, value, pre) runs on head lanes.
+template <typename ACC, typename X, typename Pre, typename Post>
+__device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const SellView& T, uint32_t gwarp,
+                                         uint32_t nwarps, int lane, uint32_t count, const X* __restrict__ x,
+                                         Pre pre, Post post) {
+    for (uint32_t i = 0; i < count; ++i) {
+        const uint64_t e = st.consumed;
+        const unsigned slot = static_cast<unsigned>(e % st.ns);
+        const long long c0 = g_debug_mode == 2 ? clock64() : 0;
+        mbar_wait(st.bars + slot, static_cast<unsigned>((e / st.ns) & 1u));
+        const long long c1 = g_debug_mode == 2 ? clock64() : 0;
+        const uint32_t meta = st.meta[slot];
+        const uint32_t np = meta & 0xffu;
+        const uint4* rec = st.slots + slot * kRecU4;
+        const uint32_t info = reinterpret_cast<const uint32_t*>(rec)[lane];
+        const auto pv = pre(info == kNoRow ? kNoRow : (info & kRowMask));
+        const uint4* p = rec + 8 + lane;
+        uint4 q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = j < static_cast<int>(np) ? p[j * kWarp] : make_uint4(0, 0, 0, 0);
+        X g[16];
+        const uint32_t cmask = g_debug_mode == 1 ? 0u : 0xffffffffu;  // diagnostics: 1 = no gathers
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            g[2 * j] = j < static_cast<int>(np) ? x[q[j].y & cmask] : X(0);
+            g[2 * j + 1] = j < static_cast<int>(np) ? x[q[j].w & cmask] : X(0);
+        }
+        ACC acc = ACC(0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j < static_cast<int>(np)) {
+                acc = fma(static_cast<ACC>(__uint_as_float(q[j].x)), static_cast<ACC>(g[2 * j]), acc);
+                acc = fma(static_cast<ACC>(__uint_as_float(q[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
+            }
+        }
+        if (g_debug_mode == 2) acc += static_cast<ACC>(clock64() & 0) ;
+        const long long c2 = g_debug_mode == 2 ? clock64() : 0;
+        const uint32_t row = combine_info(info, meta, acc);
+        __syncwarp();  // every lane is done with the slot before it is refilled
+        const long long c2a = g_debug_mode == 2 ? clock64() : 0;
+        st.consumed = e + 1;
+        if (st.issued < st.limit) st_issue(st, A, T, gwarp, nwarps, lane);
+        if (g_debug_mode == 2) __syncwarp();
+        const long long c2b = g_debug_mode == 2 ? clock64() : 0;
+        if (row != kNoRow) post(row, acc, pv);
+        if (g_debug_mode == 2) {
+            __syncwarp();
+            const long long c3 = clock64();
+            st.prof[0] += static_cast<unsigned long long>(c1 - c0);
+            st.prof[1] += static_cast<unsigned long long>(c2 - c1);
+            st.prof[2] += static_cast<unsigned long long>(c2a - c2);
+            st.prof[3] += static_cast<unsigned long long>(c2b - c2a);
+            st.prof[4] += static_cast<unsigned long long>(c3 - c2b);
+            st.prof[5] += 1;
+        }
+    }
+}
+
+// Wait for copies still in flight (early loop exit) before the CTA may retire.
+__device__ __forceinline__ void st_drain(Streamer& st) {
+    for (uint64_t e = st.consumed; e < st.issued; ++e)
+        mbar_wait(st.bars + e % st.ns, static_cast<unsigned>((e / st.ns) & 1u));
+    st.consumed = st.issued;
+    if (g_debug_mode == 2 && (threadIdx.x & 31) == 0)
+        for (int i = 0; i < 6; ++i) atomicAdd(&g_prof[i], st.prof[i]);
+}
+
 // ---------------------------------------------------------------- estimate_step kernel
 // Power iteration on P^-1/2 Theta^T Theta P^-1/2 (solver.cpp:69-99). The reference's
 // v_k = w_k / |w_k| followed by u = P^-1/2 v is folded into the next product:
@@ -507,8 +688,19 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
-    const Plan pA = sizeof(T) == 4 ? make_plan(a.A, gwarp, nwarps, lane) : Plan{};
-    const Plan pT = sizeof(T) == 4 ? make_plan(a.T, gwarp, nwarps, lane) : Plan{};
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    Streamer st{};
+    if constexpr (sizeof(T) == 4)
+        st_init(st, dsmem + (threadIdx.x >> 5) * warp_smem_bytes(a.nslots), a.A, a.T, gwarp, nwarps, lane, 200,
+                false, a.nslots);
+    // row loop of one phase: TMA-staged fp32 operator (T = float) or exact fp64 layout
+    auto phase = [&](bool isT, const double* x, auto pre, auto post) {
+        if constexpr (sizeof(T) == 4)
+            st_phase<double, double>(st, a.A, a.T, gwarp, nwarps, lane, isT ? st.nT : st.nA, x, pre, post);
+        else
+            for_rows_exact(isT ? a.T : a.A, gwarp, nwarps, lane, x,
+                           [&](uint32_t r, double v) { post(r, v, pre(r)); });
+    };
 
     // v0 = CounterRng(0x5eed) normals over ALL n, normalised by the full norm; only the
     // C part ever meets Theta (Theta^T output is zero outside C).
@@ -530,19 +722,22 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
     for (; it < 200; ++it) {
         // t = Theta (P^-1/2 v) = Theta (P^-1/2 w_prev) / |w_prev|
         const double inv = nw_prev;
-        for_rows<T, double, double>(a.A, pA, gwarp, nwarps, lane, a.uC,
-                                    [&](uint32_t r, double t) { a.t64[r] = t / inv; });
+        phase(
+            false, a.uC, [](uint32_t) { return 0; }, [&](uint32_t r, double t, int) { a.t64[r] = t / inv; });
         grid_sync(a.sync, epoch, smem);
         // w = P^-1/2 Theta^T t ; <v, w>, <w, w> with v = w_prev / |w_prev|
         double acc[2] = {0.0, 0.0};
-        for_rows<T, double, double>(a.T, pT, gwarp, nwarps, lane, a.t64, [&](uint32_t c, double g) {
-            const double w = g * a.ispC[c];
-            const double v = a.wv[c] / inv;
-            acc[0] += v * w;
-            acc[1] += w * w;
-            a.wv[c] = w;
-            a.uC[c] = a.ispC[c] * w;
-        });
+        phase(
+            true, a.t64,
+            [&](uint32_t c) { return c != kNoRow ? make_double2(a.ispC[c], a.wv[c]) : make_double2(0.0, 0.0); },
+            [&](uint32_t c, double g, double2 pv) {
+                const double w = g * pv.x;
+                const double v = pv.y / inv;
+                acc[0] += v * w;
+                acc[1] += w * w;
+                a.wv[c] = w;
+                a.uC[c] = pv.x * w;
+            });
         grid_sync_reduce<2>(a.sync, epoch, acc, smem);
         const double lambda = acc[0];
         const double nw = sqrt(acc[1]);
@@ -559,6 +754,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
         lambda_prev = lambda;
         nw_prev = nw;
     }
+    if constexpr (sizeof(T) == 4) st_drain(st);
     if (gthread == 0) {
         a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
         a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
@@ -583,9 +779,34 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
     T* x0R = static_cast<T*>(a.x0R);
     T* tpC = static_cast<T*>(a.tpC);
     T* thrC = static_cast<T*>(a.thrC);
-    const Plan pA = sizeof(T) == 4 ? make_plan(a.A, gwarp, nwarps, lane) : Plan{};
-    const Plan pT = sizeof(T) == 4 ? make_plan(a.T, gwarp, nwarps, lane) : Plan{};
+    const Plan pA = sizeof(T) == 4 && a.track ? make_plan(a.A, gwarp, nwarps, lane) : Plan{};
     const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    Streamer st{};
+    if constexpr (sizeof(T) == 4)
+        st_init(st, dsmem + (threadIdx.x >> 5) * warp_smem_bytes(a.nslots), a.A, a.T, gwarp, nwarps, lane,
+                static_cast<uint64_t>(a.max_iters), a.track != 0, a.nslots);
+    auto phase = [&](bool isT, const T* x, auto pre, auto post) {
+        if constexpr (sizeof(T) == 4)
+            st_phase<float, float>(st, a.A, a.T, gwarp, nwarps, lane, isT ? st.nT : st.nA, x, pre, post);
+        else
+            for_rows_exact(isT ? a.T : a.A, gwarp, nwarps, lane, x, [&](uint32_t r, T v) { post(r, v, pre(r)); });
+    };
+    auto pre_x0 = [&](uint32_t r) { return r != kNoRow ? x0R[r] : T(0); };
+    // epilogue operands of the fused update, loaded before the gathers
+    struct Coord {
+        T y, xp, tp, thr;
+    };
+    auto pre_coord = [&](uint32_t c) {
+        Coord q{T(0), T(0), T(0), T(0)};
+        if (c != kNoRow) {
+            q.y = yC[c];
+            q.xp = xpC[c];
+            q.tp = tpC[c];
+            q.thr = thrC[c];
+        }
+        return q;
+    };
 
     // ---- init: compacted copies of x0; warm start x = x_prev = y = x0 (solver.cpp:115-117);
     // per-coordinate tau/p and tau*lambda*w/p on C
@@ -628,17 +849,15 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
     int k = 1;
     for (; k <= a.max_iters; ++k) {
         // phase A: res = Theta y - x0 on nonempty rows
-        for_rows<T, T, T>(a.A, pA, gwarp, nwarps, lane, yC,
-                          [&](uint32_t r, T acc) { res[r] = Prec<T>::sub(acc, x0R[r]); });
+        phase(false, yC, pre_x0, [&](uint32_t r, T acc, T x0) { res[r] = Prec<T>::sub(acc, x0); });
         grid_sync(a.sync, epoch, smem);
         // phase T: gradient on nonempty columns + fused step / prox / momentum
         const T beta = Prec<T>::beta(a, k);
         double tr[3] = {0.0, 0.0, 0.0};
-        for_rows<T, T, T>(a.T, pT, gwarp, nwarps, lane, res, [&](uint32_t c, T g) {
-            const T y = yC[c], xp = xpC[c];
-            const T z0 = Prec<T>::z0(y, g, tpC[c], tau, a.pC[c]);
-            const T xn = Prec<T>::prox(z0, thrC[c]);
-            yC[c] = Prec<T>::momentum(xn, xp, beta);
+        phase(true, res, pre_coord, [&](uint32_t c, T g, const Coord& q) {
+            const T z0 = Prec<T>::z0(q.y, g, q.tp, tau, sizeof(T) == 8 ? a.pC[c] : 0.0);
+            const T xn = Prec<T>::prox(z0, q.thr);
+            yC[c] = Prec<T>::momentum(xn, q.xp, beta);
             xpC[c] = xn;
             if (a.track) {
                 tr[1] += a.wC[c] * fabs(static_cast<double>(xn));
@@ -648,8 +867,8 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
         grid_sync(a.sync, epoch, smem);
         if (a.track) {
             // energy(x') (solver.cpp:130, :44-55): Theta x' on rows R
-            for_rows<T, T, T>(a.A, pA, gwarp, nwarps, lane, xpC, [&](uint32_t r, T t) {
-                const double d = static_cast<double>(t) - static_cast<double>(x0R[r]);
+            phase(false, xpC, pre_x0, [&](uint32_t r, T t, T x0) {
+                const double d = static_cast<double>(t) - static_cast<double>(x0);
                 tr[0] += d * d;
             });
             grid_sync_reduce<3>(a.sync, epoch, tr, smem);
@@ -668,6 +887,7 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
             }
         }
     }
+    if constexpr (sizeof(T) == 4) st_drain(st);
     const int used = k - 1 > a.max_iters ? a.max_iters : k - 1;
     if (gthread == 0) a.out[OUT_ITERS_USED] = used;
     // ---- x_final on C back into the full coefficient vector
@@ -727,6 +947,7 @@ struct wbx_solver {
     uint64_t trace_cap = 0;
     wbx::DevBuf<double> u0, x0full, xfull, uout;
     int grid_fista = 0, grid_tau = 0;
+    int nslots = 3;  // TMA slots in flight per warp
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     uint64_t last_launches = 0;
@@ -737,9 +958,17 @@ namespace wbx {
 
 namespace {
 
-int blocks_per_sm(const void* kernel) {
+// dynamic shared memory of the persistent kernels: the per-warp TMA slot rings (fp32)
+template <typename T>
+unsigned dyn_smem(int nslots) {
+    return sizeof(T) == 4 ? kWarpsPerBlock * warp_smem_bytes(nslots) : 0u;
+}
+
+int blocks_per_sm(const void* kernel, unsigned smem) {
+    if (smem > 0)
+        WBX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+    WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
     if (per_sm < 1) fail(WBX_CUDA_ERROR, "solver kernel cannot be resident");
     // tuning override: WBX_SOLVER_BLOCKS_PER_SM (clamped to what is co-resident)
     if (const char* e = std::getenv("WBX_SOLVER_BLOCKS_PER_SM")) {
@@ -808,6 +1037,7 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.sync.red = s->red.p;
     a.sync.trace = s->trace.p;
     a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
+    a.nslots = s->nslots;
     {
         const char* e = std::getenv("WBX_BARRIER");
         a.sync.mode = (e && std::string(e) == "allpoll") ? 1 : 0;
@@ -818,7 +1048,7 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
 template <typename T>
 void launch_coop(const void* kernel, int grid, SolveArgs& a, cudaStream_t st) {
     void* params[] = {&a};
-    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, 0, st));
+    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, dyn_smem<T>(a.nslots), st));
 }
 
 template <typename T>
@@ -862,10 +1092,16 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
 template <typename T>
 void alloc_state(wbx_solver* s) {
     const wbx_op* op = s->op;
+    if (const char* e = std::getenv("WBX_DEBUG_MODE")) {
+        const int mode = std::atoi(e);
+        WBX_CUDA(cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof mode));
+    }
     auto rnd = [](uint64_t count) { return ((count * sizeof(T) + 255) / 256) * 256; };
     s->state.alloc(4 * rnd(op->nC) + 2 * rnd(op->nR) + 256);
-    s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_kernel<T>)) * s->ctx->num_sms;
-    s->grid_tau = blocks_per_sm(reinterpret_cast<const void*>(tau_kernel<T>)) * s->ctx->num_sms;
+    s->nslots = 3;
+    if (const char* e = std::getenv("WBX_SLOTS")) s->nslots = std::max(1, std::min(kMaxSlots, std::atoi(e)));
+    s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
+    s->grid_tau = blocks_per_sm(reinterpret_cast<const void*>(tau_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
 }
 
 }  // namespace
