@@ -497,6 +497,11 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
 // Diagnostics switch (WBX_DEBUG_MODE, timing experiments only; results are wrong when set):
 // 1 = gather x[0] instead of x[col] (removes the gather dependency).
 __device__ int g_debug_mode = 0;
+// Compile-time diagnostics (make WBX_PROFILE=1|2): 1 = gathers hit x[0] only (removes the
+// gather dependency, timing experiment), 2 = per-slice cycle accounting (wbx_diag_slice_profile).
+#ifndef WBX_PROFILE
+#define WBX_PROFILE 0
+#endif
 // 2 = per-slice cycle accounting: [tma wait, load+gather+fma, combine+issue+epilogue, slices]
 __device__ unsigned long long g_prof[6];
 
@@ -615,9 +620,9 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
     for (uint32_t i = 0; i < count; ++i) {
         const uint64_t e = st.consumed;
         const unsigned slot = static_cast<unsigned>(e % st.ns);
-        const long long c0 = g_debug_mode == 2 ? clock64() : 0;
+        const long long c0 = WBX_PROFILE == 2 ? clock64() : 0;
         mbar_wait(st.bars + slot, static_cast<unsigned>((e / st.ns) & 1u));
-        const long long c1 = g_debug_mode == 2 ? clock64() : 0;
+        const long long c1 = WBX_PROFILE == 2 ? clock64() : 0;
         const uint32_t meta = st.meta[slot];
         const uint32_t np = meta & 0xffu;
         const uint4* rec = st.slots + slot * kRecU4;
@@ -628,7 +633,7 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
 #pragma unroll
         for (int j = 0; j < 8; ++j) q[j] = j < static_cast<int>(np) ? p[j * kWarp] : make_uint4(0, 0, 0, 0);
         X g[16];
-        const uint32_t cmask = g_debug_mode == 1 ? 0u : 0xffffffffu;  // diagnostics: 1 = no gathers
+        const uint32_t cmask = WBX_PROFILE == 1 ? 0u : 0xffffffffu;  // diagnostics: 1 = no gathers
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             g[2 * j] = j < static_cast<int>(np) ? x[q[j].y & cmask] : X(0);
@@ -642,17 +647,17 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
                 acc = fma(static_cast<ACC>(__uint_as_float(q[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
             }
         }
-        if (g_debug_mode == 2) acc += static_cast<ACC>(clock64() & 0) ;
-        const long long c2 = g_debug_mode == 2 ? clock64() : 0;
+        if (WBX_PROFILE == 2)acc += static_cast<ACC>(clock64() & 0) ;
+        const long long c2 = WBX_PROFILE == 2 ? clock64() : 0;
         const uint32_t row = combine_info(info, meta, acc);
         __syncwarp();  // every lane is done with the slot before it is refilled
-        const long long c2a = g_debug_mode == 2 ? clock64() : 0;
+        const long long c2a = WBX_PROFILE == 2 ? clock64() : 0;
         st.consumed = e + 1;
         if (st.issued < st.limit) st_issue(st, A, T, gwarp, nwarps, lane);
-        if (g_debug_mode == 2) __syncwarp();
-        const long long c2b = g_debug_mode == 2 ? clock64() : 0;
+        if (WBX_PROFILE == 2)__syncwarp();
+        const long long c2b = WBX_PROFILE == 2 ? clock64() : 0;
         if (row != kNoRow) post(row, acc, pv);
-        if (g_debug_mode == 2) {
+        if (WBX_PROFILE == 2){
             __syncwarp();
             const long long c3 = clock64();
             st.prof[0] += static_cast<unsigned long long>(c1 - c0);
@@ -670,7 +675,7 @@ __device__ __forceinline__ void st_drain(Streamer& st) {
     for (uint64_t e = st.consumed; e < st.issued; ++e)
         mbar_wait(st.bars + e % st.ns, static_cast<unsigned>((e / st.ns) & 1u));
     st.consumed = st.issued;
-    if (g_debug_mode == 2 && (threadIdx.x & 31) == 0)
+    if (WBX_PROFILE == 2 && (threadIdx.x & 31) == 0)
         for (int i = 0; i < 6; ++i) atomicAdd(&g_prof[i], st.prof[i]);
 }
 
