@@ -149,6 +149,21 @@ int wbx_theta_expand(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n
                      const double* values, uint64_t* nnz, uint64_t* row_offsets,
                      uint32_t* col_indices, double* out_values);
 
+/* Spatially varying Theta_K (BASELINE configs C3/C4; the reference has no 2-D spatially
+ * varying operator): column mu = the column of the stationary operator whose
+ * Gaussian sigma matches the spatial row of psi_mu, sigma varying linearly from
+ * sigma_first_row (image row 0) to sigma_last_row (row H), linearly interpolated between
+ * the two bracketing levels of a sigma ladder; the column's index set is the union of the
+ * two levels' sets. Levels are given as concatenated generator lists (wbx_theta_expand
+ * format) with level_ngens[l] records each. Output arrays are allocated by the library
+ * (malloc) and released with wbx_free. */
+int wbx_theta_varying(uint32_t ndim, const uint64_t* dims, uint32_t J, uint32_t nlevels,
+                      const double* sigmas, const uint64_t* level_ngens, const uint32_t* blocks,
+                      const uint32_t* gen_index, const uint64_t* counts, const double* values,
+                      double sigma_first_row, double sigma_last_row, uint64_t* nnz,
+                      uint64_t** row_offsets, uint32_t** col_indices, double** out_values);
+void wbx_free(void* p);
+
 /* ---------------------------------------------------------------- preconditioners */
 /* gram_diagonals (precond.cpp:16-67), spai (:79-87), jacobi (:69-77); fp64, bitwise */
 int wbx_gram_diagonals(wbx_ctx* ctx, const wbx_op* op, uint64_t nnz_cap_factor, double* diagM,
@@ -187,6 +202,14 @@ int wbx_solver_destroy(wbx_solver* s);
 int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp);
 /* host pointers: H2D copy, deblur, D2H copy, synchronise */
 int wbx_deblur(wbx_solver* s, const double* u0, double* u, int clamp, wbx_report* report);
+/* Batched deblur (BASELINE config C5): `batch` (1, 4 or 8) independent images share Theta_K,
+ * P, w, lambda and tau; the operator is streamed once per batch (SpMM). Images are stored
+ * back to back (batch * n doubles) for wbx_deblur / wbx_deblur_dev. fp32, fixed iteration
+ * count. */
+int wbx_solver_create_batch(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* basis, const double* p,
+                            const double* w, double lambda, const wbx_solver_cfg* cfg, int batch,
+                            wbx_solver** out);
+int wbx_solver_batch(const wbx_solver* s);
 /* launches of the last deblur, and the solver kernel's device time (ms) */
 int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);
 

@@ -88,11 +88,46 @@ def run_case(name: str, args: list, keep: list) -> None:
               f"-> {(GOLDEN / (name + '.npz')).stat().st_size / 1e3:.0f} kB", flush=True)
 
 
+LADDER_SIGMAS = [2.5 + 5.0 * l / 7.0 for l in range(8)]
+
+
+def make_ladder(size: int) -> None:
+    """BASELINE configs C3/C4 (spatially varying blur, no reference implementation):
+    the stationary Gaussian operators of an 8-level sigma ladder 2.5..7.5 px, each built
+    and thresholded (K=3N, dyadic weights) by the reference itself. The spatially varying
+    Theta_K is assembled from these by wbx_theta_varying (column-wise interpolation,
+    SURVEY §8d)."""
+    arrays = {"sigmas": np.array(LADDER_SIGMAS)}
+    metas = []
+    for l, s in enumerate(LADDER_SIGMAS):
+        with tempfile.TemporaryDirectory() as td:
+            out = Path(td)
+            args = ["--dims", str(size), str(size), "--family", "daubechies", "--order", "4", "--J", "4",
+                    "--sigma", repr(s), "--no-solve"]
+            r = subprocess.run([str(DRIVER), "--out", str(out), *args], capture_output=True, text=True)
+            if r.returncode != 0:
+                raise SystemExit(f"ladder {size} level {l}: driver failed\n{r.stderr}")
+            meta = json.loads((out / "meta.json").read_text())
+            assert meta["expand_ok"]
+            gens = np.frombuffer((out / "gens.bin").read_bytes(),
+                                 dtype=np.dtype([("b", "<u4"), ("g", "<u4"), ("c", "<u8"), ("v", "<f8")]))
+            for k, f in (("gen_block", "b"), ("gen_index", "g"), ("gen_count", "c"), ("gen_value", "v")):
+                arrays[f"l{l}_{k}"] = gens[f].copy()
+            metas.append(meta)
+            print(f"ladder {size} sigma={s:.4f}: gens={meta['n_gens']} nnz={meta['nnz']}", flush=True)
+    arrays["meta_json"] = np.frombuffer(json.dumps({"dims": [size, size], "family": "daubechies", "order": 4,
+                                                    "J": 4, "levels": metas}).encode(), dtype=np.uint8)
+    np.savez_compressed(GOLDEN / f"c3_ladder_{size}.npz", **arrays)
+
+
 def main(names: list) -> None:
     if not DRIVER.exists():
         raise SystemExit("build the oracle first: make -C oracle ref driver")
-    for name in names or CASES:
-        run_case(name, *CASES[name])
+    for name in names or list(CASES) + ["ladder256", "ladder1024"]:
+        if name.startswith("ladder"):
+            make_ladder(int(name[6:]))
+        else:
+            run_case(name, *CASES[name])
 
 
 if __name__ == "__main__":

@@ -77,6 +77,10 @@ SIGNATURES = {
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
     "wbx_theta_expand": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                    _U64, _U64, _U32, _D]),
+    "wbx_theta_varying": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint32, _D, _U64, _U32, _U32, _U64, _D,
+                                    C.c_double, C.c_double, _U64, C.POINTER(_U64), C.POINTER(_U32),
+                                    C.POINTER(_D)]),
+    "wbx_free": (None, [C.c_void_p]),
     "wbx_gram_diagonals": (C.c_int, [_P, _P, C.c_uint64, _D, _D]),
     "wbx_spai": (C.c_int, [_P, _P, _D]),
     "wbx_jacobi": (C.c_int, [_P, _P, C.c_double, _D]),
@@ -89,6 +93,9 @@ SIGNATURES = {
                           C.POINTER(wbx_report)]),
     "wbx_solver_create": (C.c_int, [_P, _P, _P, _D, _D, C.c_double, C.POINTER(wbx_solver_cfg),
                                     C.POINTER(_P)]),
+    "wbx_solver_create_batch": (C.c_int, [_P, _P, _P, _D, _D, C.c_double, C.POINTER(wbx_solver_cfg), C.c_int,
+                                          C.POINTER(_P)]),
+    "wbx_solver_batch": (C.c_int, [_P]),
     "wbx_solver_destroy": (C.c_int, [_P]),
     "wbx_deblur_dev": (C.c_int, [_P, _P, _P, C.c_int]),
     "wbx_deblur": (C.c_int, [_P, _D, _D, C.c_int, C.POINTER(wbx_report)]),

@@ -467,60 +467,11 @@ int wbx_theta_expand(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n
         }
         need(col_indices, "col_indices");
         need(out_values, "values");
-        uint64_t n = dims[0] * (ndim == 2 ? dims[1] : 1);
-        struct Tri {
-            uint32_t row, col;
-            double v;
-        };
-        std::vector<Tri> tri;
-        tri.reserve(total);
-        const uint32_t d = ndim;
-        for (uint64_t g = 0; g < n_gens; ++g) {
-            const wbx_band& bi = bands[blocks[g] % nb];
-            const wbx_band& bo = bands[blocks[g] / nb];
-            const bool in_finer = bi.level <= bo.level;
-            const uint64_t* gshape = in_finer ? bi.shape : bo.shape;
-            const wbx_band& small = in_finer ? bo : bi;
-            uint64_t v[2] = {0, 0}, rem = gen_index[g];
-            for (uint32_t k = d; k-- > 0;) {
-                v[k] = rem % gshape[k];
-                rem /= gshape[k];
-            }
-            for (uint64_t q = 0; q < counts[g]; ++q) {
-                uint64_t idx[2] = {0, 0}, r = q;
-                for (uint32_t k = d; k-- > 0;) {
-                    idx[k] = r % small.shape[k];
-                    r /= small.shape[k];
-                }
-                uint64_t nf = 0, mf = 0;
-                for (uint32_t k = 0; k < d; ++k) {
-                    uint64_t nk, mk;
-                    if (in_finer) {
-                        const uint64_t s = bi.shape[k] / bo.shape[k];
-                        nk = idx[k];
-                        mk = (v[k] + s * idx[k]) % bi.shape[k];
-                    } else {
-                        const uint64_t s = bo.shape[k] / bi.shape[k];
-                        mk = idx[k];
-                        nk = (v[k] + s * idx[k]) % bo.shape[k];
-                    }
-                    nf = nf * bo.shape[k] + nk;
-                    mf = mf * bi.shape[k] + mk;
-                }
-                tri.push_back({static_cast<uint32_t>(bo.offset + nf), static_cast<uint32_t>(bi.offset + mf),
-                               values[g]});
-            }
-        }
-        std::sort(tri.begin(), tri.end(), [](const Tri& a, const Tri& b) {
-            return a.row != b.row ? a.row < b.row : a.col < b.col;
-        });
-        for (uint64_t i = 0; i <= n; ++i) row_offsets[i] = 0;
-        for (uint64_t k = 0; k < tri.size(); ++k) {
-            ++row_offsets[tri[k].row + 1];
-            col_indices[k] = tri[k].col;
-            out_values[k] = tri[k].v;
-        }
-        for (uint64_t i = 0; i < n; ++i) row_offsets[i + 1] += row_offsets[i];
+        const uint64_t n = dims[0] * (ndim == 2 ? dims[1] : 1);
+        wbx::HostCsr csr = wbx::expand_generators(bands, ndim, n, n_gens, blocks, gen_index, counts, values);
+        std::copy(csr.rowptr.begin(), csr.rowptr.end(), row_offsets);
+        std::copy(csr.col.begin(), csr.col.end(), col_indices);
+        std::copy(csr.val.begin(), csr.val.end(), out_values);
         *nnz = total;
     });
 }

@@ -158,4 +158,14 @@ SellView view_of(const wbx_sell& m);
 void build_op(wbx_op* op, uint64_t n, const uint64_t* rowptr, const uint32_t* col,
               const double* val);
 
+// theta_build.cu (host): CSR assembly of thresholded circulant operators
+struct HostCsr {
+    std::vector<uint64_t> rowptr;
+    std::vector<uint32_t> col;
+    std::vector<double> val;
+};
+HostCsr expand_generators(const std::vector<wbx_band>& bands, uint32_t ndim, uint64_t n, uint64_t n_gens,
+                          const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
+                          const double* values);
+
 }  // namespace wbx

@@ -899,6 +899,176 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
     for (uint64_t c = gthread; c < a.nC; c += nthreads) a.x_full[a.C_glob[c]] = static_cast<double>(xpC[c]);
 }
 
+// ---------------------------------------------------------------- batched FISTA (C5)
+// B independent images sharing Theta_K, P, w, lambda and tau (BASELINE config C5): the
+// operator stream is read once per B right-hand sides (SpMM). Vectors are interleaved
+// [coordinate][B] so a gathered column is one 4*B-byte segment (B=8: one 32-B sector).
+template <int B, typename Pre, typename Post>
+__device__ __forceinline__ void st_phase_batch(Streamer& st, const SellView& A, const SellView& T, uint32_t gwarp,
+                                               uint32_t nwarps, int lane, uint32_t count,
+                                               const float* __restrict__ x, Pre pre, Post post) {
+    static_assert(B % 4 == 0, "batch must be a multiple of 4");
+    constexpr int V = B / 4;
+    for (uint32_t i = 0; i < count; ++i) {
+        const uint64_t e = st.consumed;
+        const unsigned slot = static_cast<unsigned>(e % st.ns);
+        mbar_wait(st.bars + slot, static_cast<unsigned>((e / st.ns) & 1u));
+        const uint32_t meta = st.meta[slot];
+        const int np = static_cast<int>(meta & 0xffu);
+        const uint4* rec = st.slots + slot * kRecU4;
+        const uint32_t info = reinterpret_cast<const uint32_t*>(rec)[lane];
+        const auto pv = pre(info == kNoRow ? kNoRow : (info & kRowMask));
+        const uint4* p = rec + 8 + lane;
+        float acc[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // two halves of 4 element pairs each
+            uint4 q[4];
+            float4 g[8][V];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[j] = (4 * h + j) < np ? p[(4 * h + j) * kWarp] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const bool on = (4 * h + j) < np;
+                    g[2 * j][v] = on ? reinterpret_cast<const float4*>(x + static_cast<uint64_t>(q[j].y) * B)[v]
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                    g[2 * j + 1][v] = on ? reinterpret_cast<const float4*>(x + static_cast<uint64_t>(q[j].w) * B)[v]
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float v0 = __uint_as_float(q[j].x), v1 = __uint_as_float(q[j].z);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    acc[4 * v + 0] = fmaf(v0, g[2 * j][v].x, acc[4 * v + 0]);
+                    acc[4 * v + 1] = fmaf(v0, g[2 * j][v].y, acc[4 * v + 1]);
+                    acc[4 * v + 2] = fmaf(v0, g[2 * j][v].z, acc[4 * v + 2]);
+                    acc[4 * v + 3] = fmaf(v0, g[2 * j][v].w, acc[4 * v + 3]);
+                    acc[4 * v + 0] = fmaf(v1, g[2 * j + 1][v].x, acc[4 * v + 0]);
+                    acc[4 * v + 1] = fmaf(v1, g[2 * j + 1][v].y, acc[4 * v + 1]);
+                    acc[4 * v + 2] = fmaf(v1, g[2 * j + 1][v].z, acc[4 * v + 2]);
+                    acc[4 * v + 3] = fmaf(v1, g[2 * j + 1][v].w, acc[4 * v + 3]);
+                }
+            }
+        }
+        // segment partials -> head lane, fixed order (as combine_info, B values)
+        const uint32_t m = meta >> 8;
+        const uint32_t nseg = info == kNoRow ? 1u : (info >> 27);
+        const uint32_t maxseg = __reduce_max_sync(0xffffffffu, nseg);
+        for (uint32_t j = 1; j < maxseg; ++j) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const float t = __shfl_down_sync(0xffffffffu, acc[b], j * m);
+                if (j < nseg) acc[b] += t;
+            }
+        }
+        __syncwarp();
+        st.consumed = e + 1;
+        if (st.issued < st.limit) st_issue(st, A, T, gwarp, nwarps, lane);
+        if (info != kNoRow) post(info & kRowMask, acc, pv);
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_batch_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
+    const int lane = threadIdx.x & 31;
+    const uint32_t gwarp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    float* yC = static_cast<float*>(a.yC);   // [nC][B]
+    float* xpC = static_cast<float*>(a.xpC);  // [nC][B]
+    float* res = static_cast<float*>(a.res);  // [nR][B]
+    float* x0R = static_cast<float*>(a.x0R);  // [nR][B]
+    float* tpC = static_cast<float*>(a.tpC);  // [nC]
+    float* thrC = static_cast<float*>(a.thrC);
+    const double tau = a.out[OUT_TAU];
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    Streamer st{};
+    st_init(st, dsmem + (threadIdx.x >> 5) * warp_smem_bytes(a.nslots), a.A, a.T, gwarp, nwarps, lane,
+            static_cast<uint64_t>(a.max_iters), false, a.nslots);
+    const uint64_t n = a.n;
+    for (uint64_t c = gthread; c < a.nC; c += nthreads) {
+        const uint32_t g = a.C_glob[c];
+        for (int b = 0; b < B; ++b) {
+            const float v = static_cast<float>(a.x0_full[b * n + g]);
+            yC[c * B + b] = v;
+            xpC[c * B + b] = v;
+        }
+        tpC[c] = static_cast<float>(tau / a.pC[c]);
+        thrC[c] = static_cast<float>(thr_exact(tau, a.lambda, a.wC[c], a.pC[c]));
+    }
+    for (uint64_t r = gthread; r < a.nR; r += nthreads) {
+        const uint32_t g = a.R_glob[r];
+        for (int b = 0; b < B; ++b) x0R[r * B + b] = static_cast<float>(a.x0_full[b * n + g]);
+    }
+    for (int b = 0; b < B; ++b) {
+        SolveArgs ab = a;
+        ab.x0_full = a.x0_full + b * n;
+        ab.x_full = a.x_full + b * n;
+        decoupled_pass<float>(ab, tau, a.max_iters, 0, gthread, nthreads, nullptr, nullptr, 0);
+    }
+    grid_sync(a.sync, epoch, smem);
+    struct VecB {
+        float v[B];
+    };
+    for (int k = 1; k <= a.max_iters; ++k) {
+        st_phase_batch<B>(
+            st, a.A, a.T, gwarp, nwarps, lane, st.nA, yC,
+            [&](uint32_t r) {
+                VecB q;
+#pragma unroll
+                for (int b = 0; b < B; ++b) q.v[b] = r != kNoRow ? x0R[static_cast<uint64_t>(r) * B + b] : 0.f;
+                return q;
+            },
+            [&](uint32_t r, const float (&acc)[B], const VecB& x0) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) res[static_cast<uint64_t>(r) * B + b] = acc[b] - x0.v[b];
+            });
+        grid_sync(a.sync, epoch, smem);
+        const float beta = a.beta32[k - 1];
+        struct CoordB {
+            float y[B], xp[B], tp, thr;
+        };
+        st_phase_batch<B>(
+            st, a.A, a.T, gwarp, nwarps, lane, st.nT, res,
+            [&](uint32_t c) {
+                CoordB q;
+                const bool on = c != kNoRow;
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    q.y[b] = on ? yC[static_cast<uint64_t>(c) * B + b] : 0.f;
+                    q.xp[b] = on ? xpC[static_cast<uint64_t>(c) * B + b] : 0.f;
+                }
+                q.tp = on ? tpC[c] : 0.f;
+                q.thr = on ? thrC[c] : 0.f;
+                return q;
+            },
+            [&](uint32_t c, const float (&g)[B], const CoordB& q) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const float z0 = fmaf(-q.tp, g[b], q.y[b]);
+                    const float xn = Prec<float>::prox(z0, q.thr);
+                    yC[static_cast<uint64_t>(c) * B + b] = fmaf(beta, xn - q.xp[b], xn);
+                    xpC[static_cast<uint64_t>(c) * B + b] = xn;
+                }
+            });
+        grid_sync(a.sync, epoch, smem);
+    }
+    st_drain(st);
+    if (gthread == 0) a.out[OUT_ITERS_USED] = a.max_iters;
+    for (uint64_t c = gthread; c < a.nC; c += nthreads) {
+        const uint32_t g = a.C_glob[c];
+        for (int b = 0; b < B; ++b) a.x_full[b * n + g] = static_cast<double>(xpC[c * B + b]);
+    }
+}
+
 // Decoupled pass as its own kernel (tracking mode: per-iteration sums, then the final
 // write with the iteration count the solve actually used).
 template <typename T>
@@ -942,6 +1112,7 @@ struct wbx_solver {
     double lambda = 0.0;
     wbx_solver_cfg cfg{};
     int accelerate = 1;
+    int batch = 1;  // images per solve (C5): 1, 4 or 8
     wbx::DevBuf<double> pC, wC, ispC, w_full, p_full, beta64;
     wbx::DevBuf<float> beta32;
     wbx::DevBuf<unsigned char> state;  // yC, xpC, res, x0R, tpC, thrC (T-typed)
@@ -1022,10 +1193,11 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
         st += ((count * sizeof(T) + 255) / 256) * 256;
         return p;
     };
-    a.yC = carve(nC);
-    a.xpC = carve(nC);
-    a.res = carve(nR);
-    a.x0R = carve(nR);
+    const uint64_t B = static_cast<uint64_t>(s->batch);
+    a.yC = carve(nC * B);
+    a.xpC = carve(nC * B);
+    a.res = carve(nR * B);
+    a.x0R = carve(nR * B);
     a.tpC = carve(nC);
     a.thrC = carve(nC);
     a.wv = s->wv.p;
@@ -1068,6 +1240,14 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
+    if (s->batch > 1) {  // C5: B images per solve (fp32, no tracking; checked at creation)
+        const void* k = s->batch == 4 ? reinterpret_cast<const void*>(fista_batch_kernel<4>)
+                                      : reinterpret_cast<const void*>(fista_batch_kernel<8>);
+        launch_coop<T>(k, s->grid_fista, a, st);
+        count_launch(ctx);
+        WBX_CUDA(cudaGetLastError());
+        return;
+    }
     if (!a.track) {
         launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
         count_launch(ctx);
@@ -1102,11 +1282,16 @@ void alloc_state(wbx_solver* s) {
         WBX_CUDA(cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof mode));
     }
     auto rnd = [](uint64_t count) { return ((count * sizeof(T) + 255) / 256) * 256; };
-    s->state.alloc(4 * rnd(op->nC) + 2 * rnd(op->nR) + 256);
+    const uint64_t B = static_cast<uint64_t>(s->batch);
+    s->state.alloc(2 * rnd(op->nC * B) + 2 * rnd(op->nC) + 2 * rnd(op->nR * B) + 256);
     s->nslots = 3;
     if (const char* e = std::getenv("WBX_SLOTS")) s->nslots = std::max(1, std::min(kMaxSlots, std::atoi(e)));
     s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     s->grid_tau = blocks_per_sm(reinterpret_cast<const void*>(tau_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
+    if (s->batch == 4)
+        s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<4>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
+    else if (s->batch == 8)
+        s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<8>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
 }
 
 }  // namespace
@@ -1254,10 +1439,11 @@ void solver_free(wbx_solver* s) {
 }
 
 void solver_alloc_images(wbx_solver* s) {
-    s->u0.alloc(s->n);
-    s->x0full.alloc(s->n);
-    s->xfull.alloc(s->n);
-    s->uout.alloc(s->n);
+    const uint64_t B = static_cast<uint64_t>(s->batch);
+    s->u0.alloc(s->n * B);
+    s->x0full.alloc(s->n * B);
+    s->xfull.alloc(s->n * B);
+    s->uout.alloc(s->n * B);
 }
 
 }  // namespace wbx
@@ -1269,10 +1455,11 @@ int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp
         if (!s || !u0_dev || !u_dev) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_deblur_dev");
         cudaStream_t st = s->ctx->stream;
         const uint64_t before = s->ctx->launches;
-        wbx::analyze_dev(s->basis, u0_dev, s->x0full.p, st);
+        const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
+        for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
         wbx::solver_run(s, s->x0full.p, s->xfull.p);
-        wbx::synthesize_dev(s->basis, s->xfull.p, u_dev, st);
-        if (clamp) wbx::launch_clamp(s->ctx, u_dev, s->n, st);
+        for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st);
+        if (clamp) wbx::launch_clamp(s->ctx, u_dev, n * B, st);
         WBX_CUDA(cudaGetLastError());
         s->last_launches = s->ctx->launches - before;
         return WBX_OK;
@@ -1286,10 +1473,11 @@ int wbx_deblur(wbx_solver* s, const double* u0, double* u, int clamp, wbx_report
     try {
         if (!s || !u0 || !u) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_deblur");
         cudaStream_t st = s->ctx->stream;
-        WBX_CUDA(cudaMemcpyAsync(s->u0.p, u0, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
+        const uint64_t bytes = s->n * static_cast<uint64_t>(s->batch) * sizeof(double);
+        WBX_CUDA(cudaMemcpyAsync(s->u0.p, u0, bytes, cudaMemcpyHostToDevice, st));
         const int rc = wbx_deblur_dev(s, s->u0.p, s->uout.p, clamp);
         if (rc != WBX_OK) return rc;
-        WBX_CUDA(cudaMemcpyAsync(u, s->uout.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        WBX_CUDA(cudaMemcpyAsync(u, s->uout.p, bytes, cudaMemcpyDeviceToHost, st));
         wbx::solver_report(s, report);  // synchronises
         return WBX_OK;
     } catch (const wbx::Error& e) {
@@ -1310,3 +1498,30 @@ int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_
 }
 
 }  // extern "C"
+
+extern "C" int wbx_solver_create_batch(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* basis, const double* p,
+                                       const double* w, double lambda, const wbx_solver_cfg* cfg, int batch,
+                                       wbx_solver** out) {
+    wbx_solver* s = nullptr;
+    try {
+        if (!ctx || !op || !basis || !p || !w || !cfg || !out)
+            wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_solver_create_batch");
+        if (batch != 1 && batch != 4 && batch != 8) wbx::fail(WBX_BAD_SPEC, "batch must be 1, 4 or 8");
+        if (basis->n != op->n) wbx::fail(WBX_SHAPE_MISMATCH, "operator and basis sizes differ");
+        if (batch > 1 && (cfg->precision != WBX_FP32 || cfg->track_energy || cfg->track_support ||
+                          std::isfinite(cfg->ref_energy)))
+            wbx::fail(WBX_BAD_SPEC, "batched solves are fp32 with a fixed iteration count (no energy tracking)");
+        s = wbx::solver_new(ctx, op, const_cast<wbx_basis*>(basis), lambda, *cfg, 1);
+        s->batch = batch;
+        wbx::solver_setup(s, p, w);
+        wbx::solver_alloc_images(s);
+        *out = s;
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        if (s) wbx::solver_free(s);
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+extern "C" int wbx_solver_batch(const wbx_solver* s) { return s ? s->batch : 0; }

@@ -519,6 +519,57 @@ def theta_from_generators(gl: GeneratorList) -> SparseOperator:
     return SparseOperator(n, ro, ci[: nnz.value], va[: nnz.value], layout, gl.family, gl.order)
 
 
+@dataclass
+class SigmaLadder:
+    """Stationary Gaussian Theta_K operators at increasing sigmas (one GeneratorList each)."""
+    sigmas: np.ndarray
+    levels: list   # [GeneratorList]
+
+    @staticmethod
+    def from_npz(z, dims=None, J=4, family=FilterFamily.Daubechies, order=4) -> "SigmaLadder":
+        sig = np.asarray(z["sigmas"], dtype=np.float64)
+        meta_dims = tuple(json_dims(z)) if dims is None else tuple(dims)
+        lv = []
+        for l in range(sig.size):
+            lv.append(GeneratorList(meta_dims, J, FilterFamily(family), order,
+                                    z[f"l{l}_gen_block"].astype(np.uint32), z[f"l{l}_gen_index"].astype(np.uint32),
+                                    z[f"l{l}_gen_count"].astype(np.uint64), z[f"l{l}_gen_value"]))
+        return SigmaLadder(sig, lv)
+
+
+def json_dims(z):
+    import json
+    return json.loads(bytes(z["meta_json"]).decode())["dims"]
+
+
+def theta_varying(ladder: SigmaLadder, sigma_first_row: float = 2.5, sigma_last_row: float = 7.5) -> SparseOperator:
+    """Spatially varying Theta_K (BASELINE C3/C4): column-wise interpolation across a sigma
+    ladder of stationary operators (wbx_theta_varying; no reference implementation)."""
+    g0 = ladder.levels[0]
+    dims = np.array(g0.dims, dtype=np.uint64)
+    ngens = np.array([g.blocks.size for g in ladder.levels], dtype=np.uint64)
+    cat = lambda attr, dt: np.ascontiguousarray(np.concatenate([getattr(g, attr) for g in ladder.levels]).astype(dt))
+    blocks, gidx = cat("blocks", np.uint32), cat("gen_index", np.uint32)
+    counts, vals = cat("counts", np.uint64), cat("values", np.float64)
+    sig = np.ascontiguousarray(ladder.sigmas, dtype=np.float64)
+    nnz = C.c_uint64()
+    ro_p, ci_p, va_p = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_double)()
+    _check(lib.wbx_theta_varying(len(g0.dims), _u64ptr(dims), g0.J, sig.size, _dptr(sig), _u64ptr(ngens),
+                                 _u32ptr(blocks), _u32ptr(gidx), _u64ptr(counts), _dptr(vals),
+                                 float(sigma_first_row), float(sigma_last_row), C.byref(nnz), C.byref(ro_p),
+                                 C.byref(ci_p), C.byref(va_p)))
+    layout = make_layout(g0.dims, g0.J)
+    n = layout.total()
+    try:
+        ro = np.ctypeslib.as_array(ro_p, shape=(n + 1,)).copy()
+        ci = np.ctypeslib.as_array(ci_p, shape=(max(nnz.value, 1),))[: nnz.value].copy()
+        va = np.ctypeslib.as_array(va_p, shape=(max(nnz.value, 1),))[: nnz.value].copy()
+    finally:
+        for p in (ro_p, ci_p, va_p):
+            lib.wbx_free(C.cast(p, C.c_void_p))
+    return SparseOperator(n, ro, ci, va, layout, g0.family, g0.order)
+
+
 # ----------------------------------------------------------------------------- weights
 @dataclass
 class WeightVector:
@@ -755,25 +806,28 @@ class Deblurrer:
     synthesize (→ clamp). `deblur` takes host arrays; `deblur_dev` device pointers."""
 
     def __init__(self, op: SparseOperator, basis: WaveletBasis, P: DiagonalPreconditioner, weights,
-                 lambda_: float, config: SolverConfig, ctx: Optional[Context] = None):
+                 lambda_: float, config: SolverConfig, ctx: Optional[Context] = None, batch: int = 1):
         self.ctx = ctx or op._ctx or default_context()
         self.op, self.basis, self.config = op, basis, config
         self.n = op.n
+        self.batch = int(batch)
         p = _f64(P.p, op.n, "preconditioner")
         w = _f64(weights, op.n, "weights")
         cfg = config.to_c()
         h = C.c_void_p()
-        _check(lib.wbx_solver_create(self.ctx.handle, op.device(self.ctx), basis.device(self.ctx), _dptr(p),
-                                     _dptr(w), float(lambda_), C.byref(cfg), C.byref(h)))
+        _check(lib.wbx_solver_create_batch(self.ctx.handle, op.device(self.ctx), basis.device(self.ctx), _dptr(p),
+                                           _dptr(w), float(lambda_), C.byref(cfg), self.batch, C.byref(h)))
         self.handle = h
 
     def deblur(self, u0: np.ndarray, clamp: bool = True, out: Optional[np.ndarray] = None):
-        u = _f64(u0, self.n, "u0")
-        res = out if out is not None else np.empty(self.n)
+        """u0: one image (batch 1) or `batch` images stacked on the first axis."""
+        u = _f64(u0, self.n * self.batch, "u0")
+        res = out if out is not None else np.empty(self.n * self.batch)
         rep = N.wbx_report()
         _check(lib.wbx_deblur(self.handle, _dptr(u), res.ctypes.data_as(C.POINTER(C.c_double)), int(clamp),
                               C.byref(rep)))
-        return res.reshape(self.basis.layout.dims), rep
+        shape = tuple(self.basis.layout.dims) if self.batch == 1 else (self.batch,) + tuple(self.basis.layout.dims)
+        return res.reshape(shape), rep
 
     def deblur_dev(self, u0_ptr: int, u_ptr: int, clamp: bool = True) -> None:
         _check(lib.wbx_deblur_dev(self.handle, C.c_void_p(u0_ptr), C.c_void_p(u_ptr), int(clamp)))
