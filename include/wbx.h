@@ -210,6 +210,36 @@ int wbx_solver_create_batch(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* bas
                             const double* w, double lambda, const wbx_solver_cfg* cfg, int batch,
                             wbx_solver** out);
 int wbx_solver_batch(const wbx_solver* s);
+/* ---------------------------------------------------------------- row-sharded solve (C4)
+ * One image across `world` ranks (one per GPU). Rank `rank` owns a contiguous,
+ * nnz-balanced range of the compacted rows of Theta and of Theta^T. Cross-rank vectors live in
+ * caller-owned PADDED device buffers (rank q's slice at q * max_range): y (fp32, world*maxC),
+ * res (fp32, world*maxR), u (fp64, world*maxC), t (fp64, world*maxR). After each phase the
+ * caller all-gathers the owned slice (NCCL all_gather over NVLink, or a copy when emulated).
+ * Per FISTA iteration k: phase_a -> all-gather res -> phase_t(k) -> all-gather y.
+ * Per power iteration: power_a(|w_prev|) -> all-gather t -> power_t(|w_prev|, sums) ->
+ * all-reduce the two sums (<v,w>, |w|^2) -> all-gather u. A sharded solve is bitwise equal
+ * to the single-GPU fp32 solve given the same tau, for any world size. */
+typedef struct wbx_shard wbx_shard;
+int wbx_shard_create(wbx_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
+                     const double* values, uint32_t world, uint32_t rank, wbx_shard** out);
+int wbx_shard_destroy(wbx_shard* s);
+/* host-only partition plan (what wbx_shard_create uses): rbounds/cbounds[world + 1] */
+int wbx_shard_plan(uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices, uint32_t world,
+                   uint64_t* rbounds, uint64_t* cbounds);
+/* info8 = {world, rank, row_lo, row_hi, col_lo, col_hi, maxR, maxC} */
+int wbx_shard_get_info(const wbx_shard* s, uint64_t* info8);
+int wbx_shard_bind(wbx_shard* s, float* y_pad, float* res_pad, double* u_pad, double* t_pad);
+int wbx_shard_setup(wbx_shard* s, const double* p, const double* w, double lambda, int max_iters,
+                    int accelerate);
+int wbx_shard_init(wbx_shard* s, double tau, const double* x0_full_dev, double* x_full_dev);
+int wbx_shard_phase_a(wbx_shard* s);
+int wbx_shard_phase_t(wbx_shard* s, int k);
+int wbx_shard_finalize(wbx_shard* s, double* x_full_dev);
+int wbx_shard_power_init(wbx_shard* s, double* sums2);
+int wbx_shard_power_a(wbx_shard* s, double inv);
+int wbx_shard_power_t(wbx_shard* s, double inv, double* sums2);
+
 /* launches of the last deblur, and the solver kernel's device time (ms) */
 int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);
 

@@ -100,6 +100,19 @@ SIGNATURES = {
     "wbx_deblur_dev": (C.c_int, [_P, _P, _P, C.c_int]),
     "wbx_deblur": (C.c_int, [_P, _D, _D, C.c_int, C.POINTER(wbx_report)]),
     "wbx_solver_last_stats": (C.c_int, [_P, _U64, C.POINTER(C.c_float)]),
+    "wbx_shard_create": (C.c_int, [_P, C.c_uint64, _U64, _U32, _D, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
+    "wbx_shard_destroy": (C.c_int, [_P]),
+    "wbx_shard_plan": (C.c_int, [C.c_uint64, _U64, _U32, C.c_uint32, _U64, _U64]),
+    "wbx_shard_get_info": (C.c_int, [_P, _U64]),
+    "wbx_shard_bind": (C.c_int, [_P, _P, _P, _P, _P]),
+    "wbx_shard_setup": (C.c_int, [_P, _D, _D, C.c_double, C.c_int, C.c_int]),
+    "wbx_shard_init": (C.c_int, [_P, C.c_double, _P, _P]),
+    "wbx_shard_phase_a": (C.c_int, [_P]),
+    "wbx_shard_phase_t": (C.c_int, [_P, C.c_int]),
+    "wbx_shard_finalize": (C.c_int, [_P, _P]),
+    "wbx_shard_power_init": (C.c_int, [_P, _D]),
+    "wbx_shard_power_a": (C.c_int, [_P, C.c_double]),
+    "wbx_shard_power_t": (C.c_int, [_P, C.c_double, _D]),
 }
 
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -157,6 +158,11 @@ SellView view_of(const wbx_sell& m);
 
 void build_op(wbx_op* op, uint64_t n, const uint64_t* rowptr, const uint32_t* col,
               const double* val);
+// SELL layouts (both the segmented fp32 and the exact fp64 one) of `nrows` rows given by
+// len(i) and get(i, j, col, val), uploaded into `out`.
+void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint64_t)>& len,
+                const std::function<void(uint64_t, uint64_t, uint32_t&, double&)>& get, cudaStream_t s,
+                uint64_t& bytes);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

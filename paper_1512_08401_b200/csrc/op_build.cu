@@ -185,6 +185,20 @@ void upload_sell(wbx_sell& d, const HostSell& h, uint64_t rows, cudaStream_t s, 
 
 }  // namespace
 
+void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint64_t)>& len,
+                const std::function<void(uint64_t, uint64_t, uint32_t&, double&)>& get, cudaStream_t s,
+                uint64_t& bytes) {
+    struct Range {
+        const std::function<uint64_t(uint64_t)>* l;
+        const std::function<void(uint64_t, uint64_t, uint32_t&, double&)>* g;
+        uint64_t len(uint64_t i) const { return (*l)(i); }
+        void get(uint64_t i, uint64_t j, uint32_t& c, double& v) const { (*g)(i, j, c, v); }
+    } r{&len, &get};
+    HostSell h = make_sell(nrows, r);
+    upload_sell(out, h, nrows, s, bytes);
+    WBX_CUDA(cudaStreamSynchronize(s));
+}
+
 SellView view_of(const wbx_sell& m) {
     SellView v;
     v.xslice_ptr = m.xslice_ptr.p;

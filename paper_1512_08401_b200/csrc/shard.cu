@@ -1,0 +1,563 @@
+// Row-sharded solve of ONE image across ranks (BASELINE config C4).
+//
+// The compacted coordinate sets of the single-GPU solver (R = nonempty rows of Theta,
+// C = nonempty columns, both sorted by descending length exactly as op_build.cu) are cut
+// into `world` contiguous ranges balanced by nonzeros. Rank p owns rows R_p of Theta and
+// rows C_p of Theta^T (= columns C_p of Theta) and the coordinates C_p of x and y. Vectors
+// that cross ranks live in PADDED global buffers (rank q's slice at q * max_range) so the
+// exchange after each phase is one equal-size all-gather (NCCL over NVLink/NVSwitch, driven
+// by the host; or a local copy when the shards are emulated on one GPU):
+//     phase A   res[R_p] = Theta[R_p, :] y - x0[R_p]         -> all-gather res
+//     phase T   g = Theta^T[C_p, :] res; fused update on C_p  -> all-gather y
+// No reductions cross ranks in FISTA, and every row is summed by the same lane arithmetic
+// as the persistent single-GPU kernel, so a sharded solve is BITWISE equal to the
+// single-GPU solve for any world size (given tau). estimate_step needs two scalars per
+// power iteration (sum over ranks), exchanged by the host.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <numeric>
+
+#include "internal.hpp"
+#include "sell.cuh"
+
+extern "C" void wbx_set_last_error(const char* msg);
+
+struct wbx_shard {
+    wbx_ctx* ctx = nullptr;
+    uint32_t world = 1, rank = 0;
+    uint64_t n = 0, nnz = 0, nR = 0, nC = 0;
+    uint64_t rlo = 0, rhi = 0, clo = 0, chi = 0, maxR = 0, maxC = 0;
+    wbx_sell A, T;                          // A: rows R_p (cols: padded C); T: rows C_p (cols: padded R)
+    wbx::DevBuf<uint32_t> R_own, C_own;     // original indices of the owned rows / coordinates
+    wbx::DevBuf<uint32_t> isC;              // global bitmask of nonempty columns (decoupled pass)
+    // bound exchange buffers (device pointers owned by the caller)
+    float* y_pad = nullptr;
+    float* res_pad = nullptr;
+    double* u_pad = nullptr;
+    double* t_pad = nullptr;
+    // owned state
+    wbx::DevBuf<float> xp, x0R, tp, thr, beta;
+    wbx::DevBuf<double> pC, wC, ispC, wv, p_full, w_full, part;
+    double lambda = 0.0, tau = 0.0;
+    int max_iters = 0;
+    uint64_t device_bytes = 0;
+};
+
+namespace wbx {
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ bool bit_set(const uint32_t* m, uint64_t i) { return (m[i >> 5] >> (i & 31)) & 1u; }
+
+__device__ __forceinline__ double rng_normal(uint64_t seed, uint64_t i) {
+    auto at = [](uint64_t s, uint64_t k) {
+        uint64_t z = s + 0x9e3779b97f4a7c15ull * (k + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    auto u01 = [](uint64_t v) { return (static_cast<double>(v >> 11) + 0.5) * 0x1p-53; };
+    const uint64_t m = i >> 1;
+    const double u1 = u01(at(seed, 2 * m)), u2 = u01(at(seed, 2 * m + 1));
+    const double r = sqrt(-2.0 * log(u1)), a = 2.0 * M_PI * u2;
+    return (i & 1) ? r * sin(a) : r * cos(a);
+}
+
+struct ShardArgs {
+    SellView A, T;
+    uint32_t rank;
+    uint64_t n, nR_own, nC_own, maxR, maxC;
+    const uint32_t* R_own;
+    const uint32_t* C_own;
+    const uint32_t* isC;
+    float* y_pad;
+    float* res_pad;
+    double* u_pad;
+    double* t_pad;
+    float* xp;
+    float* x0R;
+    float* tp;
+    float* thr;
+    const float* beta;
+    const double* pC;
+    const double* wC;
+    const double* ispC;
+    double* wv;
+    const double* p_full;
+    const double* w_full;
+    double* part;
+    double lambda, tau;
+};
+
+ShardArgs args_of(wbx_shard* s) {
+    ShardArgs a{};
+    a.A = view_of(s->A);
+    a.T = view_of(s->T);
+    a.rank = s->rank;
+    a.n = s->n;
+    a.nR_own = s->rhi - s->rlo;
+    a.nC_own = s->chi - s->clo;
+    a.maxR = s->maxR;
+    a.maxC = s->maxC;
+    a.R_own = s->R_own.p;
+    a.C_own = s->C_own.p;
+    a.isC = s->isC.p;
+    a.y_pad = s->y_pad;
+    a.res_pad = s->res_pad;
+    a.u_pad = s->u_pad;
+    a.t_pad = s->t_pad;
+    a.xp = s->xp.p;
+    a.x0R = s->x0R.p;
+    a.tp = s->tp.p;
+    a.thr = s->thr.p;
+    a.beta = s->beta.p;
+    a.pC = s->pC.p;
+    a.wC = s->wC.p;
+    a.ispC = s->ispC.p;
+    a.wv = s->wv.p;
+    a.p_full = s->p_full.p;
+    a.w_full = s->w_full.p;
+    a.part = s->part.p;
+    a.lambda = s->lambda;
+    a.tau = s->tau;
+    return a;
+}
+
+// one warp per slice of the segmented fp32 layout (same arithmetic as the persistent kernel)
+template <typename ACC, typename X, typename Epi>
+__device__ __forceinline__ void slice_rows(const SellView& M, const X* x, Epi epi) {
+    const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s < M.slices) {  // whole warps in or out; no early return (block reductions follow)
+        ACC acc = seg_partial<ACC, X>(M, s, lane, x);
+        const uint32_t row = seg_combine(M, s, lane, acc);
+        if (row != kNoRow) epi(row, acc);
+    }
+}
+
+__global__ void init_kernel(ShardArgs a, const double* x0_full) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < a.nC_own) {
+        const float v = static_cast<float>(x0_full[a.C_own[i]]);
+        a.y_pad[a.rank * a.maxC + i] = v;
+        a.xp[i] = v;
+        a.tp[i] = static_cast<float>(a.tau / a.pC[i]);
+        a.thr[i] = static_cast<float>(__ddiv_rn(__dmul_rn(__dmul_rn(a.tau, a.lambda), a.wC[i]), a.pC[i]));
+    }
+    if (i < a.nR_own) a.x0R[i] = static_cast<float>(x0_full[a.R_own[i]]);
+}
+
+__global__ void phase_a_kernel(ShardArgs a) {
+    float* res = a.res_pad + a.rank * a.maxR;
+    slice_rows<float, float>(a.A, a.y_pad, [&](uint32_t r, float acc) { res[r] = acc - a.x0R[r]; });
+}
+
+__global__ void phase_t_kernel(ShardArgs a, int k) {
+    const float beta = a.beta[k - 1];
+    float* y = a.y_pad + a.rank * a.maxC;
+    slice_rows<float, float>(a.T, a.res_pad, [&](uint32_t c, float g) {
+        const float z0 = fmaf(-a.tp[c], g, y[c]);
+        const float t = fabsf(z0) - a.thr[c];
+        const float xn = t > 0.f ? (z0 > 0.f ? t : -t) : 0.f;
+        y[c] = fmaf(beta, xn - a.xp[c], xn);
+        a.xp[c] = xn;
+    });
+}
+
+// decoupled coordinates of this rank's slice of [0, n): prox + momentum in registers
+__global__ void decoupled_kernel(ShardArgs a, uint64_t lo, uint64_t hi, int K, const double* x0_full,
+                                 double* x_full) {
+    const uint64_t i = lo + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= hi || bit_set(a.isC, i)) return;
+    const double w = a.w_full[i];
+    const float thr = static_cast<float>(__ddiv_rn(__dmul_rn(__dmul_rn(a.tau, a.lambda), w), a.p_full[i]));
+    float x = static_cast<float>(x0_full[i]), xp = x, y = x;
+    for (int k = 1; k <= K; ++k) {
+        const float t = fabsf(y) - thr;
+        const float xn = t > 0.f ? (y > 0.f ? t : -t) : 0.f;
+        const bool fixed = xn == 0.f && xp == 0.f;
+        y = fmaf(a.beta[k - 1], xn - xp, xn);
+        xp = xn;
+        x = xn;
+        if (fixed) break;
+    }
+    x_full[i] = static_cast<double>(x);
+}
+
+__global__ void finalize_kernel(ShardArgs a, double* x_full) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < a.nC_own) x_full[a.C_own[i]] = static_cast<double>(a.xp[i]);
+}
+
+// ---- estimate_step pieces (fp64 vectors, fp32 operator values)
+__global__ void power_init_kernel(ShardArgs a, uint64_t lo, uint64_t hi) {
+    __shared__ double sm[kBlock / 32 + 1];
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    double s2 = 0.0;
+    for (uint64_t i = lo + t; i < hi; i += nt) {
+        const double v = rng_normal(0x5eedull, i);
+        s2 += v * v;
+    }
+    for (uint64_t c = t; c < a.nC_own; c += nt) {
+        const double v = rng_normal(0x5eedull, a.C_own[c]);
+        a.wv[c] = v;
+        a.u_pad[a.rank * a.maxC + c] = a.ispC[c] * v;
+    }
+    s2 = block_sum<kBlock>(s2, sm);
+    if (threadIdx.x == 0) a.part[2 * blockIdx.x] = s2;
+    if (threadIdx.x == 0) a.part[2 * blockIdx.x + 1] = 0.0;
+}
+
+__global__ void power_a_kernel(ShardArgs a, double inv) {
+    double* t = a.t_pad + a.rank * a.maxR;
+    slice_rows<double, double>(a.A, a.u_pad, [&](uint32_t r, double acc) { t[r] = acc / inv; });
+}
+
+__global__ void power_t_kernel(ShardArgs a, double inv) {
+    __shared__ double sm[kBlock / 32 + 1];
+    double pl = 0.0, pn = 0.0;
+    double* u = a.u_pad + a.rank * a.maxC;
+    slice_rows<double, double>(a.T, a.t_pad, [&](uint32_t c, double g) {
+        const double w = g * a.ispC[c];
+        const double v = a.wv[c] / inv;
+        pl += v * w;
+        pn += w * w;
+        a.wv[c] = w;
+        u[c] = a.ispC[c] * w;
+    });
+    pl = block_sum<kBlock>(pl, sm);
+    pn = block_sum<kBlock>(pn, sm);
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = pl;
+        a.part[2 * blockIdx.x + 1] = pn;
+    }
+}
+
+unsigned blocks_for(uint64_t threads) { return static_cast<unsigned>(std::max<uint64_t>(1, (threads + kBlock - 1) / kBlock)); }
+
+}  // namespace
+}  // namespace wbx
+
+using wbx::kBlock;
+
+extern "C" {
+
+int wbx_shard_create(wbx_ctx* ctx, uint64_t n, const uint64_t* rowptr, const uint32_t* col, const double* val,
+                     uint32_t world, uint32_t rank, wbx_shard** out) {
+    try {
+        if (!ctx || !rowptr || !out) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_shard_create");
+        if (world < 1 || rank >= world) wbx::fail(WBX_BAD_SPEC, "bad world / rank");
+        if (rowptr[0] != 0) wbx::fail(WBX_SHAPE_MISMATCH, "inconsistent row offsets");
+        const uint64_t nnz = rowptr[n];
+        for (uint64_t r = 0; r < n; ++r) {
+            if (rowptr[r] > rowptr[r + 1]) wbx::fail(WBX_SHAPE_MISMATCH, "row offsets not nondecreasing");
+            for (uint64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+                if (col[k] >= n) wbx::fail(WBX_SHAPE_MISMATCH, "column index out of range");
+                if (k > rowptr[r] && col[k] <= col[k - 1])
+                    wbx::fail(WBX_SHAPE_MISMATCH, "columns not strictly increasing in a row");
+            }
+        }
+        auto s = std::make_unique<wbx_shard>();
+        s->ctx = ctx;
+        s->world = world;
+        s->rank = rank;
+        s->n = n;
+        s->nnz = nnz;
+        // transpose (ascending original row within a column)
+        std::vector<uint64_t> toff(n + 1, 0);
+        for (uint64_t k = 0; k < nnz; ++k) ++toff[col[k] + 1];
+        for (uint64_t i = 0; i < n; ++i) toff[i + 1] += toff[i];
+        std::vector<uint32_t> trow(nnz);
+        std::vector<double> tval(nnz);
+        {
+            std::vector<uint64_t> cur(toff.begin(), toff.end() - 1);
+            for (uint64_t r = 0; r < n; ++r)
+                for (uint64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+                    const uint64_t p = cur[col[k]]++;
+                    trow[p] = static_cast<uint32_t>(r);
+                    tval[p] = val[k];
+                }
+        }
+        // global R, C in the single-GPU solver's order (op_build.cu)
+        std::vector<uint32_t> R, C;
+        for (uint64_t r = 0; r < n; ++r)
+            if (rowptr[r + 1] > rowptr[r]) R.push_back(static_cast<uint32_t>(r));
+        for (uint64_t c = 0; c < n; ++c)
+            if (toff[c + 1] > toff[c]) C.push_back(static_cast<uint32_t>(c));
+        std::stable_sort(R.begin(), R.end(), [&](uint32_t a, uint32_t b) {
+            return rowptr[a + 1] - rowptr[a] > rowptr[b + 1] - rowptr[b];
+        });
+        std::stable_sort(C.begin(), C.end(),
+                         [&](uint32_t a, uint32_t b) { return toff[a + 1] - toff[a] > toff[b + 1] - toff[b]; });
+        s->nR = R.size();
+        s->nC = C.size();
+        // contiguous ranges balanced by nonzeros
+        auto cut = [&](const std::vector<uint32_t>& ids, auto len) {
+            std::vector<uint64_t> bounds(world + 1, ids.size());
+            bounds[0] = 0;
+            uint64_t total = 0;
+            for (uint32_t id : ids) total += len(id);
+            uint64_t acc = 0, q = 1;
+            for (uint64_t i = 0; i < ids.size() && q < world; ++i) {
+                acc += len(ids[i]);
+                while (q < world && acc * world >= total * q) bounds[q++] = i + 1;
+            }
+            return bounds;
+        };
+        const auto rb = cut(R, [&](uint32_t r) { return rowptr[r + 1] - rowptr[r]; });
+        const auto cb = cut(C, [&](uint32_t c) { return toff[c + 1] - toff[c]; });
+        for (uint32_t q = 0; q < world; ++q) {
+            s->maxR = std::max<uint64_t>(s->maxR, rb[q + 1] - rb[q]);
+            s->maxC = std::max<uint64_t>(s->maxC, cb[q + 1] - cb[q]);
+        }
+        s->maxR = std::max<uint64_t>(s->maxR, 1);
+        s->maxC = std::max<uint64_t>(s->maxC, 1);
+        s->rlo = rb[rank];
+        s->rhi = rb[rank + 1];
+        s->clo = cb[rank];
+        s->chi = cb[rank + 1];
+        // padded global positions
+        std::vector<uint32_t> rpad(n, 0xffffffffu), cpad(n, 0xffffffffu);
+        for (uint32_t q = 0; q < world; ++q) {
+            for (uint64_t i = rb[q]; i < rb[q + 1]; ++i) rpad[R[i]] = static_cast<uint32_t>(q * s->maxR + (i - rb[q]));
+            for (uint64_t i = cb[q]; i < cb[q + 1]; ++i) cpad[C[i]] = static_cast<uint32_t>(q * s->maxC + (i - cb[q]));
+        }
+        if (static_cast<uint64_t>(world) * s->maxR > 0xffffffffull || static_cast<uint64_t>(world) * s->maxC > 0xffffffffull)
+            wbx::fail(WBX_TOO_LARGE, "padded index space exceeds 32 bits");
+        cudaStream_t st = ctx->stream;
+        uint64_t bytes = 0;
+        const uint64_t r0 = s->rlo, c0 = s->clo;
+        wbx::build_sell(
+            s->A, s->rhi - s->rlo, [&](uint64_t i) { return rowptr[R[r0 + i] + 1] - rowptr[R[r0 + i]]; },
+            [&](uint64_t i, uint64_t j, uint32_t& c, double& v) {
+                const uint64_t k = rowptr[R[r0 + i]] + j;
+                c = cpad[col[k]];
+                v = val[k];
+            },
+            st, bytes);
+        wbx::build_sell(
+            s->T, s->chi - s->clo, [&](uint64_t i) { return toff[C[c0 + i] + 1] - toff[C[c0 + i]]; },
+            [&](uint64_t i, uint64_t j, uint32_t& c, double& v) {
+                const uint64_t k = toff[C[c0 + i]] + j;
+                c = rpad[trow[k]];
+                v = tval[k];
+            },
+            st, bytes);
+        std::vector<uint32_t> Rown(R.begin() + static_cast<long>(s->rlo), R.begin() + static_cast<long>(s->rhi));
+        std::vector<uint32_t> Cown(C.begin() + static_cast<long>(s->clo), C.begin() + static_cast<long>(s->chi));
+        if (Rown.empty()) Rown.push_back(0);
+        if (Cown.empty()) Cown.push_back(0);
+        s->R_own.upload(Rown, st);
+        s->C_own.upload(Cown, st);
+        std::vector<uint32_t> mask((n + 31) / 32, 0);
+        for (uint32_t c : C) mask[c / 32] |= 1u << (c % 32);
+        s->isC.upload(mask, st);
+        WBX_CUDA(cudaStreamSynchronize(st));
+        s->device_bytes = bytes;
+        *out = s.release();
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+// Host-only: the partition wbx_shard_create uses (row/column range bounds per rank), for
+// planning and for testing without a GPU. rbounds/cbounds: world + 1 entries each.
+int wbx_shard_plan(uint64_t n, const uint64_t* rowptr, const uint32_t* col, uint32_t world, uint64_t* rbounds,
+                   uint64_t* cbounds) {
+    try {
+        if (!rowptr || !rbounds || !cbounds || world < 1) wbx::fail(WBX_INVALID_ARGUMENT, "bad wbx_shard_plan args");
+        const uint64_t nnz = rowptr[n];
+        std::vector<uint64_t> clen(n, 0);
+        for (uint64_t k = 0; k < nnz; ++k) {
+            if (col[k] >= n) wbx::fail(WBX_SHAPE_MISMATCH, "column index out of range");
+            ++clen[col[k]];
+        }
+        std::vector<uint32_t> R, C;
+        for (uint64_t r = 0; r < n; ++r)
+            if (rowptr[r + 1] > rowptr[r]) R.push_back(static_cast<uint32_t>(r));
+        for (uint64_t c = 0; c < n; ++c)
+            if (clen[c]) C.push_back(static_cast<uint32_t>(c));
+        std::stable_sort(R.begin(), R.end(), [&](uint32_t a, uint32_t b) {
+            return rowptr[a + 1] - rowptr[a] > rowptr[b + 1] - rowptr[b];
+        });
+        std::stable_sort(C.begin(), C.end(), [&](uint32_t a, uint32_t b) { return clen[a] > clen[b]; });
+        auto cut = [&](const std::vector<uint32_t>& ids, auto len, uint64_t* bounds) {
+            for (uint32_t q = 0; q <= world; ++q) bounds[q] = ids.size();
+            bounds[0] = 0;
+            uint64_t total = 0;
+            for (uint32_t id : ids) total += len(id);
+            uint64_t acc = 0, q = 1;
+            for (uint64_t i = 0; i < ids.size() && q < world; ++i) {
+                acc += len(ids[i]);
+                while (q < world && acc * world >= total * q) bounds[q++] = i + 1;
+            }
+        };
+        cut(R, [&](uint32_t r) { return rowptr[r + 1] - rowptr[r]; }, rbounds);
+        cut(C, [&](uint32_t c) { return clen[c]; }, cbounds);
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_shard_destroy(wbx_shard* s) {
+    if (s) {
+        cudaStreamSynchronize(s->ctx->stream);
+        delete s;
+    }
+    return WBX_OK;
+}
+
+int wbx_shard_get_info(const wbx_shard* s, uint64_t* info8) {
+    if (!s || !info8) return WBX_INVALID_ARGUMENT;
+    const uint64_t v[8] = {s->world, s->rank, s->rlo, s->rhi, s->clo, s->chi, s->maxR, s->maxC};
+    std::copy(v, v + 8, info8);
+    return WBX_OK;
+}
+
+int wbx_shard_bind(wbx_shard* s, float* y_pad, float* res_pad, double* u_pad, double* t_pad) {
+    if (!s || !y_pad || !res_pad || !u_pad || !t_pad) return WBX_INVALID_ARGUMENT;
+    s->y_pad = y_pad;
+    s->res_pad = res_pad;
+    s->u_pad = u_pad;
+    s->t_pad = t_pad;
+    return WBX_OK;
+}
+
+int wbx_shard_setup(wbx_shard* s, const double* p, const double* w, double lambda, int max_iters,
+                    int accelerate) {
+    try {
+        if (!s || !p || !w) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_shard_setup");
+        cudaStream_t st = s->ctx->stream;
+        const uint64_t nC = std::max<uint64_t>(1, s->chi - s->clo);
+        std::vector<uint32_t> Cown(nC);
+        WBX_CUDA(cudaMemcpy(Cown.data(), s->C_own.p, nC * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        std::vector<double> hp(nC), hw(nC), hi(nC);
+        for (uint64_t i = 0; i < nC; ++i) {
+            hp[i] = p[Cown[i]];
+            hw[i] = w[Cown[i]];
+            if (!(hp[i] > 0.0)) wbx::fail(WBX_BAD_SPEC, "preconditioner entries must be strictly positive");
+            hi[i] = 1.0 / std::sqrt(hp[i]);
+        }
+        s->pC.upload(hp, st);
+        s->wC.upload(hw, st);
+        s->ispC.upload(hi, st);
+        s->p_full.alloc(s->n);
+        s->p_full.upload(p, s->n, st);
+        s->w_full.alloc(s->n);
+        s->w_full.upload(w, s->n, st);
+        std::vector<float> b(std::max(1, max_iters), 0.f);
+        for (int k = 1; k <= max_iters; ++k)
+            b[k - 1] = accelerate ? static_cast<float>((static_cast<double>(k) - 1.0) / (static_cast<double>(k) + 2.0)) : 0.f;
+        s->beta.upload(b, st);
+        s->xp.alloc(nC);
+        s->tp.alloc(nC);
+        s->thr.alloc(nC);
+        s->wv.alloc(nC);
+        s->x0R.alloc(std::max<uint64_t>(1, s->rhi - s->rlo));
+        s->part.alloc(2 * std::max<uint64_t>(wbx::blocks_for(uint64_t(s->T.slices) * 32),
+                                             2 * static_cast<uint64_t>(s->ctx->num_sms)));
+        s->lambda = lambda;
+        s->max_iters = max_iters;
+        WBX_CUDA(cudaStreamSynchronize(st));
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+// step 0: x0 -> owned state (needs tau), decoupled coordinates of this rank's index range
+int wbx_shard_init(wbx_shard* s, double tau, const double* x0_full_dev, double* x_full_dev) {
+    if (!s || !x0_full_dev || !x_full_dev || !s->y_pad) return WBX_INVALID_ARGUMENT;
+    s->tau = tau;
+    cudaStream_t st = s->ctx->stream;
+    wbx::ShardArgs a = wbx::args_of(s);
+    const uint64_t m = std::max(a.nC_own, a.nR_own);
+    wbx::init_kernel<<<wbx::blocks_for(m), kBlock, 0, st>>>(a, x0_full_dev);
+    const uint64_t lo = s->n * s->rank / s->world, hi = s->n * (s->rank + 1) / s->world;
+    wbx::decoupled_kernel<<<wbx::blocks_for(hi - lo), kBlock, 0, st>>>(a, lo, hi, s->max_iters, x0_full_dev, x_full_dev);
+    wbx::count_launch(s->ctx, 2);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_phase_a(wbx_shard* s) {
+    if (!s) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    if (a.A.slices) wbx::phase_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_phase_t(wbx_shard* s, int k) {
+    if (!s || k < 1 || k > s->max_iters) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    if (a.T.slices) wbx::phase_t_kernel<<<wbx::blocks_for(uint64_t(a.T.slices) * 32), kBlock, 0, s->ctx->stream>>>(a, k);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_finalize(wbx_shard* s, double* x_full_dev) {
+    if (!s || !x_full_dev) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    wbx::finalize_kernel<<<wbx::blocks_for(a.nC_own), kBlock, 0, s->ctx->stream>>>(a, x_full_dev);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+// estimate_step pieces: partial sums of this rank land in sums2[0..1] (host, synchronous)
+static int reduce_parts(wbx_shard* s, unsigned blocks, double* sums2) {
+    std::vector<double> h(2 * blocks);
+    if (cudaMemcpyAsync(h.data(), s->part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s->ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+        return WBX_CUDA_ERROR;
+    double a = 0.0, b = 0.0;
+    for (unsigned i = 0; i < blocks; ++i) {
+        a += h[2 * i];
+        b += h[2 * i + 1];
+    }
+    sums2[0] = a;
+    sums2[1] = b;
+    return WBX_OK;
+}
+
+int wbx_shard_power_init(wbx_shard* s, double* sums2) {
+    if (!s || !sums2 || !s->u_pad) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    const unsigned blocks = 2 * static_cast<unsigned>(s->ctx->num_sms);
+    const uint64_t lo = s->n * s->rank / s->world, hi = s->n * (s->rank + 1) / s->world;
+    wbx::power_init_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a, lo, hi);
+    wbx::count_launch(s->ctx);
+    return reduce_parts(s, blocks, sums2);
+}
+
+int wbx_shard_power_a(wbx_shard* s, double inv) {
+    if (!s) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    if (a.A.slices) wbx::power_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a, inv);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_power_t(wbx_shard* s, double inv, double* sums2) {
+    if (!s || !sums2) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    const unsigned blocks = wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.slices, 1)) * 32);
+    if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
+    if (a.T.slices) {
+        wbx::power_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a, inv);
+    } else {
+        cudaMemsetAsync(s->part.p, 0, 2 * blocks * sizeof(double), s->ctx->stream);
+    }
+    wbx::count_launch(s->ctx);
+    return reduce_parts(s, blocks, sums2);
+}
+
+}  // extern "C"
