@@ -42,6 +42,7 @@ class _Shard:
         _check(lib.wbx_shard_create(ctx.handle, op.n, W._u64ptr(op.row_offsets), W._u32ptr(op.col_indices),
                                     W._dptr(op.values), world, rank, C.byref(h)))
         self.h = h
+        self.ctx = ctx  # the context (stream) must outlive the shard
         info = np.zeros(8, dtype=np.uint64)
         _check(lib.wbx_shard_get_info(h, W._u64ptr(info)))
         self.world, self.rank, self.rlo, self.rhi, self.clo, self.chi, self.maxR, self.maxC = (int(v) for v in info)

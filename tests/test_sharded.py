@@ -107,7 +107,10 @@ def test_sharded_bitwise_equals_single_gpu(world):
     sh.deblur_dev(u0.data_ptr(), out.data_ptr(), tau=tau, clamp=True)
     ctx.synchronize()
     assert np.array_equal(out.cpu().numpy().reshape(256, 256), ref)
-    # estimate_step through the sharded power iteration
+    # estimate_step through the sharded power iteration: same stopping iteration as the
+    # single-GPU kernel
     t2 = sh.estimate_step(1.01)
     assert abs(t2 - tau) <= 1e-6 * tau
-    assert sh.tau_iters == 142  # the reference's iteration count at 256^2
+    t1, it1 = W.estimate_step(W.SparseThetaOp(op, ctx), P, 1.01, ctx=ctx, return_iters=True)
+    assert sh.tau_iters == it1
+    del sh, single
