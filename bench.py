@@ -321,6 +321,71 @@ def cpu_reference(steps: int, warmup: int, budget_s: float = 150.0):
             "sample": "1 full deblur through the C restatement (oracle/wbx_oracle.c), 1 thread"}
 
 
+def run_c4(args, rank, world, local_rank):
+    """BASELINE config C4: one size^2 spatially varying deblur (sigma 2.5 -> 7.5 px), Theta_K
+    row-sharded over `world` GPUs; NCCL all-gathers of the padded y / res slices over NVLink
+    after every phase (strong scaling: total work fixed)."""
+    import torch
+    from paper_1512_08401_b200 import synthetic as S
+    from paper_1512_08401_b200 import waveblur as W
+    from paper_1512_08401_b200.sharded import LocalExchange, ShardedDeblurrer, TorchExchange
+    size = args.size
+    dims = (size, size)
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(local_rank)
+    t_setup = time.perf_counter()
+    lad = W.SigmaLadder.from_npz(np.load(ROOT / "tests" / "golden" / "c3_ladder_1024.npz"))
+    if size != 1024:
+        lad = W.SigmaLadder(lad.sigmas, [W.rescale_generators(g, dims) for g in lad.levels])
+    op = W.theta_varying(lad, 2.5, 7.5)
+    ctx = W.Context(local_rank)
+    basis = W.make_basis(W.FilterFamily.Daubechies, 4, dims, 4)
+    clean = S.synthetic_scene(dims)
+    x = W.analyze(clean, basis, ctx).values
+    u0 = S.add_noise(W.synthesize(W.spmv(op, x, ctx), basis, ctx), 5e-3, 2024)
+    P = W.spai(op, ctx)
+    w = W.scale_weights(basis.layout)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        ex = TorchExchange(torch, dist, stream)
+        ranks = [rank]
+    else:
+        ex, ranks = LocalExchange(), [0]
+    sh = ShardedDeblurrer(torch, ctx, op, basis, P, w, 1e-4, ITERS, world, ranks, ex)
+    with torch.cuda.stream(stream):
+        u0_dev = torch.from_numpy(u0.ravel().copy()).to(dev)
+        out = torch.empty_like(u0_dev)
+    setup_s = time.perf_counter() - t_setup
+    for _ in range(max(1, args.warmup)):
+        sh.deblur_dev(u0_dev.data_ptr(), out.data_ptr())
+    ctx.synchronize()
+    steps = max(1, min(args.steps, 5))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        a.record(stream)
+    for _ in range(steps):
+        sh.deblur_dev(u0_dev.data_ptr(), out.data_ptr())
+    with torch.cuda.stream(stream):
+        b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    restored = out.cpu().numpy().reshape(dims)
+    return {"metric": f"ms per {size}x{size} spatially varying deblur (C4, row-sharded)", "value": round(ms, 3),
+            "unit": "ms", "n_gpus": world, "steps": steps, "higher_is_better": False, "scaling": "strong",
+            "impl": "ours", "config": {"workload": f"C4: {size}^2 varying Gaussian 2.5->7.5 px, db4 J=4, K~3.4N, "
+                                                   f"SPAI, 100 FISTA iters incl. tau", "nnz": int(op.nnz()),
+                                       "parallelism": f"Theta row-sharded x{world}, NCCL all-gather of y/res"},
+            "tau_iters": sh.tau_iters, "setup_s": round(setup_s, 1),
+            "psnr_observed_db": round(S.psnr(u0, clean), 3), "psnr_restored_db": round(S.psnr(restored, clean), 3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,6 +394,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3/C5/cached-tau side measurements")
+    ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
+                    help="c4: one 4096^2 spatially varying deblur row-sharded over the --gpus ranks")
+    ap.add_argument("--size", type=int, default=4096, help="image side for --workload c4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -357,6 +425,14 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.workload == "c4":
+        line = run_c4(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     result = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline:

@@ -537,6 +537,44 @@ class SigmaLadder:
         return SigmaLadder(sig, lv)
 
 
+def rescale_generators(gl: GeneratorList, new_dims) -> GeneratorList:
+    """Carry a thresholded stationary operator to a larger grid (BASELINE config C4: the
+    4096^2 operators are derived from the reference's 1024^2 ones). A generator entry is a
+    circular offset on its band grid: offsets in the upper half are negative and keep their
+    distance to the end of the grid; multiplicities scale with the band size (a partially
+    walked group keeps its fraction). At K = 3N the reference's kept generator sets at 256^2
+    and 1024^2 agree up to near-tie order (tests/test_varying.py)."""
+    old = make_layout(gl.dims, gl.J)
+    new = make_layout(new_dims, gl.J)
+    nb = len(old.bands)
+    gi = np.empty_like(gl.gen_index)
+    cnt = np.empty_like(gl.counts)
+    for k in range(gl.blocks.size):
+        b = int(gl.blocks[k])
+        bi_o, bo_o = old.bands[b % nb], old.bands[b // nb]
+        bi_n, bo_n = new.bands[b % nb], new.bands[b // nb]
+        in_finer = bi_o.level <= bo_o.level
+        gs_o = bi_o.shape if in_finer else bo_o.shape
+        gs_n = bi_n.shape if in_finer else bo_n.shape
+        small_o = bo_o if in_finer else bi_o
+        small_n = bo_n if in_finer else bi_n
+        rem = int(gl.gen_index[k])
+        v = []
+        for s in reversed(gs_o):
+            v.append(rem % s)
+            rem //= s
+        v = v[::-1]
+        v2 = [vk if vk < so // 2 else vk + (sn - so) for vk, so, sn in zip(v, gs_o, gs_n)]
+        flat = 0
+        for vk, sn in zip(v2, gs_n):
+            flat = flat * sn + vk
+        gi[k] = flat
+        c = int(gl.counts[k])
+        cnt[k] = small_n.count() if c == small_o.count() else int(round(c * small_n.count() / small_o.count()))
+    return GeneratorList(tuple(int(d) for d in new_dims), gl.J, gl.family, gl.order, gl.blocks.copy(), gi, cnt,
+                         gl.values.copy())
+
+
 def json_dims(z):
     import json
     return json.loads(bytes(z["meta_json"]).decode())["dims"]

@@ -91,3 +91,18 @@ def test_c3_deblur_matches_oracle(size, iters):
     err = np.linalg.norm(u.ravel() - ur) / np.linalg.norm(ur)
     assert err <= 1e-5, err
     assert S.psnr(np.clip(u, 0, 1), clean) > S.psnr(u0, clean)  # it deblurs
+
+
+def test_rescaled_generators_reproduce_the_reference_at_1024():
+    """C4 derives 4096^2 operators by rescaling; check the rule where the reference itself is
+    available: the 256^2 lists rescaled to 1024^2 give the reference's 1024^2 operator (same
+    index set; values equal to ~1e-13, the periodisation difference of the two grids)."""
+    z256, z1024 = np.load(GOLDEN / "c1_db4_256.npz"), np.load(GOLDEN / "c2_db4_1024.npz")
+    mk = lambda z, d: W.GeneratorList(d, 4, W.FilterFamily.Daubechies, 4, z["gen_block"].astype(np.uint32),
+                                      z["gen_index"].astype(np.uint32), z["gen_count"].astype(np.uint64),
+                                      z["gen_value"])
+    a = W.theta_from_generators(W.rescale_generators(mk(z256, (256, 256)), (1024, 1024)))
+    b = W.theta_from_generators(mk(z1024, (1024, 1024)))
+    assert np.array_equal(a.row_offsets, b.row_offsets)
+    assert np.array_equal(a.col_indices, b.col_indices)
+    assert np.max(np.abs(a.values - b.values) / np.abs(b.values)) < 1e-12
