@@ -114,8 +114,18 @@ struct wbx_sell {
     wbx::DevBuf<uint4> rec;
 };
 
+// A compacted operator side on the host: rows in the solver's sorted order, columns as
+// positions in the compacted space of the vector they multiply.
+struct HostCompact {
+    std::vector<uint64_t> ptr;
+    std::vector<uint32_t> col;
+    std::vector<double> val;
+    uint64_t rows() const { return ptr.empty() ? 0 : ptr.size() - 1; }
+};
+
 struct wbx_op {
     wbx_ctx* ctx = nullptr;
+    HostCompact hA, hT;           // host copies of the two compacted sides
     uint64_t n = 0, nnz = 0;
     uint64_t nR = 0, nC = 0;      // nonempty rows / nonempty columns
     wbx_sell A;                   // Theta   : rows = R (sorted), cols -> C positions
@@ -163,6 +173,18 @@ void build_op(wbx_op* op, uint64_t n, const uint64_t* rowptr, const uint32_t* co
 void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint64_t)>& len,
                 const std::function<void(uint64_t, uint64_t, uint32_t&, double&)>& get, cudaStream_t s,
                 uint64_t& bytes);
+
+// winlayout.cu: per-CTA window layout of one operator side (win.cuh)
+struct WinSide {
+    uint32_t G = 0, max_u = 0, max_rows = 0;
+    DevBuf<uint32_t> u_off, u_idx, s_off, s_meta, r_off;
+    DevBuf<uint64_t> s_rec;
+    DevBuf<uint4> rec;
+    uint64_t bytes = 0;
+};
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st);
+struct WinView;
+WinView view_of(const WinSide& w);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

@@ -302,6 +302,18 @@ void build_op(wbx_op* op, uint64_t n, const uint64_t* rowptr, const uint32_t* co
         }
     } tr{toff.data(), trow.data(), tval.data(), &C, &rpos};
 
+    // compacted host forms (rows in sorted order, columns as positions) for the per-block
+    // window layouts built at solver setup (winlayout.cu)
+    auto compact = [](HostCompact& hc, uint64_t nrows, auto& range) {
+        hc.ptr.assign(nrows + 1, 0);
+        for (uint64_t i = 0; i < nrows; ++i) hc.ptr[i + 1] = hc.ptr[i] + range.len(i);
+        hc.col.resize(hc.ptr[nrows]);
+        hc.val.resize(hc.ptr[nrows]);
+        for (uint64_t i = 0; i < nrows; ++i)
+            for (uint64_t j = 0; j < range.len(i); ++j) range.get(i, j, hc.col[hc.ptr[i] + j], hc.val[hc.ptr[i] + j]);
+    };
+    compact(op->hA, R.size(), ar);
+    compact(op->hT, C.size(), tr);
     HostSell ha = make_sell(R.size(), ar);
     HostSell ht = make_sell(C.size(), tr);
     cudaStream_t s = op->ctx->stream;

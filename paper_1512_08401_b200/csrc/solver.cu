@@ -36,6 +36,7 @@
 #include "internal.hpp"
 #include "sell.cuh"
 #include "stream.cuh"
+#include "win.cuh"
 
 extern "C" void wbx_set_last_error(const char* msg);
 
@@ -95,6 +96,9 @@ struct SolveArgs {
     const float* beta32;
     double lambda, tau_given, step_safety, ref_energy, rel_tol;
     int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline, nslots;
+    // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
+    WinView wA, wT;
+    uint32_t win_max_slices;
     // T-typed state
     void* yC;
     void* xpC;
@@ -899,6 +903,273 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
     for (uint64_t c = gthread; c < a.nC; c += nthreads) a.x_full[a.C_glob[c]] = static_cast<double>(xpC[c]);
 }
 
+// ---------------------------------------------------------------- window engine (win.cuh)
+// Shared memory of a CTA: [uA: maxUA u32][uT: maxUT u32][slice table A][slice table T]
+// [window: maxU x WIN]. The index lists and slice tables are loaded once per solve.
+// Shared memory of a CTA: [uA][uT][slice table A][slice table T][own A][own T][window].
+// "own" holds the per-row state of the CTA's own contiguous row range (e.g. y, x_prev, tau/p,
+// threshold of its coordinates): only this CTA updates those rows, so the state lives on chip
+// for the whole solve and the slice chain carries no dependent global load.
+__host__ __device__ constexpr uint32_t win_align16(uint32_t b) { return (b + 15u) & ~15u; }
+
+struct WinSmem {
+    uint32_t* uA;
+    uint32_t* uT;
+    uint2* sA;  // {rec offset (uint4 units), meta}
+    uint2* sT;
+    void* ownA;
+    void* ownT;
+    void* win;
+    uint32_t nuA, nuT, nsA, nsT;
+    uint32_t rA0, rT0, nrA, nrT;  // own row ranges
+};
+
+template <uint32_t OWN_A, uint32_t OWN_T>
+__host__ __device__ inline uint32_t win_smem_head(uint32_t maxuA, uint32_t maxuT, uint32_t max_slices,
+                                                  uint32_t maxrA, uint32_t maxrT) {
+    return win_align16(maxuA * 4u) + win_align16(maxuT * 4u) + 2u * max_slices * 8u +
+           win_align16(maxrA * OWN_A) + win_align16(maxrT * OWN_T);
+}
+
+template <uint32_t OWN_A, uint32_t OWN_T>
+__device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const SolveArgs& a) {
+    WinSmem w;
+    const uint32_t b = blockIdx.x;
+    w.nuA = a.wA.u_off[b + 1] - a.wA.u_off[b];
+    w.nuT = a.wT.u_off[b + 1] - a.wT.u_off[b];
+    w.nsA = a.wA.s_off[b + 1] - a.wA.s_off[b];
+    w.nsT = a.wT.s_off[b + 1] - a.wT.s_off[b];
+    w.rA0 = a.wA.r_off[b];
+    w.rT0 = a.wT.r_off[b];
+    w.nrA = a.wA.r_off[b + 1] - w.rA0;
+    w.nrT = a.wT.r_off[b + 1] - w.rT0;
+    unsigned char* p = base;
+    w.uA = reinterpret_cast<uint32_t*>(p);
+    p += win_align16(a.wA.max_u * 4u);
+    w.uT = reinterpret_cast<uint32_t*>(p);
+    p += win_align16(a.wT.max_u * 4u);
+    w.sA = reinterpret_cast<uint2*>(p);
+    p += a.win_max_slices * 8u;
+    w.sT = reinterpret_cast<uint2*>(p);
+    p += a.win_max_slices * 8u;
+    w.ownA = p;
+    p += win_align16(a.wA.max_rows * OWN_A);
+    w.ownT = p;
+    p += win_align16(a.wT.max_rows * OWN_T);
+    w.win = p;
+    for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nsA; i += kBlock) {
+        const uint32_t s = a.wA.s_off[b] + i;
+        w.sA[i] = make_uint2(static_cast<uint32_t>(a.wA.s_rec[s]), a.wA.s_meta[s]);
+    }
+    for (uint32_t i = threadIdx.x; i < w.nsT; i += kBlock) {
+        const uint32_t s = a.wT.s_off[b] + i;
+        w.sT[i] = make_uint2(static_cast<uint32_t>(a.wT.s_rec[s]), a.wT.s_meta[s]);
+    }
+    __syncthreads();
+    return w;
+}
+
+// Slice data of one lane in registers: info word + up to 4 quads of values and columns.
+struct WinSlice {
+    uint32_t info, meta;
+    uint4 v[4];
+    uint2 c[4];
+};
+
+__device__ __forceinline__ void win_load(const uint4* rec_base, uint2 sm, int lane, uint64_t pol, WinSlice& d) {
+    const uint4* rec = rec_base + sm.x;
+    const int nq = static_cast<int>(sm.y & 0xffu);
+    d.meta = sm.y;
+    d.info = ld_stream(reinterpret_cast<const uint32_t*>(rec) + lane, pol);
+    const uint2* cols = reinterpret_cast<const uint2*>(rec + 8 + nq * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        d.v[q] = q < nq ? ld_stream(rec + 8 + q * 32 + lane, pol) : make_uint4(0, 0, 0, 0);
+        d.c[q] = q < nq ? __ldg(cols + q * 32 + lane) : make_uint2(0, 0);
+    }
+}
+
+// One phase on the window engine: fill the CTA's window from x (one parallel round trip),
+// then every warp runs its slices (round robin) with a one-slice load lookahead; the
+// vector operand comes from shared memory.
+template <typename ACC, typename WIN, typename X, typename Pre, typename Post>
+__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint2* stab,
+                                          uint32_t ns, const X* __restrict__ x, WIN* win, Pre pre, Post post) {
+    // all loads of a batch issued before any store: one round trip per 16 entries per thread
+    for (uint32_t base = threadIdx.x; base < nu; base += 16u * kBlock) {
+        WIN v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t i = base + j * kBlock;
+            v[j] = i < nu ? static_cast<WIN>(x[uidx[i]]) : WIN(0);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t i = base + j * kBlock;
+            if (i < nu) win[i] = v[j];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint64_t pol = l2_keep_policy();
+    WinSlice cur, nxt;
+    if (wib < ns) win_load(W.rec, stab[wib], lane, pol, nxt);
+    for (uint32_t s = wib; s < ns; s += kWarpsPerBlock) {
+        cur = nxt;
+        if (s + kWarpsPerBlock < ns) win_load(W.rec, stab[s + kWarpsPerBlock], lane, pol, nxt);
+        const uint32_t info = cur.info;
+        const uint32_t row = info == kNoRow ? kNoRow : (info & kRowMask);
+        const auto pv = pre(row);
+        const int nq = static_cast<int>(cur.meta & 0xffu);
+        ACC acc = ACC(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q < nq) {
+                const float v0 = __uint_as_float(cur.v[q].x), v1 = __uint_as_float(cur.v[q].y);
+                const float v2 = __uint_as_float(cur.v[q].z), v3 = __uint_as_float(cur.v[q].w);
+                const WIN g0 = win[cur.c[q].x & 0xffffu], g1 = win[cur.c[q].x >> 16];
+                const WIN g2 = win[cur.c[q].y & 0xffffu], g3 = win[cur.c[q].y >> 16];
+                acc = fma(static_cast<ACC>(v0), static_cast<ACC>(g0), acc);
+                acc = fma(static_cast<ACC>(v1), static_cast<ACC>(g1), acc);
+                acc = fma(static_cast<ACC>(v2), static_cast<ACC>(g2), acc);
+                acc = fma(static_cast<ACC>(v3), static_cast<ACC>(g3), acc);
+            }
+        }
+        const uint32_t r = combine_info(info, cur.meta, acc);
+        if (r != kNoRow) post(r, acc, pv);
+    }
+    __syncthreads();  // the window is refilled by the next phase
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    float* yC = static_cast<float*>(a.yC);
+    float* xpC = static_cast<float*>(a.xpC);
+    float* res = static_cast<float*>(a.res);
+    float* x0R = static_cast<float*>(a.x0R);
+    float* tpC = static_cast<float*>(a.tpC);
+    float* thrC = static_cast<float*>(a.thrC);
+    const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
+    const WinSmem ws = win_smem_init<4, 16>(dsmem, a);
+    float* win = static_cast<float*>(ws.win);
+    float* x0s = static_cast<float*>(ws.ownA);   // x0 of the CTA's Theta rows
+    float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
+    (void)xpC;
+    (void)tpC;
+    (void)thrC;
+    (void)x0R;
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) {
+        const uint32_t c = ws.rT0 + i;
+        const float v = static_cast<float>(a.x0_full[a.C_glob[c]]);
+        yC[c] = v;
+        cs[i] = make_float4(v, v, static_cast<float>(tau / a.pC[c]),
+                            static_cast<float>(thr_exact(tau, a.lambda, a.wC[c], a.pC[c])));
+    }
+    for (uint32_t i = threadIdx.x; i < ws.nrA; i += kBlock)
+        x0s[i] = static_cast<float>(a.x0_full[a.R_glob[ws.rA0 + i]]);
+    if (a.decoupled_inline) decoupled_pass<float>(a, tau, a.max_iters, 0, gthread, nthreads, nullptr, nullptr, 0);
+    grid_sync(a.sync, epoch, smem);
+    for (int k = 1; k <= a.max_iters; ++k) {
+        win_phase<float, float>(
+            a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, yC, win, [](uint32_t) { return 0; },
+            [&](uint32_t r, float acc, int) { res[r] = acc - x0s[r - ws.rA0]; });
+        grid_sync(a.sync, epoch, smem);
+        const float beta = a.beta32[k - 1];
+        win_phase<float, float>(
+            a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, res, win, [](uint32_t) { return 0; },
+            [&](uint32_t c, float g, int) {
+                float4& q = cs[c - ws.rT0];
+                const float z0 = fmaf(-q.z, g, q.x);
+                const float xn = Prec<float>::prox(z0, q.w);
+                const float yn = fmaf(beta, xn - q.y, xn);
+                q.x = yn;
+                q.y = xn;
+                yC[c] = yn;
+            });
+        grid_sync(a.sync, epoch, smem);
+    }
+    if (gthread == 0) a.out[OUT_ITERS_USED] = a.max_iters;
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
+}
+
+// estimate_step on the window engine (fp64 window and accumulation, fp32 operator values)
+__global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    const WinSmem ws = win_smem_init<0, 16>(dsmem, a);
+    double* win = static_cast<double*>(ws.win);
+    double2* cs = static_cast<double2*>(ws.ownT);  // {P^-1/2, w} of the CTA's coordinates
+    double s2[1] = {0.0};
+    for (uint64_t i = gthread; i < a.n; i += nthreads) {
+        const double v = rng_normal(0x5eedull, i);
+        s2[0] += v * v;
+    }
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) {
+        const uint32_t c = ws.rT0 + i;
+        const double v = rng_normal(0x5eedull, a.C_glob[c]);
+        const double isp = a.ispC[c];
+        cs[i] = make_double2(isp, v);
+        a.uC[c] = isp * v;
+    }
+    grid_sync_reduce<1>(a.sync, epoch, s2, smem);
+    double nw_prev = sqrt(s2[0]);
+    double lambda_prev = 0.0;
+    int it = 0;
+    bool zero_op = false;
+    for (; it < 200; ++it) {
+        const double inv = nw_prev;
+        win_phase<double, double>(
+            a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, a.uC, win, [](uint32_t) { return 0; },
+            [&](uint32_t r, double t, int) { a.t64[r] = t / inv; });
+        grid_sync(a.sync, epoch, smem);
+        double acc[2] = {0.0, 0.0};
+        win_phase<double, double>(
+            a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, a.t64, win, [](uint32_t) { return 0; },
+            [&](uint32_t c, double g, int) {
+                double2& q = cs[c - ws.rT0];
+                const double w = g * q.x;
+                const double v = q.y / inv;
+                acc[0] += v * w;
+                acc[1] += w * w;
+                q.y = w;
+                a.uC[c] = q.x * w;
+            });
+        grid_sync_reduce<2>(a.sync, epoch, acc, smem);
+        const double lambda = acc[0];
+        const double nw = sqrt(acc[1]);
+        if (nw == 0.0) {
+            zero_op = true;
+            ++it;
+            break;
+        }
+        if (it > 0 && fabs(lambda - lambda_prev) <= 1e-6 * fabs(lambda)) {
+            lambda_prev = lambda;
+            ++it;
+            break;
+        }
+        lambda_prev = lambda;
+        nw_prev = nw;
+    }
+    if (gthread == 0) {
+        a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
+        a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
+        a.out[OUT_LAMBDA_MAX] = lambda_prev;
+    }
+}
+
 // ---------------------------------------------------------------- batched FISTA (C5)
 // B independent images sharing Theta_K, P, w, lambda and tau (BASELINE config C5): the
 // operator stream is read once per B right-hand sides (SpMM). Vectors are interleaved
@@ -1124,6 +1395,12 @@ struct wbx_solver {
     wbx::DevBuf<double> u0, x0full, xfull, uout;
     int grid_fista = 0, grid_tau = 0;
     int nslots = 3;  // TMA slots in flight per warp
+    // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
+    bool win = false;
+    int grid_win = 0;
+    unsigned win_smem_fista = 0, win_smem_tau = 0;
+    uint32_t win_max_slices = 0;
+    wbx::WinSide wA, wT;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     uint64_t last_launches = 0;
@@ -1215,6 +1492,11 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.sync.trace = s->trace.p;
     a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
     a.nslots = s->nslots;
+    if (s->win) {
+        a.wA = view_of(s->wA);
+        a.wT = view_of(s->wT);
+        a.win_max_slices = s->win_max_slices;
+    }
     {
         const char* e = std::getenv("WBX_BARRIER");
         a.sync.mode = (e && std::string(e) == "allpoll") ? 1 : 0;
@@ -1234,12 +1516,25 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     wbx_ctx* ctx = s->ctx;
     WBX_CUDA(cudaMemsetAsync(s->out.p, 0, s->out.bytes(), st));
     // step: estimate_step on the device, or the given one
+    const bool win = s->win && !a.track && s->batch == 1;
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
+    } else if (s->win) {
+        void* params[] = {&a};
+        WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tau_win_kernel), dim3(s->grid_win),
+                                             dim3(kBlock), params, s->win_smem_tau, st));
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
+    if (win) {
+        void* params[] = {&a};
+        WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fista_win_kernel<float>), dim3(s->grid_win),
+                                             dim3(kBlock), params, s->win_smem_fista, st));
+        count_launch(ctx);
+        WBX_CUDA(cudaGetLastError());
+        return;
+    }
     if (s->batch > 1) {  // C5: B images per solve (fp32, no tracking; checked at creation)
         const void* k = s->batch == 4 ? reinterpret_cast<const void*>(fista_batch_kernel<4>)
                                       : reinterpret_cast<const void*>(fista_batch_kernel<8>);
@@ -1292,6 +1587,41 @@ void alloc_state(wbx_solver* s) {
         s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<4>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     else if (s->batch == 8)
         s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<8>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
+    // window engine: fp32, single image; try 2 then 1 CTA per SM; fall back to the streamed
+    // engine if a CTA's window does not fit (WBX_ENGINE=stream forces the fallback)
+    const char* eng = std::getenv("WBX_ENGINE");
+    if (sizeof(T) == 4 && s->batch == 1 && !(eng && std::string(eng) == "stream")) {
+        for (int bps = 2; bps >= 1 && !s->win; --bps) {
+            const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
+            try {
+                build_win(s->wA, s->op->hA, G, s->ctx->stream);
+                build_win(s->wT, s->op->hT, G, s->ctx->stream);
+            } catch (const Error&) {
+                continue;  // a window exceeded 16-bit local indices
+            }
+            std::vector<uint32_t> sa(G + 1), stt(G + 1);
+            WBX_CUDA(cudaMemcpy(sa.data(), s->wA.s_off.p, (G + 1) * 4, cudaMemcpyDeviceToHost));
+            WBX_CUDA(cudaMemcpy(stt.data(), s->wT.s_off.p, (G + 1) * 4, cudaMemcpyDeviceToHost));
+            uint32_t ms = 1;
+            for (uint32_t b = 0; b < G; ++b) ms = std::max({ms, sa[b + 1] - sa[b], stt[b + 1] - stt[b]});
+            s->win_max_slices = ms;
+            const unsigned mu = std::max(s->wA.max_u, s->wT.max_u);
+            s->win_smem_fista = win_smem_head<4, 16>(s->wA.max_u, s->wT.max_u, ms, s->wA.max_rows, s->wT.max_rows) + mu * 4u;
+            s->win_smem_tau = win_smem_head<0, 16>(s->wA.max_u, s->wT.max_u, ms, s->wA.max_rows, s->wT.max_rows) + mu * 8u;
+            const unsigned limit = bps == 2 ? 110u * 1024u : 220u * 1024u;
+            if (s->win_smem_tau > limit) continue;
+            WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fista_win_kernel<float>),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s->win_smem_fista)));
+            WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(tau_win_kernel),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s->win_smem_tau)));
+            int pf = 0, pt = 0;
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, fista_win_kernel<float>, kBlock, s->win_smem_fista));
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, tau_win_kernel, kBlock, s->win_smem_tau));
+            if (pf < bps || pt < bps) continue;
+            s->grid_win = static_cast<int>(G);
+            s->win = true;
+        }
+    }
 }
 
 }  // namespace
