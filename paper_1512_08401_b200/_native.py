@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libwbx.so"
+# WBX_LIB selects a diagnostics build (e.g. lib/libwbx_prof.so from `make prof`)
+LIB_PATH = Path(os.environ.get("WBX_LIB") or Path(__file__).resolve().parent / "lib" / "libwbx.so")
 
 WBX_OK = 0
 WBX_FP32 = 32

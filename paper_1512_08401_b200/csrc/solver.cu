@@ -74,7 +74,7 @@ struct Sync {
     double* red;       // [kRedSlots] grid totals of the last reduction
     unsigned long long* trace;  // optional [trace_cap][grid][2] globaltimer stamps
     unsigned trace_cap;
-    int mode;  // 0: master block releases (default), 1: every block polls all arrivals
+    int mode;  // 0: master block releases, 1: every block polls all arrivals, 2: counter (default)
 };
 
 struct SolveArgs {
@@ -151,6 +151,7 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     return v;
 }
 
+
 // Master warp: poll all arrival words, every lane its strided subset with independent
 // loads per round (one memory round trip per round, not one per block), then acquire.
 __device__ __forceinline__ void wait_arrivals(const Sync& s, unsigned epoch, unsigned G) {
@@ -185,6 +186,19 @@ struct Epoch {
     unsigned cur, start;
 };
 
+// Counter barrier (mode 2): one arrival counter, zeroed by the host before each cooperative
+// launch; barrier k of the launch completes when the counter reaches k * G. Arrival is a
+// fire-and-forget reduction, and every block polls the one word directly (no master hop).
+constexpr unsigned kCounterWord = 32;  // Sync::gen[kCounterWord], its own 128-B line
+
+__device__ __forceinline__ void counter_arrive_wait(const Sync& s, const Epoch& e) {
+    unsigned* cnt = s.gen + kCounterWord;
+    asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const unsigned target = (e.cur - e.start) * gridDim.x;
+    while (static_cast<int>(ld_acquire(cnt) - target) < 0) {
+    }
+}
+
 // Optional phase trace (WBX_TRACE_FILE): per barrier and block, the time the block
 // arrived and the time it saw the release.
 __device__ __forceinline__ void trace_point(const Sync& s, const Epoch& e, int which) {
@@ -212,6 +226,26 @@ __device__ __forceinline__ void grid_sync_reduce(const Sync& s, Epoch& epoch, do
         if (threadIdx.x == 0) part[k * G + blockIdx.x] = b;
     }
     trace_point(s, epoch, 0);
+    if (s.mode == 2) {  // counter barrier, then every block reduces the partials itself
+        __syncthreads();
+        if (threadIdx.x == 0) counter_arrive_wait(s, epoch);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                double t = 0.0;
+                for (unsigned i = threadIdx.x; i < G; i += 32) t += part[k * G + i];
+                t = warp_sum(t);
+                if (threadIdx.x == 0) smem[k] = t;
+            }
+        }
+        trace_point(s, epoch, 1);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = smem[k];
+        __syncthreads();
+        return;
+    }
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         st_release(s.arrive + blockIdx.x, epoch.cur);
@@ -259,6 +293,12 @@ __device__ __forceinline__ void grid_sync(const Sync& s, Epoch& epoch, double* s
     ++epoch.cur;
     __syncthreads();
     trace_point(s, epoch, 0);
+    if (s.mode == 2) {
+        if (threadIdx.x == 0) counter_arrive_wait(s, epoch);
+        trace_point(s, epoch, 1);
+        __syncthreads();
+        return;
+    }
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         st_release(s.arrive + blockIdx.x, epoch.cur);
@@ -515,8 +555,12 @@ __device__ unsigned long long g_prof[6];
 extern "C" int wbx_diag_slice_profile(double* out4) {
     unsigned long long h[6];
     if (cudaMemcpyFromSymbol(h, wbx::g_prof, sizeof h) != cudaSuccess) return WBX_CUDA_ERROR;
-    for (int i = 0; i < 5; ++i) out4[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
-    out4[5] = static_cast<double>(h[5]);
+    if (WBX_PROFILE == 3) {  // window engine: totals, slot 4 = max cycles of one warp's slice loop
+        for (int i = 0; i < 6; ++i) out4[i] = static_cast<double>(h[i]);
+    } else {
+        for (int i = 0; i < 5; ++i) out4[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
+        out4[5] = static_cast<double>(h[5]);
+    }
     const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(wbx::g_prof, z, sizeof z);
     return WBX_OK;
@@ -994,29 +1038,40 @@ __device__ __forceinline__ void win_load(const uint4* rec_base, uint2 sm, int la
 // One phase on the window engine: fill the CTA's window from x (one parallel round trip),
 // then every warp runs its slices (round robin) with a one-slice load lookahead; the
 // vector operand comes from shared memory.
-template <typename ACC, typename WIN, typename X, typename Pre, typename Post>
-__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint2* stab,
-                                          uint32_t ns, const X* __restrict__ x, WIN* win, Pre pre, Post post) {
-    // all loads of a batch issued before any store: one round trip per 16 entries per thread
-    for (uint32_t base = threadIdx.x; base < nu; base += 16u * kBlock) {
-        WIN v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t i = base + j * kBlock;
-            v[j] = i < nu ? static_cast<WIN>(x[uidx[i]]) : WIN(0);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t i = base + j * kBlock;
-            if (i < nu) win[i] = v[j];
+// WBX_PROFILE=3: per-warp cycle accounting of the window engine
+// [fill, slice loop, slices, barrier, max slice loop] (wbx_diag_slice_profile)
+struct WinProf {
+    unsigned long long c[5] = {0, 0, 0, 0, 0};
+    __device__ __forceinline__ void flush() {
+        if (WBX_PROFILE == 3 && (threadIdx.x & 31) == 0) {
+            for (int i = 0; i < 4; ++i) atomicAdd(&g_prof[i], c[i]);
+            atomicMax(&g_prof[4], c[4]);
         }
     }
-    __syncthreads();
+};
+
+template <typename ACC, typename WIN, typename X, typename Pre, typename Post>
+__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint2* stab,
+                                          uint32_t ns, const X* __restrict__ x, WIN* win, Pre pre, Post post,
+                                          WinProf& pf) {
+    static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
+    const long long t0 = WBX_PROFILE == 3 ? clock64() : 0;
     const int lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint64_t pol = l2_keep_policy();
     WinSlice cur, nxt;
+    // the first slice does not depend on x: its load overlaps the window fill
     if (wib < ns) win_load(W.rec, stab[wib], lane, pol, nxt);
+    // window fill with asynchronous global->shared copies: every entry in flight at once,
+    // no registers held (L1 lines are invalidated by the grid barrier's acquire)
+    for (uint32_t i = threadIdx.x; i < nu; i += kBlock) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const long long t1 = WBX_PROFILE == 3 ? clock64() : 0;
     for (uint32_t s = wib; s < ns; s += kWarpsPerBlock) {
         cur = nxt;
         if (s + kWarpsPerBlock < ns) win_load(W.rec, stab[s + kWarpsPerBlock], lane, pol, nxt);
@@ -1040,6 +1095,13 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
         }
         const uint32_t r = combine_info(info, cur.meta, acc);
         if (r != kNoRow) post(r, acc, pv);
+    }
+    if (WBX_PROFILE == 3) {
+        const long long t2 = clock64();
+        pf.c[0] += t1 - t0;
+        pf.c[1] += t2 - t1;
+        pf.c[2] += ns > wib ? (ns - wib + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
+        pf.c[4] = max(pf.c[4], static_cast<unsigned long long>(t2 - t1));
     }
     __syncthreads();  // the window is refilled by the next phase
 }
@@ -1078,11 +1140,17 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
         x0s[i] = static_cast<float>(a.x0_full[a.R_glob[ws.rA0 + i]]);
     if (a.decoupled_inline) decoupled_pass<float>(a, tau, a.max_iters, 0, gthread, nthreads, nullptr, nullptr, 0);
     grid_sync(a.sync, epoch, smem);
+    WinProf pf;
+    auto sync = [&]() {
+        const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
+        grid_sync(a.sync, epoch, smem);
+        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
+    };
     for (int k = 1; k <= a.max_iters; ++k) {
         win_phase<float, float>(
             a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, yC, win, [](uint32_t) { return 0; },
-            [&](uint32_t r, float acc, int) { res[r] = acc - x0s[r - ws.rA0]; });
-        grid_sync(a.sync, epoch, smem);
+            [&](uint32_t r, float acc, int) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
+        sync();
         const float beta = a.beta32[k - 1];
         win_phase<float, float>(
             a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, res, win, [](uint32_t) { return 0; },
@@ -1094,9 +1162,11 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
                 q.x = yn;
                 q.y = xn;
                 yC[c] = yn;
-            });
-        grid_sync(a.sync, epoch, smem);
+            },
+            pf);
+        sync();
     }
+    pf.flush();
     if (gthread == 0) a.out[OUT_ITERS_USED] = a.max_iters;
     for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
 }
@@ -1129,12 +1199,15 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     double lambda_prev = 0.0;
     int it = 0;
     bool zero_op = false;
+    WinProf pf;
     for (; it < 200; ++it) {
         const double inv = nw_prev;
         win_phase<double, double>(
             a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, a.uC, win, [](uint32_t) { return 0; },
-            [&](uint32_t r, double t, int) { a.t64[r] = t / inv; });
+            [&](uint32_t r, double t, int) { a.t64[r] = t / inv; }, pf);
+        const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
+        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
         double acc[2] = {0.0, 0.0};
         win_phase<double, double>(
             a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, a.t64, win, [](uint32_t) { return 0; },
@@ -1146,8 +1219,11 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
                 acc[1] += w * w;
                 q.y = w;
                 a.uC[c] = q.x * w;
-            });
+            },
+            pf);
+        const long long b1 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync_reduce<2>(a.sync, epoch, acc, smem);
+        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b1;
         const double lambda = acc[0];
         const double nw = sqrt(acc[1]);
         if (nw == 0.0) {
@@ -1163,6 +1239,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
         lambda_prev = lambda;
         nw_prev = nw;
     }
+    pf.flush();
     if (gthread == 0) {
         a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
         a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
@@ -1499,15 +1576,21 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
-        a.sync.mode = (e && std::string(e) == "allpoll") ? 1 : 0;
+        a.sync.mode = !e ? 2 : std::string(e) == "allpoll" ? 1 : std::string(e) == "master" ? 0 : 2;
     }
     return a;
 }
 
+void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st) {
+    if (a.sync.mode == 2)  // the counter barrier counts from zero in every launch
+        WBX_CUDA(cudaMemsetAsync(a.sync.gen + kCounterWord, 0, sizeof(unsigned), st));
+    void* params[] = {&a};
+    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, smem, st));
+}
+
 template <typename T>
 void launch_coop(const void* kernel, int grid, SolveArgs& a, cudaStream_t st) {
-    void* params[] = {&a};
-    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, dyn_smem<T>(a.nslots), st));
+    launch_coop_smem(kernel, grid, dyn_smem<T>(a.nslots), a, st);
 }
 
 template <typename T>
@@ -1520,17 +1603,13 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
-        void* params[] = {&a};
-        WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tau_win_kernel), dim3(s->grid_win),
-                                             dim3(kBlock), params, s->win_smem_tau, st));
+        launch_coop_smem(reinterpret_cast<const void*>(tau_win_kernel), s->grid_win, s->win_smem_tau, a, st);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
     if (win) {
-        void* params[] = {&a};
-        WBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fista_win_kernel<float>), dim3(s->grid_win),
-                                             dim3(kBlock), params, s->win_smem_fista, st));
+        launch_coop_smem(reinterpret_cast<const void*>(fista_win_kernel<float>), s->grid_win, s->win_smem_fista, a, st);
         count_launch(ctx);
         WBX_CUDA(cudaGetLastError());
         return;
@@ -1620,6 +1699,13 @@ void alloc_state(wbx_solver* s) {
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
+            if (std::getenv("WBX_VERBOSE"))
+                std::fprintf(stderr,
+                             "wbx window engine: G=%u max_u A/T=%u/%u max_rows A/T=%u/%u max_slices=%u "
+                             "rec bytes A/T=%llu/%llu smem fista/tau=%u/%u\n",
+                             G, s->wA.max_u, s->wT.max_u, s->wA.max_rows, s->wT.max_rows, ms,
+                             static_cast<unsigned long long>(s->wA.rec.bytes()),
+                             static_cast<unsigned long long>(s->wT.rec.bytes()), s->win_smem_fista, s->win_smem_tau);
         }
     }
 }
@@ -1670,7 +1756,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     s->t64.alloc(op->nR ? op->nR : 1);
     s->out.alloc(OUT_COUNT);
     const uint64_t gmax = static_cast<uint64_t>(std::max(s->grid_fista, s->grid_tau));
-    s->gen.alloc(32);
+    s->gen.alloc(64);
     s->arrive.alloc(gmax);
     s->part.alloc(2 * kRedSlots * gmax);
     s->red.alloc(kRedSlots);
