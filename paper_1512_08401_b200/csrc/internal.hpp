@@ -176,10 +176,10 @@ void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint
 
 // winlayout.cu: per-CTA window layout of one operator side (win.cuh)
 struct WinSide {
-    uint32_t G = 0, max_u = 0, max_rows = 0;
-    DevBuf<uint32_t> u_off, u_idx, s_off, s_meta, r_off;
-    DevBuf<uint64_t> s_rec;
-    DevBuf<uint4> rec;
+    uint32_t G = 0, max_u = 0, max_rows = 0, max_slices = 0, max_dict = 0;
+    DevBuf<uint32_t> u_off, u_idx, s_off, r_off, d_off;
+    DevBuf<uint4> s_tab, rec;
+    DevBuf<float> d_val;
     uint64_t bytes = 0;
 };
 void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st);

@@ -98,7 +98,6 @@ struct SolveArgs {
     int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline, nslots;
     // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
     WinView wA, wT;
-    uint32_t win_max_slices;
     // T-typed state
     void* yC;
     void* xpC;
@@ -948,19 +947,23 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
 }
 
 // ---------------------------------------------------------------- window engine (win.cuh)
-// Shared memory of a CTA: [uA: maxUA u32][uT: maxUT u32][slice table A][slice table T]
-// [window: maxU x WIN]. The index lists and slice tables are loaded once per solve.
-// Shared memory of a CTA: [uA][uT][slice table A][slice table T][own A][own T][window].
-// "own" holds the per-row state of the CTA's own contiguous row range (e.g. y, x_prev, tau/p,
-// threshold of its coordinates): only this CTA updates those rows, so the state lives on chip
-// for the whole solve and the slice chain carries no dependent global load.
+// Shared memory of a CTA:
+//   [uA][uT]          window index lists of the two sides              } loaded once
+//   [sA][sT]          slice tables {record offset, meta, first row}    } per solve
+//   [dA][dT]          value dictionaries (dictionary format)           }
+//   [own A][own T]    per-row state of the CTA's own contiguous row ranges (e.g. y, x_prev,
+//                     tau/p, threshold of its coordinates): only this CTA updates those rows,
+//                     so the state lives on chip for the whole solve
+//   [window]          x[U_b] of the current phase
 __host__ __device__ constexpr uint32_t win_align16(uint32_t b) { return (b + 15u) & ~15u; }
 
 struct WinSmem {
     uint32_t* uA;
     uint32_t* uT;
-    uint2* sA;  // {rec offset (uint4 units), meta}
-    uint2* sT;
+    uint4* sA;
+    uint4* sT;
+    float* dA;
+    float* dT;
     void* ownA;
     void* ownT;
     void* win;
@@ -969,10 +972,10 @@ struct WinSmem {
 };
 
 template <uint32_t OWN_A, uint32_t OWN_T>
-__host__ __device__ inline uint32_t win_smem_head(uint32_t maxuA, uint32_t maxuT, uint32_t max_slices,
-                                                  uint32_t maxrA, uint32_t maxrT) {
-    return win_align16(maxuA * 4u) + win_align16(maxuT * 4u) + 2u * max_slices * 8u +
-           win_align16(maxrA * OWN_A) + win_align16(maxrT * OWN_T);
+__host__ __device__ inline uint32_t win_smem_head(const WinView& A, const WinView& T) {
+    return win_align16(A.max_u * 4u) + win_align16(T.max_u * 4u) + 16u * (A.max_slices + T.max_slices) +
+           win_align16(A.max_dict * 4u) + win_align16(T.max_dict * 4u) + win_align16(A.max_rows * OWN_A) +
+           win_align16(T.max_rows * OWN_T);
 }
 
 template <uint32_t OWN_A, uint32_t OWN_T>
@@ -988,56 +991,57 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     w.nrA = a.wA.r_off[b + 1] - w.rA0;
     w.nrT = a.wT.r_off[b + 1] - w.rT0;
     unsigned char* p = base;
-    w.uA = reinterpret_cast<uint32_t*>(p);
-    p += win_align16(a.wA.max_u * 4u);
-    w.uT = reinterpret_cast<uint32_t*>(p);
-    p += win_align16(a.wT.max_u * 4u);
-    w.sA = reinterpret_cast<uint2*>(p);
-    p += a.win_max_slices * 8u;
-    w.sT = reinterpret_cast<uint2*>(p);
-    p += a.win_max_slices * 8u;
-    w.ownA = p;
-    p += win_align16(a.wA.max_rows * OWN_A);
-    w.ownT = p;
-    p += win_align16(a.wT.max_rows * OWN_T);
+    auto carve = [&](uint32_t bytes) {
+        unsigned char* q = p;
+        p += bytes;
+        return q;
+    };
+    w.uA = reinterpret_cast<uint32_t*>(carve(win_align16(a.wA.max_u * 4u)));
+    w.uT = reinterpret_cast<uint32_t*>(carve(win_align16(a.wT.max_u * 4u)));
+    w.sA = reinterpret_cast<uint4*>(carve(16u * a.wA.max_slices));
+    w.sT = reinterpret_cast<uint4*>(carve(16u * a.wT.max_slices));
+    w.dA = reinterpret_cast<float*>(carve(win_align16(a.wA.max_dict * 4u)));
+    w.dT = reinterpret_cast<float*>(carve(win_align16(a.wT.max_dict * 4u)));
+    w.ownA = carve(win_align16(a.wA.max_rows * OWN_A));
+    w.ownT = carve(win_align16(a.wT.max_rows * OWN_T));
     w.win = p;
     for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
     for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nsA; i += kBlock) {
-        const uint32_t s = a.wA.s_off[b] + i;
-        w.sA[i] = make_uint2(static_cast<uint32_t>(a.wA.s_rec[s]), a.wA.s_meta[s]);
-    }
-    for (uint32_t i = threadIdx.x; i < w.nsT; i += kBlock) {
-        const uint32_t s = a.wT.s_off[b] + i;
-        w.sT[i] = make_uint2(static_cast<uint32_t>(a.wT.s_rec[s]), a.wT.s_meta[s]);
-    }
+    for (uint32_t i = threadIdx.x; i < w.nsA; i += kBlock) w.sA[i] = a.wA.s_tab[a.wA.s_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nsT; i += kBlock) w.sT[i] = a.wT.s_tab[a.wT.s_off[b] + i];
+    if (a.wA.max_dict)
+        for (uint32_t i = a.wA.d_off[b] + threadIdx.x; i < a.wA.d_off[b + 1]; i += kBlock)
+            w.dA[i - a.wA.d_off[b]] = a.wA.d_val[i];
+    if (a.wT.max_dict)
+        for (uint32_t i = a.wT.d_off[b] + threadIdx.x; i < a.wT.d_off[b + 1]; i += kBlock)
+            w.dT[i - a.wT.d_off[b]] = a.wT.d_val[i];
     __syncthreads();
     return w;
 }
 
-// Slice data of one lane in registers: info word + up to 4 quads of values and columns.
+// One lane's share of a slice record in registers: dictionary offset (dictionary format)
+// or values (full format), and up to 4 quads of 16-bit window columns.
+template <bool DICT>
 struct WinSlice {
-    uint32_t info, meta;
-    uint4 v[4];
+    uint32_t pb;
+    uint4 v[DICT ? 1 : 4];
     uint2 c[4];
 };
 
-__device__ __forceinline__ void win_load(const uint4* rec_base, uint2 sm, int lane, uint64_t pol, WinSlice& d) {
-    const uint4* rec = rec_base + sm.x;
-    const int nq = static_cast<int>(sm.y & 0xffu);
-    d.meta = sm.y;
-    d.info = ld_stream(reinterpret_cast<const uint32_t*>(rec) + lane, pol);
-    const uint2* cols = reinterpret_cast<const uint2*>(rec + 8 + nq * 32);
+template <bool DICT>
+__device__ __forceinline__ void win_load(const uint4* rec_base, const uint4& sl, int lane, uint64_t pol,
+                                         WinSlice<DICT>& d) {
+    const uint4* rec = rec_base + sl.x;
+    const int nq = static_cast<int>(sl.y & 0xffu);
+    const uint2* cols = reinterpret_cast<const uint2*>(rec + (DICT ? 4 : nq * 32));
+    if (DICT) d.pb = ld_stream(reinterpret_cast<const uint16_t*>(rec) + lane, pol);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        d.v[q] = q < nq ? ld_stream(rec + 8 + q * 32 + lane, pol) : make_uint4(0, 0, 0, 0);
-        d.c[q] = q < nq ? __ldg(cols + q * 32 + lane) : make_uint2(0, 0);
+        if (!DICT) d.v[q] = q < nq ? ld_stream(rec + q * 32 + lane, pol) : make_uint4(0, 0, 0, 0);
+        d.c[q] = q < nq ? ld_stream(cols + q * 32 + lane, pol) : make_uint2(0, 0);
     }
 }
 
-// One phase on the window engine: fill the CTA's window from x (one parallel round trip),
-// then every warp runs its slices (round robin) with a one-slice load lookahead; the
-// vector operand comes from shared memory.
 // WBX_PROFILE=3: per-warp cycle accounting of the window engine
 // [fill, slice loop, slices, barrier, max slice loop] (wbx_diag_slice_profile)
 struct WinProf {
@@ -1050,20 +1054,26 @@ struct WinProf {
     }
 };
 
-template <typename ACC, typename WIN, typename X, typename Pre, typename Post>
-__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint2* stab,
-                                          uint32_t ns, const X* __restrict__ x, WIN* win, Pre pre, Post post,
-                                          WinProf& pf) {
+// One phase on the window engine: fill the CTA's window from x (asynchronous copies, one
+// parallel round trip; the first slices' record loads are issued before it since they do
+// not depend on x), then every warp runs its slices (w, w+8, ...) with NB-1 slices of
+// record loads in flight; the vector operand and (dictionary format) the values come from
+// shared memory.
+template <typename ACC, typename WIN, bool DICT, int NB, typename X, typename Post>
+__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint4* stab,
+                                          uint32_t ns, const float* dict, const X* __restrict__ x, WIN* win,
+                                          Post post, WinProf& pf) {
     static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
+    static_assert(NB == 2 || NB == 3, "lookahead buffers");
     const long long t0 = WBX_PROFILE == 3 ? clock64() : 0;
     const int lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint64_t pol = l2_keep_policy();
-    WinSlice cur, nxt;
-    // the first slice does not depend on x: its load overlaps the window fill
-    if (wib < ns) win_load(W.rec, stab[wib], lane, pol, nxt);
-    // window fill with asynchronous global->shared copies: every entry in flight at once,
-    // no registers held (L1 lines are invalidated by the grid barrier's acquire)
+    WinSlice<DICT> b0, b1, b2;
+    if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
+    if (NB == 3 && wib + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + kWarpsPerBlock], lane, pol, b1);
+    if (NB == 3 && wib + 2 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWarpsPerBlock], lane, pol, b2);
+    // window fill (L1 lines are invalidated by the grid barrier's acquire)
     for (uint32_t i = threadIdx.x; i < nu; i += kBlock) {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + i));
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
@@ -1072,29 +1082,57 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const long long t1 = WBX_PROFILE == 3 ? clock64() : 0;
-    for (uint32_t s = wib; s < ns; s += kWarpsPerBlock) {
-        cur = nxt;
-        if (s + kWarpsPerBlock < ns) win_load(W.rec, stab[s + kWarpsPerBlock], lane, pol, nxt);
-        const uint32_t info = cur.info;
-        const uint32_t row = info == kNoRow ? kNoRow : (info & kRowMask);
-        const auto pv = pre(row);
-        const int nq = static_cast<int>(cur.meta & 0xffu);
+    // process slice s from d
+    auto run = [&](const WinSlice<DICT>& d, uint32_t s) {
+        const uint4 sl = stab[s];  // {record offset, meta, first row, -}
+        const uint32_t nq = sl.y & 0xffu, m = (sl.y >> 8) & 0xffu, nseg = (sl.y >> 16) & 0xffu;
+        const uint32_t cnt = sl.y >> 24;
         ACC acc = ACC(0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (q < nq) {
-                const float v0 = __uint_as_float(cur.v[q].x), v1 = __uint_as_float(cur.v[q].y);
-                const float v2 = __uint_as_float(cur.v[q].z), v3 = __uint_as_float(cur.v[q].w);
-                const WIN g0 = win[cur.c[q].x & 0xffffu], g1 = win[cur.c[q].x >> 16];
-                const WIN g2 = win[cur.c[q].y & 0xffffu], g3 = win[cur.c[q].y >> 16];
-                acc = fma(static_cast<ACC>(v0), static_cast<ACC>(g0), acc);
-                acc = fma(static_cast<ACC>(v1), static_cast<ACC>(g1), acc);
-                acc = fma(static_cast<ACC>(v2), static_cast<ACC>(g2), acc);
-                acc = fma(static_cast<ACC>(v3), static_cast<ACC>(g3), acc);
+        for (uint32_t qd = 0; qd < 4; ++qd) {
+            if (qd < nq) {
+                float4 v;
+                if (DICT) {
+                    v = *reinterpret_cast<const float4*>(dict + d.pb + qd * 4);
+                } else {
+                    v = make_float4(__uint_as_float(d.v[qd].x), __uint_as_float(d.v[qd].y),
+                                    __uint_as_float(d.v[qd].z), __uint_as_float(d.v[qd].w));
+                }
+                const WIN g0 = win[d.c[qd].x & 0xffffu], g1 = win[d.c[qd].x >> 16];
+                const WIN g2 = win[d.c[qd].y & 0xffffu], g3 = win[d.c[qd].y >> 16];
+                acc = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), acc);
+                acc = fma(static_cast<ACC>(v.y), static_cast<ACC>(g1), acc);
+                acc = fma(static_cast<ACC>(v.z), static_cast<ACC>(g2), acc);
+                acc = fma(static_cast<ACC>(v.w), static_cast<ACC>(g3), acc);
             }
         }
-        const uint32_t r = combine_info(info, cur.meta, acc);
-        if (r != kNoRow) post(r, acc, pv);
+        // segments of row i sit in lanes i, i+m, ..., i+(nseg-1)m: fold into the head lane
+        for (uint32_t t = 1; t < nseg; ++t) {
+            const ACC o = __shfl_down_sync(0xffffffffu, acc, t * m);
+            if (static_cast<uint32_t>(lane) < m) acc += o;
+        }
+        if (static_cast<uint32_t>(lane) < cnt) post(sl.z + lane, acc);
+    };
+    // process slice s from d, then refill d with slice s + NB*8
+    auto step = [&](WinSlice<DICT>& d, uint32_t s) {
+        run(d, s);
+        const uint32_t sn = s + NB * kWarpsPerBlock;
+        if (sn < ns) win_load<DICT>(W.rec, stab[sn], lane, pol, d);
+    };
+    if (NB == 3) {
+        for (uint32_t s = wib; s < ns; s += NB * kWarpsPerBlock) {
+            step(b0, s);
+            if (s + kWarpsPerBlock >= ns) break;
+            step(b1, s + kWarpsPerBlock);
+            if (s + 2 * kWarpsPerBlock >= ns) break;
+            step(b2, s + 2 * kWarpsPerBlock);
+        }
+    } else {  // two buffers: the next load is issued before the current slice computes
+        for (uint32_t s = wib; s < ns; s += kWarpsPerBlock) {
+            b1 = b0;
+            if (s + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[s + kWarpsPerBlock], lane, pol, b0);
+            run(b1, s);
+        }
     }
     if (WBX_PROFILE == 3) {
         const long long t2 = clock64();
@@ -1106,8 +1144,9 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     __syncthreads();  // the window is refilled by the next phase
 }
 
-template <typename T>
+template <bool DICT>
 __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(SolveArgs a) {
+    constexpr int NB = DICT ? 3 : 2;
     __shared__ double smem[kWarpsPerBlock + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -1115,20 +1154,12 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
     float* yC = static_cast<float*>(a.yC);
-    float* xpC = static_cast<float*>(a.xpC);
     float* res = static_cast<float*>(a.res);
-    float* x0R = static_cast<float*>(a.x0R);
-    float* tpC = static_cast<float*>(a.tpC);
-    float* thrC = static_cast<float*>(a.thrC);
     const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
     const WinSmem ws = win_smem_init<4, 16>(dsmem, a);
     float* win = static_cast<float*>(ws.win);
     float* x0s = static_cast<float*>(ws.ownA);   // x0 of the CTA's Theta rows
     float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
-    (void)xpC;
-    (void)tpC;
-    (void)thrC;
-    (void)x0R;
     for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) {
         const uint32_t c = ws.rT0 + i;
         const float v = static_cast<float>(a.x0_full[a.C_glob[c]]);
@@ -1147,23 +1178,21 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
         if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
     };
     for (int k = 1; k <= a.max_iters; ++k) {
-        win_phase<float, float>(
-            a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, yC, win, [](uint32_t) { return 0; },
-            [&](uint32_t r, float acc, int) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
+        win_phase<float, float, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
+                                          [&](uint32_t r, float acc) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
         sync();
         const float beta = a.beta32[k - 1];
-        win_phase<float, float>(
-            a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, res, win, [](uint32_t) { return 0; },
-            [&](uint32_t c, float g, int) {
-                float4& q = cs[c - ws.rT0];
-                const float z0 = fmaf(-q.z, g, q.x);
-                const float xn = Prec<float>::prox(z0, q.w);
-                const float yn = fmaf(beta, xn - q.y, xn);
-                q.x = yn;
-                q.y = xn;
-                yC[c] = yn;
-            },
-            pf);
+        win_phase<float, float, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
+                                          [&](uint32_t c, float g) {
+                                              float4& s = cs[c - ws.rT0];
+                                              const float z0 = fmaf(-s.z, g, s.x);
+                                              const float xn = Prec<float>::prox(z0, s.w);
+                                              const float yn = fmaf(beta, xn - s.y, xn);
+                                              s.x = yn;
+                                              s.y = xn;
+                                              yC[c] = yn;
+                                          },
+                                          pf);
         sync();
     }
     pf.flush();
@@ -1172,7 +1201,9 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
 }
 
 // estimate_step on the window engine (fp64 window and accumulation, fp32 operator values)
+template <bool DICT>
 __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs a) {
+    constexpr int NB = DICT ? 3 : 2;
     __shared__ double smem[kWarpsPerBlock + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -1202,25 +1233,23 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     WinProf pf;
     for (; it < 200; ++it) {
         const double inv = nw_prev;
-        win_phase<double, double>(
-            a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, a.uC, win, [](uint32_t) { return 0; },
-            [&](uint32_t r, double t, int) { a.t64[r] = t / inv; }, pf);
+        win_phase<double, double, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, a.uC, win,
+                                            [&](uint32_t r, double t) { a.t64[r] = t / inv; }, pf);
         const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
         if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
         double acc[2] = {0.0, 0.0};
-        win_phase<double, double>(
-            a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, a.t64, win, [](uint32_t) { return 0; },
-            [&](uint32_t c, double g, int) {
-                double2& q = cs[c - ws.rT0];
-                const double w = g * q.x;
-                const double v = q.y / inv;
-                acc[0] += v * w;
-                acc[1] += w * w;
-                q.y = w;
-                a.uC[c] = q.x * w;
-            },
-            pf);
+        win_phase<double, double, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, a.t64, win,
+                                            [&](uint32_t c, double g) {
+                                                double2& s = cs[c - ws.rT0];
+                                                const double w = g * s.x;
+                                                const double v = s.y / inv;
+                                                acc[0] += v * w;
+                                                acc[1] += w * w;
+                                                s.y = w;
+                                                a.uC[c] = s.x * w;
+                                            },
+                                            pf);
         const long long b1 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync_reduce<2>(a.sync, epoch, acc, smem);
         if (WBX_PROFILE == 3) pf.c[3] += clock64() - b1;
@@ -1473,10 +1502,9 @@ struct wbx_solver {
     int grid_fista = 0, grid_tau = 0;
     int nslots = 3;  // TMA slots in flight per warp
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
-    bool win = false;
+    bool win = false, win_dict = false;
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
-    uint32_t win_max_slices = 0;
     wbx::WinSide wA, wT;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1572,7 +1600,6 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     if (s->win) {
         a.wA = view_of(s->wA);
         a.wT = view_of(s->wT);
-        a.win_max_slices = s->win_max_slices;
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
@@ -1603,13 +1630,17 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
-        launch_coop_smem(reinterpret_cast<const void*>(tau_win_kernel), s->grid_win, s->win_smem_tau, a, st);
+        const void* k = s->win_dict ? reinterpret_cast<const void*>(tau_win_kernel<true>)
+                                    : reinterpret_cast<const void*>(tau_win_kernel<false>);
+        launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
     if (win) {
-        launch_coop_smem(reinterpret_cast<const void*>(fista_win_kernel<float>), s->grid_win, s->win_smem_fista, a, st);
+        const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
+                                    : reinterpret_cast<const void*>(fista_win_kernel<false>);
+        launch_coop_smem(k, s->grid_win, s->win_smem_fista, a, st);
         count_launch(ctx);
         WBX_CUDA(cudaGetLastError());
         return;
@@ -1678,32 +1709,33 @@ void alloc_state(wbx_solver* s) {
             } catch (const Error&) {
                 continue;  // a window exceeded 16-bit local indices
             }
-            std::vector<uint32_t> sa(G + 1), stt(G + 1);
-            WBX_CUDA(cudaMemcpy(sa.data(), s->wA.s_off.p, (G + 1) * 4, cudaMemcpyDeviceToHost));
-            WBX_CUDA(cudaMemcpy(stt.data(), s->wT.s_off.p, (G + 1) * 4, cudaMemcpyDeviceToHost));
-            uint32_t ms = 1;
-            for (uint32_t b = 0; b < G; ++b) ms = std::max({ms, sa[b + 1] - sa[b], stt[b + 1] - stt[b]});
-            s->win_max_slices = ms;
+            const WinView vA = view_of(s->wA), vT = view_of(s->wT);
             const unsigned mu = std::max(s->wA.max_u, s->wT.max_u);
-            s->win_smem_fista = win_smem_head<4, 16>(s->wA.max_u, s->wT.max_u, ms, s->wA.max_rows, s->wT.max_rows) + mu * 4u;
-            s->win_smem_tau = win_smem_head<0, 16>(s->wA.max_u, s->wT.max_u, ms, s->wA.max_rows, s->wT.max_rows) + mu * 8u;
+            s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
+            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + mu * 8u;
+            s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
+            const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
+                                         : reinterpret_cast<const void*>(fista_win_kernel<false>);
+            const void* kt = s->win_dict ? reinterpret_cast<const void*>(tau_win_kernel<true>)
+                                         : reinterpret_cast<const void*>(tau_win_kernel<false>);
             const unsigned limit = bps == 2 ? 110u * 1024u : 220u * 1024u;
             if (s->win_smem_tau > limit) continue;
-            WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fista_win_kernel<float>),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s->win_smem_fista)));
-            WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(tau_win_kernel),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s->win_smem_tau)));
+            WBX_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(s->win_smem_fista)));
+            WBX_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(s->win_smem_tau)));
             int pf = 0, pt = 0;
-            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, fista_win_kernel<float>, kBlock, s->win_smem_fista));
-            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, tau_win_kernel, kBlock, s->win_smem_tau));
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, kf, kBlock, s->win_smem_fista));
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, kt, kBlock, s->win_smem_tau));
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
             if (std::getenv("WBX_VERBOSE"))
                 std::fprintf(stderr,
-                             "wbx window engine: G=%u max_u A/T=%u/%u max_rows A/T=%u/%u max_slices=%u "
-                             "rec bytes A/T=%llu/%llu smem fista/tau=%u/%u\n",
-                             G, s->wA.max_u, s->wT.max_u, s->wA.max_rows, s->wT.max_rows, ms,
+                             "wbx window engine: G=%u max_u A/T=%u/%u max_rows A/T=%u/%u max_slices A/T=%u/%u "
+                             "dict floats A/T=%u/%u rec bytes A/T=%llu/%llu smem fista/tau=%u/%u\n",
+                             G, s->wA.max_u, s->wT.max_u, s->wA.max_rows, s->wT.max_rows, s->wA.max_slices,
+                             s->wT.max_slices, s->wA.max_dict, s->wT.max_dict,
                              static_cast<unsigned long long>(s->wA.rec.bytes()),
                              static_cast<unsigned long long>(s->wT.rec.bytes()), s->win_smem_fista, s->win_smem_tau);
         }

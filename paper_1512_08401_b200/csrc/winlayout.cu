@@ -1,40 +1,84 @@
 // Host construction of the per-CTA window layouts (see win.cuh).
 #include <algorithm>
-#include <array>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "internal.hpp"
 #include "win.cuh"
 
 namespace wbx {
 
-void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) {
+namespace {
+
+uint64_t segs_of(uint64_t len) { return std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems); }
+
+// Contiguous row ranges per CTA balanced by COST = 16 per lane segment + nonzeros: a
+// slice's time is dominated by its load round trip, not by its nonzeros, so balancing
+// nonzeros alone leaves the CTAs of short rows with many more slices.
+std::vector<uint64_t> balance(const HostCompact& M, uint32_t G) {
     const uint64_t nrows = M.rows();
-    const uint64_t nnz = nrows ? M.ptr[nrows] : 0;
-    // contiguous row ranges per CTA balanced by COST = lane segments + nonzeros / 16: a
-    // slice's time is dominated by its load round trip, not by its nonzeros, so balancing
-    // nonzeros alone leaves the CTAs of short rows with many more slices
     auto cost = [&](uint64_t i) {
         const uint64_t len = M.ptr[i + 1] - M.ptr[i];
-        return 16 * std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems) + len;
+        return 16 * segs_of(len) + len;
     };
     uint64_t total = 0;
     for (uint64_t i = 0; i < nrows; ++i) total += cost(i);
     std::vector<uint64_t> rb(G + 1, nrows);
     rb[0] = 0;
-    {
-        uint64_t acc = 0, q = 1;
-        for (uint64_t i = 0; i < nrows && q < G; ++i) {
-            acc += cost(i);
-            while (q < G && acc * G >= total * q) rb[q++] = i + 1;
-        }
+    uint64_t acc = 0, q = 1;
+    for (uint64_t i = 0; i < nrows && q < G; ++i) {
+        acc += cost(i);
+        while (q < G && acc * G >= total * q) rb[q++] = i + 1;
     }
-    (void)nnz;
-    std::vector<uint32_t> u_off(G + 1, 0), u_idx, s_off(G + 1, 0), s_meta;
-    std::vector<uint64_t> s_rec;
-    std::vector<uint4> rec;
-    uint32_t max_u = 0;
-    std::vector<uint32_t> local;  // position -> local window index (scratch)
+    return rb;
+}
+
+// Per-CTA dictionary of distinct fp32 value sequences: offset (floats) of every row's
+// q x 16 block, or false when the dictionary exceeds the budget.
+bool build_dict(const HostCompact& M, uint64_t r0, uint64_t r1, std::vector<float>& dict,
+                std::vector<uint32_t>& row_off) {
+    dict.assign(16, 0.0f);  // offset 0: the zero block of padding lanes
+    row_off.assign(r1 - r0, 0);
+    std::map<std::vector<uint32_t>, uint32_t> seen;
+    for (uint64_t r = r0; r < r1; ++r) {
+        const uint64_t len = M.ptr[r + 1] - M.ptr[r];
+        std::vector<uint32_t> key(len);
+        for (uint64_t k = 0; k < len; ++k) {
+            const float f = static_cast<float>(M.val[M.ptr[r] + k]);
+            std::memcpy(&key[k], &f, 4);
+        }
+        auto it = seen.find(key);
+        if (it == seen.end()) {
+            const uint64_t q = segs_of(len);
+            const uint32_t off = static_cast<uint32_t>(dict.size());
+            dict.resize(dict.size() + q * 16, 0.0f);
+            for (uint64_t t = 0; t < q; ++t) {
+                const uint64_t beg = t * len / q, end = (t + 1) * len / q;
+                for (uint64_t j = beg; j < end; ++j) std::memcpy(&dict[off + t * 16 + (j - beg)], &key[j], 4);
+            }
+            if (dict.size() * 4 > kWinDictBudget) return false;
+            it = seen.emplace(std::move(key), off).first;
+        }
+        row_off[r - r0] = it->second;
+    }
+    return true;
+}
+
+}  // namespace
+
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) {
+    const std::vector<uint64_t> rb = balance(M, G);
+    // format: the dictionary when every CTA's fits the budget
+    bool dict_fmt = std::getenv("WBX_WIN_FULL") == nullptr;  // diagnostics: force the full format
+    std::vector<std::vector<float>> dicts(G);
+    std::vector<std::vector<uint32_t>> roffs(G);
+    for (uint32_t b = 0; b < G && dict_fmt; ++b) dict_fmt = build_dict(M, rb[b], rb[b + 1], dicts[b], roffs[b]);
+
+    std::vector<uint32_t> u_off(G + 1, 0), u_idx, s_off(G + 1, 0), d_off(G + 1, 0);
+    std::vector<uint4> s_tab, rec;
+    std::vector<float> d_val;
+    uint32_t max_u = 0, max_slices = 0, max_dict = 0;
     for (uint32_t b = 0; b < G; ++b) {
         const uint64_t r0 = rb[b], r1 = rb[b + 1];
         // window: sorted unique referenced positions
@@ -48,52 +92,61 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) 
         u_idx.insert(u_idx.end(), u.begin(), u.end());
         u_off[b + 1] = static_cast<uint32_t>(u_idx.size());
         auto loc = [&](uint32_t pos) {
-            return static_cast<uint32_t>(std::lower_bound(u.begin(), u.end(), pos) - u.begin());
+            return static_cast<uint16_t>(std::lower_bound(u.begin(), u.end(), pos) - u.begin());
         };
-        // slices: segment-major placement of rows with equal segment counts
-        struct Seg {
-            uint64_t row, beg, len;
-            uint32_t info;
-        };
+        if (dict_fmt) {
+            d_val.insert(d_val.end(), dicts[b].begin(), dicts[b].end());
+            max_dict = std::max<uint32_t>(max_dict, static_cast<uint32_t>(dicts[b].size()));
+        }
+        d_off[b + 1] = static_cast<uint32_t>(d_val.size());
+        // slices: up to m consecutive rows with equal segment count q, segment-major lanes
+        const size_t slice0 = s_tab.size();
         uint64_t r = r0;
         while (r < r1) {
-            const uint64_t len0 = M.ptr[r + 1] - M.ptr[r];
-            const uint64_t q = std::max<uint64_t>(1, (len0 + kSegElems - 1) / kSegElems);
+            const uint64_t q = segs_of(M.ptr[r + 1] - M.ptr[r]);
             if (q > 31) fail(WBX_TOO_LARGE, "row longer than 31 segments");
-            const uint64_t m = 32 / q;
-            std::array<Seg, 32> a;
-            for (auto& g : a) g = Seg{0, 0, 0, 0xffffffffu};
-            for (uint64_t i = 0; i < m && r < r1; ++i, ++r) {
-                const uint64_t len = M.ptr[r + 1] - M.ptr[r];
-                if (std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems) != q) break;
-                for (uint64_t t = 0; t < q; ++t) {
-                    const uint64_t beg = t * len / q, end = (t + 1) * len / q;
-                    a[t * m + i] = Seg{r, beg, end - beg,
-                                       t == 0 ? static_cast<uint32_t>(r | (q << kInfoShift)) : 0xffffffffu};
-                }
+            const uint64_t m = 32 / q, first = r;
+            uint64_t cnt = 0;
+            while (cnt < m && r < r1 && segs_of(M.ptr[r + 1] - M.ptr[r]) == q) {
+                ++cnt;
+                ++r;
             }
-            uint64_t nq = 0;
-            for (const auto& g : a) nq = std::max<uint64_t>(nq, (g.len + 3) / 4);
-            if (nq == 0) nq = 1;
-            s_rec.push_back(rec.size());
-            s_meta.push_back(static_cast<uint32_t>(nq) | (static_cast<uint32_t>(m) << 8));
+            uint64_t nq = 1;
+            for (uint64_t i = 0; i < cnt; ++i) {
+                const uint64_t len = M.ptr[first + i + 1] - M.ptr[first + i];
+                for (uint64_t t = 0; t < q; ++t) nq = std::max<uint64_t>(nq, ((t + 1) * len / q - t * len / q + 3) / 4);
+            }
             const uint64_t base = rec.size();
-            rec.resize(base + 8 + nq * 32 + nq * 16, make_uint4(0, 0, 0, 0));
-            uint32_t* info = reinterpret_cast<uint32_t*>(&rec[base]);
-            float* vals = reinterpret_cast<float*>(&rec[base + 8]);
-            uint16_t* cols = reinterpret_cast<uint16_t*>(&rec[base + 8 + nq * 32]);
-            for (uint64_t lane = 0; lane < 32; ++lane) {
-                const Seg& g = a[lane];
-                info[lane] = g.info;
-                for (uint64_t j = 0; j < g.len; ++j) {
-                    const uint64_t k = M.ptr[g.row] + g.beg + j;
-                    const uint64_t qd = j / 4, e = j % 4;
-                    vals[(qd * 32 + lane) * 4 + e] = static_cast<float>(M.val[k]);
-                    cols[(qd * 32 + lane) * 4 + e] = static_cast<uint16_t>(loc(M.col[k]));
+            const uint64_t head = dict_fmt ? 4 : nq * 32;  // pb words, or values
+            rec.resize(base + head + nq * 16, make_uint4(0, 0, 0, 0));
+            uint16_t* pb = reinterpret_cast<uint16_t*>(&rec[base]);
+            float* vals = reinterpret_cast<float*>(&rec[base]);
+            uint16_t* cols = reinterpret_cast<uint16_t*>(&rec[base + head]);
+            for (uint64_t i = 0; i < cnt; ++i) {
+                const uint64_t row = first + i, len = M.ptr[row + 1] - M.ptr[row];
+                for (uint64_t t = 0; t < q; ++t) {
+                    const uint64_t lane = t * m + i, beg = t * len / q, end = (t + 1) * len / q;
+                    if (dict_fmt) {
+                        const uint32_t o = roffs[b][row - r0] + static_cast<uint32_t>(t * 16);
+                        if (o > 0xffffu) fail(WBX_TOO_LARGE, "dictionary offset exceeds 16 bits");
+                        pb[lane] = static_cast<uint16_t>(o);
+                    }
+                    for (uint64_t j = 0; j < end - beg; ++j) {
+                        const uint64_t k = M.ptr[row] + beg + j;
+                        const uint64_t slot = ((j / 4) * 32 + lane) * 4 + j % 4;
+                        if (!dict_fmt) vals[slot] = static_cast<float>(M.val[k]);
+                        cols[slot] = loc(M.col[k]);
+                    }
                 }
             }
+            if (base > 0xffffffffull) fail(WBX_TOO_LARGE, "window records exceed 32-bit offsets");
+            s_tab.push_back(make_uint4(static_cast<uint32_t>(base),
+                                       win_meta(static_cast<uint32_t>(nq), static_cast<uint32_t>(m),
+                                                static_cast<uint32_t>(q), static_cast<uint32_t>(cnt)),
+                                       static_cast<uint32_t>(first), 0));
         }
-        s_off[b + 1] = static_cast<uint32_t>(s_rec.size());
+        s_off[b + 1] = static_cast<uint32_t>(s_tab.size());
+        max_slices = std::max<uint32_t>(max_slices, static_cast<uint32_t>(s_tab.size() - slice0));
     }
     std::vector<uint32_t> r_off(G + 1);
     uint32_t max_rows = 0;
@@ -102,23 +155,24 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) 
         if (b < G) max_rows = std::max<uint32_t>(max_rows, static_cast<uint32_t>(rb[b + 1] - rb[b]));
     }
     if (u_idx.empty()) u_idx.push_back(0);
-    if (s_rec.empty()) {
-        s_rec.push_back(0);
-        s_meta.push_back(1);
-    }
+    if (s_tab.empty()) s_tab.push_back(make_uint4(0, 0, 0, 0));
     if (rec.empty()) rec.resize(1, make_uint4(0, 0, 0, 0));
+    if (d_val.empty()) d_val.push_back(0.0f);
     out.G = G;
     out.max_u = max_u;
     out.max_rows = max_rows;
+    out.max_slices = max_slices;
+    out.max_dict = dict_fmt ? max_dict : 0;
     out.r_off.upload(r_off, st);
     out.u_off.upload(u_off, st);
     out.u_idx.upload(u_idx, st);
     out.s_off.upload(s_off, st);
-    out.s_rec.upload(s_rec, st);
-    out.s_meta.upload(s_meta, st);
+    out.s_tab.upload(s_tab, st);
+    out.d_off.upload(d_off, st);
+    out.d_val.upload(d_val, st);
     out.rec.upload(rec, st);
-    out.bytes = out.r_off.bytes() + out.u_off.bytes() + out.u_idx.bytes() + out.s_off.bytes() + out.s_rec.bytes() + out.s_meta.bytes() +
-                out.rec.bytes();
+    out.bytes = out.r_off.bytes() + out.u_off.bytes() + out.u_idx.bytes() + out.s_off.bytes() + out.s_tab.bytes() +
+                out.d_off.bytes() + out.d_val.bytes() + out.rec.bytes();
     WBX_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -127,12 +181,15 @@ WinView view_of(const WinSide& w) {
     v.u_off = w.u_off.p;
     v.u_idx = w.u_idx.p;
     v.s_off = w.s_off.p;
-    v.s_rec = w.s_rec.p;
-    v.s_meta = w.s_meta.p;
+    v.s_tab = w.s_tab.p;
     v.r_off = w.r_off.p;
+    v.d_off = w.d_off.p;
+    v.d_val = w.d_val.p;
     v.rec = w.rec.p;
     v.max_u = w.max_u;
     v.max_rows = w.max_rows;
+    v.max_slices = w.max_slices;
+    v.max_dict = w.max_dict;
     return v;
 }
 

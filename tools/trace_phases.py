@@ -46,3 +46,14 @@ print(json.dumps({"grid": G, "barriers": len(used),
                   "phase_us_median_odd": round(float(np.median(phases[1::2])), 2) if phases else None,
                   "barrier_us_median": round(float(np.median(bars)), 2),
                   "arrival_skew_us_median": round(float(np.median(skews)), 2)}))
+if len(sys.argv) > 3 and sys.argv[3] == "blocks":
+    # per-block work time of each phase (own arrival - own previous release), A = even, T = odd
+    work = (arr[1:, :, 0] - arr[:-1, :, 1]) / 1e3
+    out = {}
+    for name, sl in (("A", work[0::2]), ("T", work[1::2])):
+        m = sl.mean(axis=0)
+        out[name] = {"p10": round(float(np.percentile(m, 10)), 2), "p50": round(float(np.median(m)), 2),
+                     "p90": round(float(np.percentile(m, 90)), 2), "max": round(float(m.max()), 2),
+                     "slowest": [int(b) for b in np.argsort(-m)[:12]],
+                     "by_sm_pair": [round(float(x), 2) for x in m.reshape(-1, 2).mean(axis=1)[::16]]}
+    print(json.dumps(out))
