@@ -185,6 +185,11 @@ struct Epoch {
     unsigned cur, start;
 };
 
+// Back-off between barrier polls (ns; 0 = spin)
+#ifndef WBX_POLL_NS
+#define WBX_POLL_NS 0
+#endif
+
 // Counter barrier (mode 2): one arrival counter, zeroed by the host before each cooperative
 // launch; barrier k of the launch completes when the counter reaches k * G. Arrival is a
 // fire-and-forget reduction, and every block polls the one word directly (no master hop).
@@ -194,7 +199,10 @@ __device__ __forceinline__ void counter_arrive_wait(const Sync& s, const Epoch& 
     unsigned* cnt = s.gen + kCounterWord;
     asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
     const unsigned target = (e.cur - e.start) * gridDim.x;
+    // acquiring polls: measured faster than relaxed polls + one acquire fence (the fence
+    // costs more than the per-poll L1 invalidations)
     while (static_cast<int>(ld_acquire(cnt) - target) < 0) {
+        if (WBX_POLL_NS) __nanosleep(WBX_POLL_NS);
     }
 }
 
@@ -546,6 +554,10 @@ __device__ int g_debug_mode = 0;
 #define WBX_PROFILE 0
 #endif
 // 2 = per-slice cycle accounting: [tma wait, load+gather+fma, combine+issue+epilogue, slices]
+// Window engine lookahead (dictionary format): 3 = three slices in flight, 4 = two pairs
+#ifndef WBX_WIN_NB
+#define WBX_WIN_NB 4
+#endif
 __device__ unsigned long long g_prof[6];
 
 }  // namespace
@@ -1064,15 +1076,16 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
                                           uint32_t ns, const float* dict, const X* __restrict__ x, WIN* win,
                                           Post post, WinProf& pf) {
     static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
-    static_assert(NB == 2 || NB == 3, "lookahead buffers");
+    static_assert(NB == 2 || NB == 3 || NB == 4, "lookahead buffers (4: slices computed in pairs)");
     const long long t0 = WBX_PROFILE == 3 ? clock64() : 0;
     const int lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint64_t pol = l2_keep_policy();
-    WinSlice<DICT> b0, b1, b2;
+    WinSlice<DICT> b0, b1, b2, b3;
     if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
-    if (NB == 3 && wib + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + kWarpsPerBlock], lane, pol, b1);
-    if (NB == 3 && wib + 2 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWarpsPerBlock], lane, pol, b2);
+    if (NB >= 3 && wib + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + kWarpsPerBlock], lane, pol, b1);
+    if (NB >= 3 && wib + 2 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWarpsPerBlock], lane, pol, b2);
+    if (NB == 4 && wib + 3 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 3 * kWarpsPerBlock], lane, pol, b3);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
     for (uint32_t i = threadIdx.x; i < nu; i += kBlock) {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + i));
@@ -1119,7 +1132,59 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
         const uint32_t sn = s + NB * kWarpsPerBlock;
         if (sn < ns) win_load<DICT>(W.rec, stab[sn], lane, pol, d);
     };
-    if (NB == 3) {
+    // two slices at once (independent latency chains interleave): sa from da and, if
+    // sb < ns, sb from db
+    auto run2 = [&](const WinSlice<DICT>& da, uint32_t sa, const WinSlice<DICT>& db, uint32_t sb) {
+        const bool hb = sb < ns;
+        const uint4 la = stab[sa];
+        const uint4 lb = hb ? stab[sb] : make_uint4(0, 1u << 16, 0, 0);
+        const uint32_t nqa = la.y & 0xffu, ma = (la.y >> 8) & 0xffu, nsa = (la.y >> 16) & 0xffu, ca = la.y >> 24;
+        const uint32_t nqb = lb.y & 0xffu, mb = (lb.y >> 8) & 0xffu, nsb = (lb.y >> 16) & 0xffu, cb = lb.y >> 24;
+        ACC aa = ACC(0), ab = ACC(0);
+#pragma unroll
+        for (uint32_t qd = 0; qd < 4; ++qd) {
+            if (qd < nqa) {
+                const float4 v = *reinterpret_cast<const float4*>(dict + da.pb + qd * 4);
+                const WIN g0 = win[da.c[qd].x & 0xffffu], g1 = win[da.c[qd].x >> 16];
+                const WIN g2 = win[da.c[qd].y & 0xffffu], g3 = win[da.c[qd].y >> 16];
+                aa = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), aa);
+                aa = fma(static_cast<ACC>(v.y), static_cast<ACC>(g1), aa);
+                aa = fma(static_cast<ACC>(v.z), static_cast<ACC>(g2), aa);
+                aa = fma(static_cast<ACC>(v.w), static_cast<ACC>(g3), aa);
+            }
+            if (qd < nqb) {
+                const float4 v = *reinterpret_cast<const float4*>(dict + db.pb + qd * 4);
+                const WIN g0 = win[db.c[qd].x & 0xffffu], g1 = win[db.c[qd].x >> 16];
+                const WIN g2 = win[db.c[qd].y & 0xffffu], g3 = win[db.c[qd].y >> 16];
+                ab = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), ab);
+                ab = fma(static_cast<ACC>(v.y), static_cast<ACC>(g1), ab);
+                ab = fma(static_cast<ACC>(v.z), static_cast<ACC>(g2), ab);
+                ab = fma(static_cast<ACC>(v.w), static_cast<ACC>(g3), ab);
+            }
+        }
+        const uint32_t nsm = nsa > nsb ? nsa : nsb;
+        for (uint32_t t = 1; t < nsm; ++t) {
+            const ACC oa = __shfl_down_sync(0xffffffffu, aa, t * ma);
+            const ACC ob = __shfl_down_sync(0xffffffffu, ab, t * mb);
+            if (t < nsa && static_cast<uint32_t>(lane) < ma) aa += oa;
+            if (t < nsb && static_cast<uint32_t>(lane) < mb) ab += ob;
+        }
+        if (static_cast<uint32_t>(lane) < ca) post(la.z + lane, aa);
+        if (static_cast<uint32_t>(lane) < cb) post(lb.z + lane, ab);
+    };
+    if (NB == 4) {
+        static_assert(NB != 4 || DICT, "paired slices use the dictionary format");
+        constexpr uint32_t W8 = kWarpsPerBlock;
+        for (uint32_t s = wib; s < ns; s += 4 * W8) {
+            run2(b0, s, b1, s + W8);
+            if (s + 4 * W8 < ns) win_load<DICT>(W.rec, stab[s + 4 * W8], lane, pol, b0);
+            if (s + 5 * W8 < ns) win_load<DICT>(W.rec, stab[s + 5 * W8], lane, pol, b1);
+            if (s + 2 * W8 >= ns) break;
+            run2(b2, s + 2 * W8, b3, s + 3 * W8);
+            if (s + 6 * W8 < ns) win_load<DICT>(W.rec, stab[s + 6 * W8], lane, pol, b2);
+            if (s + 7 * W8 < ns) win_load<DICT>(W.rec, stab[s + 7 * W8], lane, pol, b3);
+        }
+    } else if (NB == 3) {
         for (uint32_t s = wib; s < ns; s += NB * kWarpsPerBlock) {
             step(b0, s);
             if (s + kWarpsPerBlock >= ns) break;
@@ -1146,7 +1211,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
 
 template <bool DICT>
 __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(SolveArgs a) {
-    constexpr int NB = DICT ? 3 : 2;
+    constexpr int NB = DICT ? WBX_WIN_NB : 2;
     __shared__ double smem[kWarpsPerBlock + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -1203,7 +1268,7 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
 // estimate_step on the window engine (fp64 window and accumulation, fp32 operator values)
 template <bool DICT>
 __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs a) {
-    constexpr int NB = DICT ? 3 : 2;
+    constexpr int NB = DICT ? WBX_WIN_NB : 2;
     __shared__ double smem[kWarpsPerBlock + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -1228,21 +1293,73 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     grid_sync_reduce<1>(a.sync, epoch, s2, smem);
     double nw_prev = sqrt(s2[0]);
     double lambda_prev = 0.0;
-    int it = 0;
+    int it = 0, iters = 0;
     bool zero_op = false;
     WinProf pf;
-    for (; it < 200; ++it) {
-        const double inv = nw_prev;
-        win_phase<double, double, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, a.uC, win,
-                                            [&](uint32_t r, double t) { a.t64[r] = t / inv; }, pf);
+    __shared__ double red[2];
+    const unsigned G = gridDim.x;
+    // staging of the 2 x G block partials, after the window
+    double* pstage = win + (a.wA.max_u > a.wT.max_u ? a.wA.max_u : a.wT.max_u);
+    // Deferred reduction: phase A computes Theta u WITHOUT the 1/|w_prev| normalisation (it is
+    // applied to Theta^T t in phase T instead), so A does not wait for the previous
+    // iteration's grid reduction; the block partials of iteration it-1 are summed by warp 0
+    // while phase A of iteration it runs, and its stopping test is taken after A. Every
+    // barrier is a plain one. (On convergence one extra phase A has been computed.)
+    for (it = 0;; ++it) {
+        const double* part = a.sync.part + static_cast<uint64_t>((it + 1) & 1) * kRedSlots * G;
+        if (it > 0 && threadIdx.x < 32)  // asynchronous copies, complete during the phase
+            for (unsigned i = threadIdx.x; i < 2 * G; i += 32) {
+                const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(pstage + i));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                             "l"(part + i) : "memory");
+            }
+        if (it < 200)
+            win_phase<double, double, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, a.uC, win,
+                                                [&](uint32_t r, double t) { a.t64[r] = t; }, pf);
+        if (it > 0 && threadIdx.x < 32) {
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            double p0 = 0.0, p1 = 0.0;
+            for (unsigned i = threadIdx.x; i < G; i += 32) {
+                p0 += pstage[i];
+                p1 += pstage[G + i];
+            }
+            p0 = warp_sum(p0);
+            p1 = warp_sum(p1);
+            if (threadIdx.x == 0) {
+                red[0] = p0;
+                red[1] = p1;
+            }
+        }
         const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
         if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
+        if (it > 0) {  // stopping test of iteration it-1 (solver.cpp:84-88)
+            const double lambda = red[0];
+            const double nw = sqrt(red[1]);
+            if (nw == 0.0) {
+                zero_op = true;
+                iters = it;
+                break;
+            }
+            if (it > 1 && fabs(lambda - lambda_prev) <= 1e-6 * fabs(lambda)) {
+                lambda_prev = lambda;
+                iters = it;
+                break;
+            }
+            lambda_prev = lambda;
+            nw_prev = nw;
+        }
+        if (it == 200) {
+            iters = 200;
+            break;
+        }
+        const double inv = nw_prev;
         double acc[2] = {0.0, 0.0};
         win_phase<double, double, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, a.t64, win,
                                             [&](uint32_t c, double g) {
                                                 double2& s = cs[c - ws.rT0];
-                                                const double w = g * s.x;
+                                                const double w = (g / inv) * s.x;
                                                 const double v = s.y / inv;
                                                 acc[0] += v * w;
                                                 acc[1] += w * w;
@@ -1250,24 +1367,18 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
                                                 a.uC[c] = s.x * w;
                                             },
                                             pf);
+        double* wpart = a.sync.part + static_cast<uint64_t>(it & 1) * kRedSlots * G;
+        const double s0 = block_sum<kBlock>(acc[0], smem);
+        const double s1 = block_sum<kBlock>(acc[1], smem);
+        if (threadIdx.x == 0) {
+            wpart[blockIdx.x] = s0;
+            wpart[G + blockIdx.x] = s1;
+        }
         const long long b1 = WBX_PROFILE == 3 ? clock64() : 0;
-        grid_sync_reduce<2>(a.sync, epoch, acc, smem);
+        grid_sync(a.sync, epoch, smem);
         if (WBX_PROFILE == 3) pf.c[3] += clock64() - b1;
-        const double lambda = acc[0];
-        const double nw = sqrt(acc[1]);
-        if (nw == 0.0) {
-            zero_op = true;
-            ++it;
-            break;
-        }
-        if (it > 0 && fabs(lambda - lambda_prev) <= 1e-6 * fabs(lambda)) {
-            lambda_prev = lambda;
-            ++it;
-            break;
-        }
-        lambda_prev = lambda;
-        nw_prev = nw;
     }
+    it = iters;
     pf.flush();
     if (gthread == 0) {
         a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
@@ -1712,7 +1823,7 @@ void alloc_state(wbx_solver* s) {
             const WinView vA = view_of(s->wA), vT = view_of(s->wT);
             const unsigned mu = std::max(s->wA.max_u, s->wT.max_u);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
-            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + mu * 8u;
+            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + mu * 8u + 16u * G;  // + partials staging
             s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
             const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                          : reinterpret_cast<const void*>(fista_win_kernel<false>);

@@ -1,5 +1,6 @@
 // Host construction of the per-CTA window layouts (see win.cuh).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -13,14 +14,21 @@ namespace {
 
 uint64_t segs_of(uint64_t len) { return std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems); }
 
-// Contiguous row ranges per CTA balanced by COST = 16 per lane segment + nonzeros: a
-// slice's time is dominated by its load round trip, not by its nonzeros, so balancing
-// nonzeros alone leaves the CTAs of short rows with many more slices.
+// Contiguous row ranges per CTA balanced by COST = wseg per lane segment + wnnz per nonzero
+// (a slice's time has a fixed part and a part growing with its quads and segment folds).
 std::vector<uint64_t> balance(const HostCompact& M, uint32_t G) {
     const uint64_t nrows = M.rows();
+    uint64_t wseg = 4, wnnz = 1;  // measured (trace_phases blocks): ~2.5x slice time for 99-long rows
+    if (const char* e = std::getenv("WBX_WIN_COST")) {  // diagnostics: "segment_weight,nonzero_weight"
+        unsigned long long a = 0, b = 0;
+        if (std::sscanf(e, "%llu,%llu", &a, &b) == 2) {
+            wseg = a;
+            wnnz = b;
+        }
+    }
     auto cost = [&](uint64_t i) {
         const uint64_t len = M.ptr[i + 1] - M.ptr[i];
-        return 16 * segs_of(len) + len;
+        return wseg * segs_of(len) + wnnz * len;
     };
     uint64_t total = 0;
     for (uint64_t i = 0; i < nrows; ++i) total += cost(i);
