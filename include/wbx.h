@@ -242,6 +242,9 @@ int wbx_shard_power_t(wbx_shard* s, double inv, double* sums2);
 
 /* launches of the last deblur, and the solver kernel's device time (ms) */
 int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);
+// Device time of the last solve split into the step-size estimate (estimate_step, 0 when tau
+// was given) and the iteration kernel(s), from CUDA events on the context stream.
+int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms);
 
 #ifdef __cplusplus
 }

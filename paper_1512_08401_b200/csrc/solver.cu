@@ -1618,7 +1618,7 @@ struct wbx_solver {
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     wbx::WinSide wA, wT;
     int dec_grid = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     uint64_t last_launches = 0;
     float last_solve_ms = 0.f;
 };
@@ -1748,6 +1748,7 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
+    WBX_CUDA(cudaEventRecord(s->ev_mid, st));  // tau | iterations split (wbx_solver_phase_ms)
     if (win) {
         const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                     : reinterpret_cast<const void*>(fista_win_kernel<false>);
@@ -1922,6 +1923,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     }
     WBX_CUDA(cudaEventCreate(&s->ev0));
     WBX_CUDA(cudaEventCreate(&s->ev1));
+    WBX_CUDA(cudaEventCreate(&s->ev_mid));
     WBX_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -1994,6 +1996,7 @@ void solver_free(wbx_solver* s) {
     cudaStreamSynchronize(s->ctx->stream);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->ev_mid) cudaEventDestroy(s->ev_mid);
     delete s;
 }
 
@@ -2053,6 +2056,13 @@ int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_
         if (cudaEventElapsedTime(&ms, s->ev0, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
         *solve_ms = ms;
     }
+    return WBX_OK;
+}
+
+int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms) {
+    if (!s || !tau_ms || !iters_ms) return WBX_INVALID_ARGUMENT;
+    if (cudaEventElapsedTime(tau_ms, s->ev0, s->ev_mid) != cudaSuccess) return WBX_CUDA_ERROR;
+    if (cudaEventElapsedTime(iters_ms, s->ev_mid, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
     return WBX_OK;
 }
 

@@ -876,6 +876,12 @@ class Deblurrer:
         _check(lib.wbx_solver_last_stats(self.handle, C.byref(launches), C.byref(ms)))
         return int(launches.value), float(ms.value)
 
+    def phase_ms(self):
+        """(estimate_step ms, iteration-kernel ms) of the last solve (device events)."""
+        t, i = C.c_float(), C.c_float()
+        _check(lib.wbx_solver_phase_ms(self.handle, C.byref(t), C.byref(i)))
+        return float(t.value), float(i.value)
+
     def __del__(self):
         if getattr(self, "handle", None):
             lib.wbx_solver_destroy(self.handle)
