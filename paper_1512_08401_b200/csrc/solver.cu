@@ -558,21 +558,22 @@ __device__ int g_debug_mode = 0;
 #ifndef WBX_WIN_NB
 #define WBX_WIN_NB 4
 #endif
-__device__ unsigned long long g_prof[6];
+__device__ unsigned long long g_prof[8];
 
 }  // namespace
 }  // namespace wbx
 
-extern "C" int wbx_diag_slice_profile(double* out4) {
-    unsigned long long h[6];
+extern "C" int wbx_diag_slice_profile(double* out) {
+    unsigned long long h[8];
     if (cudaMemcpyFromSymbol(h, wbx::g_prof, sizeof h) != cudaSuccess) return WBX_CUDA_ERROR;
-    if (WBX_PROFILE == 3) {  // window engine: totals, slot 4 = max cycles of one warp's slice loop
-        for (int i = 0; i < 6; ++i) out4[i] = static_cast<double>(h[i]);
+    if (WBX_PROFILE == 3) {  // window engine: raw cycle totals (8 slots, see WinProf)
+        for (int i = 0; i < 8; ++i) out[i] = static_cast<double>(h[i]);
     } else {
-        for (int i = 0; i < 5; ++i) out4[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
-        out4[5] = static_cast<double>(h[5]);
+        for (int i = 0; i < 5; ++i) out[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
+        out[5] = static_cast<double>(h[5]);
+        out[6] = out[7] = 0.0;
     }
-    const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(wbx::g_prof, z, sizeof z);
     return WBX_OK;
 }
@@ -1054,15 +1055,15 @@ __device__ __forceinline__ void win_load(const uint4* rec_base, const uint4& sl,
     }
 }
 
-// WBX_PROFILE=3: per-warp cycle accounting of the window engine
-// [fill, slice loop, slices, barrier, max slice loop] (wbx_diag_slice_profile)
+// WBX_PROFILE=3: per-warp cycle accounting of the window engine (wbx_diag_slice_profile)
 struct WinProf {
-    unsigned long long c[5] = {0, 0, 0, 0, 0};
+    // [A fill, A slice loop, A barrier, T fill, T slice loop, T barrier, A data wait,
+    //  T data wait] (cycles, summed)
+    unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int side = 0;  // 0 = phase A, 3 = phase T (set before each phase, used by the timers)
     __device__ __forceinline__ void flush() {
-        if (WBX_PROFILE == 3 && (threadIdx.x & 31) == 0) {
-            for (int i = 0; i < 4; ++i) atomicAdd(&g_prof[i], c[i]);
-            atomicMax(&g_prof[4], c[4]);
-        }
+        if (WBX_PROFILE == 3 && (threadIdx.x & 31) == 0)
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[i], c[i]);
     }
 };
 
@@ -1136,30 +1137,46 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     // sb < ns, sb from db
     auto run2 = [&](const WinSlice<DICT>& da, uint32_t sa, const WinSlice<DICT>& db, uint32_t sb) {
         const bool hb = sb < ns;
+        if (WBX_PROFILE == 3) {  // time until this pair's record data has arrived
+            const long long w0 = clock64();
+            long long w1;
+            asm volatile(
+                "{\n\t.reg .u32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 t, t, %3;\n\tadd.u32 t, t, %4;\n\t"
+                "mov.u64 %0, %%clock64;\n\t}"
+                : "=l"(w1)
+                : "r"(da.pb), "r"(da.c[0].x), "r"(db.pb), "r"(db.c[0].x)
+                : "memory");
+            pf.c[6 + pf.side / 3] += w1 - w0;
+        }
         const uint4 la = stab[sa];
         const uint4 lb = hb ? stab[sb] : make_uint4(0, 1u << 16, 0, 0);
         const uint32_t nqa = la.y & 0xffu, ma = (la.y >> 8) & 0xffu, nsa = (la.y >> 16) & 0xffu, ca = la.y >> 24;
         const uint32_t nqb = lb.y & 0xffu, mb = (lb.y >> 8) & 0xffu, nsb = (lb.y >> 16) & 0xffu, cb = lb.y >> 24;
         ACC aa = ACC(0), ab = ACC(0);
+        // both slices in one basic block per quad (their latency chains interleave); a quad
+        // beyond a slice's own count contributes exact zeros through window entry 0
+        const uint32_t nqm = nqa > nqb ? nqa : nqb;
+        const uint32_t pa = da.pb, pbb = hb ? db.pb : 0u;
 #pragma unroll
         for (uint32_t qd = 0; qd < 4; ++qd) {
-            if (qd < nqa) {
-                const float4 v = *reinterpret_cast<const float4*>(dict + da.pb + qd * 4);
-                const WIN g0 = win[da.c[qd].x & 0xffffu], g1 = win[da.c[qd].x >> 16];
-                const WIN g2 = win[da.c[qd].y & 0xffffu], g3 = win[da.c[qd].y >> 16];
-                aa = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), aa);
-                aa = fma(static_cast<ACC>(v.y), static_cast<ACC>(g1), aa);
-                aa = fma(static_cast<ACC>(v.z), static_cast<ACC>(g2), aa);
-                aa = fma(static_cast<ACC>(v.w), static_cast<ACC>(g3), aa);
-            }
-            if (qd < nqb) {
-                const float4 v = *reinterpret_cast<const float4*>(dict + db.pb + qd * 4);
-                const WIN g0 = win[db.c[qd].x & 0xffffu], g1 = win[db.c[qd].x >> 16];
-                const WIN g2 = win[db.c[qd].y & 0xffffu], g3 = win[db.c[qd].y >> 16];
-                ab = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), ab);
-                ab = fma(static_cast<ACC>(v.y), static_cast<ACC>(g1), ab);
-                ab = fma(static_cast<ACC>(v.z), static_cast<ACC>(g2), ab);
-                ab = fma(static_cast<ACC>(v.w), static_cast<ACC>(g3), ab);
+            if (qd < nqm) {
+                const bool ia = qd < nqa, ib = qd < nqb;
+                float4 va = *reinterpret_cast<const float4*>(dict + pa + qd * 4);
+                float4 vb = *reinterpret_cast<const float4*>(dict + pbb + qd * 4);
+                const uint2 ca = ia ? da.c[qd] : make_uint2(0, 0);
+                const uint2 cb = ib ? db.c[qd] : make_uint2(0, 0);
+                if (!ia) va = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!ib) vb = make_float4(0.f, 0.f, 0.f, 0.f);
+                const WIN a0 = win[ca.x & 0xffffu], a1 = win[ca.x >> 16], a2 = win[ca.y & 0xffffu], a3 = win[ca.y >> 16];
+                const WIN b0 = win[cb.x & 0xffffu], b1 = win[cb.x >> 16], b2 = win[cb.y & 0xffffu], b3 = win[cb.y >> 16];
+                aa = fma(static_cast<ACC>(va.x), static_cast<ACC>(a0), aa);
+                ab = fma(static_cast<ACC>(vb.x), static_cast<ACC>(b0), ab);
+                aa = fma(static_cast<ACC>(va.y), static_cast<ACC>(a1), aa);
+                ab = fma(static_cast<ACC>(vb.y), static_cast<ACC>(b1), ab);
+                aa = fma(static_cast<ACC>(va.z), static_cast<ACC>(a2), aa);
+                ab = fma(static_cast<ACC>(vb.z), static_cast<ACC>(b2), ab);
+                aa = fma(static_cast<ACC>(va.w), static_cast<ACC>(a3), aa);
+                ab = fma(static_cast<ACC>(vb.w), static_cast<ACC>(b3), ab);
             }
         }
         const uint32_t nsm = nsa > nsb ? nsa : nsb;
@@ -1201,10 +1218,8 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     }
     if (WBX_PROFILE == 3) {
         const long long t2 = clock64();
-        pf.c[0] += t1 - t0;
-        pf.c[1] += t2 - t1;
-        pf.c[2] += ns > wib ? (ns - wib + kWarpsPerBlock - 1) / kWarpsPerBlock : 0;
-        pf.c[4] = max(pf.c[4], static_cast<unsigned long long>(t2 - t1));
+        pf.c[pf.side] += t1 - t0;
+        pf.c[pf.side + 1] += t2 - t1;
     }
     __syncthreads();  // the window is refilled by the next phase
 }
@@ -1240,13 +1255,15 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     auto sync = [&]() {
         const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
-        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
+        if (WBX_PROFILE == 3) pf.c[pf.side + 2] += clock64() - b0;
     };
     for (int k = 1; k <= a.max_iters; ++k) {
+        pf.side = 0;
         win_phase<float, float, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
                                           [&](uint32_t r, float acc) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
         sync();
         const float beta = a.beta32[k - 1];
+        pf.side = 3;
         win_phase<float, float, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
                                           [&](uint32_t c, float g) {
                                               float4& s = cs[c - ws.rT0];
@@ -1265,8 +1282,10 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
 }
 
-// estimate_step on the window engine (fp64 window and accumulation, fp32 operator values)
-template <bool DICT>
+// estimate_step on the window engine: fp64 accumulation, own state and reductions; fp32
+// operator values; vector windows in WINT (float: the gathered u and t entries are rounded
+// to fp32, the products are exact in fp64; double: fp64 windows, WBX_TAU_WINDOW=64)
+template <bool DICT, typename WINT>
 __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs a) {
     constexpr int NB = DICT ? WBX_WIN_NB : 2;
     __shared__ double smem[kWarpsPerBlock + 1];
@@ -1276,8 +1295,11 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
     const WinSmem ws = win_smem_init<0, 16>(dsmem, a);
-    double* win = static_cast<double*>(ws.win);
+    WINT* win = static_cast<WINT*>(ws.win);
     double2* cs = static_cast<double2*>(ws.ownT);  // {P^-1/2, w} of the CTA's coordinates
+    constexpr bool W64 = sizeof(WINT) == 8;
+    WINT* uC = W64 ? reinterpret_cast<WINT*>(a.uC) : static_cast<WINT*>(a.yC);  // u = P^-1/2 w on C
+    WINT* tR = W64 ? reinterpret_cast<WINT*>(a.t64) : static_cast<WINT*>(a.res);  // t = Theta u on R
     double s2[1] = {0.0};
     for (uint64_t i = gthread; i < a.n; i += nthreads) {
         const double v = rng_normal(0x5eedull, i);
@@ -1288,7 +1310,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
         const double v = rng_normal(0x5eedull, a.C_glob[c]);
         const double isp = a.ispC[c];
         cs[i] = make_double2(isp, v);
-        a.uC[c] = isp * v;
+        uC[c] = static_cast<WINT>(isp * v);
     }
     grid_sync_reduce<1>(a.sync, epoch, s2, smem);
     double nw_prev = sqrt(s2[0]);
@@ -1299,7 +1321,8 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     __shared__ double red[2];
     const unsigned G = gridDim.x;
     // staging of the 2 x G block partials, after the window
-    double* pstage = win + (a.wA.max_u > a.wT.max_u ? a.wA.max_u : a.wT.max_u);
+    double* pstage = reinterpret_cast<double*>(
+        static_cast<unsigned char*>(ws.win) + win_align16((a.wA.max_u > a.wT.max_u ? a.wA.max_u : a.wT.max_u) * sizeof(WINT)));
     // Deferred reduction: phase A computes Theta u WITHOUT the 1/|w_prev| normalisation (it is
     // applied to Theta^T t in phase T instead), so A does not wait for the previous
     // iteration's grid reduction; the block partials of iteration it-1 are summed by warp 0
@@ -1313,9 +1336,10 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
                              "l"(part + i) : "memory");
             }
+        pf.side = 0;
         if (it < 200)
-            win_phase<double, double, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, a.uC, win,
-                                                [&](uint32_t r, double t) { a.t64[r] = t; }, pf);
+            win_phase<double, WINT, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
+                                              [&](uint32_t r, double t) { tR[r] = static_cast<WINT>(t); }, pf);
         if (it > 0 && threadIdx.x < 32) {
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
             __syncwarp();
@@ -1333,7 +1357,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
         }
         const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
-        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b0;
+        if (WBX_PROFILE == 3) pf.c[pf.side + 2] += clock64() - b0;
         if (it > 0) {  // stopping test of iteration it-1 (solver.cpp:84-88)
             const double lambda = red[0];
             const double nw = sqrt(red[1]);
@@ -1354,29 +1378,39 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
             iters = 200;
             break;
         }
-        const double inv = nw_prev;
+        const double rinv = 1.0 / nw_prev;
         double acc[2] = {0.0, 0.0};
-        win_phase<double, double, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, a.t64, win,
+        pf.side = 3;
+        win_phase<double, WINT, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
                                             [&](uint32_t c, double g) {
                                                 double2& s = cs[c - ws.rT0];
-                                                const double w = (g / inv) * s.x;
-                                                const double v = s.y / inv;
+                                                const double w = (g * rinv) * s.x;
+                                                const double v = s.y * rinv;
                                                 acc[0] += v * w;
                                                 acc[1] += w * w;
                                                 s.y = w;
-                                                a.uC[c] = s.x * w;
+                                                uC[c] = static_cast<WINT>(s.x * w);
                                             },
                                             pf);
         double* wpart = a.sync.part + static_cast<uint64_t>(it & 1) * kRedSlots * G;
-        const double s0 = block_sum<kBlock>(acc[0], smem);
-        const double s1 = block_sum<kBlock>(acc[1], smem);
-        if (threadIdx.x == 0) {
-            wpart[blockIdx.x] = s0;
-            wpart[G + blockIdx.x] = s1;
+        {  // block partials of both sums, one fixed tree
+            __shared__ double2 bs[kWarpsPerBlock];
+            const double s0 = warp_sum(acc[0]), s1 = warp_sum(acc[1]);
+            if ((threadIdx.x & 31) == 0) bs[threadIdx.x >> 5] = make_double2(s0, s1);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t0 = 0.0, t1 = 0.0;
+                for (int k = 0; k < kWarpsPerBlock; ++k) {
+                    t0 += bs[k].x;
+                    t1 += bs[k].y;
+                }
+                wpart[blockIdx.x] = t0;
+                wpart[G + blockIdx.x] = t1;
+            }
         }
         const long long b1 = WBX_PROFILE == 3 ? clock64() : 0;
         grid_sync(a.sync, epoch, smem);
-        if (WBX_PROFILE == 3) pf.c[3] += clock64() - b1;
+        if (WBX_PROFILE == 3) pf.c[pf.side + 2] += clock64() - b1;
     }
     it = iters;
     pf.flush();
@@ -1613,7 +1647,7 @@ struct wbx_solver {
     int grid_fista = 0, grid_tau = 0;
     int nslots = 3;  // TMA slots in flight per warp
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
-    bool win = false, win_dict = false;
+    bool win = false, win_dict = false, tau_win64 = false;
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     wbx::WinSide wA, wT;
@@ -1719,6 +1753,14 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     return a;
 }
 
+const void* tau_win_fn(bool dict, bool w64) {
+    if (dict)
+        return w64 ? reinterpret_cast<const void*>(tau_win_kernel<true, double>)
+                   : reinterpret_cast<const void*>(tau_win_kernel<true, float>);
+    return w64 ? reinterpret_cast<const void*>(tau_win_kernel<false, double>)
+               : reinterpret_cast<const void*>(tau_win_kernel<false, float>);
+}
+
 void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st) {
     if (a.sync.mode == 2)  // the counter barrier counts from zero in every launch
         WBX_CUDA(cudaMemsetAsync(a.sync.gen + kCounterWord, 0, sizeof(unsigned), st));
@@ -1741,8 +1783,7 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
-        const void* k = s->win_dict ? reinterpret_cast<const void*>(tau_win_kernel<true>)
-                                    : reinterpret_cast<const void*>(tau_win_kernel<false>);
+        const void* k = tau_win_fn(s->win_dict, s->tau_win64);
         launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
@@ -1824,12 +1865,13 @@ void alloc_state(wbx_solver* s) {
             const WinView vA = view_of(s->wA), vT = view_of(s->wT);
             const unsigned mu = std::max(s->wA.max_u, s->wT.max_u);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
-            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + mu * 8u + 16u * G;  // + partials staging
+            s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
+            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
+                              16u * G;  // + partials staging
             s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
             const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                          : reinterpret_cast<const void*>(fista_win_kernel<false>);
-            const void* kt = s->win_dict ? reinterpret_cast<const void*>(tau_win_kernel<true>)
-                                         : reinterpret_cast<const void*>(tau_win_kernel<false>);
+            const void* kt = tau_win_fn(s->win_dict, s->tau_win64);
             const unsigned limit = bps == 2 ? 110u * 1024u : 220u * 1024u;
             if (s->win_smem_tau > limit) continue;
             WBX_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,

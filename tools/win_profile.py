@@ -1,7 +1,7 @@
 """Cycle accounting of the window engine (needs the diagnostics build):
   make -C paper_1512_08401_b200 prof && WBX_LIB=paper_1512_08401_b200/lib/libwbx_prof.so python tools/win_profile.py
-Per warp and phase: fill (window cp.async + barrier wait of the CTA), slice loop, slices,
-barrier, and the slowest warp's slice loop, in SM cycles."""
+Per warp and phase of each side (A = Theta rows, T = Theta^T rows), in SM cycles: window
+fill, slice loop, grid barrier (incl. waiting for the slowest CTA)."""
 import ctypes as C
 import json
 import sys
@@ -20,7 +20,7 @@ P = W.spai(op, ctx)
 w = W.scale_weights(basis.layout)
 x0 = W.analyze(u0, basis, ctx).values
 prob = W.DeblurProblem(W.SparseThetaOp(op, ctx), x0, w, 1e-4)
-buf = (C.c_double * 6)()
+buf = (C.c_double * 8)()
 res = {}
 for name, cfg, phases in [("fista", dict(max_iters=100, tau=meta["tau"]), 200), ("tau", dict(max_iters=0), None)]:
     W.fista(prob, P, W.SolverConfig(track_energy=False, precision=32, **cfg), ctx)
@@ -28,10 +28,12 @@ for name, cfg, phases in [("fista", dict(max_iters=100, tau=meta["tau"]), 200), 
     r = W.fista(prob, P, W.SolverConfig(track_energy=False, precision=32, **cfg), ctx)
     lib.wbx_diag_slice_profile(buf)
     h = list(buf)
-    nph = phases if phases else 2 * r.tau_iters
+    nph = phases // 2 if phases else r.tau_iters  # phases of each side
     warps = 296 * 8
     per = warps * nph
     res[name] = {"ms": round(r.wall_time_s * 1e3, 3), "phases": nph,
-                 "fill_cyc": round(h[0] / per), "loop_cyc": round(h[1] / per), "slices_per_warp": round(h[2] / per, 2),
-                 "barrier_cyc": round(h[3] / per), "max_loop_cyc": int(h[4])}
+                 "A": {"fill": round(h[0] / per), "loop": round(h[1] / per), "data_wait": round(h[6] / per),
+                       "barrier": round(h[2] / per)},
+                 "T": {"fill": round(h[3] / per), "loop": round(h[4] / per), "data_wait": round(h[7] / per),
+                       "barrier": round(h[5] / per)}}
 print(json.dumps(res))
