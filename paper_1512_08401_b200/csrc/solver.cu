@@ -556,7 +556,11 @@ __device__ int g_debug_mode = 0;
 // 2 = per-slice cycle accounting: [tma wait, load+gather+fma, combine+issue+epilogue, slices]
 // Window engine lookahead (dictionary format): 3 = three slices in flight, 4 = two pairs
 #ifndef WBX_WIN_NB
-#define WBX_WIN_NB 4
+#define WBX_WIN_NB 2
+#endif
+// Per-lane register cache of the last dictionary block (single-slice mode)
+#ifndef WBX_DICT_CACHE
+#define WBX_DICT_CACHE 1
 #endif
 __device__ unsigned long long g_prof[8];
 
@@ -973,6 +977,8 @@ __host__ __device__ constexpr uint32_t win_align16(uint32_t b) { return (b + 15u
 struct WinSmem {
     uint32_t* uA;
     uint32_t* uT;
+    uint16_t* usA;  // window slot of each entry
+    uint16_t* usT;
     uint4* sA;
     uint4* sT;
     float* dA;
@@ -986,7 +992,8 @@ struct WinSmem {
 
 template <uint32_t OWN_A, uint32_t OWN_T>
 __host__ __device__ inline uint32_t win_smem_head(const WinView& A, const WinView& T) {
-    return win_align16(A.max_u * 4u) + win_align16(T.max_u * 4u) + 16u * (A.max_slices + T.max_slices) +
+    return win_align16(A.max_u * 4u) + win_align16(T.max_u * 4u) + win_align16(A.max_u * 2u) +
+           win_align16(T.max_u * 2u) + 16u * (A.max_slices + T.max_slices) +
            win_align16(A.max_dict * 4u) + win_align16(T.max_dict * 4u) + win_align16(A.max_rows * OWN_A) +
            win_align16(T.max_rows * OWN_T);
 }
@@ -1011,6 +1018,8 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     };
     w.uA = reinterpret_cast<uint32_t*>(carve(win_align16(a.wA.max_u * 4u)));
     w.uT = reinterpret_cast<uint32_t*>(carve(win_align16(a.wT.max_u * 4u)));
+    w.usA = reinterpret_cast<uint16_t*>(carve(win_align16(a.wA.max_u * 2u)));
+    w.usT = reinterpret_cast<uint16_t*>(carve(win_align16(a.wT.max_u * 2u)));
     w.sA = reinterpret_cast<uint4*>(carve(16u * a.wA.max_slices));
     w.sT = reinterpret_cast<uint4*>(carve(16u * a.wT.max_slices));
     w.dA = reinterpret_cast<float*>(carve(win_align16(a.wA.max_dict * 4u)));
@@ -1020,6 +1029,8 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     w.win = p;
     for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
     for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.usT[i] = a.wT.u_slot[a.wT.u_off[b] + i];
     for (uint32_t i = threadIdx.x; i < w.nsA; i += kBlock) w.sA[i] = a.wA.s_tab[a.wA.s_off[b] + i];
     for (uint32_t i = threadIdx.x; i < w.nsT; i += kBlock) w.sT[i] = a.wT.s_tab[a.wT.s_off[b] + i];
     if (a.wA.max_dict)
@@ -1073,7 +1084,8 @@ struct WinProf {
 // record loads in flight; the vector operand and (dictionary format) the values come from
 // shared memory.
 template <typename ACC, typename WIN, bool DICT, int NB, typename X, typename Post>
-__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, uint32_t nu, const uint4* stab,
+__device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, const uint16_t* uslot, uint32_t nu,
+                                          const uint4* stab,
                                           uint32_t ns, const float* dict, const X* __restrict__ x, WIN* win,
                                           Post post, WinProf& pf) {
     static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
@@ -1089,7 +1101,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     if (NB == 4 && wib + 3 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 3 * kWarpsPerBlock], lane, pol, b3);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
     for (uint32_t i = threadIdx.x; i < nu; i += kBlock) {
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + i));
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
                      : "memory");
     }
@@ -1097,17 +1109,27 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     __syncthreads();
     const long long t1 = WBX_PROFILE == 3 ? clock64() : 0;
     // process slice s from d
+    // dictionary values of the lane's last segment block: consecutive slices of a warp are
+    // mostly the same band rows at the same positions, so a lane's block rarely changes and
+    // the reload (4 x LDS.128) is skipped
+    uint32_t cpb = 0xffffffffu;
+    float4 cv[4];
     auto run = [&](const WinSlice<DICT>& d, uint32_t s) {
         const uint4 sl = stab[s];  // {record offset, meta, first row, -}
         const uint32_t nq = sl.y & 0xffu, m = (sl.y >> 8) & 0xffu, nseg = (sl.y >> 16) & 0xffu;
         const uint32_t cnt = sl.y >> 24;
+        if (DICT && WBX_DICT_CACHE && d.pb != cpb) {
+            cpb = d.pb;
+#pragma unroll
+            for (uint32_t qd = 0; qd < 4; ++qd) cv[qd] = *reinterpret_cast<const float4*>(dict + cpb + qd * 4);
+        }
         ACC acc = ACC(0);
 #pragma unroll
         for (uint32_t qd = 0; qd < 4; ++qd) {
             if (qd < nq) {
                 float4 v;
                 if (DICT) {
-                    v = *reinterpret_cast<const float4*>(dict + d.pb + qd * 4);
+                    v = WBX_DICT_CACHE ? cv[qd] : *reinterpret_cast<const float4*>(dict + d.pb + qd * 4);
                 } else {
                     v = make_float4(__uint_as_float(d.v[qd].x), __uint_as_float(d.v[qd].y),
                                     __uint_as_float(d.v[qd].z), __uint_as_float(d.v[qd].w));
@@ -1259,12 +1281,12 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     };
     for (int k = 1; k <= a.max_iters; ++k) {
         pf.side = 0;
-        win_phase<float, float, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
+        win_phase<float, float, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
                                           [&](uint32_t r, float acc) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
         sync();
         const float beta = a.beta32[k - 1];
         pf.side = 3;
-        win_phase<float, float, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
+        win_phase<float, float, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
                                           [&](uint32_t c, float g) {
                                               float4& s = cs[c - ws.rT0];
                                               const float z0 = fmaf(-s.z, g, s.x);
@@ -1322,7 +1344,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
     const unsigned G = gridDim.x;
     // staging of the 2 x G block partials, after the window
     double* pstage = reinterpret_cast<double*>(
-        static_cast<unsigned char*>(ws.win) + win_align16((a.wA.max_u > a.wT.max_u ? a.wA.max_u : a.wT.max_u) * sizeof(WINT)));
+        static_cast<unsigned char*>(ws.win) + win_align16((a.wA.max_win > a.wT.max_win ? a.wA.max_win : a.wT.max_win) * sizeof(WINT)));
     // Deferred reduction: phase A computes Theta u WITHOUT the 1/|w_prev| normalisation (it is
     // applied to Theta^T t in phase T instead), so A does not wait for the previous
     // iteration's grid reduction; the block partials of iteration it-1 are summed by warp 0
@@ -1338,7 +1360,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
             }
         pf.side = 0;
         if (it < 200)
-            win_phase<double, WINT, DICT, NB>(a.wA, ws.uA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
+            win_phase<double, WINT, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
                                               [&](uint32_t r, double t) { tR[r] = static_cast<WINT>(t); }, pf);
         if (it > 0 && threadIdx.x < 32) {
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -1381,7 +1403,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
         const double rinv = 1.0 / nw_prev;
         double acc[2] = {0.0, 0.0};
         pf.side = 3;
-        win_phase<double, WINT, DICT, NB>(a.wT, ws.uT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
+        win_phase<double, WINT, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
                                             [&](uint32_t c, double g) {
                                                 double2& s = cs[c - ws.rT0];
                                                 const double w = (g * rinv) * s.x;
@@ -1863,7 +1885,7 @@ void alloc_state(wbx_solver* s) {
                 continue;  // a window exceeded 16-bit local indices
             }
             const WinView vA = view_of(s->wA), vT = view_of(s->wT);
-            const unsigned mu = std::max(s->wA.max_u, s->wT.max_u);
+            const unsigned mu = std::max(s->wA.max_win, s->wT.max_win);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
             s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
             s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +

@@ -32,13 +32,15 @@ constexpr uint32_t kWinDictBudget = 16384;  // bytes of dictionary per CTA and s
 struct WinView {
     const uint32_t* u_off;   // [G+1] window offsets into u_idx
     const uint32_t* u_idx;   // window entries: positions in the source vector
+    const uint16_t* u_slot;  // shared-memory slot of each window entry (bank-aware placement)
     const uint32_t* s_off;   // [G+1] slice offsets of each CTA
     const uint4* s_tab;      // per slice {record offset (uint4), meta, first row, 0}
     const uint32_t* r_off;   // [G+1] first compacted row of each CTA (rows are contiguous)
     const uint32_t* d_off;   // [G+1] dictionary offsets (floats) of each CTA (dictionary format)
     const float* d_val;      // dictionaries: per CTA a zero block then q x 16-value blocks per sequence
     const uint4* rec;
-    uint32_t max_u;          // largest window of any CTA
+    uint32_t max_u;          // most window entries of any CTA
+    uint32_t max_win;        // largest window slot extent of any CTA (>= max_u)
     uint32_t max_rows;       // most rows of any CTA (per-row state owned in shared memory)
     uint32_t max_slices;     // most slices of any CTA
     uint32_t max_dict;       // largest dictionary of any CTA (floats; 0 = full format)

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
 
 #include "internal.hpp"
 #include "win.cuh"
@@ -73,6 +74,72 @@ bool build_dict(const HostCompact& M, uint64_t r0, uint64_t r1, std::vector<floa
     return true;
 }
 
+// Greedy bank assignment of one CTA's window (nu entries, ranks 0..nu-1) from the gather
+// groups of its slices (slices slice0.. in s_tab/rec, columns as ranks): larger groups
+// first; each unplaced member goes to the bank least used by the group so far (ties: the
+// least filled bank). slot = bank + 32 * (fill of that bank). Returns rank -> slot; updates
+// *max_win with the window's slot extent. WBX_WIN_PLACE=sorted keeps slot = rank.
+std::vector<uint16_t> place_window(const std::vector<uint4>& rec, const std::vector<uint4>& s_tab, size_t slice0,
+                                   bool dict_fmt, size_t nu, uint32_t* max_win) {
+    std::vector<uint16_t> slot(nu);
+    const char* mode = std::getenv("WBX_WIN_PLACE");
+    if (mode && std::string(mode) == "sorted") {
+        for (size_t i = 0; i < nu; ++i) slot[i] = static_cast<uint16_t>(i);
+        *max_win = std::max<uint32_t>(*max_win, static_cast<uint32_t>(nu));
+        return slot;
+    }
+    constexpr int kBanks = 32;
+    std::vector<std::vector<uint16_t>> groups;
+    for (size_t sidx = slice0; sidx < s_tab.size(); ++sidx) {
+        const uint32_t nq = s_tab[sidx].y & 0xffu;
+        const uint16_t* cols = reinterpret_cast<const uint16_t*>(&rec[s_tab[sidx].x + (dict_fmt ? 4 : nq * 32)]);
+        for (uint32_t qd = 0; qd < nq; ++qd)
+            for (uint32_t e = 0; e < 4; ++e) {
+                std::vector<uint16_t> g;
+                for (uint32_t lane = 0; lane < 32; ++lane) g.push_back(cols[(qd * 32 + lane) * 4 + e]);
+                std::sort(g.begin(), g.end());
+                g.erase(std::unique(g.begin(), g.end()), g.end());
+                if (g.size() > 1) groups.push_back(std::move(g));
+            }
+    }
+    std::stable_sort(groups.begin(), groups.end(),
+                     [](const std::vector<uint16_t>& x, const std::vector<uint16_t>& y) { return x.size() > y.size(); });
+    std::vector<int> bank(nu, -1);
+    std::vector<uint32_t> fill(kBanks, 0);
+    for (const auto& g : groups) {
+        int used[kBanks] = {0};
+        for (uint16_t e : g)
+            if (bank[e] >= 0) ++used[bank[e]];
+        for (uint16_t e : g) {
+            if (bank[e] >= 0) continue;
+            int best = 0;
+            for (int k = 1; k < kBanks; ++k)
+                if (used[k] < used[best] || (used[k] == used[best] && fill[k] < fill[best])) best = k;
+            bank[e] = best;
+            ++used[best];
+            ++fill[best];
+        }
+    }
+    for (size_t i = 0; i < nu; ++i)  // entries no group constrains (only in 1-distinct groups)
+        if (bank[i] < 0) {
+            int best = 0;
+            for (int k = 1; k < kBanks; ++k)
+                if (fill[k] < fill[best]) best = k;
+            bank[i] = best;
+            ++fill[best];
+        }
+    std::vector<uint32_t> next(kBanks, 0);
+    uint32_t extent = 0;
+    for (size_t i = 0; i < nu; ++i) {
+        const uint32_t sl = static_cast<uint32_t>(bank[i]) + kBanks * next[bank[i]]++;
+        if (sl > 0xffffu) fail(WBX_TOO_LARGE, "CTA window exceeds 16-bit slots");
+        slot[i] = static_cast<uint16_t>(sl);
+        extent = std::max(extent, sl + 1);
+    }
+    *max_win = std::max(*max_win, extent);
+    return slot;
+}
+
 }  // namespace
 
 void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) {
@@ -86,7 +153,8 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) 
     std::vector<uint32_t> u_off(G + 1, 0), u_idx, s_off(G + 1, 0), d_off(G + 1, 0);
     std::vector<uint4> s_tab, rec;
     std::vector<float> d_val;
-    uint32_t max_u = 0, max_slices = 0, max_dict = 0;
+    uint32_t max_u = 0, max_slices = 0, max_dict = 0, max_win = 0;
+    std::vector<uint16_t> u_slot;
     for (uint32_t b = 0; b < G; ++b) {
         const uint64_t r0 = rb[b], r1 = rb[b + 1];
         // window: sorted unique referenced positions
@@ -155,6 +223,16 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) 
         }
         s_off[b + 1] = static_cast<uint32_t>(s_tab.size());
         max_slices = std::max<uint32_t>(max_slices, static_cast<uint32_t>(s_tab.size() - slice0));
+        // bank-aware placement of the window: the entries one gather instruction reads (one
+        // element position across the 32 lanes of a slice) go to distinct shared-memory
+        // banks where possible; records are rewritten from ranks to slots
+        const std::vector<uint16_t> slot = place_window(rec, s_tab, slice0, dict_fmt, u.size(), &max_win);
+        for (size_t sidx = slice0; sidx < s_tab.size(); ++sidx) {
+            const uint32_t nq = s_tab[sidx].y & 0xffu;
+            uint16_t* cols = reinterpret_cast<uint16_t*>(&rec[s_tab[sidx].x + (dict_fmt ? 4 : nq * 32)]);
+            for (uint32_t e = 0; e < nq * 128; ++e) cols[e] = slot[cols[e]];
+        }
+        u_slot.insert(u_slot.end(), slot.begin(), slot.end());
     }
     std::vector<uint32_t> r_off(G + 1);
     uint32_t max_rows = 0;
@@ -163,23 +241,26 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) 
         if (b < G) max_rows = std::max<uint32_t>(max_rows, static_cast<uint32_t>(rb[b + 1] - rb[b]));
     }
     if (u_idx.empty()) u_idx.push_back(0);
+    if (u_slot.empty()) u_slot.push_back(0);
     if (s_tab.empty()) s_tab.push_back(make_uint4(0, 0, 0, 0));
     if (rec.empty()) rec.resize(1, make_uint4(0, 0, 0, 0));
     if (d_val.empty()) d_val.push_back(0.0f);
     out.G = G;
     out.max_u = max_u;
+    out.max_win = std::max(max_win, max_u);
     out.max_rows = max_rows;
     out.max_slices = max_slices;
     out.max_dict = dict_fmt ? max_dict : 0;
     out.r_off.upload(r_off, st);
     out.u_off.upload(u_off, st);
     out.u_idx.upload(u_idx, st);
+    out.u_slot.upload(u_slot, st);
     out.s_off.upload(s_off, st);
     out.s_tab.upload(s_tab, st);
     out.d_off.upload(d_off, st);
     out.d_val.upload(d_val, st);
     out.rec.upload(rec, st);
-    out.bytes = out.r_off.bytes() + out.u_off.bytes() + out.u_idx.bytes() + out.s_off.bytes() + out.s_tab.bytes() +
+    out.bytes = out.r_off.bytes() + out.u_off.bytes() + out.u_idx.bytes() + out.u_slot.bytes() + out.s_off.bytes() + out.s_tab.bytes() +
                 out.d_off.bytes() + out.d_val.bytes() + out.rec.bytes();
     WBX_CUDA(cudaStreamSynchronize(st));
 }
@@ -188,6 +269,7 @@ WinView view_of(const WinSide& w) {
     WinView v;
     v.u_off = w.u_off.p;
     v.u_idx = w.u_idx.p;
+    v.u_slot = w.u_slot.p;
     v.s_off = w.s_off.p;
     v.s_tab = w.s_tab.p;
     v.r_off = w.r_off.p;
@@ -195,6 +277,7 @@ WinView view_of(const WinSide& w) {
     v.d_val = w.d_val.p;
     v.rec = w.rec.p;
     v.max_u = w.max_u;
+    v.max_win = w.max_win;
     v.max_rows = w.max_rows;
     v.max_slices = w.max_slices;
     v.max_dict = w.max_dict;
