@@ -221,7 +221,7 @@ __device__ __forceinline__ void trace_point(const Sync& s, const Epoch& e, int w
 // published block partials itself in the same fixed order, so all blocks obtain
 // bit-identical totals. Partials are double-buffered by epoch parity (a block cannot
 // run two barriers ahead of any other block).
-template <int NV>
+template <int NV, int BS = kBlock>
 __device__ __forceinline__ void grid_sync_reduce(const Sync& s, Epoch& epoch, double (&v)[NV],
                                                  double* smem) {
     const unsigned G = gridDim.x;
@@ -229,7 +229,7 @@ __device__ __forceinline__ void grid_sync_reduce(const Sync& s, Epoch& epoch, do
     double* part = s.part + static_cast<uint64_t>(epoch.cur & 1u) * kRedSlots * G;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const double b = block_sum<kBlock>(v[k], smem);
+        const double b = block_sum<BS>(v[k], smem);
         if (threadIdx.x == 0) part[k * G + blockIdx.x] = b;
     }
     trace_point(s, epoch, 0);
@@ -964,6 +964,13 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
 }
 
 // ---------------------------------------------------------------- window engine (win.cuh)
+// CTA size of the window engine (WBX_WIN_BLOCK=512: one CTA per SM, experiment)
+#ifndef WBX_WIN_BLOCK
+#define WBX_WIN_BLOCK 256
+#endif
+constexpr int kWinBlock = WBX_WIN_BLOCK;
+constexpr int kWinWarps = kWinBlock / 32;
+constexpr int kWinMinBlocks = 512 / kWinBlock;
 // Shared memory of a CTA:
 //   [uA][uT]          window index lists of the two sides              } loaded once
 //   [sA][sT]          slice tables {record offset, meta, first row}    } per solve
@@ -1027,17 +1034,17 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     w.ownA = carve(win_align16(a.wA.max_rows * OWN_A));
     w.ownT = carve(win_align16(a.wT.max_rows * OWN_T));
     w.win = p;
-    for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuA; i += kBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuT; i += kBlock) w.usT[i] = a.wT.u_slot[a.wT.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nsA; i += kBlock) w.sA[i] = a.wA.s_tab[a.wA.s_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nsT; i += kBlock) w.sT[i] = a.wT.s_tab[a.wT.s_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.usT[i] = a.wT.u_slot[a.wT.u_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nsA; i += kWinBlock) w.sA[i] = a.wA.s_tab[a.wA.s_off[b] + i];
+    for (uint32_t i = threadIdx.x; i < w.nsT; i += kWinBlock) w.sT[i] = a.wT.s_tab[a.wT.s_off[b] + i];
     if (a.wA.max_dict)
-        for (uint32_t i = a.wA.d_off[b] + threadIdx.x; i < a.wA.d_off[b + 1]; i += kBlock)
+        for (uint32_t i = a.wA.d_off[b] + threadIdx.x; i < a.wA.d_off[b + 1]; i += kWinBlock)
             w.dA[i - a.wA.d_off[b]] = a.wA.d_val[i];
     if (a.wT.max_dict)
-        for (uint32_t i = a.wT.d_off[b] + threadIdx.x; i < a.wT.d_off[b + 1]; i += kBlock)
+        for (uint32_t i = a.wT.d_off[b] + threadIdx.x; i < a.wT.d_off[b + 1]; i += kWinBlock)
             w.dT[i - a.wT.d_off[b]] = a.wT.d_val[i];
     __syncthreads();
     return w;
@@ -1096,11 +1103,11 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     const uint64_t pol = l2_keep_policy();
     WinSlice<DICT> b0, b1, b2, b3;
     if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
-    if (NB >= 3 && wib + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + kWarpsPerBlock], lane, pol, b1);
-    if (NB >= 3 && wib + 2 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWarpsPerBlock], lane, pol, b2);
-    if (NB == 4 && wib + 3 * kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[wib + 3 * kWarpsPerBlock], lane, pol, b3);
+    if (NB >= 3 && wib + kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + kWinWarps], lane, pol, b1);
+    if (NB >= 3 && wib + 2 * kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWinWarps], lane, pol, b2);
+    if (NB == 4 && wib + 3 * kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + 3 * kWinWarps], lane, pol, b3);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
-    for (uint32_t i = threadIdx.x; i < nu; i += kBlock) {
+    for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
                      : "memory");
@@ -1152,7 +1159,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     // process slice s from d, then refill d with slice s + NB*8
     auto step = [&](WinSlice<DICT>& d, uint32_t s) {
         run(d, s);
-        const uint32_t sn = s + NB * kWarpsPerBlock;
+        const uint32_t sn = s + NB * kWinWarps;
         if (sn < ns) win_load<DICT>(W.rec, stab[sn], lane, pol, d);
     };
     // two slices at once (independent latency chains interleave): sa from da and, if
@@ -1213,7 +1220,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     };
     if (NB == 4) {
         static_assert(NB != 4 || DICT, "paired slices use the dictionary format");
-        constexpr uint32_t W8 = kWarpsPerBlock;
+        constexpr uint32_t W8 = kWinWarps;
         for (uint32_t s = wib; s < ns; s += 4 * W8) {
             run2(b0, s, b1, s + W8);
             if (s + 4 * W8 < ns) win_load<DICT>(W.rec, stab[s + 4 * W8], lane, pol, b0);
@@ -1224,17 +1231,17 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
             if (s + 7 * W8 < ns) win_load<DICT>(W.rec, stab[s + 7 * W8], lane, pol, b3);
         }
     } else if (NB == 3) {
-        for (uint32_t s = wib; s < ns; s += NB * kWarpsPerBlock) {
+        for (uint32_t s = wib; s < ns; s += NB * kWinWarps) {
             step(b0, s);
-            if (s + kWarpsPerBlock >= ns) break;
-            step(b1, s + kWarpsPerBlock);
-            if (s + 2 * kWarpsPerBlock >= ns) break;
-            step(b2, s + 2 * kWarpsPerBlock);
+            if (s + kWinWarps >= ns) break;
+            step(b1, s + kWinWarps);
+            if (s + 2 * kWinWarps >= ns) break;
+            step(b2, s + 2 * kWinWarps);
         }
     } else {  // two buffers: the next load is issued before the current slice computes
-        for (uint32_t s = wib; s < ns; s += kWarpsPerBlock) {
+        for (uint32_t s = wib; s < ns; s += kWinWarps) {
             b1 = b0;
-            if (s + kWarpsPerBlock < ns) win_load<DICT>(W.rec, stab[s + kWarpsPerBlock], lane, pol, b0);
+            if (s + kWinWarps < ns) win_load<DICT>(W.rec, stab[s + kWinWarps], lane, pol, b0);
             run(b1, s);
         }
     }
@@ -1247,12 +1254,12 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
 }
 
 template <bool DICT>
-__global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(SolveArgs a) {
     constexpr int NB = DICT ? WBX_WIN_NB : 2;
-    __shared__ double smem[kWarpsPerBlock + 1];
+    __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
-    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
     float* yC = static_cast<float*>(a.yC);
@@ -1262,14 +1269,14 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     float* win = static_cast<float*>(ws.win);
     float* x0s = static_cast<float*>(ws.ownA);   // x0 of the CTA's Theta rows
     float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
-    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) {
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) {
         const uint32_t c = ws.rT0 + i;
         const float v = static_cast<float>(a.x0_full[a.C_glob[c]]);
         yC[c] = v;
         cs[i] = make_float4(v, v, static_cast<float>(tau / a.pC[c]),
                             static_cast<float>(thr_exact(tau, a.lambda, a.wC[c], a.pC[c])));
     }
-    for (uint32_t i = threadIdx.x; i < ws.nrA; i += kBlock)
+    for (uint32_t i = threadIdx.x; i < ws.nrA; i += kWinBlock)
         x0s[i] = static_cast<float>(a.x0_full[a.R_glob[ws.rA0 + i]]);
     if (a.decoupled_inline) decoupled_pass<float>(a, tau, a.max_iters, 0, gthread, nthreads, nullptr, nullptr, 0);
     grid_sync(a.sync, epoch, smem);
@@ -1301,19 +1308,19 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_win_kernel(Solve
     }
     pf.flush();
     if (gthread == 0) a.out[OUT_ITERS_USED] = a.max_iters;
-    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
 }
 
 // estimate_step on the window engine: fp64 accumulation, own state and reductions; fp32
 // operator values; vector windows in WINT (float: the gathered u and t entries are rounded
 // to fp32, the products are exact in fp64; double: fp64 windows, WBX_TAU_WINDOW=64)
 template <bool DICT, typename WINT>
-__global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(SolveArgs a) {
     constexpr int NB = DICT ? WBX_WIN_NB : 2;
-    __shared__ double smem[kWarpsPerBlock + 1];
+    __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
-    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
     const WinSmem ws = win_smem_init<0, 16>(dsmem, a);
@@ -1327,14 +1334,14 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
         const double v = rng_normal(0x5eedull, i);
         s2[0] += v * v;
     }
-    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kBlock) {
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) {
         const uint32_t c = ws.rT0 + i;
         const double v = rng_normal(0x5eedull, a.C_glob[c]);
         const double isp = a.ispC[c];
         cs[i] = make_double2(isp, v);
         uC[c] = static_cast<WINT>(isp * v);
     }
-    grid_sync_reduce<1>(a.sync, epoch, s2, smem);
+    grid_sync_reduce<1, kWinBlock>(a.sync, epoch, s2, smem);
     double nw_prev = sqrt(s2[0]);
     double lambda_prev = 0.0;
     int it = 0, iters = 0;
@@ -1416,13 +1423,13 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_win_kernel(SolveArgs
                                             pf);
         double* wpart = a.sync.part + static_cast<uint64_t>(it & 1) * kRedSlots * G;
         {  // block partials of both sums, one fixed tree
-            __shared__ double2 bs[kWarpsPerBlock];
+            __shared__ double2 bs[kWinWarps];
             const double s0 = warp_sum(acc[0]), s1 = warp_sum(acc[1]);
             if ((threadIdx.x & 31) == 0) bs[threadIdx.x >> 5] = make_double2(s0, s1);
             __syncthreads();
             if (threadIdx.x == 0) {
                 double t0 = 0.0, t1 = 0.0;
-                for (int k = 0; k < kWarpsPerBlock; ++k) {
+                for (int k = 0; k < kWinWarps; ++k) {
                     t0 += bs[k].x;
                     t1 += bs[k].y;
                 }
@@ -1783,11 +1790,12 @@ const void* tau_win_fn(bool dict, bool w64) {
                : reinterpret_cast<const void*>(tau_win_kernel<false, float>);
 }
 
-void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st) {
+void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st,
+                      int block = kBlock) {
     if (a.sync.mode == 2)  // the counter barrier counts from zero in every launch
         WBX_CUDA(cudaMemsetAsync(a.sync.gen + kCounterWord, 0, sizeof(unsigned), st));
     void* params[] = {&a};
-    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(kBlock), params, smem, st));
+    WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(block), params, smem, st));
 }
 
 template <typename T>
@@ -1806,7 +1814,7 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
         const void* k = tau_win_fn(s->win_dict, s->tau_win64);
-        launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st);
+        launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st, kWinBlock);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
@@ -1815,7 +1823,7 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     if (win) {
         const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                     : reinterpret_cast<const void*>(fista_win_kernel<false>);
-        launch_coop_smem(k, s->grid_win, s->win_smem_fista, a, st);
+        launch_coop_smem(k, s->grid_win, s->win_smem_fista, a, st, kWinBlock);
         count_launch(ctx);
         WBX_CUDA(cudaGetLastError());
         return;
@@ -1872,11 +1880,12 @@ void alloc_state(wbx_solver* s) {
         s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<4>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     else if (s->batch == 8)
         s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<8>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
-    // window engine: fp32, single image; try 2 then 1 CTA per SM; fall back to the streamed
-    // engine if a CTA's window does not fit (WBX_ENGINE=stream forces the fallback)
+    // window engine: fp32 (single images; batches use it for tau); try 2 then 1 CTA per SM;
+    // fall back to the streamed engine if a CTA's window does not fit (WBX_ENGINE=stream
+    // forces the fallback)
     const char* eng = std::getenv("WBX_ENGINE");
-    if (sizeof(T) == 4 && s->batch == 1 && !(eng && std::string(eng) == "stream")) {
-        for (int bps = 2; bps >= 1 && !s->win; --bps) {
+    if (sizeof(T) == 4 && !(eng && std::string(eng) == "stream")) {  // batches use it for tau
+        for (int bps = kWinMinBlocks; bps >= 1 && !s->win; --bps) {
             const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
             try {
                 build_win(s->wA, s->op->hA, G, s->ctx->stream);
@@ -1901,8 +1910,8 @@ void alloc_state(wbx_solver* s) {
             WBX_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(s->win_smem_tau)));
             int pf = 0, pt = 0;
-            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, kf, kBlock, s->win_smem_fista));
-            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, kt, kBlock, s->win_smem_tau));
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, kf, kWinBlock, s->win_smem_fista));
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, kt, kWinBlock, s->win_smem_tau));
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
