@@ -321,3 +321,23 @@ def test_deblurrer_c2_1024_vs_oracle(golden):
     x_ours = W.analyze(u.reshape(1024, 1024), b).values
     e = W.energy(x_ours, W.DeblurProblem(W.SparseThetaOp(op), W.analyze(u0, b).values, w, 1e-4))
     assert abs(e - g.meta["final_energy"]) < 1e-5 * g.meta["final_energy"]
+
+
+# ----------------------------------------------------------------------------- engine / format variants
+@pytest.mark.parametrize("env", [{}, {"WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"}, {"WBX_TAU_WINDOW": "64"},
+                                 {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
+                                 {"WBX_WIN_COST": "16,1"}])
+def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
+    """Every solver engine / window format / placement / barrier the library can select
+    (environment switches read at solver creation) meets the same parity bar on C1."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = golden("c1_db4_256")
+    op = g.operator()
+    d = W.Deblurrer(op, basis_of(g), W.spai(op), g.weights(), g.meta["lambda"],
+                    W.SolverConfig(max_iters=50, track_energy=False))
+    u, rep = d.deblur(g["u0"], clamp=False)
+    assert abs(rep.tau - g.meta["tau"]) <= 1e-6 * g.meta["tau"]
+    assert rel_l2(u, g["restored"]) <= RTOL_IMAGE
+    u2, _ = d.deblur(g["u0"], clamp=False)
+    assert np.array_equal(u, u2)  # run-to-run deterministic
