@@ -217,9 +217,13 @@ int wbx_solver_batch(const wbx_solver* s);
  * res (fp32, world*maxR), u (fp64, world*maxC), t (fp64, world*maxR). After each phase the
  * caller all-gathers the owned slice (NCCL all_gather over NVLink, or a copy when emulated).
  * Per FISTA iteration k: phase_a -> all-gather res -> phase_t(k) -> all-gather y.
- * Per power iteration: power_a(|w_prev|) -> all-gather t -> power_t(|w_prev|, sums) ->
- * all-reduce the two sums (<v,w>, |w|^2) -> all-gather u. A sharded solve is bitwise equal
- * to the single-GPU fp32 solve given the same tau, for any world size. */
+ * estimate_step (solver.cpp:69-99) stays on the device: bind_power gives the caller-owned
+ * fp64 sums buffer [world][2]; power_begin -> all-gather sums -> power_update(first=1) ->
+ * 200 x { power_step_a -> all-gather t -> power_step_t -> all-gather sums ->
+ * power_update(0) -> all-gather u } -> power_result. Every rank sums the slots in rank
+ * order and applies the stopping rule itself; once stopped the remaining enqueued steps are
+ * no-ops, so the host never waits inside the loop. A sharded solve is bitwise equal to the
+ * single-GPU fp32 solve given the same tau, for any world size. */
 typedef struct wbx_shard wbx_shard;
 int wbx_shard_create(wbx_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
                      const double* values, uint32_t world, uint32_t rank, wbx_shard** out);
@@ -236,9 +240,13 @@ int wbx_shard_init(wbx_shard* s, double tau, const double* x0_full_dev, double* 
 int wbx_shard_phase_a(wbx_shard* s);
 int wbx_shard_phase_t(wbx_shard* s, int k);
 int wbx_shard_finalize(wbx_shard* s, double* x_full_dev);
-int wbx_shard_power_init(wbx_shard* s, double* sums2);
-int wbx_shard_power_a(wbx_shard* s, double inv);
-int wbx_shard_power_t(wbx_shard* s, double inv, double* sums2);
+int wbx_shard_bind_power(wbx_shard* s, double* sums_pad);
+int wbx_shard_power_begin(wbx_shard* s);
+int wbx_shard_power_update(wbx_shard* s, int first);
+int wbx_shard_power_step_a(wbx_shard* s);
+int wbx_shard_power_step_t(wbx_shard* s);
+/* tau = 1 / (lambda * step_safety) (1 for a zero operator) and the iteration count */
+int wbx_shard_power_result(wbx_shard* s, double step_safety, double* tau, uint32_t* iters);
 
 /* launches of the last deblur, and the solver kernel's device time (ms) */
 int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);

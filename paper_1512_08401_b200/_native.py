@@ -112,9 +112,12 @@ SIGNATURES = {
     "wbx_shard_phase_a": (C.c_int, [_P]),
     "wbx_shard_phase_t": (C.c_int, [_P, C.c_int]),
     "wbx_shard_finalize": (C.c_int, [_P, _P]),
-    "wbx_shard_power_init": (C.c_int, [_P, _D]),
-    "wbx_shard_power_a": (C.c_int, [_P, C.c_double]),
-    "wbx_shard_power_t": (C.c_int, [_P, C.c_double, _D]),
+    "wbx_shard_bind_power": (C.c_int, [_P, _P]),
+    "wbx_shard_power_begin": (C.c_int, [_P]),
+    "wbx_shard_power_update": (C.c_int, [_P, C.c_int]),
+    "wbx_shard_power_step_a": (C.c_int, [_P]),
+    "wbx_shard_power_step_t": (C.c_int, [_P]),
+    "wbx_shard_power_result": (C.c_int, [_P, C.c_double, _D, C.POINTER(C.c_uint32)]),
 }
 
 

@@ -6,13 +6,16 @@
 // rows C_p of Theta^T (= columns C_p of Theta) and the coordinates C_p of x and y. Vectors
 // that cross ranks live in PADDED global buffers (rank q's slice at q * max_range) so the
 // exchange after each phase is one equal-size all-gather (NCCL over NVLink/NVSwitch, driven
-// by the host; or a local copy when the shards are emulated on one GPU):
+// by the host; or nothing when the shards are emulated on one GPU and share the buffers):
 //     phase A   res[R_p] = Theta[R_p, :] y - x0[R_p]         -> all-gather res
 //     phase T   g = Theta^T[C_p, :] res; fused update on C_p  -> all-gather y
 // No reductions cross ranks in FISTA, and every row is summed by the same lane arithmetic
 // as the persistent single-GPU kernel, so a sharded solve is BITWISE equal to the
 // single-GPU solve for any world size (given tau). estimate_step needs two scalars per
-// power iteration (sum over ranks), exchanged by the host.
+// power iteration: each rank writes its block-ordered sums into its slot of a [world][2]
+// buffer, the buffer is all-gathered, and every rank sums the slots in rank order on the
+// device (deterministic for any world size) and updates the iteration state there. The host
+// only enqueues: nothing in the power iteration synchronises with it.
 #include <algorithm>
 #include <cmath>
 #include <memory>
@@ -36,9 +39,11 @@ struct wbx_shard {
     float* res_pad = nullptr;
     double* u_pad = nullptr;
     double* t_pad = nullptr;
+    double* sums_pad = nullptr;  // [world][2] per-rank power-iteration sums (all-gathered)
     // owned state
     wbx::DevBuf<float> xp, x0R, tp, thr, beta;
     wbx::DevBuf<double> pC, wC, ispC, wv, p_full, w_full, part;
+    wbx::DevBuf<double> pstate;  // power iteration: {nw_prev, lambda_prev, iterations, flag}
     double lambda = 0.0, tau = 0.0;
     int max_iters = 0;
     uint64_t device_bytes = 0;
@@ -88,6 +93,9 @@ struct ShardArgs {
     const double* p_full;
     const double* w_full;
     double* part;
+    double* sums_pad;
+    double* pstate;
+    uint32_t world;
     double lambda, tau;
 };
 
@@ -120,17 +128,21 @@ ShardArgs args_of(wbx_shard* s) {
     a.p_full = s->p_full.p;
     a.w_full = s->w_full.p;
     a.part = s->part.p;
+    a.sums_pad = s->sums_pad;
+    a.pstate = s->pstate.p;
+    a.world = s->world;
     a.lambda = s->lambda;
     a.tau = s->tau;
     return a;
 }
 
-// one warp per slice of the segmented fp32 layout (same arithmetic as the persistent kernel)
+// one warp per slice of the segmented fp32 layout (same arithmetic as the persistent kernel),
+// grid-stride over the slices; whole warps in or out, no early return (block reductions follow)
 template <typename ACC, typename X, typename Epi>
 __device__ __forceinline__ void slice_rows(const SellView& M, const X* x, Epi epi) {
-    const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (s < M.slices) {  // whole warps in or out; no early return (block reductions follow)
+    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.slices; s += nw) {
         ACC acc = seg_partial<ACC, X>(M, s, lane, x);
         const uint32_t row = seg_combine(M, s, lane, acc);
         if (row != kNoRow) epi(row, acc);
@@ -211,13 +223,18 @@ __global__ void power_init_kernel(ShardArgs a, uint64_t lo, uint64_t hi) {
     if (threadIdx.x == 0) a.part[2 * blockIdx.x + 1] = 0.0;
 }
 
-__global__ void power_a_kernel(ShardArgs a, double inv) {
+// power-iteration state flags: 0 running, 1 converged, 2 zero operator, 3 iteration cap
+__global__ void power_a_kernel(ShardArgs a) {
+    if (a.pstate[3] != 0.0) return;  // stopped: the remaining enqueued iterations are no-ops
+    const double inv = a.pstate[0];
     double* t = a.t_pad + a.rank * a.maxR;
     slice_rows<double, double>(a.A, a.u_pad, [&](uint32_t r, double acc) { t[r] = acc / inv; });
 }
 
-__global__ void power_t_kernel(ShardArgs a, double inv) {
+__global__ void power_t_kernel(ShardArgs a) {
+    if (a.pstate[3] != 0.0) return;
     __shared__ double sm[kBlock / 32 + 1];
+    const double inv = a.pstate[0];
     double pl = 0.0, pn = 0.0;
     double* u = a.u_pad + a.rank * a.maxC;
     slice_rows<double, double>(a.T, a.t_pad, [&](uint32_t c, double g) {
@@ -234,6 +251,53 @@ __global__ void power_t_kernel(ShardArgs a, double inv) {
         a.part[2 * blockIdx.x] = pl;
         a.part[2 * blockIdx.x + 1] = pn;
     }
+}
+
+// this rank's sums: block partials in block order -> sums_pad[rank]
+__global__ void rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
+    if (!init && a.pstate[3] != 0.0) return;
+    if (threadIdx.x != 0) return;
+    double s0 = 0.0, s1 = 0.0;
+    for (unsigned i = 0; i < blocks; ++i) {
+        s0 += a.part[2 * i];
+        s1 += a.part[2 * i + 1];
+    }
+    a.sums_pad[2 * a.rank] = s0;
+    a.sums_pad[2 * a.rank + 1] = s1;
+}
+
+// stopping rule of estimate_step (solver.cpp:84-95) on the all-gathered sums, rank order
+__global__ void power_update_kernel(ShardArgs a, int first) {
+    if (threadIdx.x != 0) return;
+    double* st = a.pstate;
+    double s0 = 0.0, s1 = 0.0;
+    for (uint32_t r = 0; r < a.world; ++r) {
+        s0 += a.sums_pad[2 * r];
+        s1 += a.sums_pad[2 * r + 1];
+    }
+    if (first) {
+        st[0] = sqrt(s0);  // |v0|
+        st[1] = 0.0;
+        st[2] = 0.0;
+        st[3] = 0.0;
+        return;
+    }
+    if (st[3] != 0.0) return;
+    const double lam = s0, nw = sqrt(s1);
+    const double it = st[2] + 1.0;
+    st[2] = it;
+    if (nw == 0.0) {
+        st[3] = 2.0;
+        return;
+    }
+    if (it > 1.0 && fabs(lam - st[1]) <= 1e-6 * fabs(lam)) {
+        st[1] = lam;
+        st[3] = 1.0;
+        return;
+    }
+    st[1] = lam;
+    st[0] = nw;
+    if (it >= 200.0) st[3] = 3.0;
 }
 
 unsigned blocks_for(uint64_t threads) { return static_cast<unsigned>(std::max<uint64_t>(1, (threads + kBlock - 1) / kBlock)); }
@@ -511,53 +575,77 @@ int wbx_shard_finalize(wbx_shard* s, double* x_full_dev) {
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
 
-// estimate_step pieces: partial sums of this rank land in sums2[0..1] (host, synchronous)
-static int reduce_parts(wbx_shard* s, unsigned blocks, double* sums2) {
-    std::vector<double> h(2 * blocks);
-    if (cudaMemcpyAsync(h.data(), s->part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s->ctx->stream) !=
-            cudaSuccess ||
-        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
-        return WBX_CUDA_ERROR;
-    double a = 0.0, b = 0.0;
-    for (unsigned i = 0; i < blocks; ++i) {
-        a += h[2 * i];
-        b += h[2 * i + 1];
+// estimate_step, device-resident (see the header comment): begin -> [all-gather sums] ->
+// update(first) -> repeat { step_a -> [all-gather t] -> step_t -> [all-gather sums] ->
+// update -> [all-gather u] } -> result.
+int wbx_shard_bind_power(wbx_shard* s, double* sums_pad) {
+    if (!s || !sums_pad) return WBX_INVALID_ARGUMENT;
+    s->sums_pad = sums_pad;
+    if (!s->pstate.p) {
+        try {
+            s->pstate.alloc(4);
+        } catch (const wbx::Error& e) {
+            wbx_set_last_error(e.what());
+            return e.status;
+        }
     }
-    sums2[0] = a;
-    sums2[1] = b;
     return WBX_OK;
 }
 
-int wbx_shard_power_init(wbx_shard* s, double* sums2) {
-    if (!s || !sums2 || !s->u_pad) return WBX_INVALID_ARGUMENT;
+int wbx_shard_power_begin(wbx_shard* s) {
+    if (!s || !s->u_pad || !s->sums_pad || !s->pstate.p) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
     const unsigned blocks = 2 * static_cast<unsigned>(s->ctx->num_sms);
+    if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
     const uint64_t lo = s->n * s->rank / s->world, hi = s->n * (s->rank + 1) / s->world;
     wbx::power_init_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a, lo, hi);
-    wbx::count_launch(s->ctx);
-    return reduce_parts(s, blocks, sums2);
+    wbx::rank_sums_kernel<<<1, 32, 0, s->ctx->stream>>>(a, blocks, 1);
+    wbx::count_launch(s->ctx, 2);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
 
-int wbx_shard_power_a(wbx_shard* s, double inv) {
-    if (!s) return WBX_INVALID_ARGUMENT;
-    wbx::ShardArgs a = wbx::args_of(s);
-    if (a.A.slices) wbx::power_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a, inv);
+int wbx_shard_power_update(wbx_shard* s, int first) {
+    if (!s || !s->sums_pad || !s->pstate.p) return WBX_INVALID_ARGUMENT;
+    wbx::power_update_kernel<<<1, 32, 0, s->ctx->stream>>>(wbx::args_of(s), first);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
 
-int wbx_shard_power_t(wbx_shard* s, double inv, double* sums2) {
-    if (!s || !sums2) return WBX_INVALID_ARGUMENT;
+int wbx_shard_power_step_a(wbx_shard* s) {
+    if (!s || !s->pstate.p) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
-    const unsigned blocks = wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.slices, 1)) * 32);
+    if (a.A.slices) wbx::power_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_power_step_t(wbx_shard* s) {
+    if (!s || !s->sums_pad || !s->pstate.p) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    // a bounded grid (grid-stride over slices) keeps the partials few for the ordered sum
+    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.slices, 1)) * 32),
+                                               8u * static_cast<unsigned>(s->ctx->num_sms));
     if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
     if (a.T.slices) {
-        wbx::power_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a, inv);
+        wbx::power_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
     } else {
         cudaMemsetAsync(s->part.p, 0, 2 * blocks * sizeof(double), s->ctx->stream);
     }
-    wbx::count_launch(s->ctx);
-    return reduce_parts(s, blocks, sums2);
+    wbx::rank_sums_kernel<<<1, 32, 0, s->ctx->stream>>>(a, blocks, 0);
+    wbx::count_launch(s->ctx, 2);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_power_result(wbx_shard* s, double step_safety, double* tau, uint32_t* iters) {
+    if (!s || !tau || !iters || !s->pstate.p) return WBX_INVALID_ARGUMENT;
+    double st[4];
+    if (cudaMemcpyAsync(st, s->pstate.p, sizeof st, cudaMemcpyDeviceToHost, s->ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+        return WBX_CUDA_ERROR;
+    const bool zero = st[3] == 2.0;
+    *iters = static_cast<uint32_t>(st[2]);
+    *tau = (zero || st[1] <= 0.0) ? 1.0 : 1.0 / (st[1] * step_safety);  // solver.cpp:89,97
+    return WBX_OK;
 }
 
 }  // extern "C"

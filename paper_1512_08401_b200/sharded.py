@@ -6,16 +6,15 @@ module is the host-side orchestration:
     - `LocalExchange`: all shards live in this process on one GPU and bind the SAME padded
       buffers, so the exchange is implicit (used to test the partition code on one GPU);
     - `TorchExchange`: one rank per GPU, NCCL `all_gather_into_tensor` over NVLink on the
-      solver's stream, `all_reduce` for the two power-iteration scalars.
-  * `ShardedDeblurrer`: analyze -> estimate_step (power iteration, 2 scalars all-reduced per
-    iteration) -> FISTA (phase A, all-gather res, phase T, all-gather y) -> assemble x ->
-    synthesize.
+      solver's stream (gloo list form on CPU for the tests).
+  * `ShardedDeblurrer`: analyze -> estimate_step (device-resident power iteration: per-rank
+    sums all-gathered and reduced in rank order on every rank, no host round trip) ->
+    FISTA (phase A, all-gather res, phase T, all-gather y) -> assemble x -> synthesize.
 A sharded solve is bitwise equal to the single-GPU fp32 solve given the same tau.
 """
 from __future__ import annotations
 
 import ctypes as C
-import math
 from typing import List, Optional
 
 import numpy as np
@@ -59,9 +58,6 @@ class LocalExchange:
     def gather(self, buf, rank_slices):
         return None
 
-    def allreduce2(self, per_shard_sums: List[np.ndarray]) -> np.ndarray:
-        return np.sum(np.stack(per_shard_sums), axis=0)
-
     def allreduce_sum_(self, t):
         return None
 
@@ -89,13 +85,6 @@ class TorchExchange:
                 for q in range(world):
                     buf[q * m:(q + 1) * m] = parts[q]
 
-    def allreduce2(self, per_shard_sums: List[np.ndarray]) -> np.ndarray:
-        dev = self.stream.device if self.stream is not None else "cpu"
-        t = self.torch.tensor(per_shard_sums[0], dtype=self.torch.float64, device=dev)
-        with self._ctx():
-            self.dist.all_reduce(t)
-        return t.cpu().numpy()
-
     def allreduce_sum_(self, t):
         with self._ctx():
             self.dist.all_reduce(t)
@@ -120,6 +109,7 @@ class ShardedDeblurrer:
             self.res = torch.zeros(world * s0.maxR, dtype=torch.float32, device=self.dev)
             self.u = torch.zeros(world * s0.maxC, dtype=torch.float64, device=self.dev)
             self.t = torch.zeros(world * s0.maxR, dtype=torch.float64, device=self.dev)
+            self.sums = torch.zeros(world * 2, dtype=torch.float64, device=self.dev)
             self.x0 = torch.empty(self.n, dtype=torch.float64, device=self.dev)
             self.x = torch.empty(self.n, dtype=torch.float64, device=self.dev)
         p = W._f64(P.p, op.n, "preconditioner")
@@ -128,42 +118,34 @@ class ShardedDeblurrer:
             _check(lib.wbx_shard_bind(s.h, C.c_void_p(self.y.data_ptr()), C.c_void_p(self.res.data_ptr()),
                                       C.c_void_p(self.u.data_ptr()), C.c_void_p(self.t.data_ptr())))
             _check(lib.wbx_shard_setup(s.h, W._dptr(p), W._dptr(w), float(lambda_), self.iters, int(accelerate)))
+            _check(lib.wbx_shard_bind_power(s.h, C.c_void_p(self.sums.data_ptr())))
         self.basis_h = basis.device(ctx)
         self.tau_iters = 0
 
-    # ---- estimate_step (solver.cpp:69-99), power iteration with two all-reduced scalars
+    # ---- estimate_step (solver.cpp:69-99): device-resident power iteration. Each step is
+    # enqueued blindly; the device applies the stopping rule and turns the remaining steps
+    # into no-ops, so the host waits only once, for the result.
     def estimate_step(self, step_safety: float = 1.01) -> float:
-        sums = []
         for s in self.shards:
-            v = np.zeros(2)
-            _check(lib.wbx_shard_power_init(s.h, W._dptr(v)))
-            sums.append(v)
-        tot = self.exchange.allreduce2(sums)
+            _check(lib.wbx_shard_power_begin(s.h))
+        self.exchange.gather(self.sums, None)
+        for s in self.shards:
+            _check(lib.wbx_shard_power_update(s.h, 1))
         self.exchange.gather(self.u, None)
-        nw_prev = math.sqrt(tot[0])
-        lam_prev, it, zero = 0.0, 0, False
-        while it < 200:
+        for _ in range(200):
             for s in self.shards:
-                _check(lib.wbx_shard_power_a(s.h, nw_prev))
+                _check(lib.wbx_shard_power_step_a(s.h))
             self.exchange.gather(self.t, None)
-            sums = []
             for s in self.shards:
-                v = np.zeros(2)
-                _check(lib.wbx_shard_power_t(s.h, nw_prev, W._dptr(v)))
-                sums.append(v)
-            tot = self.exchange.allreduce2(sums)
-            lam, nw = float(tot[0]), math.sqrt(float(tot[1]))
-            it += 1
-            if nw == 0.0:
-                zero = True
-                break
-            if it > 1 and abs(lam - lam_prev) <= 1e-6 * abs(lam):
-                lam_prev = lam
-                break
-            lam_prev, nw_prev = lam, nw
+                _check(lib.wbx_shard_power_step_t(s.h))
+            self.exchange.gather(self.sums, None)
+            for s in self.shards:
+                _check(lib.wbx_shard_power_update(s.h, 0))
             self.exchange.gather(self.u, None)
-        self.tau_iters = it
-        return 1.0 if (zero or lam_prev <= 0.0) else 1.0 / (lam_prev * step_safety)
+        tau, iters = C.c_double(), C.c_uint32()
+        _check(lib.wbx_shard_power_result(self.shards[0].h, float(step_safety), C.byref(tau), C.byref(iters)))
+        self.tau_iters = int(iters.value)
+        return float(tau.value)
 
     def deblur_dev(self, u0_ptr: int, u_ptr: int, tau: Optional[float] = None, clamp: bool = True) -> float:
         torch = self.torch

@@ -58,8 +58,12 @@ def _gloo_worker(rank, world, port, q):
     buf[rank * maxC: rank * maxC + own.numel()] = own
     ex = TorchExchange(torch, dist, None)
     ex.gather(buf, None)
-    sums = ex.allreduce2([np.array([float(rank + 1), 2.0 * rank])])
-    q.put((rank, buf.numpy().tolist(), sums.tolist(), maxC, cb.tolist()))
+    # power-iteration sums: each rank fills its [2] slot, the all-gather gives every rank the
+    # same [world][2] buffer, which the device then sums in rank order
+    sums = torch.zeros(2 * world, dtype=torch.float64)
+    sums[2 * rank:2 * rank + 2] = torch.tensor([float(rank + 1), 2.0 * rank], dtype=torch.float64)
+    ex.gather(sums, None)
+    q.put((rank, buf.numpy().tolist(), sums.numpy().tolist(), maxC, cb.tolist()))
     dist.destroy_process_group()
 
 
@@ -82,7 +86,7 @@ def test_exchange_protocol_world2_gloo():
     for q_ in range(2):
         seg = b0[q_ * maxC: q_ * maxC + (cb[q_ + 1] - cb[q_])]
         assert seg == list(map(float, range(cb[q_], cb[q_ + 1])))
-    assert s0 == s1 == [3.0, 2.0]
+    assert s0 == s1 == [1.0, 0.0, 2.0, 2.0]
 
 
 @pytest.mark.gpu
