@@ -1,5 +1,6 @@
 // extern "C" entry points of libwbx.so (declared in include/wbx.h).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -96,6 +97,22 @@ __global__ void delta_kernel(double* x, uint64_t i) { x[i] = 1.0; }
 unsigned nblocks(uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 // Gram diagonals (precond.cpp:16-67), exact: same accumulation and first-touch order.
+void gram_host(const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
+
+// Gram diagonals: on the device (gram.cu, same operation order, bitwise equal) when a context
+// is given; the host path (also the fallback when a column's 2-hop set overflows the device
+// table) otherwise.
+// WBX_GRAM=host|device forces one path (device: fail instead of falling back).
+void gram(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2) {
+    const char* e = std::getenv("WBX_GRAM");
+    const std::string mode = e ? e : "";
+    if (ctx && mode != "host") {
+        if (wbx::gram_device(ctx, op, cap_factor, diagM, diagM2)) return;
+        if (mode == "device") wbx::fail(WBX_TOO_LARGE, "gram_diagonals: a column's 2-hop set exceeds the device table");
+    }
+    gram_host(op, cap_factor, diagM, diagM2);
+}
+
 void gram_host(const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2) {
     const uint64_t n = op->n, nnz = op->nnz;
     const auto& rp = op->h_rowptr;
@@ -483,8 +500,7 @@ int wbx_gram_diagonals(wbx_ctx* ctx, const wbx_op* op, uint64_t nnz_cap_factor, 
         need(op, "op");
         need(diagM, "diagM");
         need(diagM2, "diagM2");
-        (void)ctx;
-        gram_host(op, nnz_cap_factor, diagM, diagM2);
+        gram(ctx, op, nnz_cap_factor, diagM, diagM2);
     });
 }
 
@@ -492,9 +508,8 @@ int wbx_spai(wbx_ctx* ctx, const wbx_op* op, double* p) {
     return guard([&] {
         need(op, "op");
         need(p, "p");
-        (void)ctx;
         std::vector<double> m(op->n), m2(op->n);
-        gram_host(op, 50, m.data(), m2.data());
+        gram(ctx, op, 50, m.data(), m2.data());
         for (uint64_t i = 0; i < op->n; ++i) p[i] = m[i] > 0.0 ? m2[i] / m[i] : 1.0;
     });
 }
@@ -503,10 +518,9 @@ int wbx_jacobi(wbx_ctx* ctx, const wbx_op* op, double eps, double* p) {
     return guard([&] {
         need(op, "op");
         need(p, "p");
-        (void)ctx;
         if (eps <= 0.0) wbx::fail(WBX_BAD_EPSILON, "jacobi: epsilon must be positive");
         std::vector<double> m(op->n), m2(op->n);
-        gram_host(op, 50, m.data(), m2.data());
+        gram(ctx, op, 50, m.data(), m2.data());
         for (uint64_t i = 0; i < op->n; ++i) p[i] = std::max(m[i], eps);
     });
 }

@@ -187,6 +187,9 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st);
 struct WinView;
 WinView view_of(const WinSide& w);
 
+// gram.cu: Gram diagonals on the device; false if a column overflowed the per-warp table
+bool gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
+
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {
     std::vector<uint64_t> rowptr;
