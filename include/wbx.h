@@ -149,6 +149,20 @@ int wbx_theta_expand(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n
                      const double* values, uint64_t* nnz, uint64_t* row_offsets,
                      uint32_t* col_indices, double* out_values);
 
+/* Theta_K construction on the device (build_theta_conv theta.cpp:40-79 + threshold_impl
+ * theta.cpp:206-276): the blurred single wavelets of every band (FFT convolution in the
+ * oracle build's exact arithmetic, see csrc/theta_gpu.cu), their analyses, the weighted keys
+ * |g| * band_weight[in] of every generator entry and the global top-K walk. Output: the kept
+ * generator groups in the reference's walk order (wbx_theta_expand input); n_records <=
+ * max_records. band_weight[b] is the per-band sigma of threshold_weighted (dyadic_weights:
+ * 2^(level - J); all ones for threshold_naive). psf: the kernel image (row-major). */
+int wbx_theta_conv_topk(wbx_ctx* ctx, wbx_basis* basis, const double* psf, const double* band_weight, uint64_t K,
+                        uint64_t max_records, uint32_t* gen_block, uint32_t* gen_index, uint64_t* gen_count,
+                        double* gen_value, uint64_t* n_records);
+/* gaussian_kernel + normalize_sum (operators.cpp:100-120, 84-89): the PSF image of
+ * generate_psf(GaussianSpec{sigma}) (host). */
+int wbx_psf_gaussian(uint32_t ndim, const uint64_t* dims, double sigma, double* kernel);
+
 /* Spatially varying Theta_K (BASELINE configs C3/C4; the reference has no 2-D spatially
  * varying operator): column mu = the column of the stationary operator whose
  * Gaussian sigma matches the spatial row of psi_mu, sigma varying linearly from

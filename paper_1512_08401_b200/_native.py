@@ -76,6 +76,8 @@ SIGNATURES = {
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
+    "wbx_theta_conv_topk": (C.c_int, [_P, _P, _D, _D, C.c_uint64, C.c_uint64, _U32, _U32, _U64, _D, _U64]),
+    "wbx_psf_gaussian": (C.c_int, [C.c_uint32, _U64, C.c_double, _D]),
     "wbx_theta_expand": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                    _U64, _U64, _U32, _D]),
     "wbx_theta_varying": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint32, _D, _U64, _U32, _U32, _U64, _D,

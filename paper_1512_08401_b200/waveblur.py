@@ -519,6 +519,45 @@ def theta_from_generators(gl: GeneratorList) -> SparseOperator:
     return SparseOperator(n, ro, ci[: nnz.value], va[: nnz.value], layout, gl.family, gl.order)
 
 
+def gaussian_psf_kernel(dims, sigma: float) -> np.ndarray:
+    """generate_psf(GaussianSpec{sigma}, dims).kernel (operators.cpp:100-120, 298-318), with the
+    reference's expressions (host libm exp), as the row-major kernel image."""
+    d = np.array(dims, dtype=np.uint64)
+    k = np.zeros(int(np.prod(dims)), dtype=np.float64)
+    _check(lib.wbx_psf_gaussian(len(dims), _u64ptr(d), float(sigma), _dptr(k)))
+    return k.reshape(dims)
+
+
+def dyadic_band_weights(layout: SubbandLayout) -> np.ndarray:
+    """Per-band sigma of dyadic_weights (theta.cpp:153-165): 2^(level - J)."""
+    return np.array([2.0 ** (b.level - layout.J) for b in layout.bands], dtype=np.float64)
+
+
+def theta_conv_topk(basis: WaveletBasis, psf_kernel, K: int, band_weights=None, ctx: Optional[Context] = None,
+                    max_records: int = 1 << 20) -> GeneratorList:
+    """build_theta_conv (theta.cpp:40-79) + threshold_weighted / threshold_naive
+    (theta.cpp:206-296) ON THE DEVICE, returned in compressed form (the kept generator
+    groups; expand with theta_from_generators). band_weights: per band (default all ones =
+    threshold_naive; dyadic_band_weights(...) = threshold_weighted with dyadic_weights)."""
+    ctx = ctx or default_context()
+    layout = basis.layout
+    nb = len(layout.bands)
+    w = np.ones(nb) if band_weights is None else np.asarray(band_weights, dtype=np.float64)
+    if w.size != nb:
+        raise ShapeMismatch("theta_conv_topk: one weight per band")
+    psf = _f64(np.asarray(psf_kernel, dtype=np.float64).ravel(), layout.total(), "psf kernel")
+    blocks = np.zeros(max_records, dtype=np.uint32)
+    gidx = np.zeros(max_records, dtype=np.uint32)
+    cnt = np.zeros(max_records, dtype=np.uint64)
+    val = np.zeros(max_records, dtype=np.float64)
+    nrec = C.c_uint64()
+    _check(lib.wbx_theta_conv_topk(ctx.handle, basis.device(ctx), _dptr(psf), _dptr(w), int(K), max_records,
+                                   _u32ptr(blocks), _u32ptr(gidx), _u64ptr(cnt), _dptr(val), C.byref(nrec)))
+    m = nrec.value
+    return GeneratorList(tuple(layout.dims), layout.J, basis.filters.family, basis.filters.order,
+                         blocks[:m].copy(), gidx[:m].copy(), cnt[:m].copy(), val[:m].copy())
+
+
 @dataclass
 class SigmaLadder:
     """Stationary Gaussian Theta_K operators at increasing sigmas (one GeneratorList each)."""
