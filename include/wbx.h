@@ -203,6 +203,20 @@ int wbx_pgd(wbx_ctx* ctx, const wbx_op* op, const double* x0, const double* w, d
             const double* p, const wbx_solver_cfg* cfg, int accelerate, double* x_final,
             wbx_report* report);
 
+/* ---------------------------------------------------------------- exact FFT operator
+ * ExactThetaOp (solver.cpp:21-29): Theta x = analyze(convolve(synthesize(x), psf)), the
+ * adjoint with the conjugated kernel spectrum; bitwise the reference's (oracle FFT
+ * arithmetic, fft.cuh). estimate_step / run_pgd over it (solver.cpp:69-157): the reference's
+ * per-coordinate expressions in fp64, fixed-order reductions. psf: the kernel image. */
+typedef struct wbx_exact_op wbx_exact_op;
+int wbx_exact_op_create(wbx_ctx* ctx, wbx_basis* basis, const double* psf, wbx_exact_op** out);
+int wbx_exact_op_destroy(wbx_exact_op* e);
+int wbx_exact_apply(wbx_exact_op* e, int adjoint, const double* x, double* y);
+int wbx_exact_apply_dev(wbx_exact_op* e, int adjoint, const double* x_dev, double* y_dev);
+int wbx_estimate_step_exact(wbx_exact_op* e, const double* p, double step_safety, double* tau, uint32_t* iters);
+int wbx_pgd_exact(wbx_exact_op* e, const double* x0, const double* w, double lambda, const double* p,
+                  const wbx_solver_cfg* cfg, int accelerate, double* x_final, wbx_report* report);
+
 /* ---------------------------------------------------------------- prepared deblur (hot path)
  * The unit the bench times: u0 (observed image) -> analyze -> [estimate_step] ->
  * preconditioned FISTA -> synthesize -> restored image (pre-clamp; clamp=1 applies the

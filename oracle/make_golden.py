@@ -53,6 +53,11 @@ CASES = {
                       "--sigma", "2", "--K", "3000", "--noise", "1e-3", "--seed", "7",
                       "--precond", "jacobi", "--iters", "60"],
                      ["u0", "x0", "p", "x_final", "restored", "energies"]),
+    # ExactThetaOp (the FFT operator): kernel, apply / adjoint, tau, FISTA
+    "exact_s64_sym6": (["--dims", "64", "64", "--family", "symmlet", "--order", "6", "--J", "3",
+                        "--sigma", "3", "--K", "40000", "--noise", "5e-3", "--seed", "5",
+                        "--precond", "identity", "--iters", "30", "--exact"],
+                       ["u0", "x0", "psf", "exact_apply", "exact_adjoint", "exact_x_final", "exact_energies"]),
 }
 
 

@@ -19,7 +19,7 @@
 //                 [--psf gaussian --sigma S] [--K K | --Kfactor F] [--mode dyadic|uniform]
 //                 [--noise SIG] [--seed SEED] [--lambda L] [--iters I]
 //                 [--precond spai|jacobi|identity] [--write-op] [--u0 FILE]
-//                 [--bench-reps R] [--no-solve]
+//                 [--bench-reps R] [--no-solve] [--exact]
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -203,7 +203,7 @@ int main(int argc, char** argv) {
     double sigma = 5.0, noise = 5e-3, lambda = 1e-4, kfactor = 3.0;
     std::size_t K = 0, iters = 50, bench_reps = 0;
     std::uint64_t seed = 2024;
-    bool write_op = false, solve = true;
+    bool write_op = false, solve = true, exact = false;
     for (int i = 1; i < argc; ++i) {
         std::string a = argv[i];
         auto next = [&]() -> std::string {
@@ -231,6 +231,7 @@ int main(int argc, char** argv) {
         else if (a == "--bench-reps") bench_reps = std::stoull(next());
         else if (a == "--no-solve") solve = false;
         else if (a == "--method") method = next();
+        else if (a == "--exact") exact = true;
         else throw std::runtime_error("unknown flag " + a);
     }
     if (out.empty()) throw std::runtime_error("--out required");
@@ -358,6 +359,29 @@ int main(int argc, char** argv) {
             }
             meta << ",\n  \"bench_deblur_s\": " << json_array(times);
         }
+    }
+    // ExactThetaOp (solver.cpp:21-29, the FFT operator): the PSF kernel, one forward and one
+    // adjoint application to x0 = analyze(u0), estimate_step and `iters` FISTA iterations
+    // with the identity preconditioner (the exact-fista comparator, waveblur.cpp:387-397)
+    if (exact) {
+        write_bin(od / "psf.bin", psf.kernel.v);
+        ExactThetaOp eop(psf, basis);
+        const std::vector<double> x0 = analyze(observed, basis).values;
+        write_bin(od / "exact_apply.bin", eop.apply(x0));
+        write_bin(od / "exact_adjoint.bin", eop.apply_adjoint(x0));
+        DiagonalPreconditioner I = identity_precond(n);
+        DeblurProblem pe;
+        pe.op = &eop;
+        pe.x0 = x0;
+        pe.weights = scale_weights(basis.layout);
+        pe.lambda = lambda;
+        SolverConfig ce;
+        ce.max_iters = iters;
+        const double tau_e = estimate_step(eop, I, ce.step_safety);
+        SolveReport re = fista(pe, I, ce);
+        write_bin(od / "exact_x_final.bin", re.x_final);
+        write_bin(od / "exact_energies.bin", re.energies);
+        meta << ",\n  \"exact_tau\": " << fmt(tau_e) << ", \"exact_iters_used\": " << re.iters_used;
     }
     meta << "\n}\n";
     std::ofstream(od / "meta.json") << meta.str();

@@ -76,6 +76,13 @@ SIGNATURES = {
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
+    "wbx_exact_op_create": (C.c_int, [_P, _P, _D, C.POINTER(C.c_void_p)]),
+    "wbx_exact_op_destroy": (C.c_int, [_P]),
+    "wbx_exact_apply": (C.c_int, [_P, C.c_int, _D, _D]),
+    "wbx_exact_apply_dev": (C.c_int, [_P, C.c_int, _P, _P]),
+    "wbx_estimate_step_exact": (C.c_int, [_P, _D, C.c_double, _D, C.POINTER(C.c_uint32)]),
+    "wbx_pgd_exact": (C.c_int, [_P, _D, _D, C.c_double, _D, C.POINTER(wbx_solver_cfg), C.c_int, _D,
+                                C.POINTER(wbx_report)]),
     "wbx_theta_conv_topk": (C.c_int, [_P, _P, _D, _D, C.c_uint64, C.c_uint64, _U32, _U32, _U64, _D, _U64]),
     "wbx_psf_gaussian": (C.c_int, [C.c_uint32, _U64, C.c_double, _D]),
     "wbx_theta_expand": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,

@@ -745,6 +745,41 @@ class SparseThetaOp:
         return self._op
 
 
+class ExactThetaOp:
+    """ThetaOp of the exact FFT operator (solver.hpp:41-52, solver.cpp:21-29) on the device:
+    Theta x = analyze(convolve(synthesize(x), psf)); bitwise the reference's (oracle FFT
+    arithmetic). psf: the kernel image (e.g. gaussian_psf_kernel)."""
+
+    def __init__(self, psf_kernel, basis: WaveletBasis, ctx: Optional[Context] = None):
+        self._ctx = ctx or default_context()
+        self.basis = basis
+        self.n = basis.layout.total()
+        k = _f64(np.asarray(psf_kernel, dtype=np.float64).ravel(), self.n, "psf kernel")
+        h = C.c_void_p()
+        _check(lib.wbx_exact_op_create(self._ctx.handle, basis.device(self._ctx), _dptr(k), C.byref(h)))
+        self.handle = h
+
+    def _apply(self, x, adjoint: int) -> np.ndarray:
+        xv = _f64(x, self.n)
+        y = np.empty(self.n)
+        _check(lib.wbx_exact_apply(self.handle, adjoint, _dptr(xv), _dptr(y)))
+        return y
+
+    def apply(self, x) -> np.ndarray:
+        return self._apply(x, 0)
+
+    def apply_adjoint(self, x) -> np.ndarray:
+        return self._apply(x, 1)
+
+    def dim(self) -> int:
+        return self.n
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.wbx_exact_op_destroy(self.handle)
+            self.handle = None
+
+
 @dataclass
 class DeblurProblem:  # solver.hpp:55-61
     op: SparseThetaOp = None
@@ -794,6 +829,9 @@ class SolveReport:  # solver.hpp:76-84
 
 def energy(x, problem: DeblurProblem, ctx=None) -> float:
     """½‖Θx − x0‖² + λ Σ w|x| (solver.cpp:44-55)."""
+    if isinstance(problem.op, ExactThetaOp):
+        r = problem.op.apply(x) - _f64(problem.x0)
+        return 0.5 * float(np.dot(r, r)) + problem.lambda_ * float(np.dot(_f64(problem.weights), np.abs(_f64(x))))
     op = problem.op.sparse()
     xv = _f64(x)
     if xv.size != len(problem.x0):
@@ -822,6 +860,11 @@ def prox_weighted_l1_P(z0, tau: float, weights, lambda_: float, P: DiagonalPreco
 def estimate_step(op: SparseThetaOp, P: DiagonalPreconditioner, step_safety: float = 1.0,
                   ctx=None, return_iters: bool = False):
     """τ = 1/(step_safety ‖P^-½ΘᵀΘP^-½‖) by the reference's power iteration (solver.cpp:69-99)."""
+    if isinstance(op, ExactThetaOp):
+        p = _f64(P.p, op.n, "preconditioner")
+        tau, it = C.c_double(), C.c_uint32()
+        _check(lib.wbx_estimate_step_exact(op.handle, _dptr(p), float(step_safety), C.byref(tau), C.byref(it)))
+        return (tau.value, it.value) if return_iters else tau.value
     sp = op.sparse()
     ctx = _ctx_of(sp, ctx)
     p = _f64(P.p, sp.n, "preconditioner")
@@ -834,6 +877,8 @@ def estimate_step(op: SparseThetaOp, P: DiagonalPreconditioner, step_safety: flo
 
 def _run_pgd(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig, accelerate: int,
              ctx=None) -> SolveReport:
+    if isinstance(problem.op, ExactThetaOp):
+        return _run_pgd_exact(problem, P, config, accelerate)
     sp = problem.op.sparse()
     n = sp.n
     x0 = _f64(problem.x0)
@@ -864,6 +909,32 @@ def _run_pgd(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverCo
         initial_energy=rep.initial_energy,
         tau=rep.tau,
         tau_iters=int(rep.tau_iters))
+
+
+def _run_pgd_exact(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig,
+                   accelerate: int) -> SolveReport:
+    """run_pgd over the exact FFT operator (fp64, the reference's expressions)."""
+    op = problem.op
+    n = op.n
+    x0, w, p = _f64(problem.x0), _f64(problem.weights), _f64(P.p)
+    if x0.size != n or w.size != n or p.size != n:
+        raise ShapeMismatch("solver: inconsistent problem dimensions")
+    cfg = config.to_c()
+    K = int(config.max_iters)
+    energies = np.zeros(max(K, 1))
+    supports = np.zeros(max(K, 1), dtype=np.uint64)
+    rep = N.wbx_report()
+    rep.energies = _dptr(energies)
+    rep.support_sizes = _u64ptr(supports)
+    xf = np.empty(n)
+    _check(lib.wbx_pgd_exact(op.handle, _dptr(x0), _dptr(w), float(problem.lambda_), _dptr(p), C.byref(cfg),
+                             accelerate, _dptr(xf), C.byref(rep)))
+    used = int(rep.iters_used)
+    track = config.track_energy or math.isfinite(config.ref_energy)
+    return SolveReport(x_final=xf, energies=list(energies[:used]) if track else [], iters_used=used,
+                       support_sizes=[int(v) for v in supports[:used]] if config.track_support else [],
+                       wall_time_s=rep.wall_time_s, ops_per_pixel_per_iter=rep.ops_per_pixel_per_iter,
+                       initial_energy=rep.initial_energy, tau=rep.tau, tau_iters=int(rep.tau_iters))
 
 
 def ista(problem: DeblurProblem, P: DiagonalPreconditioner, config: SolverConfig, ctx=None) -> SolveReport:
