@@ -1681,7 +1681,9 @@ struct wbx_solver {
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     wbx::WinSide wA, wT;
     int dec_grid = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host->device image copies overlapping the step estimate
+    bool input_pending = false;          // ev_in marks a pending copy of the input image
     uint64_t last_launches = 0;
     float last_solve_ms = 0.f;
 };
@@ -1804,12 +1806,11 @@ void launch_coop(const void* kernel, int grid, SolveArgs& a, cudaStream_t st) {
 }
 
 template <typename T>
-void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
+void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
     WBX_CUDA(cudaMemsetAsync(s->out.p, 0, s->out.bytes(), st));
     // step: estimate_step on the device, or the given one
-    const bool win = s->win && !a.track && s->batch == 1;
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
@@ -1819,7 +1820,15 @@ void run_solve(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
     count_launch(ctx);
-    WBX_CUDA(cudaEventRecord(s->ev_mid, st));  // tau | iterations split (wbx_solver_phase_ms)
+    WBX_CUDA(cudaGetLastError());
+}
+
+// the iteration kernel(s) after run_tau (tau on the device in out[OUT_TAU])
+template <typename T>
+void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
+    SolveArgs a = make_args<T>(s, x0_full, x_full);
+    wbx_ctx* ctx = s->ctx;
+    const bool win = s->win && !a.track && s->batch == 1;
     if (win) {
         const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                     : reinterpret_cast<const void*>(fista_win_kernel<false>);
@@ -1997,17 +2006,44 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     WBX_CUDA(cudaEventCreate(&s->ev0));
     WBX_CUDA(cudaEventCreate(&s->ev1));
     WBX_CUDA(cudaEventCreate(&s->ev_mid));
+    WBX_CUDA(cudaEventCreate(&s->ev_it0));
+    WBX_CUDA(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+    WBX_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     WBX_CUDA(cudaStreamSynchronize(st));
 }
 
-void solver_run(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
+// Step estimate (independent of the image: it can run before the image is analysed, e.g.
+// while the image is still being copied in) and the iterations, each bracketed by events.
+void solver_tau(wbx_solver* s) {
     cudaStream_t st = s->ctx->stream;
     WBX_CUDA(cudaEventRecord(s->ev0, st));
     if (s->cfg.precision == WBX_FP64)
-        run_solve<double>(s, x0_full_dev, x_full_dev, st);
+        run_tau<double>(s, s->x0full.p, s->xfull.p, st);
     else
-        run_solve<float>(s, x0_full_dev, x_full_dev, st);
+        run_tau<float>(s, s->x0full.p, s->xfull.p, st);
+    WBX_CUDA(cudaEventRecord(s->ev_mid, st));
+}
+
+void solver_iters(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
+    cudaStream_t st = s->ctx->stream;
+    WBX_CUDA(cudaEventRecord(s->ev_it0, st));
+    if (s->cfg.precision == WBX_FP64)
+        run_iters<double>(s, x0_full_dev, x_full_dev, st);
+    else
+        run_iters<float>(s, x0_full_dev, x_full_dev, st);
     WBX_CUDA(cudaEventRecord(s->ev1, st));
+}
+
+void solver_run(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
+    solver_tau(s);
+    solver_iters(s, x0_full_dev, x_full_dev);
+}
+
+float solve_ms_of(const wbx_solver* s) {  // tau + iterations (device events)
+    float t = 0.f, i = 0.f;
+    WBX_CUDA(cudaEventElapsedTime(&t, s->ev0, s->ev_mid));
+    WBX_CUDA(cudaEventElapsedTime(&i, s->ev_it0, s->ev1));
+    return t + i;
 }
 
 void solver_report(wbx_solver* s, wbx_report* rep) {
@@ -2016,7 +2052,7 @@ void solver_report(wbx_solver* s, wbx_report* rep) {
     WBX_CUDA(cudaMemcpyAsync(out, s->out.p, sizeof out, cudaMemcpyDeviceToHost, st));
     WBX_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
-    WBX_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    ms = solve_ms_of(s);
     s->last_solve_ms = ms;
     if (s->trace.p) {
         if (FILE* f = std::fopen(std::getenv("WBX_TRACE_FILE"), "ab")) {
@@ -2070,6 +2106,9 @@ void solver_free(wbx_solver* s) {
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->ev_mid) cudaEventDestroy(s->ev_mid);
+    if (s->ev_it0) cudaEventDestroy(s->ev_it0);
+    if (s->ev_in) cudaEventDestroy(s->ev_in);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     delete s;
 }
 
@@ -2091,8 +2130,13 @@ int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp
         cudaStream_t st = s->ctx->stream;
         const uint64_t before = s->ctx->launches;
         const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
+        wbx::solver_tau(s);  // image-independent: first, so a pending image copy overlaps it
+        if (s->input_pending) {
+            WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
+            s->input_pending = false;
+        }
         for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
-        wbx::solver_run(s, s->x0full.p, s->xfull.p);
+        wbx::solver_iters(s, s->x0full.p, s->xfull.p);
         for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st);
         if (clamp) wbx::launch_clamp(s->ctx, u_dev, n * B, st);
         WBX_CUDA(cudaGetLastError());
@@ -2109,7 +2153,13 @@ int wbx_deblur(wbx_solver* s, const double* u0, double* u, int clamp, wbx_report
         if (!s || !u0 || !u) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_deblur");
         cudaStream_t st = s->ctx->stream;
         const uint64_t bytes = s->n * static_cast<uint64_t>(s->batch) * sizeof(double);
-        WBX_CUDA(cudaMemcpyAsync(s->u0.p, u0, bytes, cudaMemcpyHostToDevice, st));
+        // the image copy runs on a side stream (after everything queued so far, which may
+        // still read s->u0) and overlaps the step estimate; the analysis waits for it
+        WBX_CUDA(cudaEventRecord(s->ev_in, st));
+        WBX_CUDA(cudaStreamWaitEvent(s->copy_stream, s->ev_in, 0));
+        WBX_CUDA(cudaMemcpyAsync(s->u0.p, u0, bytes, cudaMemcpyHostToDevice, s->copy_stream));
+        WBX_CUDA(cudaEventRecord(s->ev_in, s->copy_stream));
+        s->input_pending = true;
         const int rc = wbx_deblur_dev(s, s->u0.p, s->uout.p, clamp);
         if (rc != WBX_OK) return rc;
         WBX_CUDA(cudaMemcpyAsync(u, s->uout.p, bytes, cudaMemcpyDeviceToHost, st));
@@ -2126,7 +2176,11 @@ int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_
     if (launches) *launches = s->last_launches;
     if (solve_ms) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, s->ev0, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
+        float t = 0.f, i = 0.f;
+        if (cudaEventElapsedTime(&t, s->ev0, s->ev_mid) != cudaSuccess ||
+            cudaEventElapsedTime(&i, s->ev_it0, s->ev1) != cudaSuccess)
+            return WBX_CUDA_ERROR;
+        ms = t + i;
         *solve_ms = ms;
     }
     return WBX_OK;
@@ -2135,7 +2189,7 @@ int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_
 int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms) {
     if (!s || !tau_ms || !iters_ms) return WBX_INVALID_ARGUMENT;
     if (cudaEventElapsedTime(tau_ms, s->ev0, s->ev_mid) != cudaSuccess) return WBX_CUDA_ERROR;
-    if (cudaEventElapsedTime(iters_ms, s->ev_mid, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
+    if (cudaEventElapsedTime(iters_ms, s->ev_it0, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
     return WBX_OK;
 }
 
