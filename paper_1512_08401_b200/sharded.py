@@ -47,6 +47,8 @@ class _Shard:
         self.world, self.rank, self.rlo, self.rhi, self.clo, self.chi, self.maxR, self.maxC = (int(v) for v in info)
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if getattr(self, "h", None):
             lib.wbx_shard_destroy(self.h)
             self.h = None

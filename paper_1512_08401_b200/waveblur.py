@@ -120,6 +120,8 @@ class Context:
         return int(lib.wbx_ctx_launch_count(self.handle))
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if getattr(self, "handle", None):
             lib.wbx_ctx_destroy(self.handle)
             self.handle = None
@@ -245,11 +247,15 @@ class WaveletBasis:  # wavelet.hpp:68-74, plus its device residency (wbx_basis)
         return self._handle
 
     def _release(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if self._handle is not None:
             lib.wbx_basis_destroy(self._handle)
             self._handle = None
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         self._release()
 
 
@@ -340,11 +346,15 @@ class SparseOperator:
         return inf
 
     def _release(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if self._dev is not None:
             lib.wbx_op_destroy(self._dev)
             self._dev = None
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         self._release()
 
 
@@ -775,6 +785,8 @@ class ExactThetaOp:
         return self.n
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if getattr(self, "handle", None):
             lib.wbx_exact_op_destroy(self.handle)
             self.handle = None
@@ -993,6 +1005,8 @@ class Deblurrer:
         return float(t.value), float(i.value)
 
     def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
         if getattr(self, "handle", None):
             lib.wbx_solver_destroy(self.handle)
             self.handle = None
