@@ -970,7 +970,10 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_kernel(SolveArgs
 #endif
 constexpr int kWinBlock = WBX_WIN_BLOCK;
 constexpr int kWinWarps = kWinBlock / 32;
-constexpr int kWinMinBlocks = 512 / kWinBlock;
+#ifndef WBX_WIN_MINB
+#define WBX_WIN_MINB (512 / WBX_WIN_BLOCK)
+#endif
+constexpr int kWinMinBlocks = WBX_WIN_MINB;  // CTAs per SM the window kernels are built for
 // Shared memory of a CTA:
 //   [uA][uT]          window index lists of the two sides              } loaded once
 //   [sA][sT]          slice tables {record offset, meta, first row}    } per solve
