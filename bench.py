@@ -437,7 +437,7 @@ def run_c4(args, rank, world, local_rank):
     restored = out.cpu().numpy().reshape(dims)
     if isinstance(sh, _SingleGpu):  # the power-iteration count of the solver's own run
         sh.tau_iters = int(sh.d.deblur(u0, clamp=True)[1].tau_iters)
-    return {"metric": f"ms per {size}x{size} spatially varying deblur (C4, row-sharded)", "value": round(ms, 3),
+    return {"metric": f"ms per {size}x{size} spatially varying deblur (C4)", "value": round(ms, 3),
             "unit": "ms", "n_gpus": world, "steps": steps, "higher_is_better": False, "scaling": "strong",
             "impl": "ours", "config": {"workload": f"C4: {size}^2 varying Gaussian 2.5->7.5 px, db4 J=4, K~3.4N, "
                                                    f"SPAI, 100 FISTA iters incl. tau", "nnz": int(op.nnz()),
