@@ -558,6 +558,9 @@ __device__ int g_debug_mode = 0;
 #ifndef WBX_WIN_NB
 #define WBX_WIN_NB 2
 #endif
+#ifndef WBX_TAU_ACC32
+#define WBX_TAU_ACC32 1
+#endif
 // Per-lane register cache of the last dictionary block (single-slice mode)
 #ifndef WBX_DICT_CACHE
 #define WBX_DICT_CACHE 1
@@ -1330,6 +1333,9 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
     WINT* win = static_cast<WINT*>(ws.win);
     double2* cs = static_cast<double2*>(ws.ownT);  // {P^-1/2, w} of the CTA's coordinates
     constexpr bool W64 = sizeof(WINT) == 8;
+    // row sums of the fp32 windows in fp32 (their inputs and outputs are fp32 already; the
+    // Rayleigh-quotient partial sums stay fp64); WBX_TAU_ACC32=0 accumulates in fp64
+    using TACC = typename std::conditional<WBX_TAU_ACC32 && !W64, float, double>::type;
     WINT* uC = W64 ? reinterpret_cast<WINT*>(a.uC) : static_cast<WINT*>(a.yC);  // u = P^-1/2 w on C
     WINT* tR = W64 ? reinterpret_cast<WINT*>(a.t64) : static_cast<WINT*>(a.res);  // t = Theta u on R
     double s2[1] = {0.0};
@@ -1370,7 +1376,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
             }
         pf.side = 0;
         if (it < 200)
-            win_phase<double, WINT, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
+            win_phase<TACC, WINT, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
                                               [&](uint32_t r, double t) { tR[r] = static_cast<WINT>(t); }, pf);
         if (it > 0 && threadIdx.x < 32) {
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -1413,7 +1419,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
         const double rinv = 1.0 / nw_prev;
         double acc[2] = {0.0, 0.0};
         pf.side = 3;
-        win_phase<double, WINT, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
+        win_phase<TACC, WINT, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
                                             [&](uint32_t c, double g) {
                                                 double2& s = cs[c - ws.rT0];
                                                 const double w = (g * rinv) * s.x;
