@@ -1378,19 +1378,29 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
         if (it < 200)
             win_phase<TACC, WINT, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
                                               [&](uint32_t r, double t) { tR[r] = static_cast<WINT>(t); }, pf);
-        if (it > 0 && threadIdx.x < 32) {
-            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
+        if (it > 0) {  // the whole CTA sums the staged partials (fixed order, same in every CTA)
+            if (it == 200) {  // no phase A ran: wait for the staging copies here
+                asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+                __syncthreads();
+            }
+            __shared__ double2 ps[kWinWarps];
             double p0 = 0.0, p1 = 0.0;
-            for (unsigned i = threadIdx.x; i < G; i += 32) {
+            for (unsigned i = threadIdx.x; i < G; i += kWinBlock) {
                 p0 += pstage[i];
                 p1 += pstage[G + i];
             }
             p0 = warp_sum(p0);
             p1 = warp_sum(p1);
+            if ((threadIdx.x & 31) == 0) ps[threadIdx.x >> 5] = make_double2(p0, p1);
+            __syncthreads();
             if (threadIdx.x == 0) {
-                red[0] = p0;
-                red[1] = p1;
+                double t0 = 0.0, t1 = 0.0;
+                for (int k = 0; k < kWinWarps; ++k) {
+                    t0 += ps[k].x;
+                    t1 += ps[k].y;
+                }
+                red[0] = t0;
+                red[1] = t1;
             }
         }
         const long long b0 = WBX_PROFILE == 3 ? clock64() : 0;
