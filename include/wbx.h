@@ -203,6 +203,18 @@ int wbx_pgd(wbx_ctx* ctx, const wbx_op* op, const double* x0, const double* w, d
             const double* p, const wbx_solver_cfg* cfg, int accelerate, double* x_final,
             wbx_report* report);
 
+/* ---------------------------------------------------------------- stencil operator
+ * Theta_K in circulant-compressed form: the kept generator groups
+ * (wbx_theta_expand input) applied directly, y = Theta x or Theta^T x, reading only x and y
+ * (no CSR). Row sums in record order (equal to wbx_spmv within rounding). precision:
+ * WBX_FP64 (double x, y) or WBX_FP32 (float x, y); device pointers. */
+typedef struct wbx_stencil wbx_stencil;
+int wbx_stencil_create(wbx_ctx* ctx, uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
+                       const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
+                       const double* values, wbx_stencil** out);
+int wbx_stencil_destroy(wbx_stencil* s);
+int wbx_stencil_spmv_dev(wbx_stencil* s, int transpose, int precision, const void* x_dev, void* y_dev);
+
 /* ---------------------------------------------------------------- exact FFT operator
  * ExactThetaOp (solver.cpp:21-29): Theta x = analyze(convolve(synthesize(x), psf)), the
  * adjoint with the conjugated kernel spectrum; bitwise the reference's (oracle FFT

@@ -76,6 +76,10 @@ SIGNATURES = {
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
+    "wbx_stencil_create": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
+                                     C.POINTER(C.c_void_p)]),
+    "wbx_stencil_destroy": (C.c_int, [_P]),
+    "wbx_stencil_spmv_dev": (C.c_int, [_P, C.c_int, C.c_int, _P, _P]),
     "wbx_exact_op_create": (C.c_int, [_P, _P, _D, C.POINTER(C.c_void_p)]),
     "wbx_exact_op_destroy": (C.c_int, [_P]),
     "wbx_exact_apply": (C.c_int, [_P, C.c_int, _D, _D]),

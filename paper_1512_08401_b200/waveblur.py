@@ -568,6 +568,32 @@ def theta_conv_topk(basis: WaveletBasis, psf_kernel, K: int, band_weights=None, 
                          blocks[:m].copy(), gidx[:m].copy(), cnt[:m].copy(), val[:m].copy())
 
 
+class StencilOperator:
+    """Theta_K applied straight from its kept generator groups: reads only
+    x and y. apply_dev / apply_adjoint_dev take device pointers (float64 or float32)."""
+
+    def __init__(self, gl: GeneratorList, ctx: Optional[Context] = None):
+        self._ctx = ctx or default_context()
+        self.n = int(np.prod(gl.dims))
+        dims = np.array(gl.dims, dtype=np.uint64)
+        h = C.c_void_p()
+        _check(lib.wbx_stencil_create(self._ctx.handle, len(gl.dims), _u64ptr(dims), gl.J, gl.blocks.size,
+                                      _u32ptr(gl.blocks), _u32ptr(gl.gen_index), _u64ptr(gl.counts),
+                                      _dptr(gl.values), C.byref(h)))
+        self.handle = h
+
+    def spmv_dev(self, x_ptr: int, y_ptr: int, transpose: bool = False, precision: int = N.WBX_FP64) -> None:
+        _check(lib.wbx_stencil_spmv_dev(self.handle, int(transpose), int(precision), C.c_void_p(x_ptr),
+                                        C.c_void_p(y_ptr)))
+
+    def __del__(self):
+        if lib is None:  # interpreter shutdown: the library is already gone
+            return
+        if getattr(self, "handle", None):
+            lib.wbx_stencil_destroy(self.handle)
+            self.handle = None
+
+
 @dataclass
 class SigmaLadder:
     """Stationary Gaussian Theta_K operators at increasing sigmas (one GeneratorList each)."""
