@@ -140,6 +140,8 @@ struct wbx_op {
     std::vector<uint32_t> h_col;
     std::vector<double> h_val;
     uint64_t device_bytes = 0;
+    wbx::DevBuf<double> scratch64[2];  // standalone SpMV: compacted input / output
+    wbx::DevBuf<float> scratch32[2];
 };
 
 namespace wbx {

@@ -51,13 +51,23 @@ inline unsigned blocks_for(uint64_t threads) {
 }
 
 template <typename T>
+DevBuf<T>& scratch_of(wbx_op* op, int which, uint64_t count) {
+    DevBuf<T>& b = sizeof(T) == 8 ? reinterpret_cast<DevBuf<T>&>(op->scratch64[which])
+                                  : reinterpret_cast<DevBuf<T>&>(op->scratch32[which]);
+    if (b.n < count) b.alloc(count);
+    return b;
+}
+
+template <typename T>
 void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
     const wbx_sell& M = transpose ? op->T : op->A;
     const uint32_t* in_idx = transpose ? op->R_glob.p : op->C_glob.p;   // gathered inputs
     const uint32_t* out_idx = transpose ? op->C_glob.p : op->R_glob.p;  // scattered outputs
     const uint32_t m_in = static_cast<uint32_t>(transpose ? op->nR : op->nC);
     const uint32_t m_out = static_cast<uint32_t>(M.rows);
-    DevBuf<T> xin(m_in > 0 ? m_in : 1), yout(m_out > 0 ? m_out : 1);
+    // compacted scratch cached on the operator (calls on one context are serialised)
+    DevBuf<T>& xin = scratch_of<T>(op, 0, m_in > 0 ? m_in : 1);
+    DevBuf<T>& yout = scratch_of<T>(op, 1, m_out > 0 ? m_out : 1);
     WBX_CUDA(cudaMemsetAsync(y, 0, op->n * sizeof(T), s));
     if (m_out > 0) {
         gather_kernel<T><<<blocks_for(m_in), kBlock, 0, s>>>(x, in_idx, m_in, xin.p);
@@ -70,7 +80,6 @@ void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
         count_launch(op->ctx, 3);
         WBX_CUDA(cudaGetLastError());
     }
-    WBX_CUDA(cudaStreamSynchronize(s));  // scratch buffers are freed on return
 }
 
 }  // namespace
