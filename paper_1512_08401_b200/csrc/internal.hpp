@@ -185,7 +185,7 @@ struct WinSide {
     DevBuf<float> d_val;
     uint64_t bytes = 0;
 };
-void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st);
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side);  // side 'A' or 'T'
 struct WinView;
 WinView view_of(const WinSide& w);
 

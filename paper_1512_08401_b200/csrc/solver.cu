@@ -1916,8 +1916,8 @@ void alloc_state(wbx_solver* s) {
         for (int bps = kWinMinBlocks; bps >= 1 && !s->win; --bps) {
             const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
             try {
-                build_win(s->wA, s->op->hA, G, s->ctx->stream);
-                build_win(s->wT, s->op->hT, G, s->ctx->stream);
+                build_win(s->wA, s->op->hA, G, s->ctx->stream, 'A');
+                build_win(s->wT, s->op->hT, G, s->ctx->stream, 'T');
             } catch (const Error&) {
                 continue;  // a window exceeded 16-bit local indices
             }

@@ -17,10 +17,13 @@ uint64_t segs_of(uint64_t len) { return std::max<uint64_t>(1, (len + kSegElems -
 
 // Contiguous row ranges per CTA balanced by COST = wseg per lane segment + wnnz per nonzero
 // (a slice's time has a fixed part and a part growing with its quads and segment folds).
-std::vector<uint64_t> balance(const HostCompact& M, uint32_t G) {
+std::vector<uint64_t> balance(const HostCompact& M, uint32_t G, char side) {
     const uint64_t nrows = M.rows();
-    uint64_t wseg = 4, wnnz = 1;  // measured (trace_phases blocks): ~2.5x slice time for 99-long rows
-    if (const char* e = std::getenv("WBX_WIN_COST")) {  // diagnostics: "segment_weight,nonzero_weight"
+    uint64_t wseg = 8, wnnz = 1;  // swept (tools/cost_sweep.sh): best of 4..12 per side at C2
+    const std::string key = std::string("WBX_WIN_COST_") + side;  // per side, then both sides
+    const char* e = std::getenv(key.c_str());
+    if (!e) e = std::getenv("WBX_WIN_COST");
+    if (e) {  // diagnostics: "segment_weight,nonzero_weight"
         unsigned long long a = 0, b = 0;
         if (std::sscanf(e, "%llu,%llu", &a, &b) == 2) {
             wseg = a;
@@ -142,8 +145,8 @@ std::vector<uint16_t> place_window(const std::vector<uint4>& rec, const std::vec
 
 }  // namespace
 
-void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st) {
-    const std::vector<uint64_t> rb = balance(M, G);
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side) {
+    const std::vector<uint64_t> rb = balance(M, G, side);
     // format: the dictionary when every CTA's fits the budget
     bool dict_fmt = std::getenv("WBX_WIN_FULL") == nullptr;  // diagnostics: force the full format
     std::vector<std::vector<float>> dicts(G);

@@ -1,5 +1,4 @@
-for c in 16,1 4,1 1,1 2,1 8,1; do
-  export WBX_WIN_COST=$c
-  export WBX_TRACE_FILE=/tmp/tf$c.bin; python tools/trace_phases.py run fista 32 >/dev/null; echo "$c fista $(python tools/trace_phases.py show $WBX_TRACE_FILE blocks | tr '\n' ' ' | cut -c1-420)"
-  unset WBX_TRACE_FILE; python tools/probe_solver.py | cut -c1-200
-done
+# per-side cost-weight sweep of the window partition (WBX_WIN_COST_A / _T = "segment,nonzero")
+for ca in 4,1 8,1 12,1; do for ct in 4,1 8,1 12,1; do
+  echo "A=$ca T=$ct $(WBX_WIN_COST_A=$ca WBX_WIN_COST_T=$ct python tools/probe_solver.py | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["tau only (200 power iters)"], d["fista 100 (tau given)"])')"
+done; done
