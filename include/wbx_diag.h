@@ -14,11 +14,9 @@ int wbx_diag_barrier_us(int device, int iters, int blocks_per_sm, double* us);
  * memory with `inflight` copies in flight; mode 1 = 16-byte LDG per lane (8 in flight). */
 int wbx_diag_stream_gbs(int device, int mode, uint64_t bytes, int reps, int chunk, int inflight,
                         int blocks_per_sm, double* gbs);
-/* Cycle accounting of the last solves in a diagnostics build (make prof, WBX_PROFILE=2|3);
- * fills out[8] and resets the counters. WBX_PROFILE=2 (stream engine): average cycles per
- * slice [TMA wait, load+gather+FMA, combine+issue+epilogue, -, -] and the slice count.
- * WBX_PROFILE=3 (window engine): summed per-warp cycles [A fill, A slice loop, A barrier,
- * T fill, T slice loop, T barrier, A data wait, T data wait]. */
+/* Cycle accounting of the last solves in a diagnostics build (make prof, WBX_PROFILE=3):
+ * fills out[8] with the summed per-warp cycles of the window engine [A fill, A slice loop,
+ * A barrier, T fill, T slice loop, T barrier, 0, 0] and resets the counters. */
 int wbx_diag_slice_profile(double* out);
 #ifdef __cplusplus
 }

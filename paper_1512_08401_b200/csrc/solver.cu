@@ -545,18 +545,10 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
     }
 }
 
-// Diagnostics switch (WBX_DEBUG_MODE, timing experiments only; results are wrong when set):
-// 1 = gather x[0] instead of x[col] (removes the gather dependency).
-__device__ int g_debug_mode = 0;
-// Compile-time diagnostics (make WBX_PROFILE=1|2): 1 = gathers hit x[0] only (removes the
-// gather dependency, timing experiment), 2 = per-slice cycle accounting (wbx_diag_slice_profile).
+// Compile-time diagnostics (make prof, WBX_PROFILE=3): cycle accounting of the window engine
+// (wbx_diag_slice_profile, tools/win_profile.py)
 #ifndef WBX_PROFILE
 #define WBX_PROFILE 0
-#endif
-// 2 = per-slice cycle accounting: [tma wait, load+gather+fma, combine+issue+epilogue, slices]
-// Window engine lookahead (dictionary format): 3 = three slices in flight, 4 = two pairs
-#ifndef WBX_WIN_NB
-#define WBX_WIN_NB 2
 #endif
 #ifndef WBX_TAU_ACC32
 #define WBX_TAU_ACC32 1
@@ -573,13 +565,7 @@ __device__ unsigned long long g_prof[8];
 extern "C" int wbx_diag_slice_profile(double* out) {
     unsigned long long h[8];
     if (cudaMemcpyFromSymbol(h, wbx::g_prof, sizeof h) != cudaSuccess) return WBX_CUDA_ERROR;
-    if (WBX_PROFILE == 3) {  // window engine: raw cycle totals (8 slots, see WinProf)
-        for (int i = 0; i < 8; ++i) out[i] = static_cast<double>(h[i]);
-    } else {
-        for (int i = 0; i < 5; ++i) out[i] = h[5] ? static_cast<double>(h[i]) / static_cast<double>(h[5]) : 0.0;
-        out[5] = static_cast<double>(h[5]);
-        out[6] = out[7] = 0.0;
-    }
+    for (int i = 0; i < 8; ++i) out[i] = static_cast<double>(h[i]);  // raw cycle totals (WinProf)
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(wbx::g_prof, z, sizeof z);
     return WBX_OK;
@@ -609,7 +595,6 @@ struct Streamer {
     // a global load
     uint32_t reg_meta;
     uint64_t reg_off;
-    unsigned long long prof[6];  // WBX_DEBUG_MODE=2 cycle accounting
 };
 
 __device__ __forceinline__ uint32_t count_slices(const SellView& M, uint32_t gwarp, uint32_t nwarps) {
@@ -687,9 +672,7 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
     for (uint32_t i = 0; i < count; ++i) {
         const uint64_t e = st.consumed;
         const unsigned slot = static_cast<unsigned>(e % st.ns);
-        const long long c0 = WBX_PROFILE == 2 ? clock64() : 0;
         mbar_wait(st.bars + slot, static_cast<unsigned>((e / st.ns) & 1u));
-        const long long c1 = WBX_PROFILE == 2 ? clock64() : 0;
         const uint32_t meta = st.meta[slot];
         const uint32_t np = meta & 0xffu;
         const uint4* rec = st.slots + slot * kRecU4;
@@ -700,11 +683,10 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
 #pragma unroll
         for (int j = 0; j < 8; ++j) q[j] = j < static_cast<int>(np) ? p[j * kWarp] : make_uint4(0, 0, 0, 0);
         X g[16];
-        const uint32_t cmask = WBX_PROFILE == 1 ? 0u : 0xffffffffu;  // diagnostics: 1 = no gathers
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            g[2 * j] = j < static_cast<int>(np) ? x[q[j].y & cmask] : X(0);
-            g[2 * j + 1] = j < static_cast<int>(np) ? x[q[j].w & cmask] : X(0);
+            g[2 * j] = j < static_cast<int>(np) ? x[q[j].y] : X(0);
+            g[2 * j + 1] = j < static_cast<int>(np) ? x[q[j].w] : X(0);
         }
         ACC acc = ACC(0);
 #pragma unroll
@@ -714,26 +696,11 @@ __device__ __forceinline__ void st_phase(Streamer& st, const SellView& A, const 
                 acc = fma(static_cast<ACC>(__uint_as_float(q[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
             }
         }
-        if (WBX_PROFILE == 2)acc += static_cast<ACC>(clock64() & 0) ;
-        const long long c2 = WBX_PROFILE == 2 ? clock64() : 0;
         const uint32_t row = combine_info(info, meta, acc);
         __syncwarp();  // every lane is done with the slot before it is refilled
-        const long long c2a = WBX_PROFILE == 2 ? clock64() : 0;
         st.consumed = e + 1;
         if (st.issued < st.limit) st_issue(st, A, T, gwarp, nwarps, lane);
-        if (WBX_PROFILE == 2)__syncwarp();
-        const long long c2b = WBX_PROFILE == 2 ? clock64() : 0;
         if (row != kNoRow) post(row, acc, pv);
-        if (WBX_PROFILE == 2){
-            __syncwarp();
-            const long long c3 = clock64();
-            st.prof[0] += static_cast<unsigned long long>(c1 - c0);
-            st.prof[1] += static_cast<unsigned long long>(c2 - c1);
-            st.prof[2] += static_cast<unsigned long long>(c2a - c2);
-            st.prof[3] += static_cast<unsigned long long>(c2b - c2a);
-            st.prof[4] += static_cast<unsigned long long>(c3 - c2b);
-            st.prof[5] += 1;
-        }
     }
 }
 
@@ -742,8 +709,6 @@ __device__ __forceinline__ void st_drain(Streamer& st) {
     for (uint64_t e = st.consumed; e < st.issued; ++e)
         mbar_wait(st.bars + e % st.ns, static_cast<unsigned>((e / st.ns) & 1u));
     st.consumed = st.issued;
-    if (WBX_PROFILE == 2 && (threadIdx.x & 31) == 0)
-        for (int i = 0; i < 6; ++i) atomicAdd(&g_prof[i], st.prof[i]);
 }
 
 // ---------------------------------------------------------------- estimate_step kernel
@@ -1081,8 +1046,7 @@ __device__ __forceinline__ void win_load(const uint4* rec_base, const uint4& sl,
 
 // WBX_PROFILE=3: per-warp cycle accounting of the window engine (wbx_diag_slice_profile)
 struct WinProf {
-    // [A fill, A slice loop, A barrier, T fill, T slice loop, T barrier, A data wait,
-    //  T data wait] (cycles, summed)
+    // [A fill, A slice loop, A barrier, T fill, T slice loop, T barrier, -, -] (cycles, summed)
     unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int side = 0;  // 0 = phase A, 3 = phase T (set before each phase, used by the timers)
     __device__ __forceinline__ void flush() {
@@ -1093,25 +1057,21 @@ struct WinProf {
 
 // One phase on the window engine: fill the CTA's window from x (asynchronous copies, one
 // parallel round trip; the first slices' record loads are issued before it since they do
-// not depend on x), then every warp runs its slices (w, w+8, ...) with NB-1 slices of
+// not depend on x), then every warp runs its slices (w, w+8, ...) with one slice of
 // record loads in flight; the vector operand and (dictionary format) the values come from
 // shared memory.
-template <typename ACC, typename WIN, bool DICT, int NB, typename X, typename Post>
+template <typename ACC, typename WIN, bool DICT, typename X, typename Post>
 __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, const uint16_t* uslot, uint32_t nu,
                                           const uint4* stab,
                                           uint32_t ns, const float* dict, const X* __restrict__ x, WIN* win,
                                           Post post, WinProf& pf) {
     static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
-    static_assert(NB == 2 || NB == 3 || NB == 4, "lookahead buffers (4: slices computed in pairs)");
     const long long t0 = WBX_PROFILE == 3 ? clock64() : 0;
     const int lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint64_t pol = l2_keep_policy();
-    WinSlice<DICT> b0, b1, b2, b3;
+    WinSlice<DICT> b0, b1;
     if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
-    if (NB >= 3 && wib + kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + kWinWarps], lane, pol, b1);
-    if (NB >= 3 && wib + 2 * kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + 2 * kWinWarps], lane, pol, b2);
-    if (NB == 4 && wib + 3 * kWinWarps < ns) win_load<DICT>(W.rec, stab[wib + 3 * kWinWarps], lane, pol, b3);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
     for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
@@ -1162,94 +1122,12 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
         }
         if (static_cast<uint32_t>(lane) < cnt) post(sl.z + lane, acc);
     };
-    // process slice s from d, then refill d with slice s + NB*8
-    auto step = [&](WinSlice<DICT>& d, uint32_t s) {
-        run(d, s);
-        const uint32_t sn = s + NB * kWinWarps;
-        if (sn < ns) win_load<DICT>(W.rec, stab[sn], lane, pol, d);
-    };
-    // two slices at once (independent latency chains interleave): sa from da and, if
-    // sb < ns, sb from db
-    auto run2 = [&](const WinSlice<DICT>& da, uint32_t sa, const WinSlice<DICT>& db, uint32_t sb) {
-        const bool hb = sb < ns;
-        if (WBX_PROFILE == 3) {  // time until this pair's record data has arrived
-            const long long w0 = clock64();
-            long long w1;
-            asm volatile(
-                "{\n\t.reg .u32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 t, t, %3;\n\tadd.u32 t, t, %4;\n\t"
-                "mov.u64 %0, %%clock64;\n\t}"
-                : "=l"(w1)
-                : "r"(da.pb), "r"(da.c[0].x), "r"(db.pb), "r"(db.c[0].x)
-                : "memory");
-            pf.c[6 + pf.side / 3] += w1 - w0;
-        }
-        const uint4 la = stab[sa];
-        const uint4 lb = hb ? stab[sb] : make_uint4(0, 1u << 16, 0, 0);
-        const uint32_t nqa = la.y & 0xffu, ma = (la.y >> 8) & 0xffu, nsa = (la.y >> 16) & 0xffu, ca = la.y >> 24;
-        const uint32_t nqb = lb.y & 0xffu, mb = (lb.y >> 8) & 0xffu, nsb = (lb.y >> 16) & 0xffu, cb = lb.y >> 24;
-        ACC aa = ACC(0), ab = ACC(0);
-        // both slices in one basic block per quad (their latency chains interleave); a quad
-        // beyond a slice's own count contributes exact zeros through window entry 0
-        const uint32_t nqm = nqa > nqb ? nqa : nqb;
-        const uint32_t pa = da.pb, pbb = hb ? db.pb : 0u;
-#pragma unroll
-        for (uint32_t qd = 0; qd < 4; ++qd) {
-            if (qd < nqm) {
-                const bool ia = qd < nqa, ib = qd < nqb;
-                float4 va = *reinterpret_cast<const float4*>(dict + pa + qd * 4);
-                float4 vb = *reinterpret_cast<const float4*>(dict + pbb + qd * 4);
-                const uint2 ca = ia ? da.c[qd] : make_uint2(0, 0);
-                const uint2 cb = ib ? db.c[qd] : make_uint2(0, 0);
-                if (!ia) va = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (!ib) vb = make_float4(0.f, 0.f, 0.f, 0.f);
-                const WIN a0 = win[ca.x & 0xffffu], a1 = win[ca.x >> 16], a2 = win[ca.y & 0xffffu], a3 = win[ca.y >> 16];
-                const WIN b0 = win[cb.x & 0xffffu], b1 = win[cb.x >> 16], b2 = win[cb.y & 0xffffu], b3 = win[cb.y >> 16];
-                aa = fma(static_cast<ACC>(va.x), static_cast<ACC>(a0), aa);
-                ab = fma(static_cast<ACC>(vb.x), static_cast<ACC>(b0), ab);
-                aa = fma(static_cast<ACC>(va.y), static_cast<ACC>(a1), aa);
-                ab = fma(static_cast<ACC>(vb.y), static_cast<ACC>(b1), ab);
-                aa = fma(static_cast<ACC>(va.z), static_cast<ACC>(a2), aa);
-                ab = fma(static_cast<ACC>(vb.z), static_cast<ACC>(b2), ab);
-                aa = fma(static_cast<ACC>(va.w), static_cast<ACC>(a3), aa);
-                ab = fma(static_cast<ACC>(vb.w), static_cast<ACC>(b3), ab);
-            }
-        }
-        const uint32_t nsm = nsa > nsb ? nsa : nsb;
-        for (uint32_t t = 1; t < nsm; ++t) {
-            const ACC oa = __shfl_down_sync(0xffffffffu, aa, t * ma);
-            const ACC ob = __shfl_down_sync(0xffffffffu, ab, t * mb);
-            if (t < nsa && static_cast<uint32_t>(lane) < ma) aa += oa;
-            if (t < nsb && static_cast<uint32_t>(lane) < mb) ab += ob;
-        }
-        if (static_cast<uint32_t>(lane) < ca) post(la.z + lane, aa);
-        if (static_cast<uint32_t>(lane) < cb) post(lb.z + lane, ab);
-    };
-    if (NB == 4) {
-        static_assert(NB != 4 || DICT, "paired slices use the dictionary format");
-        constexpr uint32_t W8 = kWinWarps;
-        for (uint32_t s = wib; s < ns; s += 4 * W8) {
-            run2(b0, s, b1, s + W8);
-            if (s + 4 * W8 < ns) win_load<DICT>(W.rec, stab[s + 4 * W8], lane, pol, b0);
-            if (s + 5 * W8 < ns) win_load<DICT>(W.rec, stab[s + 5 * W8], lane, pol, b1);
-            if (s + 2 * W8 >= ns) break;
-            run2(b2, s + 2 * W8, b3, s + 3 * W8);
-            if (s + 6 * W8 < ns) win_load<DICT>(W.rec, stab[s + 6 * W8], lane, pol, b2);
-            if (s + 7 * W8 < ns) win_load<DICT>(W.rec, stab[s + 7 * W8], lane, pol, b3);
-        }
-    } else if (NB == 3) {
-        for (uint32_t s = wib; s < ns; s += NB * kWinWarps) {
-            step(b0, s);
-            if (s + kWinWarps >= ns) break;
-            step(b1, s + kWinWarps);
-            if (s + 2 * kWinWarps >= ns) break;
-            step(b2, s + 2 * kWinWarps);
-        }
-    } else {  // two buffers: the next load is issued before the current slice computes
-        for (uint32_t s = wib; s < ns; s += kWinWarps) {
-            b1 = b0;
-            if (s + kWinWarps < ns) win_load<DICT>(W.rec, stab[s + kWinWarps], lane, pol, b0);
-            run(b1, s);
-        }
+    // one slice of record loads in flight: the next load is issued before the current slice
+    // computes (deeper lookahead and paired slices measured slower: register pressure)
+    for (uint32_t s = wib; s < ns; s += kWinWarps) {
+        b1 = b0;
+        if (s + kWinWarps < ns) win_load<DICT>(W.rec, stab[s + kWinWarps], lane, pol, b0);
+        run(b1, s);
     }
     if (WBX_PROFILE == 3) {
         const long long t2 = clock64();
@@ -1261,7 +1139,6 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
 
 template <bool DICT>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(SolveArgs a) {
-    constexpr int NB = DICT ? WBX_WIN_NB : 2;
     __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
@@ -1294,12 +1171,12 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(Sol
     };
     for (int k = 1; k <= a.max_iters; ++k) {
         pf.side = 0;
-        win_phase<float, float, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
+        win_phase<float, float, DICT>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
                                           [&](uint32_t r, float acc) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
         sync();
         const float beta = a.beta32[k - 1];
         pf.side = 3;
-        win_phase<float, float, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
+        win_phase<float, float, DICT>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
                                           [&](uint32_t c, float g) {
                                               float4& s = cs[c - ws.rT0];
                                               const float z0 = fmaf(-s.z, g, s.x);
@@ -1322,7 +1199,6 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(Sol
 // to fp32, the products are exact in fp64; double: fp64 windows, WBX_TAU_WINDOW=64)
 template <bool DICT, typename WINT>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(SolveArgs a) {
-    constexpr int NB = DICT ? WBX_WIN_NB : 2;
     __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
     const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
@@ -1376,7 +1252,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
             }
         pf.side = 0;
         if (it < 200)
-            win_phase<TACC, WINT, DICT, NB>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
+            win_phase<TACC, WINT, DICT>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
                                               [&](uint32_t r, double t) { tR[r] = static_cast<WINT>(t); }, pf);
         if (it > 0) {  // the whole CTA sums the staged partials (fixed order, same in every CTA)
             if (it == 200) {  // no phase A ran: wait for the staging copies here
@@ -1429,7 +1305,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
         const double rinv = 1.0 / nw_prev;
         double acc[2] = {0.0, 0.0};
         pf.side = 3;
-        win_phase<TACC, WINT, DICT, NB>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
+        win_phase<TACC, WINT, DICT>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
                                             [&](uint32_t c, double g) {
                                                 double2& s = cs[c - ws.rT0];
                                                 const double w = (g * rinv) * s.x;
@@ -1893,10 +1769,6 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
 template <typename T>
 void alloc_state(wbx_solver* s) {
     const wbx_op* op = s->op;
-    if (const char* e = std::getenv("WBX_DEBUG_MODE")) {
-        const int mode = std::atoi(e);
-        WBX_CUDA(cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof mode));
-    }
     auto rnd = [](uint64_t count) { return ((count * sizeof(T) + 255) / 256) * 256; };
     const uint64_t B = static_cast<uint64_t>(s->batch);
     s->state.alloc(2 * rnd(op->nC * B) + 2 * rnd(op->nC) + 2 * rnd(op->nR * B) + 256);

@@ -32,8 +32,8 @@ for name, cfg, phases in [("fista", dict(max_iters=100, tau=meta["tau"]), 200), 
     warps = 296 * 8
     per = warps * nph
     res[name] = {"ms": round(r.wall_time_s * 1e3, 3), "phases": nph,
-                 "A": {"fill": round(h[0] / per), "loop": round(h[1] / per), "data_wait": round(h[6] / per),
+                 "A": {"fill": round(h[0] / per), "loop": round(h[1] / per),
                        "barrier": round(h[2] / per)},
-                 "T": {"fill": round(h[3] / per), "loop": round(h[4] / per), "data_wait": round(h[7] / per),
+                 "T": {"fill": round(h[3] / per), "loop": round(h[4] / per),
                        "barrier": round(h[5] / per)}}
 print(json.dumps(res))
