@@ -730,10 +730,14 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
     if constexpr (sizeof(T) == 4)
         st_init(st, dsmem + (threadIdx.x >> 5) * warp_smem_bytes(a.nslots), a.A, a.T, gwarp, nwarps, lane, 200,
                 false, a.nslots);
-    // row loop of one phase: TMA-staged fp32 operator (T = float) or exact fp64 layout
-    auto phase = [&](bool isT, const double* x, auto pre, auto post) {
+    // row loop of one phase: TMA-staged fp32 operator with fp32 vectors (T = float, as in the
+    // window engine) or the exact fp64 layout with fp64 vectors (T = double)
+    using V = T;
+    V* uC = sizeof(T) == 4 ? reinterpret_cast<V*>(a.yC) : reinterpret_cast<V*>(a.uC);   // P^-1/2 w on C
+    V* tR = sizeof(T) == 4 ? reinterpret_cast<V*>(a.res) : reinterpret_cast<V*>(a.t64);  // Theta u on R
+    auto phase = [&](bool isT, const V* x, auto pre, auto post) {
         if constexpr (sizeof(T) == 4)
-            st_phase<double, double>(st, a.A, a.T, gwarp, nwarps, lane, isT ? st.nT : st.nA, x, pre, post);
+            st_phase<float, float>(st, a.A, a.T, gwarp, nwarps, lane, isT ? st.nT : st.nA, x, pre, post);
         else
             for_rows_exact(isT ? a.T : a.A, gwarp, nwarps, lane, x,
                            [&](uint32_t r, double v) { post(r, v, pre(r)); });
@@ -748,8 +752,8 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
     }
     for (uint64_t c = gthread; c < a.nC; c += nthreads) {
         const double v = rng_normal(0x5eedull, a.C_glob[c]);
-        a.wv[c] = v;               // "w_prev" = raw v0, |w_prev| = |v0|
-        a.uC[c] = a.ispC[c] * v;   // P^-1/2 w_prev
+        a.wv[c] = v;                              // "w_prev" = raw v0, |w_prev| = |v0|
+        uC[c] = static_cast<V>(a.ispC[c] * v);    // P^-1/2 w_prev
     }
     grid_sync_reduce<1>(a.sync, epoch, s2, smem);
     double nw_prev = sqrt(s2[0]);
@@ -760,12 +764,13 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
         // t = Theta (P^-1/2 v) = Theta (P^-1/2 w_prev) / |w_prev|
         const double inv = nw_prev;
         phase(
-            false, a.uC, [](uint32_t) { return 0; }, [&](uint32_t r, double t, int) { a.t64[r] = t / inv; });
+            false, uC, [](uint32_t) { return 0; },
+            [&](uint32_t r, double t, int) { tR[r] = static_cast<V>(t / inv); });
         grid_sync(a.sync, epoch, smem);
         // w = P^-1/2 Theta^T t ; <v, w>, <w, w> with v = w_prev / |w_prev|
         double acc[2] = {0.0, 0.0};
         phase(
-            true, a.t64,
+            true, tR,
             [&](uint32_t c) { return c != kNoRow ? make_double2(a.ispC[c], a.wv[c]) : make_double2(0.0, 0.0); },
             [&](uint32_t c, double g, double2 pv) {
                 const double w = g * pv.x;
@@ -773,7 +778,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
                 acc[0] += v * w;
                 acc[1] += w * w;
                 a.wv[c] = w;
-                a.uC[c] = pv.x * w;
+                uC[c] = static_cast<V>(pv.x * w);
             });
         grid_sync_reduce<2>(a.sync, epoch, acc, smem);
         const double lambda = acc[0];
