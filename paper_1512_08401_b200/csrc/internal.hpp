@@ -179,6 +179,7 @@ void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint
 // winlayout.cu: per-CTA window layout of one operator side (win.cuh)
 struct WinSide {
     uint32_t G = 0, max_u = 0, max_win = 0, max_rows = 0, max_slices = 0, max_dict = 0;
+    uint32_t src_len = 0;  // length of the gathered vector (set by the solver)
     DevBuf<uint32_t> u_off, u_idx, s_off, r_off, d_off;
     DevBuf<uint16_t> u_slot;
     DevBuf<uint4> s_tab, rec;

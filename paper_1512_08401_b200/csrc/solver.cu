@@ -545,6 +545,16 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
     }
 }
 
+// Debug build (make check): bounds assertions in the window engine; a violation traps the
+// kernel (the call then fails with a CUDA error) instead of reading or writing out of range.
+#ifndef WBX_CHECKS
+#define WBX_CHECKS 0
+#endif
+#define WBX_ASSERT(cond)                       \
+    do {                                       \
+        if (WBX_CHECKS && !(cond)) __trap();   \
+    } while (0)
+
 // Compile-time diagnostics (make prof, WBX_PROFILE=3): cycle accounting of the window engine
 // (wbx_diag_slice_profile, tools/win_profile.py)
 #ifndef WBX_PROFILE
@@ -1079,6 +1089,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
     for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
+        WBX_ASSERT(uslot[i] < W.max_win && uidx[i] < W.src_len);
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
                      : "memory");
@@ -1096,6 +1107,8 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
         const uint4 sl = stab[s];  // {record offset, meta, first row, -}
         const uint32_t nq = sl.y & 0xffu, m = (sl.y >> 8) & 0xffu, nseg = (sl.y >> 16) & 0xffu;
         const uint32_t cnt = sl.y >> 24;
+        WBX_ASSERT(s < ns && nq >= 1 && nq <= 4 && m >= 1 && m * nseg <= 32 && cnt <= m);
+        WBX_ASSERT(!DICT || d.pb + 15 < W.max_dict);
         if (DICT && WBX_DICT_CACHE && d.pb != cpb) {
             cpb = d.pb;
 #pragma unroll
@@ -1112,6 +1125,8 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
                     v = make_float4(__uint_as_float(d.v[qd].x), __uint_as_float(d.v[qd].y),
                                     __uint_as_float(d.v[qd].z), __uint_as_float(d.v[qd].w));
                 }
+                WBX_ASSERT((d.c[qd].x & 0xffffu) < W.max_win && (d.c[qd].x >> 16) < W.max_win &&
+                           (d.c[qd].y & 0xffffu) < W.max_win && (d.c[qd].y >> 16) < W.max_win);
                 const WIN g0 = win[d.c[qd].x & 0xffffu], g1 = win[d.c[qd].x >> 16];
                 const WIN g2 = win[d.c[qd].y & 0xffffu], g3 = win[d.c[qd].y >> 16];
                 acc = fma(static_cast<ACC>(v.x), static_cast<ACC>(g0), acc);
@@ -1177,12 +1192,16 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(Sol
     for (int k = 1; k <= a.max_iters; ++k) {
         pf.side = 0;
         win_phase<float, float, DICT>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
-                                          [&](uint32_t r, float acc) { res[r] = acc - x0s[r - ws.rA0]; }, pf);
+                                          [&](uint32_t r, float acc) {
+                                              WBX_ASSERT(r - ws.rA0 < ws.nrA);
+                                              res[r] = acc - x0s[r - ws.rA0];
+                                          }, pf);
         sync();
         const float beta = a.beta32[k - 1];
         pf.side = 3;
         win_phase<float, float, DICT>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
                                           [&](uint32_t c, float g) {
+                                              WBX_ASSERT(c - ws.rT0 < ws.nrT);
                                               float4& s = cs[c - ws.rT0];
                                               const float z0 = fmaf(-s.z, g, s.x);
                                               const float xn = Prec<float>::prox(z0, s.w);
@@ -1312,6 +1331,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
         pf.side = 3;
         win_phase<TACC, WINT, DICT>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
                                             [&](uint32_t c, double g) {
+                                                WBX_ASSERT(c - ws.rT0 < ws.nrT);
                                                 double2& s = cs[c - ws.rT0];
                                                 const double w = (g * rinv) * s.x;
                                                 const double v = s.y * rinv;
@@ -1795,6 +1815,8 @@ void alloc_state(wbx_solver* s) {
             try {
                 build_win(s->wA, s->op->hA, G, s->ctx->stream, 'A');
                 build_win(s->wT, s->op->hT, G, s->ctx->stream, 'T');
+                s->wA.src_len = static_cast<uint32_t>(s->op->nC);  // A rows gather C-space vectors
+                s->wT.src_len = static_cast<uint32_t>(s->op->nR);
             } catch (const Error&) {
                 continue;  // a window exceeded 16-bit local indices
             }

@@ -44,6 +44,7 @@ struct WinView {
     uint32_t max_rows;       // most rows of any CTA (per-row state owned in shared memory)
     uint32_t max_slices;     // most slices of any CTA
     uint32_t max_dict;       // largest dictionary of any CTA (floats; 0 = full format)
+    uint32_t src_len;        // length of the vector the windows gather from (debug checks)
 };
 
 // slice meta word: nq (quads per lane) | m (lane stride) << 8 | q (segments per row) << 16 |

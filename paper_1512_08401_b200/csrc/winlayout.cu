@@ -284,6 +284,7 @@ WinView view_of(const WinSide& w) {
     v.max_rows = w.max_rows;
     v.max_slices = w.max_slices;
     v.max_dict = w.max_dict;
+    v.src_len = w.src_len;
     return v;
 }
 
