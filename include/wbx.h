@@ -12,7 +12,7 @@
  *   * Every function returns a wbx_status; the message of the last failure on the
  *     calling thread is available from wbx_last_error(). Status codes map 1:1 onto
  *     the reference's exception types (`include/waveblur/image.hpp:10-36`), which the
- *     C++ facade (include/waveblur/*.hpp) re-throws.
+ *     reference-side binding (integration/wbx_backend.cpp) re-throws.
  *   * A context binds one CUDA device and one stream; calls on one context must be
  *     serialised by the caller (the reference's functions are pure and re-entrant;
  *     use one context per host thread for the same property).

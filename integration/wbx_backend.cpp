@@ -1,17 +1,38 @@
-// proj/src/wbx_backend.cpp — route the hot path of waveblur to libwbx.so (B200)
+// proj/src/wbx_backend.cpp — route the hot path of waveblur to libwbx.so (B200).
+//
+// Defines the reference's hot-path functions (wavelet.hpp:88,91; theta.hpp:83-89;
+// precond.hpp:26-34; solver.hpp:86-105; SparseThetaOp::apply/apply_adjoint) on top of the
+// C ABI in include/wbx.h. The reference's CPU definitions stay in the library under a
+// `*_host` name; operators that are not a SparseThetaOp (ExactThetaOp,
+// user ThetaOps) keep running there. WBX_BACKEND_PRECISION=32 selects the fp32 hot path;
+// the default is the fp64 mode, bitwise equal to the reference.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
+
+#include "waveblur/precond.hpp"
 #include "waveblur/solver.hpp"
 #include "waveblur/theta.hpp"
+#include "waveblur/wavelet.hpp"
 #include "wbx.h"
 
 namespace waveblur {
+
+// the reference's own definitions, renamed by the build
+double energy_host(const std::vector<double>& x, const DeblurProblem& problem);
+double estimate_step_host(const ThetaOp& op, const DiagonalPreconditioner& P, double step_safety);
+SolveReport ista_host(const DeblurProblem& problem, const DiagonalPreconditioner& P, const SolverConfig& c);
+SolveReport fista_host(const DeblurProblem& problem, const DiagonalPreconditioner& P, const SolverConfig& c);
+
 namespace {
-wbx_ctx* ctx() {                       // one context per host thread
-    thread_local wbx_ctx* c = [] { wbx_ctx* p = nullptr; wbx_ctx_create(0, &p); return p; }();
-    return c;
-}
-void check(int st) {                   // status -> the reference's exception types
+
+std::recursive_mutex mu;  // one libwbx context, calls serialised (the reference's are re-entrant)
+
+void check(int st) {  // status -> the reference's exception types (image.hpp:10-36)
     if (st == WBX_OK) return;
     const char* m = wbx_last_error();
     switch (st) {
@@ -27,40 +48,116 @@ void check(int st) {                   // status -> the reference's exception ty
         default: throw std::runtime_error(m);
     }
 }
-struct DeviceOp {                      // device layouts of one SparseOperator, cached by address
-    wbx_op* op = nullptr;
-    explicit DeviceOp(const SparseOperator& s) {
-        check(wbx_op_create(ctx(), s.n, s.row_offsets.data(), s.col_indices.data(), s.values.data(), &op));
-    }
-    ~DeviceOp() { wbx_op_destroy(op); }
-};
-}  // namespace
 
-std::vector<double> spmv(const SparseOperator& op, const std::vector<double>& x) {
-    if (x.size() != op.n) throw ShapeMismatch("spmv: vector length mismatch");
-    DeviceOp d(op);                    // production code caches this per operator
-    std::vector<double> y(op.n);
-    check(wbx_spmv(ctx(), d.op, 0, x.data(), y.data()));
-    return y;
+wbx_ctx* ctx() {
+    static wbx_ctx* c = [] {
+        wbx_ctx* p = nullptr;
+        check(wbx_ctx_create(0, &p));
+        return p;
+    }();
+    return c;
 }
 
-SolveReport fista(const DeblurProblem& p, const DiagonalPreconditioner& P, const SolverConfig& c) {
-    auto* sp = dynamic_cast<const SparseThetaOp*>(p.op);
-    if (!sp) throw std::invalid_argument("fista: device path needs a SparseThetaOp");
-    DeviceOp d(sp->sparse());
+int precision() {
+    static const int p = [] {
+        const char* e = std::getenv("WBX_BACKEND_PRECISION");
+        return e && std::atoi(e) == 32 ? WBX_FP32 : WBX_FP64;
+    }();
+    return p;
+}
+
+void mix(uint64_t& h, const void* data, std::size_t bytes) {
+    const auto* p = static_cast<const unsigned char*>(data);
+    for (; bytes >= 8; bytes -= 8, p += 8) {
+        uint64_t w;
+        std::memcpy(&w, p, 8);
+        h = (h ^ w) * 0x100000001b3ULL;
+    }
+    for (; bytes; --bytes, ++p) h = (h ^ *p) * 0x100000001b3ULL;
+}
+
+// Device layouts of Theta and its transpose, cached by content: building them costs more
+// than a product, and the reference's loops apply one operator many times.
+wbx_op* device_op(const SparseOperator& s) {
+    if (s.row_offsets.size() != s.n + 1 || s.col_indices.size() != s.values.size())
+        throw ShapeMismatch("SparseOperator: inconsistent CSR arrays");
+    uint64_t key = 0xcbf29ce484222325ULL;
+    mix(key, &s.n, sizeof s.n);
+    mix(key, s.row_offsets.data(), s.row_offsets.size() * sizeof(uint64_t));
+    mix(key, s.col_indices.data(), s.col_indices.size() * sizeof(uint32_t));
+    mix(key, s.values.data(), s.values.size() * sizeof(double));
+    struct Entry {
+        uint64_t key;
+        wbx_op* op;
+    };
+    static std::list<Entry> cache;  // most recent first
+    for (auto it = cache.begin(); it != cache.end(); ++it)
+        if (it->key == key) {
+            cache.splice(cache.begin(), cache, it);
+            return cache.front().op;
+        }
+    wbx_op* op = nullptr;
+    check(wbx_op_create(ctx(), s.n, s.row_offsets.data(), s.col_indices.data(), s.values.data(), &op));
+    cache.push_front({key, op});
+    if (cache.size() > 4) {
+        wbx_op_destroy(cache.back().op);
+        cache.pop_back();
+    }
+    return op;
+}
+
+wbx_basis* device_basis(const WaveletBasis& b) {
+    struct Entry {
+        uint32_t family, order, J;
+        std::vector<uint64_t> dims;
+        wbx_basis* basis;
+    };
+    static std::list<Entry> cache;
+    const auto fam = static_cast<uint32_t>(b.filters.family);
+    const std::vector<uint64_t> dims(b.dims().begin(), b.dims().end());
+    for (auto& e : cache)
+        if (e.family == fam && e.order == b.filters.order && e.J == b.levels() && e.dims == dims) return e.basis;
+    wbx_basis* p = nullptr;
+    check(wbx_basis_create(ctx(), fam, b.filters.order, static_cast<uint32_t>(dims.size()), dims.data(),
+                           b.levels(), &p));
+    cache.push_front({fam, b.filters.order, b.levels(), dims, p});
+    return p;
+}
+
+const SparseOperator* sparse_of(const ThetaOp* op) {
+    const auto* s = dynamic_cast<const SparseThetaOp*>(op);
+    return s ? &s->sparse() : nullptr;
+}
+
+void require_len(std::size_t got, std::size_t want, const char* what) {
+    if (got != want) throw ShapeMismatch(std::string(what) + ": vector length mismatch");
+}
+
+SolveReport pgd(const DeblurProblem& p, const DiagonalPreconditioner& P, const SolverConfig& c, int accelerate) {
+    const SparseOperator* s = sparse_of(p.op);
+    if (!s) return accelerate ? fista_host(p, P, c) : ista_host(p, P, c);
+    require_len(p.x0.size(), s->n, "run_pgd");
+    require_len(p.weights.size(), s->n, "run_pgd");
+    require_len(P.p.size(), s->n, "run_pgd");
+    std::lock_guard<std::recursive_mutex> g(mu);
     wbx_solver_cfg cfg;
     wbx_solver_cfg_default(&cfg);
-    cfg.max_iters = c.max_iters; cfg.rel_energy_tol = c.rel_energy_tol; cfg.step_safety = c.step_safety;
-    cfg.ref_energy = c.ref_energy; cfg.zero_momentum = c.zero_momentum;
-    cfg.track_support = c.track_support; cfg.track_energy = 1; cfg.precision = WBX_FP32;
+    cfg.max_iters = c.max_iters;
+    cfg.rel_energy_tol = c.rel_energy_tol;
+    cfg.step_safety = c.step_safety;
+    cfg.ref_energy = c.ref_energy;
+    cfg.zero_momentum = c.zero_momentum;
+    cfg.track_support = c.track_support;
+    cfg.track_energy = 1;  // SolveReport always carries E(x_k)
+    cfg.precision = precision();
     SolveReport r;
-    r.x_final.resize(p.x0.size());
+    r.x_final.resize(s->n);
     r.energies.resize(c.max_iters);
-    std::vector<std::uint64_t> supp(c.max_iters);
+    std::vector<uint64_t> supp(c.max_iters);
     wbx_report rep{};
     rep.energies = r.energies.data();
     rep.support_sizes = supp.data();
-    check(wbx_pgd(ctx(), d.op, p.x0.data(), p.weights.data(), p.lambda, P.p.data(), &cfg, 1,
+    check(wbx_pgd(ctx(), device_op(*s), p.x0.data(), p.weights.data(), p.lambda, P.p.data(), &cfg, accelerate,
                   r.x_final.data(), &rep));
     r.iters_used = rep.iters_used;
     r.energies.resize(rep.iters_used);
@@ -70,4 +167,123 @@ SolveReport fista(const DeblurProblem& p, const DiagonalPreconditioner& P, const
     r.initial_energy = rep.initial_energy;
     return r;
 }
+
+}  // namespace
+
+WaveletCoeffs analyze(const Image& signal, const WaveletBasis& basis) {
+    signal.require_dyadic();
+    if (signal.dims != basis.dims()) throw ShapeMismatch("signal dims do not match basis");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    WaveletCoeffs x;
+    x.layout = &basis.layout;
+    x.values.resize(basis.layout.total());
+    check(wbx_analyze(ctx(), device_basis(basis), signal.v.data(), x.values.data()));
+    return x;
+}
+
+Image synthesize(const WaveletCoeffs& coeffs, const WaveletBasis& basis) {
+    if (coeffs.values.size() != basis.layout.total())
+        throw ShapeMismatch("coefficient length does not match basis");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    Image u(basis.dims());
+    check(wbx_synthesize(ctx(), device_basis(basis), coeffs.values.data(), u.v.data()));
+    return u;
+}
+
+std::vector<double> spmv(const SparseOperator& op, const std::vector<double>& x) {
+    require_len(x.size(), op.n, "spmv");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> y(op.n);
+    check(wbx_spmv(ctx(), device_op(op), 0, x.data(), y.data()));
+    return y;
+}
+
+std::vector<double> spmv_t(const SparseOperator& op, const std::vector<double>& x) {
+    require_len(x.size(), op.n, "spmv_t");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> y(op.n);
+    check(wbx_spmv(ctx(), device_op(op), 1, x.data(), y.data()));
+    return y;
+}
+
+std::vector<double> approx_gradient(const SparseOperator& op, const std::vector<double>& x,
+                                    const std::vector<double>& x0) {
+    require_len(x.size(), op.n, "approx_gradient");
+    require_len(x0.size(), op.n, "approx_gradient");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> y(op.n);
+    check(wbx_approx_gradient(ctx(), device_op(op), x.data(), x0.data(), y.data()));
+    return y;
+}
+
+std::vector<double> SparseThetaOp::apply(const std::vector<double>& x) const { return spmv(sparse(), x); }
+
+std::vector<double> SparseThetaOp::apply_adjoint(const std::vector<double>& x) const {
+    return spmv_t(sparse(), x);
+}
+
+GramDiagonals gram_diagonals(const SparseOperator& op, std::size_t nnz_cap_factor) {
+    std::lock_guard<std::recursive_mutex> g(mu);
+    GramDiagonals d;
+    d.diagM.resize(op.n);
+    d.diagM2.resize(op.n);
+    check(wbx_gram_diagonals(ctx(), device_op(op), nnz_cap_factor, d.diagM.data(), d.diagM2.data()));
+    return d;
+}
+
+DiagonalPreconditioner jacobi(const SparseOperator& op, double eps) {
+    std::lock_guard<std::recursive_mutex> g(mu);
+    DiagonalPreconditioner P{std::vector<double>(op.n), PrecondKind::Jacobi};
+    check(wbx_jacobi(ctx(), device_op(op), eps, P.p.data()));
+    return P;
+}
+
+DiagonalPreconditioner spai(const SparseOperator& op) {
+    std::lock_guard<std::recursive_mutex> g(mu);
+    DiagonalPreconditioner P{std::vector<double>(op.n), PrecondKind::Spai};
+    check(wbx_spai(ctx(), device_op(op), P.p.data()));
+    return P;
+}
+
+double energy(const std::vector<double>& x, const DeblurProblem& problem) {
+    const SparseOperator* s = sparse_of(problem.op);
+    if (!s) return energy_host(x, problem);
+    require_len(x.size(), problem.x0.size(), "energy");
+    require_len(x.size(), s->n, "energy");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    double e = 0.0;
+    check(wbx_energy(ctx(), device_op(*s), x.data(), problem.x0.data(), problem.weights.data(), problem.lambda,
+                     &e));
+    return e;
+}
+
+std::vector<double> prox_weighted_l1_P(const std::vector<double>& z0, double tau, const std::vector<double>& weights,
+                                       double lambda, const DiagonalPreconditioner& P) {
+    require_len(weights.size(), z0.size(), "prox_weighted_l1_P");
+    require_len(P.p.size(), z0.size(), "prox_weighted_l1_P");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> z(z0.size());
+    check(wbx_prox_l1w(ctx(), z0.size(), z0.data(), tau, weights.data(), lambda, P.p.data(), z.data()));
+    return z;
+}
+
+double estimate_step(const ThetaOp& op, const DiagonalPreconditioner& P, double step_safety) {
+    const SparseOperator* s = sparse_of(&op);
+    if (!s) return estimate_step_host(op, P, step_safety);
+    require_len(P.p.size(), s->n, "estimate_step");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    double tau = 0.0;
+    uint32_t iters = 0;
+    check(wbx_estimate_step(ctx(), device_op(*s), P.p.data(), step_safety, &tau, &iters));
+    return tau;
+}
+
+SolveReport ista(const DeblurProblem& p, const DiagonalPreconditioner& P, const SolverConfig& c) {
+    return pgd(p, P, c, 0);
+}
+
+SolveReport fista(const DeblurProblem& p, const DiagonalPreconditioner& P, const SolverConfig& c) {
+    return pgd(p, P, c, 1);
+}
+
 }  // namespace waveblur

@@ -102,7 +102,9 @@ struct wbx_sell {
     wbx::DevBuf<double> val64;
     wbx::DevBuf<uint32_t> col;
     wbx::DevBuf<uint32_t> row_len;
-    // segmented fp32 layout (rows split into <= 16-element segments, one lane each)
+    // segmented fp32 layout (rows split into <= 16-element segments, one lane each); absent
+    // (seg_ok false, fp64 entry points only) when a row is longer than 31 segments
+    bool seg_ok = true;
     uint64_t slices = 0;
     uint64_t pairs = 0;               // uint4 element pairs incl. padding
     wbx::DevBuf<uint64_t> slice_ptr;  // pair offset of each slice

@@ -45,6 +45,7 @@ struct HostSell {
     std::vector<uint32_t> lane_info;
     std::vector<uint64_t> rec_off;  // uint4 offset of each slice record (+ total)
     std::vector<uint4> rec;
+    bool seg_ok = true;
 };
 
 // rows: list of row ids (in slice order); each row r has [beg[r], end[r]) in (cols, vals),
@@ -83,6 +84,15 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
         uint64_t row, beg, len;
         uint32_t info;
     };
+    // Rows longer than 31 segments (496 nonzeros: untruncated operators of the reference's
+    // tests) get no fp32 layout; the fp64 entry points run on the exact layout above.
+    for (uint64_t r = 0; r < nrows; ++r)
+        if (range.len(r) > 31 * kSegElems) {
+            h.seg_ok = false;
+            h.slice_ptr.assign(1, 0);
+            h.rec_off.assign(1, 0);
+            return h;
+        }
     // Segment-major placement: a slice holds m rows that all have q segments
     // (m = floor(32 / q)); segment t of the slice's i-th row sits in lane t*m + i. Lanes
     // 0..m-1 (and each further group of m) therefore hold consecutive rows, so a warp's
@@ -163,6 +173,7 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
 
 void upload_sell(wbx_sell& d, const HostSell& h, uint64_t rows, cudaStream_t s, uint64_t& bytes) {
     d.rows = rows;
+    d.seg_ok = h.seg_ok;
     d.xslices = h.xslice_len.size();
     d.slices = h.slice_np.size();
     d.pairs = h.pk.size();
@@ -195,6 +206,7 @@ void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint
         void get(uint64_t i, uint64_t j, uint32_t& c, double& v) const { (*g)(i, j, c, v); }
     } r{&len, &get};
     HostSell h = make_sell(nrows, r);
+    if (!h.seg_ok) fail(WBX_TOO_LARGE, "row longer than 31 segments");
     upload_sell(out, h, nrows, s, bytes);
     WBX_CUDA(cudaStreamSynchronize(s));
 }

@@ -1830,7 +1830,7 @@ void alloc_state(wbx_solver* s) {
             const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                          : reinterpret_cast<const void*>(fista_win_kernel<false>);
             const void* kt = tau_win_fn(s->win_dict, s->tau_win64);
-            const unsigned limit = bps == 2 ? 110u * 1024u : 220u * 1024u;
+            const unsigned limit = bps == 1 ? 220u * 1024u : (227u * 1024u) / bps - 2048u;
             if (s->win_smem_tau > limit) continue;
             WBX_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(s->win_smem_fista)));
@@ -2007,6 +2007,8 @@ wbx_solver* solver_new(wbx_ctx* ctx, const wbx_op* op, wbx_basis* basis, double 
     if (cfg.precision != WBX_FP32 && cfg.precision != WBX_FP64)
         fail(WBX_BAD_SPEC, "precision must be 32 or 64");
     if (cfg.max_iters > 0x7fffffffull) fail(WBX_TOO_LARGE, "max_iters too large");
+    if (cfg.precision == WBX_FP32 && !(op->A.seg_ok && op->T.seg_ok))
+        fail(WBX_TOO_LARGE, "operator rows longer than 496 nonzeros: fp32 layout unavailable, use precision 64");
     auto* s = new wbx_solver();
     s->ctx = ctx;
     s->op = op;

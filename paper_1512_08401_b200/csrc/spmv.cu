@@ -89,6 +89,8 @@ void spmv_full_fp64(wbx_op* op, int transpose, const double* x_dev, double* y_de
 }
 
 void spmv_full_fp32(wbx_op* op, int transpose, const float* x_dev, float* y_dev, cudaStream_t s) {
+    if (!(op->A.seg_ok && op->T.seg_ok))
+        fail(WBX_TOO_LARGE, "operator rows longer than 496 nonzeros: fp32 layout unavailable, use precision 64");
     full_spmv<float>(op, transpose, x_dev, y_dev, s);
 }
 

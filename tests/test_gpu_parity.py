@@ -129,6 +129,32 @@ def test_spmv_edge_operators():
         W.spmv(bad, np.ones(4))
 
 
+def test_long_rows_serve_fp64_and_refuse_fp32():
+    """rows beyond the fp32 segmented layout (31 segments x 16 = 496 nonzeros, e.g. the
+    untruncated operators of test_theta.cpp:401-444): fp64 products, step and solve stay
+    bitwise; an fp32 solve fails loudly with TooLarge instead of computing something else."""
+    n = 1024
+    rng = np.random.default_rng(17)
+    ro = np.zeros(n + 1, np.uint64)
+    lens = np.full(n, 3)
+    lens[::97] = 700  # a few long rows (and long columns: the dense rows cover 0..699)
+    ro[1:] = np.cumsum(lens)
+    cols = np.concatenate([np.sort(rng.choice(n, L, replace=False)) if L != 700 else np.arange(700)
+                           for L in lens]).astype(np.uint32)
+    vals = rng.standard_normal(int(ro[-1])) * 0.05
+    op = W.SparseOperator(n, ro, cols, vals)
+    A = O.Csr.of(op)
+    x = rng.standard_normal(n)
+    assert np.array_equal(W.spmv(op, x), O.spmv(A, x))
+    assert np.array_equal(W.spmv_t(op, x), O.spmv(A.transpose(), x))
+    P = W.DiagonalPreconditioner(np.ones(n), W.PrecondKind.Identity)
+    prob = W.DeblurProblem(W.SparseThetaOp(op), x, np.ones(n), 1e-3)
+    r64 = W.fista(prob, P, W.SolverConfig(max_iters=20, precision=64, tau=0.5, track_energy=False))
+    assert np.array_equal(r64.x_final, O.pgd_tau(A, A.transpose(), x, np.ones(n), 1e-3, np.ones(n), 0.5, 20))
+    with pytest.raises(W.TooLarge):
+        W.fista(prob, P, W.SolverConfig(max_iters=20, precision=32, track_energy=False))
+
+
 # ----------------------------------------------------------------------------- prox / precond / step
 def test_prox_closed_forms():
     # test_solver.cpp:76-94
