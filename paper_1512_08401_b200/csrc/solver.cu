@@ -605,6 +605,10 @@ struct Streamer {
     // a global load
     uint32_t reg_meta;
     uint64_t reg_off;
+    // P > 32: lane j holds the metadata of entry 32w + j of the current issue window w and
+    // of the next one (one coalesced load per 32 issues, a window ahead of its use)
+    uint32_t cur_meta, nx_meta;
+    uint64_t cur_off, nx_off;
 };
 
 __device__ __forceinline__ uint32_t count_slices(const SellView& M, uint32_t gwarp, uint32_t nwarps) {
@@ -619,12 +623,26 @@ __device__ __forceinline__ uint32_t entry_slice(const Streamer& st, uint32_t r, 
     return gwarp + k * nwarps;
 }
 
+__device__ __forceinline__ void st_load_window(Streamer& st, const SellView& A, const SellView& T, uint32_t gwarp,
+                                               uint32_t nwarps, int lane, uint64_t first) {
+    const uint64_t e = first + static_cast<uint64_t>(lane);
+    st.nx_meta = 0;
+    st.nx_off = 0;
+    if (e < st.limit) {
+        bool isT;
+        const uint32_t s = entry_slice(st, static_cast<uint32_t>(e % st.P), gwarp, nwarps, isT);
+        const SellView& M = isT ? T : A;
+        st.nx_meta = M.slice_np[s];
+        st.nx_off = M.rec_off[s];
+    }
+}
+
 __device__ __forceinline__ void st_issue(Streamer& st, const SellView& A, const SellView& T, uint32_t gwarp,
                                          uint32_t nwarps, int lane) {
     const uint64_t e = st.issued++;
     const uint32_t r = static_cast<uint32_t>(e % st.P);
     bool isT;
-    const uint32_t s = entry_slice(st, r, gwarp, nwarps, isT);
+    entry_slice(st, r, gwarp, nwarps, isT);
     const SellView& M = isT ? T : A;
     uint32_t meta;
     uint64_t off;
@@ -632,8 +650,13 @@ __device__ __forceinline__ void st_issue(Streamer& st, const SellView& A, const 
         meta = __shfl_sync(0xffffffffu, st.reg_meta, r);
         off = __shfl_sync(0xffffffffu, st.reg_off, r);
     } else {
-        meta = M.slice_np[s];
-        off = M.rec_off[s];
+        if ((e & 31u) == 0 && e > 0) {  // next window: the prefetched one becomes current
+            st.cur_meta = st.nx_meta;
+            st.cur_off = st.nx_off;
+            st_load_window(st, A, T, gwarp, nwarps, lane, e + 32);
+        }
+        meta = __shfl_sync(0xffffffffu, st.cur_meta, static_cast<int>(e & 31u));
+        off = __shfl_sync(0xffffffffu, st.cur_off, static_cast<int>(e & 31u));
     }
     if (lane != 0) return;
     const unsigned bytes = 128u + (meta & 0xffu) * 512u;
@@ -669,6 +692,12 @@ __device__ __forceinline__ void st_init(Streamer& st, unsigned char* warp_smem, 
         for (uint32_t i = 0; i < st.ns; ++i) mbar_init(st.bars + i, 1);
     mbar_fence_init();
     __syncwarp();
+    if (st.P > 32) {
+        st_load_window(st, A, T, gwarp, nwarps, lane, 0);
+        st.cur_meta = st.nx_meta;
+        st.cur_off = st.nx_off;
+        st_load_window(st, A, T, gwarp, nwarps, lane, 32);
+    }
     while (st.issued < st.limit && st.issued < st.ns) st_issue(st, A, T, gwarp, nwarps, lane);
 }
 
