@@ -63,6 +63,7 @@ enum : int {
     OUT_INITIAL_ENERGY = 3,
     OUT_STATUS = 4,  // 0 ok, 8 nonfinite energy
     OUT_LAMBDA_MAX = 5,
+    OUT_TAU_STEPS = 6,  // operator products (pairs) spent on tau: power iterations or Lanczos steps
     OUT_COUNT = 8
 };
 
@@ -98,6 +99,7 @@ struct SolveArgs {
     int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline, nslots;
     // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
     WinView wA, wT;
+    int lz_first, lz_every;  // Lanczos tau (tau_lanczos_win_kernel): first check, check period
     // T-typed state
     void* yC;
     void* xpC;
@@ -839,6 +841,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_kernel(SolveArgs a) 
     if (gthread == 0) {
         a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
         a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
+        a.out[OUT_TAU_STEPS] = it > 200 ? 200 : it;
         a.out[OUT_LAMBDA_MAX] = lambda_prev;
     }
 }
@@ -1104,11 +1107,15 @@ struct WinProf {
 // not depend on x), then every warp runs its slices (w, w+8, ...) with one slice of
 // record loads in flight; the vector operand and (dictionary format) the values come from
 // shared memory.
-template <typename ACC, typename WIN, bool DICT, typename X, typename Post>
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
+template <typename ACC, typename WIN, bool DICT, typename X, typename Post, typename Ready = NoHook>
 __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx, const uint16_t* uslot, uint32_t nu,
                                           const uint4* stab,
                                           uint32_t ns, const float* dict, const X* __restrict__ x, WIN* win,
-                                          Post post, WinProf& pf) {
+                                          Post post, WinProf& pf, Ready ready = Ready{}) {
     static_assert(sizeof(WIN) == sizeof(X), "the window is a verbatim copy of x entries");
     const long long t0 = WBX_PROFILE == 3 ? clock64() : 0;
     const int lane = threadIdx.x & 31;
@@ -1125,6 +1132,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    ready();  // every copy issued before the phase (window, staged partials) has landed
     const long long t1 = WBX_PROFILE == 3 ? clock64() : 0;
     // process slice s from d
     // dictionary values of the lane's last segment block: consecutive slices of a warp are
@@ -1395,7 +1403,300 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
     if (gthread == 0) {
         a.out[OUT_TAU] = (zero_op || lambda_prev <= 0.0) ? 1.0 : 1.0 / (lambda_prev * a.step_safety);
         a.out[OUT_TAU_ITERS] = it > 200 ? 200 : it;
+        a.out[OUT_TAU_STEPS] = it > 200 ? 200 : it;
         a.out[OUT_LAMBDA_MAX] = lambda_prev;
+    }
+}
+
+// ---------------------------------------------------------------- estimate_step by Lanczos
+// Window engine, fp32 hot path (WBX_TAU=power keeps tau_win_kernel; the fp64 mode keeps the
+// literal power iteration).
+//
+// estimate_step (solver.cpp:69-99) runs the power iteration lambda_it = <v_it, M v_it>,
+// v_it = M^it v0 / |M^it v0|, M = P^-1/2 Theta^T Theta P^-1/2, it < 200, and stops at the first
+// it > 0 with |lambda_it - lambda_it-1| <= 1e-6 |lambda_it|. With mu_p = v0^T M^p v0 / |v0|^2,
+// lambda_it = mu_{2it+1} / mu_{2it}. m Lanczos steps from v0 give the tridiagonal T_m with
+// e1^T T_m^p e1 |v0_C|^2 / |v0|^2 = mu_p (p >= 1; v0_C = the part of v0 on Theta's nonempty
+// columns) for every p <= 2m - 1 (Gauss quadrature). So the power iteration run on T_m from
+// e1 reproduces the reference's lambda sequence, its stopping decision and tau. A Lanczos
+// step costs the same two operator products as a power iteration, but the quadrature
+// converges super-geometrically in m: at C2, estimates from successive m agree to 1e-15
+// from m = 56 on, where the power iteration needs all 200 iterations. The kernel checks at
+// m = lz_first, lz_first + lz_every, ... and stops once two checks agree to 1e-12 with the
+// same stopping index, or at m = 200, where the identity covers every p <= 399 the
+// reference can reach.
+constexpr int kLzCap = 200;
+
+// The power iteration on T_m from e1 (warp-wide; identical inputs in every CTA give
+// identical results, so every CTA takes the same decision without communication).
+// Element i lives in lane i & 31, register i >> 5. Returns lambda at the stopping
+// iteration; *iters = the reference's iteration count; *zero = the zero-operator sentinel.
+template <int K>  // K = ceil(m / 32) registers per lane
+__device__ __forceinline__ double lz_power_on_T_k(const double* al, const double* be, int m, double r2, int* iters,
+                                               bool* zero) {
+    const int lane = threadIdx.x & 31;
+    constexpr int kk = K;
+    double a[K], bl[K], br[K], y[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int i = lane + 32 * k;
+        a[k] = i < m ? al[i] : 0.0;
+        bl[k] = (i > 0 && i < m) ? be[i] : 0.0;  // T[i][i-1]
+        br[k] = (i + 1 < m) ? be[i + 1] : 0.0;   // T[i][i+1]
+        y[k] = i == 0 ? 1.0 : 0.0;
+    }
+    auto matvec = [&]() {
+        double z[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (k < kk) {
+                double l = __shfl_up_sync(0xffffffffu, y[k], 1);
+                double r = __shfl_down_sync(0xffffffffu, y[k], 1);
+                const double lk = __shfl_sync(0xffffffffu, y[k > 0 ? k - 1 : 0], 31);
+                const double rk = __shfl_sync(0xffffffffu, y[k + 1 < K ? k + 1 : k], 0);
+                if (lane == 0) l = k > 0 ? lk : 0.0;
+                if (lane == 31) r = k + 1 < kk ? rk : 0.0;
+                z[k] = fma(bl[k], l, fma(a[k], y[k], br[k] * r));
+            } else {
+                z[k] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) y[k] = z[k];
+    };
+    double lam_prev = 0.0;
+    *zero = false;
+    for (int it = 0; it < 200; ++it) {  // y = T^it e1 / mu_2it on entry (mu_0 = 1)
+        matvec();
+        const double odd = __shfl_sync(0xffffffffu, y[0], 0);  // mu_{2it+1} / mu_{2it}
+        const double lam = it == 0 ? r2 * odd : odd;
+        matvec();
+        const double even = __shfl_sync(0xffffffffu, y[0], 0);  // |T^{it+1} e1|^2 / mu_2it
+        if (even == 0.0) {  // M v = 0: the reference's zero-operator sentinel (solver.cpp:89)
+            *zero = true;
+            *iters = it + 1;
+            return lam;
+        }
+        if (it > 0 && fabs(lam - lam_prev) <= 1e-6 * fabs(lam)) {
+            *iters = it + 1;
+            return lam;
+        }
+        lam_prev = lam;
+        const double inv = 1.0 / even;
+#pragma unroll
+        for (int k = 0; k < K; ++k) y[k] *= inv;
+    }
+    *iters = 200;
+    return lam_prev;
+}
+
+__device__ double lz_power_on_T(const double* al, const double* be, int m, double r2, int* iters, bool* zero) {
+    static_assert(kLzCap <= 7 * 32, "lz_power_on_T dispatch covers m <= 224");
+    switch ((m + 31) / 32) {
+        case 1: return lz_power_on_T_k<1>(al, be, m, r2, iters, zero);
+        case 2: return lz_power_on_T_k<2>(al, be, m, r2, iters, zero);
+        case 3: return lz_power_on_T_k<3>(al, be, m, r2, iters, zero);
+        case 4: return lz_power_on_T_k<4>(al, be, m, r2, iters, zero);
+        case 5: return lz_power_on_T_k<5>(al, be, m, r2, iters, zero);
+        case 6: return lz_power_on_T_k<6>(al, be, m, r2, iters, zero);
+        default: return lz_power_on_T_k<7>(al, be, m, r2, iters, zero);
+    }
+}
+
+// sum of G staged block partials in a fixed order (the same in every CTA); all threads
+__device__ __forceinline__ double cta_sum_staged(const double* st, unsigned G, double* red) {
+    double p = 0.0;
+    for (unsigned i = threadIdx.x; i < G; i += kWinBlock) p += st[i];
+    p = warp_sum(p);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kWinWarps; ++k) t += red[k];
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ void stage_partials(double* dst, const double* src, unsigned G) {
+    if (threadIdx.x < 32)
+        for (unsigned i = threadIdx.x; i < G; i += 32) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + i) : "memory");
+        }
+}
+
+// block partial of v (all threads) -> dst[blockIdx.x]
+__device__ __forceinline__ void cta_partial(double v, double* dst, double* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < kWinWarps; ++k) t += red[k];
+        dst[blockIdx.x] = t;
+    }
+}
+
+struct LzCtl {  // control state of tau_lanczos_win_kernel (shared memory, identical in every CTA)
+    double alpha, beta, rb;  // alpha_j, beta_j, 1 / beta_j of the current step
+    int breakdown;
+    double r2, lambda, check_prev;
+    int stop_prev, iters, steps, zero, done;
+};
+
+// Evaluate T_m (warp 0) and take the decision: `final` (the cap, a breakdown) or the
+// zero-operator sentinel end the estimate; otherwise it ends when this check agrees with the
+// previous one (same stopping index, lambda within 1e-12). All threads of the CTA call it.
+__device__ __forceinline__ bool lz_check(const double* al, const double* be, int m, bool final, LzCtl* ctl) {
+    __syncthreads();  // alpha / beta of the last step are written
+    if (threadIdx.x < 32) {
+        int its = 0;
+        bool z = false;
+        const double lam = lz_power_on_T(al, be, m, ctl->r2, &its, &z);
+        if (threadIdx.x == 0) {
+            if (final || z || (its == ctl->stop_prev && fabs(lam - ctl->check_prev) <= 1e-12 * fabs(lam))) {
+                ctl->lambda = lam;
+                ctl->iters = its;
+                ctl->zero = z;
+                ctl->steps = m;
+                ctl->done = 1;
+            }
+            ctl->check_prev = lam;
+            ctl->stop_prev = its;
+        }
+    }
+    __syncthreads();
+    return ctl->done != 0;
+}
+
+template <bool DICT>
+__global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kernel(SolveArgs a) {
+    __shared__ double smem[kWinWarps + 1];
+    __shared__ double red[kWinWarps];
+    __shared__ double bc[2];
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    const WinSmem ws = win_smem_init<0, 24>(dsmem, a);
+    float* win = static_cast<float*>(ws.win);
+    struct LzRow {
+        double isp, w, qp;  // P^-1/2, w_j (unnormalised), q_j-1 of one coordinate
+    };
+    LzRow* cs = static_cast<LzRow*>(ws.ownT);
+    float* uC = static_cast<float*>(a.yC);         // P^-1/2 w_j on C
+    float* tR = static_cast<float*>(a.res);        // t' = Theta P^-1/2 w_j on R
+    const unsigned G = gridDim.x;
+    const uint32_t mw = a.wA.max_win > a.wT.max_win ? a.wA.max_win : a.wT.max_win;
+    double* pstage = reinterpret_cast<double*>(static_cast<unsigned char*>(ws.win) + win_align16(mw * 4u));
+    double* lz_al = pstage + 2 * G;   // alpha_j
+    double* lz_be = lz_al + kLzCap;   // beta_j = |w_j| (beta_0 = |v0 on C|)
+    double s2[2] = {0.0, 0.0};
+    for (uint64_t i = gthread; i < a.n; i += nthreads) {
+        const double v = rng_normal(0x5eedull, i);
+        s2[0] += v * v;
+    }
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) {
+        const uint32_t c = ws.rT0 + i;
+        const double v = rng_normal(0x5eedull, a.C_glob[c]);
+        const double isp = a.ispC[c];
+        cs[i] = LzRow{isp, v, 0.0};
+        uC[c] = static_cast<float>(isp * v);
+        s2[1] += v * v;
+    }
+    grid_sync_reduce<2, kWinBlock>(a.sync, epoch, s2, smem);
+    // control state in shared memory (identical in every CTA): keeps the phases' registers
+    // for the slice loops
+    __shared__ LzCtl ctl;
+    if (threadIdx.x == 0) {
+        const double beta = sqrt(s2[1]);
+        ctl.beta = beta;
+        lz_be[0] = beta;
+        ctl.r2 = s2[1] / s2[0];
+        ctl.lambda = 0.0;
+        ctl.check_prev = -1.0;
+        ctl.stop_prev = -1;
+        ctl.iters = ctl.steps = 0;
+        ctl.zero = !(beta > 0.0);
+        ctl.breakdown = 0;
+        ctl.done = ctl.zero;
+    }
+    __syncthreads();
+    WinProf pf;
+    for (int j = 0; !ctl.done;) {
+        // convergence check on T_j (alpha_0..j-1, beta_1..j-1 are known)
+        const bool final = ctl.breakdown || j == kLzCap;
+        if ((final || (j > 0 && j >= a.lz_first && (j - a.lz_first) % a.lz_every == 0)) &&
+            lz_check(lz_al, lz_be, j, final, &ctl))
+            break;
+        // phase A_j: t' = Theta P^-1/2 w_j and |t'|^2; the partials of |w_j|^2 (phase T_j-1) are
+        // staged and summed meanwhile
+        double* part = a.sync.part + static_cast<uint64_t>(j & 1) * kRedSlots * G;
+        if (j > 0) stage_partials(pstage, a.sync.part + static_cast<uint64_t>((j - 1) & 1) * kRedSlots * G + 3 * G, G);
+        pf.side = 0;
+        float accA = 0.f;  // a handful of rows per thread: fp32, then fp64 across threads and CTAs
+        win_phase<float, float, DICT>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, uC, win,
+                                      [&](uint32_t r, double t) {
+                                          const float tf = static_cast<float>(t);
+                                          tR[r] = tf;
+                                          accA = fmaf(tf, tf, accA);
+                                      },
+                                      pf);
+        if (j > 0) {
+            const double bb = cta_sum_staged(pstage, G, red);
+            if (threadIdx.x == 0) {
+                const double beta = sqrt(bb);
+                ctl.beta = beta;
+                ctl.rb = 1.0 / beta;
+                ctl.breakdown = !(beta > 1e-13 * (fabs(lz_al[j - 1]) + lz_be[j - 1]));  // T_j is exact
+            }
+        } else if (threadIdx.x == 0) {
+            ctl.rb = 1.0 / ctl.beta;
+        }
+        cta_partial(static_cast<double>(accA), part + 2 * G, red);
+        grid_sync(a.sync, epoch, smem);
+        if (ctl.breakdown) continue;  // (written before the barrier) T_j is exact
+        // phase T_j: w_j+1 = M q_j - alpha_j q_j - beta_j q_j-1 on the CTA's coordinates, |w_j+1|^2;
+        // alpha_j = |t'|^2 / beta_j^2 from the staged partials of phase A_j
+        stage_partials(pstage, part + 2 * G, G);
+        pf.side = 3;
+        win_phase<float, float, DICT>(
+            a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, tR, win,
+            [&](uint32_t c, double g) {
+                WBX_ASSERT(c - ws.rT0 < ws.nrT);
+                LzRow& st = cs[c - ws.rT0];
+                const double rb = ctl.rb;
+                const double z = st.isp * g * rb;  // (M q_j)_c
+                const double q = st.w * rb;        // q_j
+                const double wn = z - ctl.alpha * q - ctl.beta * st.qp;
+                st.w = wn;
+                st.qp = q;
+                uC[c] = static_cast<float>(st.isp * wn);
+            },
+            pf, [&]() {
+                const double S = cta_sum_staged(pstage, G, red);
+                if (threadIdx.x == 0) ctl.alpha = S * ctl.rb * ctl.rb;
+                __syncthreads();
+            });
+        if (threadIdx.x == 0) {
+            lz_al[j] = ctl.alpha;
+            lz_be[j] = ctl.beta;
+        }
+        __syncthreads();
+        double accT = 0.0;
+        for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) accT = fma(cs[i].w, cs[i].w, accT);
+        cta_partial(accT, part + 3 * G, red);
+        grid_sync(a.sync, epoch, smem);
+        ++j;
+    }
+    pf.flush();
+    if (gthread == 0) {
+        const double lambda = ctl.lambda;
+        a.out[OUT_TAU] = (ctl.zero || lambda <= 0.0) ? 1.0 : 1.0 / (lambda * a.step_safety);
+        a.out[OUT_TAU_ITERS] = ctl.iters;
+        a.out[OUT_LAMBDA_MAX] = lambda;
+        a.out[OUT_TAU_STEPS] = ctl.steps;
     }
 }
 
@@ -1593,6 +1894,7 @@ __global__ void reduce_rows_kernel(const double* w, uint64_t nwarps, int K, doub
 __global__ void set_tau_kernel(double* out, double tau) {
     out[OUT_TAU] = tau;
     out[OUT_TAU_ITERS] = 0;
+    out[OUT_TAU_STEPS] = 0;
 }
 
 __global__ void clamp_kernel(double* u, uint64_t n) {
@@ -1625,7 +1927,7 @@ struct wbx_solver {
     int grid_fista = 0, grid_tau = 0;
     int nslots = 3;  // TMA slots in flight per warp
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
-    bool win = false, win_dict = false, tau_win64 = false;
+    bool win = false, win_dict = false, tau_win64 = false, tau_lanczos = false;
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     wbx::WinSide wA, wT;
@@ -1659,6 +1961,11 @@ int blocks_per_sm(const void* kernel, unsigned smem) {
         if (want >= 1 && want < per_sm) per_sm = want;
     }
     return per_sm;
+}
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* e = std::getenv(name);
+    return e ? std::max(lo, std::min(hi, std::atoi(e))) : dflt;
 }
 
 template <typename T>
@@ -1725,6 +2032,8 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     if (s->win) {
         a.wA = view_of(s->wA);
         a.wT = view_of(s->wT);
+        a.lz_first = env_int("WBX_LZ_FIRST", 48, 1, kLzCap);
+        a.lz_every = env_int("WBX_LZ_EVERY", 8, 1, kLzCap);
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
@@ -1733,7 +2042,10 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     return a;
 }
 
-const void* tau_win_fn(bool dict, bool w64) {
+const void* tau_win_fn(bool dict, bool w64, bool lanczos = false) {
+    if (lanczos)
+        return dict ? reinterpret_cast<const void*>(tau_lanczos_win_kernel<true>)
+                    : reinterpret_cast<const void*>(tau_lanczos_win_kernel<false>);
     if (dict)
         return w64 ? reinterpret_cast<const void*>(tau_win_kernel<true, double>)
                    : reinterpret_cast<const void*>(tau_win_kernel<true, float>);
@@ -1763,7 +2075,7 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->win) {
-        const void* k = tau_win_fn(s->win_dict, s->tau_win64);
+        const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
         launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st, kWinBlock);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
@@ -1853,14 +2165,25 @@ void alloc_state(wbx_solver* s) {
             const unsigned mu = std::max(s->wA.max_win, s->wT.max_win);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
             s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
-            s->win_smem_tau = win_smem_head<0, 16>(vA, vT) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
-                              16u * G;  // + partials staging
+            // tau by Lanczos + the power iteration on the tridiagonal (tau_lanczos_win_kernel);
+            // WBX_TAU=power runs the literal power iteration
+            // (falls back to the power iteration when its state does not fit next to the window)
+            const unsigned limit = bps == 1 ? 220u * 1024u : (227u * 1024u) / bps - 2048u;
+            s->tau_lanczos = !s->tau_win64 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
+            const unsigned smem_lz = win_smem_head<0, 24>(vA, vT) + win_align16(mu * 4u) + 16u * G +  // + partials
+                                     16u * kLzCap;                                                     // + alpha, beta
+            if (s->tau_lanczos && smem_lz > limit) s->tau_lanczos = false;
+            s->win_smem_tau = s->tau_lanczos ? smem_lz
+                                             : win_smem_head<0, 16>(vA, vT) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
+                                                   16u * G;  // + partials staging
             s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
             const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                          : reinterpret_cast<const void*>(fista_win_kernel<false>);
-            const void* kt = tau_win_fn(s->win_dict, s->tau_win64);
-            const unsigned limit = bps == 1 ? 220u * 1024u : (227u * 1024u) / bps - 2048u;
-            if (s->win_smem_tau > limit) continue;
+            const void* kt = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
+            if (std::getenv("WBX_VERBOSE"))
+                std::fprintf(stderr, "wbx window engine: try G=%u smem fista/tau=%u/%u limit %u\n", G,
+                             s->win_smem_fista, s->win_smem_tau, limit);
+            if (std::max(s->win_smem_fista, s->win_smem_tau) > limit) continue;
             WBX_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(s->win_smem_fista)));
             WBX_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1868,6 +2191,8 @@ void alloc_state(wbx_solver* s) {
             int pf = 0, pt = 0;
             WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, kf, kWinBlock, s->win_smem_fista));
             WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pt, kt, kWinBlock, s->win_smem_tau));
+            if (std::getenv("WBX_VERBOSE"))
+                std::fprintf(stderr, "wbx window engine: G=%u occupancy fista/tau=%d/%d\n", G, pf, pt);
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
@@ -2012,6 +2337,9 @@ void solver_report(wbx_solver* s, wbx_report* rep) {
         }
     }
     if (out[OUT_STATUS] == 8.0) fail(WBX_NONFINITE_ENERGY, "solver diverged (non-finite energy)");
+    if (std::getenv("WBX_VERBOSE"))
+        std::fprintf(stderr, "wbx tau: %.17g after %g reference iterations, %g operator product pairs (%s)\n",
+                     out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_TAU_STEPS], s->tau_lanczos ? "lanczos" : "power");
     if (rep == nullptr) return;
     rep->iters_used = static_cast<uint64_t>(out[OUT_ITERS_USED]);
     rep->tau = out[OUT_TAU];

@@ -213,6 +213,42 @@ def test_estimate_step_diagonal_operators():
     assert W.estimate_step(W.SparseThetaOp(zero), I, 1.0) == 1.0   # zero-operator sentinel
 
 
+@pytest.mark.parametrize("name", SOLVE_CASES + ["c1_sym6_256", "c2_db4_1024"])
+def test_lanczos_tau_equals_power_iteration(golden, monkeypatch, name):
+    """The fp32 hot path estimates tau by Lanczos + the power iteration on the tridiagonal
+    (tau_lanczos_win_kernel): the same reference iteration count (stopping rule) and the
+    same tau as the literal power iteration (WBX_TAU=power) and the reference."""
+    g = golden(name)
+    op = g.operator()
+    P = precond_of(g, op)
+    prob = W.DeblurProblem(W.SparseThetaOp(op), np.zeros(op.n), g.weights(), g.meta["lambda"])
+    cfg = W.SolverConfig(max_iters=0, precision=32, track_energy=False)
+    lz = W.fista(prob, P, cfg)
+    monkeypatch.setenv("WBX_TAU", "power")
+    pw = W.fista(prob, P, cfg)
+    assert lz.tau_iters == pw.tau_iters
+    assert abs(lz.tau - pw.tau) <= 2e-7 * pw.tau
+    assert abs(lz.tau - g.meta["tau"]) <= 1e-6 * g.meta["tau"]
+
+
+def test_lanczos_tau_small_spectra():
+    """Operators whose Krylov space is tiny (Lanczos breaks down or only sees noise after a
+    few steps): identity, two distinct scales, the zero operator, through the fp32 path."""
+    n = 4096
+    eye = W.SparseOperator(n, np.arange(n + 1, dtype=np.uint64), np.arange(n, dtype=np.uint32), np.ones(n))
+    v = np.ones(n)
+    v[::7] = 2.0
+    two = W.SparseOperator(n, np.arange(n + 1, dtype=np.uint64), np.arange(n, dtype=np.uint32), v)
+    zero = W.SparseOperator(n, np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), np.zeros(0))
+    I = W.identity_precond(n)
+    cfg = W.SolverConfig(max_iters=0, precision=32, track_energy=False, step_safety=1.0)
+    for op, tau in [(eye, 1.0), (two, 0.25), (zero, 1.0)]:
+        r = W.fista(W.DeblurProblem(W.SparseThetaOp(op), np.zeros(n), np.ones(n), 1e-4), I, cfg)
+        assert abs(r.tau - tau) <= 1e-6 * tau, (op.nnz(), r.tau)
+        if op.nnz():  # the reference's own iteration count (power iteration in fp64)
+            assert r.tau_iters == W.estimate_step(W.SparseThetaOp(op), I, 1.0, return_iters=True)[1]
+
+
 # ----------------------------------------------------------------------------- solver
 def _problem(g, op):
     b = basis_of(g)

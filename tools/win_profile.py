@@ -28,7 +28,9 @@ for name, cfg, phases in [("fista", dict(max_iters=100, tau=meta["tau"]), 200), 
     r = W.fista(prob, P, W.SolverConfig(track_energy=False, precision=32, **cfg), ctx)
     lib.wbx_diag_slice_profile(buf)
     h = list(buf)
-    nph = phases // 2 if phases else r.tau_iters  # phases of each side
+    # phases of each side (the Lanczos tau takes fewer product pairs than the reference's
+    # iteration count: pass them as argv[1], WBX_VERBOSE=1 prints them)
+    nph = phases // 2 if phases else (int(sys.argv[1]) if len(sys.argv) > 1 else r.tau_iters)
     warps = 296 * 8
     per = warps * nph
     res[name] = {"ms": round(r.wall_time_s * 1e3, 3), "phases": nph,
