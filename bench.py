@@ -214,6 +214,7 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = float(t.item())
 
     tau_iters = int(rep.tau_iters)
+    _, _, tau_pairs = deb.tau_stats()  # operator product pairs actually spent (Lanczos steps)
     s_ms = float(np.median(solve_ms))
     tau_ms = float(np.mean([p[0] for p in phase_ms]))
     it_ms = float(np.mean([p[1] for p in phase_ms]))
@@ -223,9 +224,10 @@ def run_ours(args, rank, world, local_rank):
     b_iter = 16 * nnz + 36 * n                       # one FISTA iteration
     b_pow = 2 * (8 * nnz + 16 * n)                   # one power iteration: 2 SpMVs, fp64 vectors
     kernels = [
-        {"kernel": "tau_win_kernel (estimate_step, persistent)", "launch_ms": round(tau_ms, 4),
-         "units": f"{tau_iters} power iterations x 2*(8*nnz+16*n) B",
-         "algorithmic_bytes": tau_iters * b_pow, "achieved": round(tau_iters * b_pow / (tau_ms * 1e-3) / 1e9, 1)},
+        {"kernel": "tau_lanczos_win_kernel (estimate_step, persistent)", "launch_ms": round(tau_ms, 4),
+         "units": f"{tau_pairs} operator product pairs (Lanczos steps standing in for the reference's "
+                  f"{tau_iters} power iterations) x 2*(8*nnz+16*n) B",
+         "algorithmic_bytes": tau_pairs * b_pow, "achieved": round(tau_pairs * b_pow / (tau_ms * 1e-3) / 1e9, 1)},
         {"kernel": "fista_win_kernel (100 FISTA iterations, persistent)", "launch_ms": round(it_ms, 4),
          "units": f"{ITERS} iterations x (16*nnz+36*n) B",
          "algorithmic_bytes": ITERS * b_iter, "achieved": round(ITERS * b_iter / (it_ms * 1e-3) / 1e9, 1)},
@@ -239,7 +241,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 DWT/tau)", "data": "synthetic",
         "config": {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic "
-                               "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau power iteration",
+                               "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau (estimate_step)",
                    "image": list(DIMS), "iters": ITERS, "nnz": nnz, "K_over_N": 3,
                    "images_per_step": world, "parallelism": f"replicas x{world} (independent images)",
                    "l2": "flushed (512 MiB write) between timed steps"},
@@ -255,7 +257,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": "operator + vectors are L2-resident across iterations (compacted, dictionary-"
                              "coded layout streams ~2 B/nonzero); algorithmic bytes per SURVEY 8(d)"},
         "breakdown": {"solve_ms": round(s_ms, 4), "tau_ms": round(tau_ms, 4), "iterations_ms": round(it_ms, 4),
-                      "tau_iters": tau_iters, "tau": rep.tau,
+                      "tau_iters": tau_iters, "tau_product_pairs": tau_pairs, "tau": rep.tau,
                       "dwt_and_idwt_ms": round(ms_per_step - s_ms, 4)},
         "clocks": clk.summary(),
     }
@@ -473,7 +475,7 @@ def main():
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "impl": "reference",
                 "config": {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic "
-                                       "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau power iteration",
+                                       "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau (estimate_step)",
                            "image": list(DIMS), "iters": ITERS},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

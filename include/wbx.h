@@ -293,6 +293,10 @@ int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_
 // Device time of the last solve split into the step-size estimate (estimate_step, 0 when tau
 // was given) and the iteration kernel(s), from CUDA events on the context stream.
 int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms);
+/* the step of the last solve: tau, the reference's power-iteration count for it
+ * (solver.cpp:81-96) and the operator product pairs spent (Lanczos steps on the fp32 hot
+ * path, power iterations otherwise; synchronises the context's stream) */
+int wbx_solver_tau_stats(const wbx_solver* s, double* tau, uint32_t* ref_iters, uint32_t* product_pairs);
 
 #ifdef __cplusplus
 }

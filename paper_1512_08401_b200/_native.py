@@ -115,6 +115,7 @@ SIGNATURES = {
     "wbx_deblur": (C.c_int, [_P, _D, _D, C.c_int, C.POINTER(wbx_report)]),
     "wbx_solver_last_stats": (C.c_int, [_P, _U64, C.POINTER(C.c_float)]),
     "wbx_solver_phase_ms": (C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "wbx_solver_tau_stats": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "wbx_shard_create": (C.c_int, [_P, C.c_uint64, _U64, _U32, _D, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
     "wbx_shard_destroy": (C.c_int, [_P]),
     "wbx_shard_plan": (C.c_int, [C.c_uint64, _U64, _U32, C.c_uint32, _U64, _U64]),

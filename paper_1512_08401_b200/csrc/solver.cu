@@ -2470,6 +2470,16 @@ int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms) {
     return WBX_OK;
 }
 
+int wbx_solver_tau_stats(const wbx_solver* s, double* tau, uint32_t* ref_iters, uint32_t* product_pairs) {
+    if (!s || !tau || !ref_iters || !product_pairs) return WBX_INVALID_ARGUMENT;
+    double out[wbx::OUT_COUNT];
+    if (cudaMemcpy(out, s->out.p, sizeof out, cudaMemcpyDeviceToHost) != cudaSuccess) return WBX_CUDA_ERROR;
+    *tau = out[wbx::OUT_TAU];
+    *ref_iters = static_cast<uint32_t>(out[wbx::OUT_TAU_ITERS]);
+    *product_pairs = static_cast<uint32_t>(out[wbx::OUT_TAU_STEPS]);
+    return WBX_OK;
+}
+
 }  // extern "C"
 
 extern "C" int wbx_solver_create_batch(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* basis, const double* p,

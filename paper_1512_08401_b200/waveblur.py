@@ -1030,6 +1030,13 @@ class Deblurrer:
         _check(lib.wbx_solver_phase_ms(self.handle, C.byref(t), C.byref(i)))
         return float(t.value), float(i.value)
 
+    def tau_stats(self):
+        """(tau, the reference's power-iteration count, operator product pairs spent) of the
+        last solve (Lanczos steps on the fp32 hot path)."""
+        t, it, pp = C.c_double(), C.c_uint32(), C.c_uint32()
+        _check(lib.wbx_solver_tau_stats(self.handle, C.byref(t), C.byref(it), C.byref(pp)))
+        return float(t.value), int(it.value), int(pp.value)
+
     def __del__(self):
         if lib is None:  # interpreter shutdown: the library is already gone
             return
