@@ -1700,6 +1700,108 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kern
     }
 }
 
+// The same Lanczos estimate on the stream engine (fp32 operator stream, fp32 vectors; the
+// operators whose windows do not fit: C3, C4 on one GPU). Per coordinate of C: w_j in a.wv,
+// q_j-1 in a.uC (fp64, unused by the fp32 power iteration); reductions are not deferred.
+__global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_lanczos_kernel(SolveArgs a) {
+    __shared__ double smem[kWarpsPerBlock + 1];
+    __shared__ double lz_al[kLzCap], lz_be[kLzCap];
+    __shared__ LzCtl ctl;
+    const int lane = threadIdx.x & 31;
+    const uint32_t gwarp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    Streamer st{};
+    st_init(st, dsmem + (threadIdx.x >> 5) * warp_smem_bytes(a.nslots), a.A, a.T, gwarp, nwarps, lane, kLzCap, false,
+            a.nslots);
+    float* uC = static_cast<float*>(a.yC);  // P^-1/2 w_j on C
+    float* tR = static_cast<float*>(a.res); // t' = Theta P^-1/2 w_j on R
+    double* qp = a.uC;                      // q_j-1 on C
+    double s2[2] = {0.0, 0.0};
+    for (uint64_t i = gthread; i < a.n; i += nthreads) {
+        const double v = rng_normal(0x5eedull, i);
+        s2[0] += v * v;
+    }
+    for (uint64_t c = gthread; c < a.nC; c += nthreads) {
+        const double v = rng_normal(0x5eedull, a.C_glob[c]);
+        a.wv[c] = v;
+        qp[c] = 0.0;
+        uC[c] = static_cast<float>(a.ispC[c] * v);
+        s2[1] += v * v;
+    }
+    grid_sync_reduce<2>(a.sync, epoch, s2, smem);
+    if (threadIdx.x == 0) {
+        const double beta = sqrt(s2[1]);
+        ctl.beta = beta;
+        ctl.rb = 1.0 / beta;
+        lz_be[0] = beta;
+        ctl.r2 = s2[1] / s2[0];
+        ctl.lambda = 0.0;
+        ctl.check_prev = -1.0;
+        ctl.stop_prev = -1;
+        ctl.iters = ctl.steps = 0;
+        ctl.zero = !(beta > 0.0);
+        ctl.done = ctl.zero;
+        ctl.breakdown = 0;
+    }
+    __syncthreads();
+    for (int j = 0; !ctl.done;) {
+        const bool final = ctl.breakdown || j == kLzCap;
+        if ((final || (j > 0 && j >= a.lz_first && (j - a.lz_first) % a.lz_every == 0)) &&
+            lz_check(lz_al, lz_be, j, final, &ctl))
+            break;
+        // phase A_j: t' = Theta P^-1/2 w_j, |t'|^2 -> alpha_j = |t'|^2 / beta_j^2
+        double accA[1] = {0.0};
+        st_phase<float, float>(st, a.A, a.T, gwarp, nwarps, lane, st.nA, uC, [](uint32_t) { return 0; },
+                               [&](uint32_t r, float t, int) {
+                                   tR[r] = t;
+                                   accA[0] = fma(static_cast<double>(t), static_cast<double>(t), accA[0]);
+                               });
+        grid_sync_reduce<1>(a.sync, epoch, accA, smem);
+        const double beta = ctl.beta, rb = ctl.rb;
+        const double alpha = accA[0] * rb * rb;
+        // phase T_j: w_j+1 = M q_j - alpha_j q_j - beta_j q_j-1, |w_j+1|^2 -> beta_j+1
+        double accT[1] = {0.0};
+        st_phase<float, float>(
+            st, a.A, a.T, gwarp, nwarps, lane, st.nT, tR,
+            [&](uint32_t c) {
+                return c != kNoRow ? make_double3(a.ispC[c], a.wv[c], qp[c]) : make_double3(0.0, 0.0, 0.0);
+            },
+            [&](uint32_t c, float g, double3 pv) {
+                const double z = pv.x * static_cast<double>(g) * rb;  // (M q_j)_c
+                const double q = pv.y * rb;                           // q_j
+                const double wn = z - alpha * q - beta * pv.z;
+                a.wv[c] = wn;
+                qp[c] = q;
+                uC[c] = static_cast<float>(pv.x * wn);
+                accT[0] = fma(wn, wn, accT[0]);
+            });
+        grid_sync_reduce<1>(a.sync, epoch, accT, smem);
+        if (threadIdx.x == 0) {
+            lz_al[j] = alpha;
+            const double bn = sqrt(accT[0]);
+            if (j + 1 < kLzCap) lz_be[j + 1] = bn;
+            ctl.beta = bn;
+            ctl.rb = 1.0 / bn;
+            ctl.breakdown = !(bn > 1e-13 * (fabs(alpha) + beta));  // T_j+1 is exact
+        }
+        __syncthreads();
+        ++j;
+    }
+    st_drain(st);
+    if (gthread == 0) {
+        const double lambda = ctl.lambda;
+        a.out[OUT_TAU] = (ctl.zero || lambda <= 0.0) ? 1.0 : 1.0 / (lambda * a.step_safety);
+        a.out[OUT_TAU_ITERS] = ctl.iters;
+        a.out[OUT_LAMBDA_MAX] = lambda;
+        a.out[OUT_TAU_STEPS] = ctl.steps;
+    }
+}
+
 // ---------------------------------------------------------------- batched FISTA (C5)
 // B independent images sharing Theta_K, P, w, lambda and tau (BASELINE config C5): the
 // operator stream is read once per B right-hand sides (SpMM). Vectors are interleaved
@@ -1928,6 +2030,7 @@ struct wbx_solver {
     int nslots = 3;  // TMA slots in flight per warp
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
     bool win = false, win_dict = false, tau_win64 = false, tau_lanczos = false;
+    int grid_tau_lz = 0;
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     wbx::WinSide wA, wT;
@@ -2029,11 +2132,11 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.sync.trace = s->trace.p;
     a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
     a.nslots = s->nslots;
+    a.lz_first = env_int("WBX_LZ_FIRST", 48, 1, kLzCap);
+    a.lz_every = env_int("WBX_LZ_EVERY", 8, 1, kLzCap);
     if (s->win) {
         a.wA = view_of(s->wA);
         a.wT = view_of(s->wT);
-        a.lz_first = env_int("WBX_LZ_FIRST", 48, 1, kLzCap);
-        a.lz_every = env_int("WBX_LZ_EVERY", 8, 1, kLzCap);
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
@@ -2077,6 +2180,8 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
     } else if (s->win) {
         const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
         launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st, kWinBlock);
+    } else if (sizeof(T) == 4 && s->tau_lanczos) {
+        launch_coop<T>(reinterpret_cast<const void*>(tau_lanczos_kernel), s->grid_tau_lz, a, st);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
     }
@@ -2142,6 +2247,11 @@ void alloc_state(wbx_solver* s) {
     if (const char* e = std::getenv("WBX_SLOTS")) s->nslots = std::max(1, std::min(kMaxSlots, std::atoi(e)));
     s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     s->grid_tau = blocks_per_sm(reinterpret_cast<const void*>(tau_kernel<T>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
+    // Lanczos tau on the stream engine (fp32; overridden below when the window engine runs)
+    s->tau_lanczos = sizeof(T) == 4 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
+    if (sizeof(T) == 4)
+        s->grid_tau_lz =
+            blocks_per_sm(reinterpret_cast<const void*>(tau_lanczos_kernel), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     if (s->batch == 4)
         s->grid_fista = blocks_per_sm(reinterpret_cast<const void*>(fista_batch_kernel<4>), dyn_smem<T>(s->nslots)) * s->ctx->num_sms;
     else if (s->batch == 8)
@@ -2206,6 +2316,8 @@ void alloc_state(wbx_solver* s) {
                              static_cast<unsigned long long>(s->wT.rec.bytes()), s->win_smem_fista, s->win_smem_tau);
         }
     }
+    if (!s->win)  // stream engine: Lanczos tau unless WBX_TAU=power (the window attempts may have reset it)
+        s->tau_lanczos = sizeof(T) == 4 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
 }
 
 }  // namespace
