@@ -99,7 +99,7 @@ struct SolveArgs {
     int tau_from_device, max_iters, track, stop_on_ref, decoupled_inline, nslots;
     // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
     WinView wA, wT;
-    int lz_first, lz_every;  // Lanczos tau (tau_lanczos_win_kernel): first check, check period
+    int lz_first, lz_every, lz_gap;  // Lanczos tau: first check, check period, compared m - gap
     // T-typed state
     void* yC;
     void* xpC;
@@ -1433,45 +1433,53 @@ constexpr int kLzCap = 200;
 // iteration; *iters = the reference's iteration count; *zero = the zero-operator sentinel.
 template <int K>  // K = ceil(m / 32) registers per lane
 __device__ __forceinline__ double lz_power_on_T_k(const double* al, const double* be, int m, double r2, int* iters,
-                                               bool* zero) {
+                                                  bool* zero) {
+    // y = T^(2it) e1 / mu_2it: one pentadiagonal product by T^2 per iteration (one dependent
+    // round of shuffles instead of two); mu_{2it+1}/mu_{2it} = (T y)_0 = alpha_0 + beta_1 y_1
     const int lane = threadIdx.x & 31;
-    constexpr int kk = K;
-    double a[K], bl[K], br[K], y[K];
+    // T^2 coefficients are rebuilt from alpha / beta (shared memory) every iteration: the
+    // check keeps only y and z in registers, so it does not crowd the phases' registers
+    auto A = [&](int i) { return (i >= 0 && i < m) ? al[i] : 0.0; };
+    auto B = [&](int i) { return (i > 0 && i < m) ? be[i] : 0.0; };  // T[i-1][i]
+    double y[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int i = lane + 32 * k;
-        a[k] = i < m ? al[i] : 0.0;
-        bl[k] = (i > 0 && i < m) ? be[i] : 0.0;  // T[i][i-1]
-        br[k] = (i + 1 < m) ? be[i + 1] : 0.0;   // T[i][i+1]
-        y[k] = i == 0 ? 1.0 : 0.0;
-    }
-    auto matvec = [&]() {
+    for (int k = 0; k < K; ++k) y[k] = lane + 32 * k == 0 ? 1.0 : 0.0;
+    const double a0 = A(0), b1 = B(1);
+    double lam_prev = 0.0;
+    *zero = false;
+    for (int it = 0; it < 200; ++it) {
+        const double y1 = __shfl_sync(0xffffffffu, y[0], 1);
+        const double lam = (it == 0 ? r2 : 1.0) * fma(b1, y1, a0);  // lambda_it (y_0 = 1)
         double z[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            if (k < kk) {
-                double l = __shfl_up_sync(0xffffffffu, y[k], 1);
-                double r = __shfl_down_sync(0xffffffffu, y[k], 1);
-                const double lk = __shfl_sync(0xffffffffu, y[k > 0 ? k - 1 : 0], 31);
-                const double rk = __shfl_sync(0xffffffffu, y[k + 1 < K ? k + 1 : k], 0);
-                if (lane == 0) l = k > 0 ? lk : 0.0;
-                if (lane == 31) r = k + 1 < kk ? rk : 0.0;
-                z[k] = fma(bl[k], l, fma(a[k], y[k], br[k] * r));
-            } else {
-                z[k] = 0.0;
+            double u1 = __shfl_up_sync(0xffffffffu, y[k], 1), u2 = __shfl_up_sync(0xffffffffu, y[k], 2);
+            double d1 = __shfl_down_sync(0xffffffffu, y[k], 1), d2 = __shfl_down_sync(0xffffffffu, y[k], 2);
+            const double p31 = __shfl_sync(0xffffffffu, y[k > 0 ? k - 1 : 0], 31);
+            const double p30 = __shfl_sync(0xffffffffu, y[k > 0 ? k - 1 : 0], 30);
+            const double n0 = __shfl_sync(0xffffffffu, y[k + 1 < K ? k + 1 : k], 0);
+            const double n1 = __shfl_sync(0xffffffffu, y[k + 1 < K ? k + 1 : k], 1);
+            if (lane == 0) {
+                u1 = k > 0 ? p31 : 0.0;
+                u2 = k > 0 ? p30 : 0.0;
             }
+            if (lane == 1) u2 = k > 0 ? p31 : 0.0;
+            if (lane == 31) {
+                d1 = k + 1 < K ? n0 : 0.0;
+                d2 = k + 1 < K ? n1 : 0.0;
+            }
+            if (lane == 30) d2 = k + 1 < K ? n0 : 0.0;
+            const int i = lane + 32 * k;
+            const double am = A(i - 1), a_ = A(i), ap = A(i + 1);
+            const double bm = B(i - 1), b_ = B(i), bp = B(i + 1), bpp = B(i + 2);
+            const double d = fma(a_, a_, fma(b_, b_, bp * bp));  // (T^2)[i][i]
+            const double e1 = bp * (a_ + ap);                     // (T^2)[i][i+1]
+            const double e2 = bp * bpp;                           // (T^2)[i][i+2]
+            const double l1 = b_ * (am + a_);                     // (T^2)[i][i-1]
+            const double l2 = bm * b_;                            // (T^2)[i][i-2]
+            z[k] = fma(l2, u2, fma(l1, u1, fma(d, y[k], fma(e1, d1, e2 * d2))));
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) y[k] = z[k];
-    };
-    double lam_prev = 0.0;
-    *zero = false;
-    for (int it = 0; it < 200; ++it) {  // y = T^it e1 / mu_2it on entry (mu_0 = 1)
-        matvec();
-        const double odd = __shfl_sync(0xffffffffu, y[0], 0);  // mu_{2it+1} / mu_{2it}
-        const double lam = it == 0 ? r2 * odd : odd;
-        matvec();
-        const double even = __shfl_sync(0xffffffffu, y[0], 0);  // |T^{it+1} e1|^2 / mu_2it
+        const double even = __shfl_sync(0xffffffffu, z[0], 0);  // mu_{2it+2} / mu_{2it} = |M v_it|^2
         if (even == 0.0) {  // M v = 0: the reference's zero-operator sentinel (solver.cpp:89)
             *zero = true;
             *iters = it + 1;
@@ -1484,7 +1492,7 @@ __device__ __forceinline__ double lz_power_on_T_k(const double* al, const double
         lam_prev = lam;
         const double inv = 1.0 / even;
 #pragma unroll
-        for (int k = 0; k < K; ++k) y[k] *= inv;
+        for (int k = 0; k < K; ++k) y[k] = z[k] * inv;
     }
     *iters = 200;
     return lam_prev;
@@ -1541,29 +1549,45 @@ struct LzCtl {  // control state of tau_lanczos_win_kernel (shared memory, ident
     double alpha, beta, rb;  // alpha_j, beta_j, 1 / beta_j of the current step
     int breakdown;
     double r2, lambda, check_prev;
-    int stop_prev, iters, steps, zero, done;
+    int stop_prev, iters, steps, zero, done, gap;
 };
 
 // Evaluate T_m (warp 0) and take the decision: `final` (the cap, a breakdown) or the
 // zero-operator sentinel end the estimate; otherwise it ends when this check agrees with the
 // previous one (same stopping index, lambda within 1e-12). All threads of the CTA call it.
-__device__ __forceinline__ bool lz_check(const double* al, const double* be, int m, bool final, LzCtl* ctl) {
+__device__ __noinline__ bool lz_check(const double* al, const double* be, int m, bool final, LzCtl* ctl) {
+    // warp 0 evaluates T_m and warp 1 T_{m-gap} at the same time (the other warps idle): two
+    // estimates per check, so the first check at which they agree ends the estimate
+    __shared__ double lam1;
+    __shared__ int its1;
     __syncthreads();  // alpha / beta of the last step are written
-    if (threadIdx.x < 32) {
+    const int w = threadIdx.x >> 5;
+    const int m1 = m - ctl->gap;
+    if (w == 1 && !final && m1 >= 1) {
+        int its = 0;
+        bool z = false;
+        const double lam = lz_power_on_T(al, be, m1, ctl->r2, &its, &z);
+        if ((threadIdx.x & 31) == 0) {
+            lam1 = lam;
+            its1 = z ? -1 : its;
+        }
+    }
+    if (w == 0) {
         int its = 0;
         bool z = false;
         const double lam = lz_power_on_T(al, be, m, ctl->r2, &its, &z);
         if (threadIdx.x == 0) {
-            if (final || z || (its == ctl->stop_prev && fabs(lam - ctl->check_prev) <= 1e-12 * fabs(lam))) {
-                ctl->lambda = lam;
-                ctl->iters = its;
-                ctl->zero = z;
-                ctl->steps = m;
-                ctl->done = 1;
-            }
-            ctl->check_prev = lam;
-            ctl->stop_prev = its;
+            ctl->lambda = lam;
+            ctl->iters = its;
+            ctl->zero = z;
+            ctl->steps = m;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double lam = ctl->lambda;
+        ctl->done = final || ctl->zero ||
+                    (m1 >= 1 && its1 == ctl->iters && fabs(lam - lam1) <= 1e-12 * fabs(lam));
     }
     __syncthreads();
     return ctl->done != 0;
@@ -1620,6 +1644,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kern
         ctl.iters = ctl.steps = 0;
         ctl.zero = !(beta > 0.0);
         ctl.breakdown = 0;
+        ctl.gap = a.lz_gap;
         ctl.done = ctl.zero;
     }
     __syncthreads();
@@ -1747,6 +1772,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_lanczos_kernel(Solve
         ctl.zero = !(beta > 0.0);
         ctl.done = ctl.zero;
         ctl.breakdown = 0;
+        ctl.gap = a.lz_gap;
     }
     __syncthreads();
     for (int j = 0; !ctl.done;) {
@@ -2132,8 +2158,9 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.sync.trace = s->trace.p;
     a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
     a.nslots = s->nslots;
-    a.lz_first = env_int("WBX_LZ_FIRST", 48, 1, kLzCap);
-    a.lz_every = env_int("WBX_LZ_EVERY", 8, 1, kLzCap);
+    a.lz_first = env_int("WBX_LZ_FIRST", 60, 1, kLzCap);
+    a.lz_every = env_int("WBX_LZ_EVERY", 4, 1, kLzCap);
+    a.lz_gap = env_int("WBX_LZ_GAP", 4, 1, kLzCap);
     if (s->win) {
         a.wA = view_of(s->wA);
         a.wT = view_of(s->wT);
