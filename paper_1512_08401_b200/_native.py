@@ -132,6 +132,12 @@ SIGNATURES = {
     "wbx_shard_power_step_a": (C.c_int, [_P]),
     "wbx_shard_power_step_t": (C.c_int, [_P]),
     "wbx_shard_power_result": (C.c_int, [_P, C.c_double, _D, C.POINTER(C.c_uint32)]),
+    "wbx_shard_lz_begin": (C.c_int, [_P]),
+    "wbx_shard_lz_update": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "wbx_shard_lz_step_a": (C.c_int, [_P]),
+    "wbx_shard_lz_step_t": (C.c_int, [_P]),
+    "wbx_shard_lz_done": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "wbx_shard_lz_result": (C.c_int, [_P, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
 }
 
 

@@ -22,6 +22,7 @@
 #include <numeric>
 
 #include "internal.hpp"
+#include "lanczos.cuh"
 #include "sell.cuh"
 
 extern "C" void wbx_set_last_error(const char* msg);
@@ -44,6 +45,7 @@ struct wbx_shard {
     wbx::DevBuf<float> xp, x0R, tp, thr, beta;
     wbx::DevBuf<double> pC, wC, ispC, wv, p_full, w_full, part;
     wbx::DevBuf<double> pstate;  // power iteration: {nw_prev, lambda_prev, iterations, flag}
+    wbx::DevBuf<double> qp, lz;  // Lanczos estimate: q_j-1 on C_p; alpha / beta / control (LzState)
     double lambda = 0.0, tau = 0.0;
     int max_iters = 0;
     uint64_t device_bytes = 0;
@@ -95,6 +97,8 @@ struct ShardArgs {
     double* part;
     double* sums_pad;
     double* pstate;
+    double* qp;
+    double* lz;
     uint32_t world;
     double lambda, tau;
 };
@@ -130,6 +134,8 @@ ShardArgs args_of(wbx_shard* s) {
     a.part = s->part.p;
     a.sums_pad = s->sums_pad;
     a.pstate = s->pstate.p;
+    a.qp = s->qp.p;
+    a.lz = s->lz.p;
     a.world = s->world;
     a.lambda = s->lambda;
     a.tau = s->tau;
@@ -303,6 +309,136 @@ __global__ void power_update_kernel(ShardArgs a, int first) {
 unsigned blocks_for(uint64_t threads) { return static_cast<unsigned>(std::max<uint64_t>(1, (threads + kBlock - 1) / kBlock)); }
 
 }  // namespace
+// ---- estimate_step by Lanczos (solver.cu tau_lanczos_win_kernel; same steps, same checks)
+// lz state: [0, kLzCap) alpha_j, [kLzCap, 2 kLzCap) beta_j, then the scalars below
+enum : int { LZ_R2 = 2 * kLzCap, LZ_DONE, LZ_LAMBDA, LZ_ITERS, LZ_STEPS, LZ_ZERO, LZ_J, LZ_COUNT };
+
+__global__ void lz_init_kernel(ShardArgs a, uint64_t lo, uint64_t hi) {
+    __shared__ double sm[kBlock / 32 + 1];
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    double s2 = 0.0, sc = 0.0;
+    for (uint64_t i = lo + t; i < hi; i += nt) {
+        const double v = rng_normal(0x5eedull, i);
+        s2 += v * v;
+    }
+    for (uint64_t c = t; c < a.nC_own; c += nt) {
+        const double v = rng_normal(0x5eedull, a.C_own[c]);
+        a.wv[c] = v;
+        a.qp[c] = 0.0;
+        a.u_pad[a.rank * a.maxC + c] = a.ispC[c] * v;
+        sc += v * v;
+    }
+    s2 = block_sum<kBlock>(s2, sm);
+    sc = block_sum<kBlock>(sc, sm);
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = s2;
+        a.part[2 * blockIdx.x + 1] = sc;
+    }
+}
+
+// phase A_j: t' = Theta[R_p, :] P^-1/2 w_j, partial |t'|^2
+__global__ void lz_a_kernel(ShardArgs a) {
+    if (a.lz[LZ_DONE] != 0.0) return;
+    __shared__ double sm[kBlock / 32 + 1];
+    double* t = a.t_pad + a.rank * a.maxR;
+    double acc = 0.0;
+    slice_rows<double, double>(a.A, a.u_pad, [&](uint32_t r, double v) {
+        t[r] = v;
+        acc += v * v;
+    });
+    acc = block_sum<kBlock>(acc, sm);
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = acc;
+        a.part[2 * blockIdx.x + 1] = 0.0;
+    }
+}
+
+// phase T_j: w_j+1 = M q_j - alpha_j q_j - beta_j q_j-1 on C_p, partial |w_j+1|^2
+__global__ void lz_t_kernel(ShardArgs a) {
+    if (a.lz[LZ_DONE] != 0.0) return;
+    __shared__ double sm[kBlock / 32 + 1];
+    const int j = static_cast<int>(a.lz[LZ_J]);
+    const double alpha = a.lz[j], beta = a.lz[kLzCap + j], rb = 1.0 / beta;
+    double* u = a.u_pad + a.rank * a.maxC;
+    double acc = 0.0;
+    slice_rows<double, double>(a.T, a.t_pad, [&](uint32_t c, double g) {
+        const double z = a.ispC[c] * g * rb;  // (M q_j)_c
+        const double q = a.wv[c] * rb;        // q_j
+        const double wn = z - alpha * q - beta * a.qp[c];
+        a.wv[c] = wn;
+        a.qp[c] = q;
+        u[c] = a.ispC[c] * wn;
+        acc += wn * wn;
+    });
+    acc = block_sum<kBlock>(acc, sm);
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = acc;
+        a.part[2 * blockIdx.x + 1] = 0.0;
+    }
+}
+
+__global__ void lz_rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
+    if (!init && a.lz[LZ_DONE] != 0.0) return;
+    if (threadIdx.x != 0) return;
+    double s0 = 0.0, s1 = 0.0;
+    for (unsigned i = 0; i < blocks; ++i) {
+        s0 += a.part[2 * i];
+        s1 += a.part[2 * i + 1];
+    }
+    a.sums_pad[2 * a.rank] = s0;
+    a.sums_pad[2 * a.rank + 1] = s1;
+}
+
+// on the all-gathered sums (rank order, every rank alike): phase 0 starts the estimate,
+// 1 takes alpha_j, 2 takes beta_j+1 and runs the scheduled check (two warps)
+__global__ void lz_update_kernel(ShardArgs a, int phase, int first, int every, int gap) {
+    __shared__ LzCtl ctl;
+    __shared__ int check, final;
+    double* lz = a.lz;
+    if (threadIdx.x == 0) {
+        check = final = 0;
+        double s0 = 0.0, s1 = 0.0;
+        for (uint32_t r = 0; r < a.world; ++r) {
+            s0 += a.sums_pad[2 * r];
+            s1 += a.sums_pad[2 * r + 1];
+        }
+        if (phase == 0) {
+            lz[LZ_R2] = s1 / s0;
+            lz[kLzCap] = sqrt(s1);
+            lz[LZ_J] = 0.0;
+            lz[LZ_LAMBDA] = lz[LZ_ITERS] = lz[LZ_STEPS] = 0.0;
+            lz[LZ_ZERO] = lz[LZ_DONE] = !(sqrt(s1) > 0.0) ? 1.0 : 0.0;
+        } else if (lz[LZ_DONE] == 0.0) {
+            const int j = static_cast<int>(lz[LZ_J]);
+            if (phase == 1) {
+                const double beta = lz[kLzCap + j];
+                lz[j] = s0 / (beta * beta);
+            } else {
+                const double bn = sqrt(s0);
+                const int jn = j + 1;
+                lz[LZ_J] = jn;
+                if (jn < kLzCap) lz[kLzCap + jn] = bn;
+                final = jn == kLzCap || !(bn > 1e-13 * (fabs(lz[j]) + lz[kLzCap + j]));  // cap / breakdown
+                check = final || (jn >= first && (jn - first) % every == 0);
+                ctl.r2 = lz[LZ_R2];
+                ctl.gap = gap;
+                ctl.done = 0;
+            }
+        }
+    }
+    __syncthreads();
+    if (!check) return;
+    const int m = static_cast<int>(lz[LZ_J]);
+    if (lz_check(lz, lz + kLzCap, m, final != 0, &ctl) && threadIdx.x == 0) {
+        lz[LZ_DONE] = 1.0;
+        lz[LZ_LAMBDA] = ctl.lambda;
+        lz[LZ_ITERS] = ctl.iters;
+        lz[LZ_STEPS] = ctl.steps;
+        lz[LZ_ZERO] = ctl.zero;
+    }
+}
+
 }  // namespace wbx
 
 using wbx::kBlock;
@@ -645,6 +781,89 @@ int wbx_shard_power_result(wbx_shard* s, double step_safety, double* tau, uint32
     const bool zero = st[3] == 2.0;
     *iters = static_cast<uint32_t>(st[2]);
     *tau = (zero || st[1] <= 0.0) ? 1.0 : 1.0 / (st[1] * step_safety);  // solver.cpp:89,97
+    return WBX_OK;
+}
+
+
+// estimate_step by Lanczos, device-resident like the power iteration above:
+// lz_begin -> [all-gather sums] -> lz_update(0) -> repeat { lz_step_a -> [all-gather t, sums]
+// -> lz_update(1) -> lz_step_t -> [all-gather sums, u] -> lz_update(2) } -> lz_result.
+// lz_done (synchronising) lets the host stop enqueueing once the scheduled check agreed.
+int wbx_shard_lz_begin(wbx_shard* s) {
+    if (!s || !s->u_pad || !s->sums_pad) return WBX_INVALID_ARGUMENT;
+    try {
+        if (!s->lz.p) s->lz.alloc(wbx::LZ_COUNT);
+        if (!s->qp.p) s->qp.alloc(std::max<uint64_t>(s->chi - s->clo, 1));
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+    wbx::ShardArgs a = wbx::args_of(s);
+    const unsigned blocks = 2 * static_cast<unsigned>(s->ctx->num_sms);
+    if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
+    const uint64_t lo = s->n * s->rank / s->world, hi = s->n * (s->rank + 1) / s->world;
+    cudaMemsetAsync(s->lz.p, 0, s->lz.bytes(), s->ctx->stream);
+    wbx::lz_init_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a, lo, hi);
+    wbx::lz_rank_sums_kernel<<<1, 32, 0, s->ctx->stream>>>(a, blocks, 1);
+    wbx::count_launch(s->ctx, 2);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_lz_update(wbx_shard* s, int phase, int first, int every, int gap) {
+    if (!s || !s->sums_pad || !s->lz.p || phase < 0 || phase > 2 || first < 1 || every < 1 || gap < 1)
+        return WBX_INVALID_ARGUMENT;
+    wbx::lz_update_kernel<<<1, 64, 0, s->ctx->stream>>>(wbx::args_of(s), phase, first, every, gap);
+    wbx::count_launch(s->ctx);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+static int lz_phase(wbx_shard* s, bool tside) {
+    if (!s || !s->lz.p || !s->sums_pad) return WBX_INVALID_ARGUMENT;
+    wbx::ShardArgs a = wbx::args_of(s);
+    const wbx::SellView& M = tside ? a.T : a.A;
+    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(M.slices, 1)) * 32),
+                                               8u * static_cast<unsigned>(s->ctx->num_sms));
+    if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
+    if (M.slices) {
+        if (tside)
+            wbx::lz_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
+        else
+            wbx::lz_a_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
+    } else {
+        cudaMemsetAsync(s->part.p, 0, 2 * blocks * sizeof(double), s->ctx->stream);
+    }
+    wbx::lz_rank_sums_kernel<<<1, 32, 0, s->ctx->stream>>>(a, blocks, 0);
+    wbx::count_launch(s->ctx, 2);
+    return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
+}
+
+int wbx_shard_lz_step_a(wbx_shard* s) { return lz_phase(s, false); }
+int wbx_shard_lz_step_t(wbx_shard* s) { return lz_phase(s, true); }
+
+int wbx_shard_lz_done(wbx_shard* s, int* done) {
+    if (!s || !done || !s->lz.p) return WBX_INVALID_ARGUMENT;
+    double d = 0.0;
+    if (cudaMemcpyAsync(&d, s->lz.p + wbx::LZ_DONE, sizeof d, cudaMemcpyDeviceToHost, s->ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+        return WBX_CUDA_ERROR;
+    *done = d != 0.0;
+    return WBX_OK;
+}
+
+int wbx_shard_lz_result(wbx_shard* s, double step_safety, double* tau, uint32_t* iters, uint32_t* steps) {
+    if (!s || !tau || !iters || !steps || !s->lz.p) return WBX_INVALID_ARGUMENT;
+    double st[wbx::LZ_COUNT];
+    if (cudaMemcpyAsync(st, s->lz.p, sizeof st, cudaMemcpyDeviceToHost, s->ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+        return WBX_CUDA_ERROR;
+    if (st[wbx::LZ_DONE] == 0.0) {
+        wbx_set_last_error("wbx_shard_lz_result: the estimate has not finished");
+        return WBX_BAD_SPEC;
+    }
+    const double lam = st[wbx::LZ_LAMBDA];
+    *iters = static_cast<uint32_t>(st[wbx::LZ_ITERS]);
+    *steps = static_cast<uint32_t>(st[wbx::LZ_STEPS]);
+    *tau = (st[wbx::LZ_ZERO] != 0.0 || lam <= 0.0) ? 1.0 : 1.0 / (lam * step_safety);  // solver.cpp:89,97
     return WBX_OK;
 }
 

@@ -15,6 +15,7 @@ A sharded solve is bitwise equal to the single-GPU fp32 solve given the same tau
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import List, Optional
 
 import numpy as np
@@ -128,6 +129,45 @@ class ShardedDeblurrer:
     # enqueued blindly; the device applies the stopping rule and turns the remaining steps
     # into no-ops, so the host waits only once, for the result.
     def estimate_step(self, step_safety: float = 1.01) -> float:
+        """tau as the single-GPU fp32 solver computes it: the reference's power-iteration
+        estimate (solver.cpp:69-99) by Lanczos (WBX_TAU=power: the literal power iteration)."""
+        if os.environ.get("WBX_TAU") == "power":
+            return self._estimate_step_power(step_safety)
+        first = int(os.environ.get("WBX_LZ_FIRST", 60))
+        every = int(os.environ.get("WBX_LZ_EVERY", 4))
+        gap = int(os.environ.get("WBX_LZ_GAP", 4))
+        for s in self.shards:
+            _check(lib.wbx_shard_lz_begin(s.h))
+        self.exchange.gather(self.sums, None)
+        for s in self.shards:
+            _check(lib.wbx_shard_lz_update(s.h, 0, first, every, gap))
+        self.exchange.gather(self.u, None)
+        done = C.c_int(0)
+        for j in range(1, 201):
+            for s in self.shards:
+                _check(lib.wbx_shard_lz_step_a(s.h))
+            self.exchange.gather(self.t, None)
+            self.exchange.gather(self.sums, None)
+            for s in self.shards:
+                _check(lib.wbx_shard_lz_update(s.h, 1, first, every, gap))
+            for s in self.shards:
+                _check(lib.wbx_shard_lz_step_t(s.h))
+            self.exchange.gather(self.sums, None)
+            self.exchange.gather(self.u, None)
+            for s in self.shards:
+                _check(lib.wbx_shard_lz_update(s.h, 2, first, every, gap))
+            if j == 200 or (j >= first and (j - first) % every == 0) or j == 1:
+                _check(lib.wbx_shard_lz_done(self.shards[0].h, C.byref(done)))  # a check ran (or breakdown)
+                if done.value:
+                    break
+        tau, iters, steps = C.c_double(), C.c_uint32(), C.c_uint32()
+        _check(lib.wbx_shard_lz_result(self.shards[0].h, float(step_safety), C.byref(tau), C.byref(iters),
+                                       C.byref(steps)))
+        self.tau_iters = int(iters.value)
+        self.tau_steps = int(steps.value)
+        return float(tau.value)
+
+    def _estimate_step_power(self, step_safety: float) -> float:
         for s in self.shards:
             _check(lib.wbx_shard_power_begin(s.h))
         self.exchange.gather(self.sums, None)

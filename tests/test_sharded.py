@@ -91,7 +91,7 @@ def test_exchange_protocol_world2_gloo():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_sharded_bitwise_equals_single_gpu(world):
+def test_sharded_bitwise_equals_single_gpu(world, monkeypatch):
     import torch
 
     from paper_1512_08401_b200.sharded import LocalExchange, ShardedDeblurrer
@@ -111,10 +111,13 @@ def test_sharded_bitwise_equals_single_gpu(world):
     sh.deblur_dev(u0.data_ptr(), out.data_ptr(), tau=tau, clamp=True)
     ctx.synchronize()
     assert np.array_equal(out.cpu().numpy().reshape(256, 256), ref)
-    # estimate_step through the sharded power iteration: same stopping iteration as the
-    # single-GPU kernel
+    # estimate_step through the sharded Lanczos estimate (default) and the sharded power
+    # iteration (WBX_TAU=power): the reference's stopping iteration and tau
+    t1, it1 = W.estimate_step(W.SparseThetaOp(op, ctx), P, 1.01, ctx=ctx, return_iters=True)
     t2 = sh.estimate_step(1.01)
     assert abs(t2 - tau) <= 1e-6 * tau
-    t1, it1 = W.estimate_step(W.SparseThetaOp(op, ctx), P, 1.01, ctx=ctx, return_iters=True)
-    assert sh.tau_iters == it1
+    assert sh.tau_iters == it1 and sh.tau_steps < it1
+    monkeypatch.setenv("WBX_TAU", "power")
+    t3 = sh.estimate_step(1.01)
+    assert abs(t3 - tau) <= 1e-6 * tau and sh.tau_iters == it1
     del sh, single
