@@ -339,10 +339,12 @@ def cpu_reference(steps: int, warmup: int, budget_s: float = 150.0):
         up = Path(td) / "u0.bin"
         u0.astype("<f8").tofile(up)
         if drv.exists():
-            # one untimed deblur happens inside the driver (golden pass); then `reps` timed ones
-            reps = max(1, min(steps, 3))
+            # the driver's golden pass plus `warmup` untimed deblurs, then `reps` timed ones
+            # (~4.4 s each on the GPU box's 16 threads: K=20, W=3 ends in ~2 minutes)
+            reps = max(1, min(steps, 20))
             r = subprocess.run([str(drv), "--out", td, "--dims", "1024", "1024", "--iters", str(ITERS),
-                                "--u0", str(up), "--bench-reps", str(reps)], capture_output=True, text=True)
+                                "--u0", str(up), "--bench-reps", str(reps), "--bench-warmup", str(warmup)],
+                               capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(r.stderr[-2000:])
             meta = json.loads((Path(td) / "meta.json").read_text())
@@ -471,7 +473,7 @@ def main():
             return
         cb = cpu_reference(args.steps, args.warmup)
         line = {"metric": METRIC, "value": cb["value"], "unit": "ms", "n_gpus": args.gpus,
-                "steps": len(cb.get("per_rep_s", [1])), "warmup": 1, "ms_per_step": cb["value"],
+                "steps": len(cb.get("per_rep_s", [1])), "warmup": args.warmup, "ms_per_step": cb["value"],
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "impl": "reference",
                 "config": {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic "

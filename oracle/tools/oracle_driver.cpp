@@ -19,7 +19,7 @@
 //                 [--psf gaussian --sigma S] [--K K | --Kfactor F] [--mode dyadic|uniform]
 //                 [--noise SIG] [--seed SEED] [--lambda L] [--iters I]
 //                 [--precond spai|jacobi|identity] [--write-op] [--u0 FILE]
-//                 [--bench-reps R] [--no-solve] [--exact]
+//                 [--bench-reps R] [--bench-warmup W] [--no-solve] [--exact]
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -201,7 +201,7 @@ int main(int argc, char** argv) {
     std::vector<std::size_t> dims = {256, 256};
     unsigned order = 4, J = 4;
     double sigma = 5.0, noise = 5e-3, lambda = 1e-4, kfactor = 3.0;
-    std::size_t K = 0, iters = 50, bench_reps = 0;
+    std::size_t K = 0, iters = 50, bench_reps = 0, bench_warmup = 0;
     std::uint64_t seed = 2024;
     bool write_op = false, solve = true, exact = false;
     for (int i = 1; i < argc; ++i) {
@@ -229,6 +229,7 @@ int main(int argc, char** argv) {
         else if (a == "--write-op") write_op = true;
         else if (a == "--u0") u0_path = next();
         else if (a == "--bench-reps") bench_reps = std::stoull(next());
+        else if (a == "--bench-warmup") bench_warmup = std::stoull(next());
         else if (a == "--no-solve") solve = false;
         else if (a == "--method") method = next();
         else if (a == "--exact") exact = true;
@@ -347,14 +348,14 @@ int main(int argc, char** argv) {
         // the reference's own code path, repeated.
         if (bench_reps > 0) {
             std::vector<double> times;
-            for (std::size_t r = 0; r < bench_reps; ++r) {
+            for (std::size_t r = 0; r < bench_warmup + bench_reps; ++r) {
                 auto b0 = clk::now();
                 DeblurProblem pb = prob;
                 pb.x0 = analyze(observed, basis).values;
                 SolveReport rr = fista(pb, P, cfg);
                 Image rs = synthesize(WaveletCoeffs{&basis.layout, rr.x_final}, basis);
                 auto b1 = clk::now();
-                times.push_back(secs(b0, b1));
+                if (r >= bench_warmup) times.push_back(secs(b0, b1));
                 if (rs.v.size() != n) return 3;
             }
             meta << ",\n  \"bench_deblur_s\": " << json_array(times);
