@@ -231,6 +231,22 @@ def test_lanczos_tau_equals_power_iteration(golden, monkeypatch, name):
     assert abs(lz.tau - g.meta["tau"]) <= 1e-6 * g.meta["tau"]
 
 
+def test_hot_path_deterministic_with_lanczos_tau(golden):
+    """The fp32 deblur with the step estimated on the device (Lanczos) is bitwise
+    reproducible run to run, like the reference (README.md:37-40): no atomics in any
+    reduction, every CTA takes the same convergence decision."""
+    g = golden("c1_db4_256")
+    op = g.operator()
+    b = basis_of(g)
+    d = W.Deblurrer(op, b, precond_of(g, op), g.weights(), g.meta["lambda"],
+                    W.SolverConfig(max_iters=g.meta["iters"], track_energy=False))
+    u1, r1 = d.deblur(g["u0"].reshape(g.dims), clamp=False)
+    u2, r2 = d.deblur(g["u0"].reshape(g.dims), clamp=False)
+    assert r1.tau == r2.tau and r1.tau_iters == r2.tau_iters
+    assert np.array_equal(u1, u2)
+    assert d.tau_stats()[2] < r1.tau_iters  # fewer product pairs than the reference's iterations
+
+
 def test_lanczos_tau_small_spectra():
     """Operators whose Krylov space is tiny (Lanczos breaks down or only sees noise after a
     few steps): identity, two distinct scales, the zero operator, through the fp32 path."""
