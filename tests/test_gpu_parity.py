@@ -247,6 +247,31 @@ def test_hot_path_deterministic_with_lanczos_tau(golden):
     assert d.tau_stats()[2] < r1.tau_iters  # fewer product pairs than the reference's iterations
 
 
+def test_lanczos_tau_random_operators():
+    """Random sparse operators and preconditioners (tools/tau_stress.py): the Lanczos
+    estimate reproduces the fp64 reference mode's iteration count (stopping rule) and tau
+    within 1e-6 on every case. (The literal fp32 power iteration does not: its fp32 rounding
+    moves the stopping decision on about a quarter of these operators.)"""
+    def random_op(rng, n, per_row):
+        lens = rng.integers(0, per_row + 1, n)
+        ro = np.zeros(n + 1, np.uint64)
+        ro[1:] = np.cumsum(lens)
+        cols = [np.sort(rng.choice(n, size=k, replace=False)) for k in lens]
+        ci = np.concatenate(cols).astype(np.uint32)
+        return W.SparseOperator(n, ro, ci, rng.standard_normal(int(ro[-1])) * rng.uniform(0.1, 2.0))
+
+    rng = np.random.default_rng(99)
+    for _ in range(12):
+        n = int(rng.choice([64, 256, 1024]))
+        op = random_op(rng, n, int(rng.integers(1, 12)))
+        P = W.DiagonalPreconditioner(rng.uniform(0.2, 3.0, n), W.PrecondKind.Spai)
+        prob = W.DeblurProblem(W.SparseThetaOp(op), np.zeros(n), np.ones(n), 1e-4)
+        lz = W.fista(prob, P, W.SolverConfig(max_iters=0, precision=32, track_energy=False))
+        t64, it64 = W.estimate_step(W.SparseThetaOp(op), P, 1.01, return_iters=True)
+        assert lz.tau_iters == it64, (n, op.nnz())
+        assert abs(lz.tau - t64) <= 1e-6 * t64
+
+
 def test_lanczos_tau_small_spectra():
     """Operators whose Krylov space is tiny (Lanczos breaks down or only sees noise after a
     few steps): identity, two distinct scales, the zero operator, through the fp32 path."""
