@@ -137,6 +137,12 @@ int wbx_op_get_info(const wbx_op* op, wbx_op_info* info);
 int wbx_spmv(wbx_ctx* ctx, const wbx_op* op, int transpose, const double* x, double* y);
 int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, const void* x_dev,
                  void* y_dev);
+/* The SELL kernel of wbx_spmv_dev alone, in the compacted spaces (no gather/scatter/memset):
+ * transpose == 0: y[|R|] = Theta[R, C] x[|C|]; 1: y[|C|] = Theta^T[C, R] x[|R|]
+ * (|R|, |C| = wbx_op_info.nonempty_rows / nonempty_cols). Same arithmetic as wbx_spmv_dev;
+ * used to measure the SpMV against the HBM roofline (tools/spmv_roofline.py). */
+int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision,
+                         const void* x_dev, void* y_dev);
 /* approx_gradient (theta.cpp:358-365): Theta^T (Theta x - x0) */
 int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0,
                         double* g);

@@ -75,6 +75,7 @@ SIGNATURES = {
     "wbx_op_get_info": (C.c_int, [_P, C.POINTER(wbx_op_info)]),
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
+    "wbx_spmv_compact_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
     "wbx_stencil_create": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                      C.POINTER(C.c_void_p)]),

@@ -433,6 +433,24 @@ int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, c
     });
 }
 
+int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision,
+                         const void* x_dev, void* y_dev) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        const wbx_sell& M = transpose ? op->T : op->A;
+        if (precision == WBX_FP64) {
+            wbx::spmv_compact<double>(ctx, M, static_cast<const double*>(x_dev), static_cast<double*>(y_dev),
+                                      ctx->stream);
+        } else {
+            if (!(op->A.seg_ok && op->T.seg_ok))
+                wbx::fail(WBX_TOO_LARGE, "operator rows longer than 496 nonzeros: fp32 layout unavailable");
+            wbx::spmv_compact<float>(ctx, M, static_cast<const float*>(x_dev), static_cast<float*>(y_dev),
+                                     ctx->stream);
+        }
+    });
+}
+
 int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0, double* g) {
     return guard([&] {
         need(ctx, "ctx");

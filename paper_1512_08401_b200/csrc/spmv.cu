@@ -5,8 +5,12 @@
 //
 // Full-length vectors are gathered into the compacted column space, multiplied, and
 // scattered back; empty rows produce 0.0 exactly as the reference's `double s = 0.0`.
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.hpp"
 #include "sell.cuh"
+#include "stream.cuh"
 
 namespace wbx {
 
@@ -46,6 +50,163 @@ __global__ void sell_f32_kernel(SellView M, const float* __restrict__ x, float* 
     if (r != kNoRow) y[r] = v;
 }
 
+// fp32 SELL SpMV with the operator stream staged by the TMA engine. Each warp walks the
+// slices gw, gw + TW, ... (TW = warps in the grid); lane 0 keeps the warp's next
+// slice records ([lane_info 32 x u32][np x 32 pairs]) in flight as 1-D bulk copies into a
+// shared-memory ring, so the bytes in flight per SM are set by shared memory, not by
+// registers. Measured slower than the register-staged sell_f32_kernel (~55 % of HBM at
+// 4096^2): the limiter is each warp's dependent record -> x-gather round trip, not the
+// bytes in flight, and the ring's shared memory caps the warps per SM at 12-24. Same loads,
+// gathers and fma order per lane as seg_partial/seg_combine: bitwise equal results.
+constexpr unsigned kRecU4Max = 8u + kSlotBytes / 16u;     // uint4 per slot
+constexpr unsigned kSlotStride = kRecU4Max * 16u + 8u + 4u; // slot + mbarrier + np word
+
+__device__ __forceinline__ uint64_t l2_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// NS slices per warp iteration (their x gathers issued together), KS ring slots per warp
+// (NS being consumed, KS - NS in flight). Per-slice arithmetic is that of seg_partial/seg_combine.
+template <int NS, int KS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) sell_f32_tma_kernel(SellView M, const float* __restrict__ x,
+                                                                   float* __restrict__ y) {
+    constexpr int kS = KS;
+    static_assert(KS >= NS, "ring smaller than a group");
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint4* ring = reinterpret_cast<uint4*>(sm) + size_t(wib) * kS * kRecU4Max;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + size_t(WARPS) * kS * kRecU4Max * 16u) + wib * kS;
+    uint32_t* snp = reinterpret_cast<uint32_t*>(sm + size_t(WARPS) * kS * (kRecU4Max * 16u + 8u)) + wib * kS;
+    const uint64_t TW = uint64_t(gridDim.x) * WARPS;
+    const uint64_t gw = uint64_t(blockIdx.x) * WARPS + wib;
+    const uint64_t pol = l2_first_policy();
+    auto issue = [&](uint64_t s, int slot) {  // lane 0
+        const uint64_t o0 = M.rec_off[s], o1 = M.rec_off[s + 1];
+        const unsigned bytes = static_cast<unsigned>((o1 - o0) * 16u);
+        snp[slot] = M.slice_np[s];
+        mbar_expect_tx(bars + slot, bytes);
+        bulk_g2s(ring + size_t(slot) * kRecU4Max, M.rec + o0, bytes, bars + slot, pol);
+    };
+    if (lane == 0) {
+        for (int i = 0; i < kS; ++i) mbar_init(bars + i, 1);
+        mbar_fence_init();
+        for (int i = 0; i < kS; ++i) {
+            const uint64_t s = gw + uint64_t(i) * TW;
+            if (s < M.slices) issue(s, i);
+        }
+    }
+    __syncwarp();
+    for (uint64_t k = 0;; k += NS) {
+        if (gw + k * TW >= M.slices) break;
+        float g[NS][16];
+        uint32_t word[NS], info[NS];
+        const uint4* r[NS];
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const uint64_t s = gw + (k + t) * TW;
+            const int slot = static_cast<int>((k + t) % kS);
+            r[t] = ring + size_t(slot) * kRecU4Max;
+            word[t] = 0;
+            info[t] = kNoRow;
+            if (s < M.slices) {
+                mbar_wait(bars + slot, ((k + t) / kS) & 1u);
+                word[t] = snp[slot];
+                info[t] = reinterpret_cast<const uint32_t*>(r[t])[lane];
+            }
+            const uint32_t np = word[t] & 0xffu;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < static_cast<int>(np)) {
+                    const uint4 e = r[t][8 + j * kWarp + lane];
+                    g[t][2 * j] = x[e.y];
+                    g[t][2 * j + 1] = x[e.w];
+                } else {
+                    g[t][2 * j] = 0.f;
+                    g[t][2 * j + 1] = 0.f;
+                }
+            }
+        }
+        float acc[NS];
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const uint32_t np = word[t] & 0xffu;
+            acc[t] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < static_cast<int>(np)) {
+                    const uint4 e = r[t][8 + j * kWarp + lane];
+                    acc[t] = fmaf(__uint_as_float(e.x), g[t][2 * j], acc[t]);
+                    acc[t] = fmaf(__uint_as_float(e.z), g[t][2 * j + 1], acc[t]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {  // the NS slots are consumed: refill them kS slices ahead
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+                const uint64_t sn = gw + (k + t + kS) * TW;
+                if (sn < M.slices) issue(sn, static_cast<int>((k + t) % kS));
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const uint32_t m = word[t] >> 8;
+            const uint32_t nseg = info[t] == kNoRow ? 1u : (info[t] >> 27);
+            const uint32_t maxseg = __reduce_max_sync(0xffffffffu, nseg);
+            float v = acc[t];
+            for (uint32_t j = 1; j < maxseg; ++j) {
+                const float u = __shfl_down_sync(0xffffffffu, v, j * m);
+                if (j < nseg) v += u;
+            }
+            if (info[t] != kNoRow) y[info[t] & kRowMask] = v;
+        }
+    }
+}
+
+// WBX_SPMV=reg (default: register-staged sell_f32_kernel, the fastest measured) | tma1 |
+// tma2 | tma3 (TMA-staged variants; 4096^2 fp32 forward: reg 118 us, tma1 137 us, tma2
+// 158 us, tma3 132 us, tools/spmv_roofline.py, profiles/r01_spmv_roofline.md)
+int spmv_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("WBX_SPMV");
+        if (e && std::strcmp(e, "tma1") == 0) return 1;
+        if (e && std::strcmp(e, "tma2") == 0) return 2;
+        if (e && std::strcmp(e, "tma3") == 0) return 3;
+        return 0;
+    }();
+    return mode;
+}
+
+template <int NS, int KS, int WARPS, int MINB>
+void launch_tma(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s) {
+    constexpr size_t smem = size_t(WARPS) * KS * kSlotStride;
+    static bool attr = false;
+    if (!attr) {
+        WBX_CUDA(cudaFuncSetAttribute(sell_f32_tma_kernel<NS, KS, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr = true;
+    }
+    const uint64_t want = (uint64_t(v.slices) + WARPS - 1) / WARPS;
+    const uint64_t cap = uint64_t(ctx->num_sms > 0 ? ctx->num_sms : 148) * MINB;
+    const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+    sell_f32_tma_kernel<NS, KS, WARPS><<<grid, WARPS * 32, smem, s>>>(v, x, y);
+}
+
+void launch_sell_f32(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s) {
+    const int mode = spmv_mode();
+    if (mode == 3)
+        launch_tma<1, 2, 12, 2>(ctx, v, x, y, s);  // 24 warps/SM, 2 slots each: 2 x 102 KB smem
+    else if (mode == 2)
+        launch_tma<2, 4, 4, 3>(ctx, v, x, y, s);   // 12 warps/SM, 2 slices per step: 3 x 68 KB
+    else if (mode == 1)
+        launch_tma<1, 3, 8, 2>(ctx, v, x, y, s);   // 16 warps/SM, 3 slots each: 2 x 102 KB
+    else
+        sell_f32_kernel<<<static_cast<unsigned>((uint64_t(v.slices) * 32 + kBlock - 1) / kBlock), kBlock, 0, s>>>(v, x, y);
+}
+
 inline unsigned blocks_for(uint64_t threads) {
     return static_cast<unsigned>((threads + kBlock - 1) / kBlock);
 }
@@ -75,7 +236,7 @@ void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
         if constexpr (sizeof(T) == 8)
             sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
         else
-            sell_f32_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
+            launch_sell_f32(op->ctx, v, xin.p, yout.p, s);
         scatter_kernel<T><<<blocks_for(m_out), kBlock, 0, s>>>(yout.p, out_idx, m_out, y);
         count_launch(op->ctx, 3);
         WBX_CUDA(cudaGetLastError());
@@ -103,7 +264,7 @@ void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_
     if constexpr (sizeof(T) == 8)
         sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, x, y);
     else
-        sell_f32_kernel<<<blocks_for(uint64_t(v.slices) * 32), kBlock, 0, s>>>(v, x, y);
+        launch_sell_f32(ctx, v, x, y, s);
     count_launch(ctx);
     WBX_CUDA(cudaGetLastError());
 }
