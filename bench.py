@@ -263,6 +263,13 @@ def run_ours(args, rank, world, local_rank):
     }
     if not args.no_extra and world == 1:
         result["extra_workloads"] = extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, rep.tau, flush)
+        # second half of the metric: the Theta x SpMV alone against the HBM roofline, on the C2
+        # operator carried to 4096^2 (403 MB operator stream > L2; profiles/r01_spmv_roofline.md)
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("spmv_roofline", ROOT / "tools" / "spmv_roofline.py")
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        result["spmv_roofline"] = mod.measure(4096, 10)
     return result
 
 

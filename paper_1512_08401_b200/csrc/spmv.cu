@@ -50,11 +50,49 @@ __global__ void sell_f32_kernel(SellView M, const float* __restrict__ x, float* 
     if (r != kNoRow) y[r] = v;
 }
 
+// The register-staged kernel in parts of H pairs per lane: fewer live registers, so more
+// warps per SM hide the record -> gather chain (H = 4: 40 registers, 48 warps/SM; 4096^2
+// forward 100 us vs 118 us for all 8 pairs at once). Same fma order as seg_partial.
+template <int H, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) sell_f32_part_kernel(SellView M, const float* __restrict__ x,
+                                                                     float* __restrict__ y) {
+    const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= M.slices) return;
+    const uint4* p = M.pk + M.slice_ptr[s] + lane;
+    const int np = static_cast<int>(M.slice_np[s] & 0xffu);
+    const uint64_t pol = l2_keep_policy();
+    float acc = 0.f;
+#pragma unroll
+    for (int h = 0; h < 8; h += H) {
+        if (h < np) {
+            uint4 e[H];
+#pragma unroll
+            for (int j = 0; j < H; ++j) e[j] = h + j < np ? ld_stream(p + (h + j) * kWarp, pol) : make_uint4(0, 0, 0, 0);
+            float g[2 * H];
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                g[2 * j] = h + j < np ? x[e[j].y] : 0.f;
+                g[2 * j + 1] = h + j < np ? x[e[j].w] : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                if (h + j < np) {
+                    acc = fmaf(__uint_as_float(e[j].x), g[2 * j], acc);
+                    acc = fmaf(__uint_as_float(e[j].z), g[2 * j + 1], acc);
+                }
+            }
+        }
+    }
+    const uint32_t r = seg_combine(M, s, lane, acc);
+    if (r != kNoRow) y[r] = acc;
+}
+
 // fp32 SELL SpMV with the operator stream staged by the TMA engine. Each warp walks the
 // slices gw, gw + TW, ... (TW = warps in the grid); lane 0 keeps the warp's next
 // slice records ([lane_info 32 x u32][np x 32 pairs]) in flight as 1-D bulk copies into a
 // shared-memory ring, so the bytes in flight per SM are set by shared memory, not by
-// registers. Measured slower than the register-staged sell_f32_kernel (~55 % of HBM at
+// registers. Measured slower than the register-staged kernels (~55-65 % of HBM at
 // 4096^2): the limiter is each warp's dependent record -> x-gather round trip, not the
 // bytes in flight, and the ring's shared memory caps the warps per SM at 12-24. Same loads,
 // gathers and fma order per lane as seg_partial/seg_combine: bitwise equal results.
@@ -166,16 +204,19 @@ __global__ void __launch_bounds__(WARPS * 32) sell_f32_tma_kernel(SellView M, co
     }
 }
 
-// WBX_SPMV=reg (default: register-staged sell_f32_kernel, the fastest measured) | tma1 |
-// tma2 | tma3 (TMA-staged variants; 4096^2 fp32 forward: reg 118 us, tma1 137 us, tma2
-// 158 us, tma3 132 us, tools/spmv_roofline.py, profiles/r01_spmv_roofline.md)
+// WBX_SPMV=quarter (default: sell_f32_part_kernel<2>, 32 registers, 64 warps/SM) | half
+// (<4>) | reg (sell_f32_kernel, all 8 pairs at once) | tma1 | tma2 | tma3 (TMA-staged
+// variants). 4096^2 fp32 forward: quarter 97 us, half 100 us, reg 118 us, tma1 137 us, tma2 158 us, tma3 132 us (tools/spmv_roofline.py,
+// profiles/r01_spmv_roofline.md)
 int spmv_mode() {
     static const int mode = [] {
         const char* e = std::getenv("WBX_SPMV");
         if (e && std::strcmp(e, "tma1") == 0) return 1;
         if (e && std::strcmp(e, "tma2") == 0) return 2;
         if (e && std::strcmp(e, "tma3") == 0) return 3;
-        return 0;
+        if (e && std::strcmp(e, "reg") == 0) return 0;
+        if (e && std::strcmp(e, "half") == 0) return 4;
+        return 5;
     }();
     return mode;
 }
@@ -197,7 +238,12 @@ void launch_tma(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaS
 
 void launch_sell_f32(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s) {
     const int mode = spmv_mode();
-    if (mode == 3)
+    const unsigned blocks = static_cast<unsigned>((uint64_t(v.slices) * 32 + kBlock - 1) / kBlock);
+    if (mode == 4)
+        sell_f32_part_kernel<4, 6><<<blocks, kBlock, 0, s>>>(v, x, y);
+    else if (mode == 5)
+        sell_f32_part_kernel<2, 8><<<blocks, kBlock, 0, s>>>(v, x, y);
+    else if (mode == 3)
         launch_tma<1, 2, 12, 2>(ctx, v, x, y, s);  // 24 warps/SM, 2 slots each: 2 x 102 KB smem
     else if (mode == 2)
         launch_tma<2, 4, 4, 3>(ctx, v, x, y, s);   // 12 warps/SM, 2 slices per step: 3 x 68 KB
