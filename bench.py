@@ -6,13 +6,19 @@ Gaussian blur sigma=5, noise 5e-3 (seed 2024), Daubechies-4 wavelets J=4, Theta_
 K = 3N by the reference's dyadic-weighted global top-K (operator = the reference's own
 threshold output, tests/golden/c2_db4_1024.npz, expanded to CSR), SPAI preconditioner,
 lambda = 1e-4, 100 FISTA iterations. One step = one deblur: u0 -> analyze -> tau
-(estimate_step, 200 power iterations, inside the step as in the reference's fista()) ->
-100 FISTA iterations -> synthesize -> clamp. fp32 hot path (fp64 DWT and tau).
+(estimate_step, inside the step as in the reference's fista()) -> 100 FISTA iterations ->
+synthesize -> clamp. fp32 hot path (fp64 DWT and tau).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1: one rank per GPU (torchrun), each deblurs its own image every step (weak scaling,
-no collective on the data path); value = max-over-ranks device time / images.
+--gpus N > 1 without torchrun re-executes itself under torch.distributed.run (one rank per
+GPU, NCCL). Each rank deblurs its own image every step (weak scaling, no collective on the
+data path); value = max-over-ranks device time / images. The C5 batch (64 images split over
+the N ranks, batches of 8 per SpMM launch) is reported beside it at every N.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref/oracle_driver linked
+against the unmodified reference library built from /root/reference; all host threads) on the
+same workload and config. It imports nothing from this repository's package.
 """
 from __future__ import annotations
 
@@ -37,12 +43,23 @@ DIMS = (1024, 1024)
 ITERS = 100
 GOLDEN = ROOT / "tests" / "golden" / "c2_db4_1024.npz"
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2: written between timed steps
+C5_IMAGES = 64
+
+
+def bench_config(world: int) -> dict:
+    """The `config` object of BOTH arms (identical dicts: the driver compares them)."""
+    z = np.load(GOLDEN)
+    return {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic top-K, SPAI, "
+                        "lambda=1e-4, 100 FISTA iters incl. tau (estimate_step)",
+            "image": list(DIMS), "iters": ITERS, "K_over_N": 3, "nnz": int(np.sum(z["gen_count"])),
+            "images_per_step": world, "parallelism": f"dp{world}: independent images, one per rank",
+            "l2": "flushed (512 MiB write) between timed steps"}
 
 
 def load_traffic():
     """DRAM bytes per launch of the solver kernels from the committed ncu --set full capture
     (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
-    p = Path(__file__).resolve().parent / "profiles" / "traffic.json"
+    p = ROOT / "profiles" / "traffic.json"
     try:
         return json.loads(p.read_text())
     except (OSError, ValueError):
@@ -55,6 +72,16 @@ def load_peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -118,6 +145,65 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+# ----------------------------------------------------------------------------- reference arm
+def reference_deblur_times(reps: int, warmup: int, threads=None) -> dict:
+    """The reference's own deblur unit (analyze + fista incl. estimate_step + synthesize) timed
+    by oracle/_ref/oracle_driver, which links the UNMODIFIED reference library built from
+    /root/reference (oracle/Makefile). The operator is the reference's C2 threshold output
+    (generator groups from the golden fixture, expanded by the reference's walk); the observed
+    image is the reference's own degrade(). Imports nothing from the repo's package."""
+    drv = ROOT / "oracle" / "_ref" / "oracle_driver"
+    if not drv.exists():
+        raise RuntimeError("oracle/_ref/oracle_driver missing (build() compiles it where /root/reference exists)")
+    z = np.load(GOLDEN)
+    rec = np.zeros(z["gen_block"].size, dtype=[("b", "<u4"), ("i", "<u4"), ("c", "<u8"), ("v", "<f8")])
+    rec["b"], rec["i"], rec["c"], rec["v"] = z["gen_block"], z["gen_index"], z["gen_count"], z["gen_value"]
+    env = dict(os.environ)
+    if threads:
+        env["OMP_NUM_THREADS"] = str(threads)
+    with tempfile.TemporaryDirectory() as td:
+        rec.tofile(Path(td) / "gens.bin")
+        r = subprocess.run([str(drv), "--out", td, "--dims", str(DIMS[0]), str(DIMS[1]), "--iters", str(ITERS),
+                            "--gens", str(Path(td) / "gens.bin"), "--bench-reps", str(reps),
+                            "--bench-warmup", str(warmup)], capture_output=True, text=True, env=env)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr[-2000:])
+        meta = json.loads((Path(td) / "meta.json").read_text())
+    times = meta["bench_deblur_s"]
+    return {"ms": 1e3 * float(np.mean(times)), "per_rep_s": times, "threads": int(meta.get("omp_threads", 1)),
+            "tau": meta.get("tau"), "psnr_restored_db": meta.get("psnr_restored_db"),
+            "fista_wall_time_s": meta.get("fista_wall_time_s")}
+
+
+def cpu_baseline_obj(multi: dict, single=None) -> dict:
+    cb = {"value": round(multi["ms"], 1), "unit": "ms", "cores": multi["threads"], "kind": "reference",
+          "sample": f"{len(multi['per_rep_s'])} full deblur(s) of the workload: analyze + fista (incl. "
+                    f"estimate_step) + synthesize, 1024^2, {ITERS} iters, the unmodified reference built from "
+                    f"/root/reference (oracle/_ref), OpenMP over {multi['threads']} threads",
+          "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if single is not None:
+        cb["value_1_thread"] = round(single["ms"], 1)
+    return cb
+
+
+def run_reference(args, world: int) -> dict:
+    reps = max(1, min(args.steps, 20))
+    multi = reference_deblur_times(reps, min(args.warmup, 3))
+    single = None
+    if not args.no_single_thread:
+        try:
+            single = reference_deblur_times(1, 0, threads=1)
+        except Exception:
+            pass
+    cb = cpu_baseline_obj(multi, single)
+    return {"metric": METRIC, "value": cb["value"], "unit": "ms", "n_gpus": world, "steps": reps,
+            "warmup": args.warmup, "ms_per_step": cb["value"], "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": bench_config(world), "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ----------------------------------------------------------------------------- our arm
 def make_inputs():
     from paper_1512_08401_b200 import synthetic as S
     from paper_1512_08401_b200 import waveblur as W
@@ -127,7 +213,17 @@ def make_inputs():
     op = W.theta_from_generators(gl)
     basis = W.make_basis(W.FilterFamily.Daubechies, 4, DIMS, 4)
     _, u0 = S.degrade(DIMS, 5.0, 5e-3, 2024)
-    return op, basis, u0, json.loads(bytes(z["meta_json"]).decode())
+    return op, basis, u0
+
+
+def _max_over_ranks(v: float, world: int, dev) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_ours(args, rank, world, local_rank):
@@ -135,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_1512_08401_b200 import waveblur as W
 
     torch.cuda.set_device(local_rank)
-    op, basis, u0, meta = make_inputs()
+    op, basis, u0 = make_inputs()
     ctx = W.Context(local_rank)
     P = W.spai(op, ctx)
     w = W.scale_weights(basis.layout)
@@ -143,8 +239,8 @@ def run_ours(args, rank, world, local_rank):
     deb = W.Deblurrer(op, basis, P, w, 1e-4, cfg, ctx)
     info = op.info(ctx)
     n = op.n
-    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     with torch.cuda.stream(stream):
         u0_dev = torch.from_numpy(u0.ravel().copy()).to(dev)
         out_dev = torch.empty(n, dtype=torch.float64, device=dev)
@@ -184,11 +280,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     launches = (ctx.launches - launches0) // args.steps
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(per_step))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = _max_over_ranks(float(sum(per_step)), world, dev)
     ms_per_step = total_ms / args.steps
     value = ms_per_step / world   # whole job: `world` images per step
 
@@ -207,44 +299,44 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         _, rep = deb.deblur(u0_np, clamp=True, out=out_np)
         e2e.append((time.perf_counter() - t0) * 1e3)
-    e2e_ms = float(np.mean(e2e))
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = _max_over_ranks(float(np.mean(e2e)), world, dev)
 
+    tau_kernel, it_kernel = deb.kernels()
     tau_iters = int(rep.tau_iters)
     _, _, tau_pairs = deb.tau_stats()  # operator product pairs actually spent (Lanczos steps)
     s_ms = float(np.median(solve_ms))
     tau_ms = float(np.mean([p[0] for p in phase_ms]))
     it_ms = float(np.mean([p[1] for p in phase_ms]))
     peak, peak_src = load_peaks()
-    nnz = int(info.nnz)
-    # SURVEY 8(d) algorithmic bytes: fp32 values + u32 indices, dense vectors read/written once
-    b_iter = 16 * nnz + 36 * n                       # one FISTA iteration
-    b_pow = 2 * (8 * nnz + 16 * n)                   # one power iteration: 2 SpMVs, fp64 vectors
+    nnz, nR, nC = int(info.nnz), int(info.nonempty_rows), int(info.nonempty_cols)
+    # Algorithmic bytes per unit, two models:
+    #  * SURVEY 8(d) dense model: fp32 values + u32 indices, dense n-vectors read/written once
+    #  * compacted model: what the kernel must move in the compacted spaces (coordinates with an
+    #    empty Theta column are iterated in registers by the decoupled pass, outside these bytes)
+    b_iter = 16 * nnz + 36 * n
+    b_iter_c = 16 * nnz + 12 * nR + 28 * nC
+    b_pair = 2 * (8 * nnz + 16 * n)             # one operator product pair, fp64 dense vectors
+    b_pair_c = 16 * nnz + 12 * nR + 16 * nC     # fp32 compacted: Θ, Θᵀ, u/t windows, own state
     kernels = [
-        {"kernel": "tau_lanczos_win_kernel (estimate_step, persistent)", "launch_ms": round(tau_ms, 4),
+        {"kernel": f"{tau_kernel} (estimate_step, persistent)", "launch_ms": round(tau_ms, 4),
          "units": f"{tau_pairs} operator product pairs (Lanczos steps standing in for the reference's "
-                  f"{tau_iters} power iterations) x 2*(8*nnz+16*n) B",
-         "algorithmic_bytes": tau_pairs * b_pow, "achieved": round(tau_pairs * b_pow / (tau_ms * 1e-3) / 1e9, 1)},
-        {"kernel": "fista_win_kernel (100 FISTA iterations, persistent)", "launch_ms": round(it_ms, 4),
-         "units": f"{ITERS} iterations x (16*nnz+36*n) B",
-         "algorithmic_bytes": ITERS * b_iter, "achieved": round(ITERS * b_iter / (it_ms * 1e-3) / 1e9, 1)},
+                  f"{tau_iters} power iterations)",
+         "algorithmic_bytes": tau_pairs * b_pair_c, "dense_model_bytes": tau_pairs * b_pair},
+        {"kernel": f"{it_kernel} ({ITERS} FISTA iterations, persistent)", "launch_ms": round(it_ms, 4),
+         "units": f"{ITERS} iterations", "algorithmic_bytes": ITERS * b_iter_c, "dense_model_bytes": ITERS * b_iter},
     ]
     for k in kernels:
+        k["achieved"] = round(k["algorithmic_bytes"] / (k["launch_ms"] * 1e-3) / 1e9, 1)
         k["frac"] = round(k["achieved"] / peak, 4)
+        k["dense_model_achieved"] = round(k["dense_model_bytes"] / (k["launch_ms"] * 1e-3) / 1e9, 1)
+        k["dense_model_frac"] = round(k["dense_model_achieved"] / peak, 4)
     dom = max(kernels, key=lambda k: k["launch_ms"])
     traffic = load_traffic()
     result = {
         "metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 DWT/tau)", "data": "synthetic",
-        "config": {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic "
-                               "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau (estimate_step)",
-                   "image": list(DIMS), "iters": ITERS, "nnz": nnz, "K_over_N": 3,
-                   "images_per_step": world, "parallelism": f"replicas x{world} (independent images)",
-                   "l2": "flushed (512 MiB write) between timed steps"},
+        "config": bench_config(world),
         "e2e": {"value": round(e2e_ms / world, 4), "unit": "ms", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "api": "wbx_deblur (host fp64 image in/out, pinned)"},
         "gpu_launches": int(launches),
@@ -252,19 +344,26 @@ def run_ours(args, rank, world, local_rank):
                      "unit": "GB/s", "frac": dom["frac"],
                      "traffic": traffic.get(dom["kernel"].split()[0]) if traffic else None,
                      "traffic_source": traffic.get("source") if traffic else None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "launch_ms": dom["launch_ms"],
-                     "kernels": kernels,
-                     "note": "operator + vectors are L2-resident across iterations (compacted, dictionary-"
-                             "coded layout streams ~2 B/nonzero); algorithmic bytes per SURVEY 8(d)"},
+                     "algorithmic_bytes_per_launch": dom["algorithmic_bytes"],
+                     "bytes_model": "compacted: per iteration 16*nnz + 12*|R| + 28*|C| (Θ and Θᵀ streams, x0/res "
+                                    "on R, y gather + y/x_prev/τ/p/threshold state on C)",
+                     "dense_model": {"bytes_per_launch": dom["dense_model_bytes"],
+                                     "achieved": dom["dense_model_achieved"], "frac": dom["dense_model_frac"],
+                                     "model": "SURVEY 8(d): per iteration 16*nnz + 36*n"},
+                     "launch_ms": dom["launch_ms"], "kernels": kernels,
+                     "limiter": "grid-barrier and gather latency: the operator (dictionary-coded, ~2.7 B/nonzero) "
+                                "and vectors stay L2-resident across iterations; HBM sees one cold read "
+                                "(`traffic`). The HBM-streamed SpMV is measured separately (`spmv_roofline`)."},
         "breakdown": {"solve_ms": round(s_ms, 4), "tau_ms": round(tau_ms, 4), "iterations_ms": round(it_ms, 4),
                       "tau_iters": tau_iters, "tau_product_pairs": tau_pairs, "tau": rep.tau,
-                      "dwt_and_idwt_ms": round(ms_per_step - s_ms, 4)},
+                      "dwt_and_idwt_ms": round(ms_per_step - s_ms, 4), "kernels": [tau_kernel, it_kernel]},
         "clocks": clk.summary(),
     }
+    result["c5_batch"] = run_c5(W, torch, ctx, stream, dev, op, basis, P, w, flush, rank, world)
     if not args.no_extra and world == 1:
         result["extra_workloads"] = extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, rep.tau, flush)
         # second half of the metric: the Theta x SpMV alone against the HBM roofline, on the C2
-        # operator carried to 4096^2 (403 MB operator stream > L2; profiles/r01_spmv_roofline.md)
+        # operator carried to 4096^2 (403 MB operator stream > L2; profiles/r02_spmv_roofline.md)
         import importlib.util
         spec = importlib.util.spec_from_file_location("spmv_roofline", ROOT / "tools" / "spmv_roofline.py")
         mod = importlib.util.module_from_spec(spec)
@@ -290,10 +389,48 @@ def _time_dev(deb, torch, stream, flush, u0_dev, out_dev, reps=5):
     return float(np.median(ts))
 
 
+def run_c5(W, torch, ctx, stream, dev, op, basis, P, w, flush, rank, world):
+    """BASELINE config C5: 64 independent 1024^2 deblurs split over the `world` ranks (64/world
+    per rank, one SpMM solve per 8 images: the operator is streamed once per 8 right-hand
+    sides), no collective on the data path; images/s of the whole job from the max over
+    ranks of the device time (strong scaling of the fixed 64-image job)."""
+    from paper_1512_08401_b200 import synthetic as S
+    B = 8
+    per_rank = C5_IMAGES // world
+    nb = max(1, per_rank // B)
+    n = op.n
+    seeds = [rank * per_rank + j for j in range(B)]
+    imgs = np.stack([S.degrade(DIMS, 5.0, 5e-3, s)[1] for s in seeds])
+    with torch.cuda.stream(stream):
+        ub = torch.from_numpy(imgs.reshape(-1).copy()).to(dev)
+        ob = torch.empty(B * n, dtype=torch.float64, device=dev)
+    db = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False), ctx, batch=B)
+    for _ in range(2):
+        db.deblur_dev(ub.data_ptr(), ob.data_ptr(), clamp=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        flush.zero_()
+        a.record(stream)
+    for _ in range(nb):   # the rank's share: nb batches of 8 (inputs resident, L2 flushed once)
+        db.deblur_dev(ub.data_ptr(), ob.data_ptr(), clamp=True)
+    with torch.cuda.stream(stream):
+        b.record(stream)
+    b.synchronize()
+    ms = _max_over_ranks(a.elapsed_time(b), world, dev)
+    del db
+    return {"images": nb * B * world, "images_per_rank": nb * B, "batch": B, "ms_job": round(ms, 3),
+            "images_per_s": round(1e3 * nb * B * world / ms, 1), "ms_per_image": round(ms / (nb * B * world), 4),
+            "tau": "estimated once per batch (inside the timed region)", "scaling": "strong (64-image job)"}
+
+
 def extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, tau, flush):
     """The other BASELINE configs on this GPU (reported beside the headline, same run):
-    C2 with tau cached per operator, C5 batches (SpMM over 8 images), C3 spatially varying."""
-    from paper_1512_08401_b200 import synthetic as S
+    C2 with tau cached per operator, C2 in the bitwise fp64 reference mode, C3 spatially
+    varying, the per-operator setup kernels."""
     out = {}
     n = op.n
     with torch.cuda.stream(stream):
@@ -302,24 +439,20 @@ def extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, tau, flush)
     # C2, tau cached (a deployment estimates tau once per operator, like P)
     d = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False, tau=tau), ctx)
     out["c2_tau_cached"] = {"ms_per_deblur": round(_time_dev(d, torch, stream, flush, u0_dev, out_dev), 4)}
-    # C5: batches of 8 images per GPU (bench --gpus N shards a 64-image batch over N GPUs)
-    B = 8
-    imgs = np.stack([S.degrade(DIMS, 5.0, 5e-3, seed)[1] for seed in range(B)])
-    with torch.cuda.stream(stream):
-        ub = torch.from_numpy(imgs.reshape(-1).copy()).to(dev)
-        ob = torch.empty(B * n, dtype=torch.float64, device=dev)
-    db = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False), ctx, batch=B)
-    ms = _time_dev(db, torch, stream, flush, ub, ob)
-    out["c5_batch8"] = {"ms_per_batch": round(ms, 4), "images_per_s_per_gpu": round(1e3 * B / ms, 1),
-                        "images_per_s_8gpu_weak": round(8e3 * B / ms, 1), "tau": "estimated once per batch"}
-    del db
+    # C2 in the fp64 reference mode (iterates bitwise equal to the reference's, literal power
+    # iteration for tau)
+    d64 = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False, precision=64), ctx)
+    out["c2_fp64_bitwise"] = {"ms_per_deblur": round(_time_dev(d64, torch, stream, flush, u0_dev, out_dev, reps=3), 3),
+                              "kernels": list(d64.kernels())}
+    del d64
     # C3: 1024^2 spatially varying blur (sigma 2.5 -> 7.5 px down the image)
     lad = W.SigmaLadder.from_npz(np.load(ROOT / "tests" / "golden" / "c3_ladder_1024.npz"))
     opv = W.theta_varying(lad, 2.5, 7.5)
     Pv = W.spai(opv, ctx)
     dv = W.Deblurrer(opv, basis, Pv, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False), ctx)
     out["c3_varying"] = {"ms_per_deblur": round(_time_dev(dv, torch, stream, flush, u0_dev, out_dev), 4),
-                         "nnz": int(opv.nnz()), "note": "u0 = the C2 observation (timing only)"}
+                         "nnz": int(opv.nnz()), "kernels": list(dv.kernels()),
+                         "note": "u0 = the C2 observation (timing only)"}
     # per-operator setup on the device (outside the timed unit): Theta_K construction
     # (build_theta_conv + weighted top-K, bitwise the reference's) and SPAI
     psf = W.gaussian_psf_kernel(DIMS, 5.0)
@@ -334,48 +467,6 @@ def extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, tau, flush)
                        "spai_ms": round(1e3 * (t2 - t1), 1),
                        "note": "wall time incl. host transfers; reference CPU: ~30 s build+threshold, ~0.2 s SPAI"}
     return out
-
-
-def cpu_reference(steps: int, warmup: int, budget_s: float = 150.0):
-    """The reference's own CPU implementation (oracle/_ref, built from /root/reference by
-    oracle/Makefile; all host threads via OpenMP) on the same workload and input image."""
-    drv = ROOT / "oracle" / "_ref" / "oracle_driver"
-    from paper_1512_08401_b200 import synthetic as S
-    _, u0 = S.degrade(DIMS, 5.0, 5e-3, 2024)
-    with tempfile.TemporaryDirectory() as td:
-        up = Path(td) / "u0.bin"
-        u0.astype("<f8").tofile(up)
-        if drv.exists():
-            # the driver's golden pass plus `warmup` untimed deblurs, then `reps` timed ones
-            # (~4.4 s each on the GPU box's 16 threads: K=20, W=3 ends in ~2 minutes)
-            reps = max(1, min(steps, 20))
-            r = subprocess.run([str(drv), "--out", td, "--dims", "1024", "1024", "--iters", str(ITERS),
-                                "--u0", str(up), "--bench-reps", str(reps), "--bench-warmup", str(warmup)],
-                               capture_output=True, text=True)
-            if r.returncode != 0:
-                raise RuntimeError(r.stderr[-2000:])
-            meta = json.loads((Path(td) / "meta.json").read_text())
-            times = meta["bench_deblur_s"]
-            return {"value": round(1e3 * float(np.mean(times)), 1), "unit": "ms",
-                    "cores": int(meta.get("omp_threads", os.cpu_count())), "kind": "reference",
-                    "sample": f"{len(times)} full deblur(s): analyze + fista (incl. estimate_step) + synthesize, "
-                              f"1024^2, {ITERS} iters, reference built from /root/reference (oracle/_ref)",
-                    "per_rep_s": times, "fista_wall_time_s": meta.get("fista_wall_time_s")}
-    # the reference could not be built here: time the C restatement (single thread)
-    from oracle import oracle as O
-    from paper_1512_08401_b200 import waveblur as W
-    op, _, _, _ = make_inputs()
-    A = O.Csr.of(op)
-    AT = A.transpose()
-    p = O.spai(A)
-    w = W.scale_weights(W.make_layout(DIMS, 4))
-    t0 = time.perf_counter()
-    x0 = O.analyze(u0, DIMS, 4, 1, 4)
-    O.pgd(A, AT, x0, w, 1e-4, p, ITERS)
-    O.synthesize(x0, DIMS, 4, 1, 4)
-    dt = time.perf_counter() - t0
-    return {"value": round(dt * 1e3, 1), "unit": "ms", "cores": 1, "kind": "port",
-            "sample": "1 full deblur through the C restatement (oracle/wbx_oracle.c), 1 thread"}
 
 
 class _SingleGpu:
@@ -396,7 +487,7 @@ def run_c4(args, rank, world, local_rank):
     import torch
     from paper_1512_08401_b200 import synthetic as S
     from paper_1512_08401_b200 import waveblur as W
-    from paper_1512_08401_b200.sharded import LocalExchange, ShardedDeblurrer, TorchExchange
+    from paper_1512_08401_b200.sharded import ShardedDeblurrer, TorchExchange
     size = args.size
     dims = (size, size)
     dev = torch.device("cuda", local_rank)
@@ -440,11 +531,7 @@ def run_c4(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         b.record(stream)
     b.synchronize()
-    ms = a.elapsed_time(b) / steps
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(a.elapsed_time(b) / steps, world, dev)
     restored = out.cpu().numpy().reshape(dims)
     if isinstance(sh, _SingleGpu):  # the power-iteration count of the solver's own run
         sh.tau_iters = int(sh.d.deblur(u0, clamp=True)[1].tau_iters)
@@ -457,6 +544,18 @@ def run_c4(args, rank, world, local_rank):
             "psnr_observed_db": round(S.psnr(u0, clean), 3), "psnr_restored_db": round(S.psnr(restored, clean), 3)}
 
 
+def relaunch_under_torchrun(gpus: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-execute under torch.distributed.run with one
+    rank per GPU (the driver's own launch line), rendezvous on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -464,56 +563,48 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the C3/C5/cached-tau side measurements")
+    ap.add_argument("--no-single-thread", action="store_true", help="reference arm: skip the 1-thread deblur")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3/fp64/setup/SpMV side measurements")
     ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
                     help="c4: one 4096^2 spatially varying deblur row-sharded over the --gpus ranks")
     ap.add_argument("--size", type=int, default=4096, help="image side for --workload c4")
+    ap.add_argument("--backend", default="nccl", help="torch.distributed backend (gloo: CPU tests of the launch)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        cb = cpu_reference(args.steps, args.warmup)
-        line = {"metric": METRIC, "value": cb["value"], "unit": "ms", "n_gpus": args.gpus,
-                "steps": len(cb.get("per_rep_s", [1])), "warmup": args.warmup, "ms_per_step": cb["value"],
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "impl": "reference",
-                "config": {"workload": "C2: 1024x1024 stationary Gaussian sigma=5 deblur, db4 J=4, K=3N dyadic "
-                                       "top-K, SPAI, lambda=1e-4, 100 FISTA iters incl. tau (estimate_step)",
-                           "image": list(DIMS), "iters": ITERS},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        if rank == 0:
+            print(json.dumps(run_reference(args, world)), flush=True)
         return
 
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(args.backend)
     if args.workload == "c4":
         line = run_c4(args, rank, world, local_rank)
         if rank == 0:
             print(json.dumps(line), flush=True)
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return
-    result = run_ours(args, rank, world, local_rank)
-    if rank == 0:
-        if not args.no_cpu_baseline:
-            try:
-                cb = cpu_reference(1, 0)
-                result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            except Exception as e:  # reported, never fatal
-                result["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": None,
-                                          "sample": f"failed: {e}"}
-        print(json.dumps(result), flush=True)
+    else:
+        result = run_ours(args, rank, world, local_rank)
+        if rank == 0:
+            if not args.no_cpu_baseline:
+                try:
+                    result["cpu_baseline"] = cpu_baseline_obj(reference_deblur_times(1, 0))
+                except Exception as e:  # reported, never fatal
+                    result["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": None,
+                                              "sample": f"failed: {e}"}
+            print(json.dumps(result), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

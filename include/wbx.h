@@ -15,7 +15,12 @@
  *     reference-side binding (integration/wbx_backend.cpp) re-throws.
  *   * A context binds one CUDA device and one stream; calls on one context must be
  *     serialised by the caller (the reference's functions are pure and re-entrant;
- *     use one context per host thread for the same property).
+ *     use one context per host thread for the same property). Per-call scratch lives
+ *     in the calling context, so two contexts may use one operator concurrently.
+ *   * Lifetimes: a basis or operator must outlive every solver, shard or exact operator
+ *     built on it (they keep pointers to its device layouts, like the reference's
+ *     non-owning `WaveletCoeffs.layout` / `DeblurProblem.op`, wavelet.hpp:81-84,
+ *     solver.hpp:56); a context must outlive every object created on it.
  */
 #ifndef WBX_H
 #define WBX_H
@@ -314,6 +319,9 @@ int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms);
  * (solver.cpp:81-96) and the operator product pairs spent (Lanczos steps on the fp32 hot
  * path, power iterations otherwise; synchronises the context's stream) */
 int wbx_solver_tau_stats(const wbx_solver* s, double* tau, uint32_t* ref_iters, uint32_t* product_pairs);
+/* The kernels this solver runs, "<step-estimate kernel> <iteration kernel>" (NUL-terminated,
+ * truncated to len): which engine the configuration and the operator selected. */
+int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,11 @@
 //                 [--noise SIG] [--seed SEED] [--lambda L] [--iters I]
 //                 [--precond spai|jacobi|identity] [--write-op] [--u0 FILE]
 //                 [--bench-reps R] [--bench-warmup W] [--no-solve] [--exact]
+//                 [--gens FILE]
+// --gens FILE: take the thresholded operator from a generator list (24-byte records
+// {u32 block, u32 gen_index, u64 count, f64 value}, e.g. tests/golden/*.npz gen_*) expanded
+// by the reference's walk, instead of running build_theta_conv + threshold (the bench's
+// reference arm: the timed unit is the deblur, not the operator build).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -197,7 +202,7 @@ std::string json_array(const std::vector<double>& v) {
 }  // namespace
 
 int main(int argc, char** argv) {
-    std::string out, family = "daubechies", mode = "dyadic", precond = "spai", u0_path, method = "fista";
+    std::string out, family = "daubechies", mode = "dyadic", precond = "spai", u0_path, method = "fista", gens_path;
     std::vector<std::size_t> dims = {256, 256};
     unsigned order = 4, J = 4;
     double sigma = 5.0, noise = 5e-3, lambda = 1e-4, kfactor = 3.0;
@@ -233,6 +238,7 @@ int main(int argc, char** argv) {
         else if (a == "--no-solve") solve = false;
         else if (a == "--method") method = next();
         else if (a == "--exact") exact = true;
+        else if (a == "--gens") gens_path = next();
         else throw std::runtime_error("unknown flag " + a);
     }
     if (out.empty()) throw std::runtime_error("--out required");
@@ -253,21 +259,35 @@ int main(int argc, char** argv) {
                                      : Image(dims);
     if (!u0_path.empty()) observed.v = read_f64(u0_path, n);
     auto t1 = clk::now();
-    CirculantTheta theta = build_theta_conv(psf, basis);
-    auto t2 = clk::now();
-    std::vector<double> band_w(basis.layout.bands.size(), 1.0);
+    std::vector<Gen> gens;
     SparseOperator sp;
-    if (mode == "uniform") {
-        sp = threshold_naive(theta, K);
+    bool expand_ok = true;
+    auto t2 = clk::now(), t3 = t2;
+    if (!gens_path.empty()) {
+        std::ifstream f(gens_path, std::ios::binary);
+        Gen g;
+        while (f.read(reinterpret_cast<char*>(&g.block), 4) && f.read(reinterpret_cast<char*>(&g.gen_index), 4) &&
+               f.read(reinterpret_cast<char*>(&g.count), 8) && f.read(reinterpret_cast<char*>(&g.value), 8))
+            gens.push_back(g);
+        if (gens.empty()) throw std::runtime_error("no generator records in " + gens_path);
+        sp = expand(basis.layout, gens);
+        t2 = t3 = clk::now();
     } else {
-        WeightVector wv = dyadic_weights(basis.layout);
-        for (std::size_t b = 0; b < band_w.size(); ++b) band_w[b] = wv.sigma[basis.layout.bands[b].offset];
-        sp = threshold_weighted(theta, K, wv);
+        CirculantTheta theta = build_theta_conv(psf, basis);
+        t2 = clk::now();
+        std::vector<double> band_w(basis.layout.bands.size(), 1.0);
+        if (mode == "uniform") {
+            sp = threshold_naive(theta, K);
+        } else {
+            WeightVector wv = dyadic_weights(basis.layout);
+            for (std::size_t b = 0; b < band_w.size(); ++b) band_w[b] = wv.sigma[basis.layout.bands[b].offset];
+            sp = threshold_weighted(theta, K, wv);
+        }
+        t3 = clk::now();
+        gens = kept_generators(theta, K, band_w);
+        SparseOperator re = expand(basis.layout, gens);
+        expand_ok = same_csr(re, sp);
     }
-    auto t3 = clk::now();
-    std::vector<Gen> gens = kept_generators(theta, K, band_w);
-    SparseOperator re = expand(basis.layout, gens);
-    const bool expand_ok = same_csr(re, sp);
     if (!expand_ok) std::fprintf(stderr, "generator-list expansion does NOT reproduce the reference CSR\n");
 
     {

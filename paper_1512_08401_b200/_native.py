@@ -117,6 +117,7 @@ SIGNATURES = {
     "wbx_solver_last_stats": (C.c_int, [_P, _U64, C.POINTER(C.c_float)]),
     "wbx_solver_phase_ms": (C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "wbx_solver_tau_stats": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "wbx_solver_kernels": (C.c_int, [_P, C.c_char_p, C.c_uint64]),
     "wbx_shard_create": (C.c_int, [_P, C.c_uint64, _U64, _U32, _D, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
     "wbx_shard_destroy": (C.c_int, [_P]),
     "wbx_shard_plan": (C.c_int, [C.c_uint64, _U64, _U32, C.c_uint32, _U64, _U64]),
@@ -142,13 +143,23 @@ SIGNATURES = {
 }
 
 
+# include/wbx_diag.h (diagnostics, not part of the drop-in boundary)
+DIAG_SIGNATURES = {
+    "wbx_diag_barrier_us": (C.c_int, [C.c_int, C.c_int, C.c_int, _D]),
+    "wbx_diag_stream_gbs": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, _D]),
+    "wbx_diag_slice_profile": (C.c_int, [_D]),
+    "wbx_diag_spmv_compact_mode": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
+    "wbx_diag_set_spmv_pf": (C.c_int, [C.c_longlong]),
+}
+
+
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
             f"libwbx.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; "
             f"g.build()'` (make -C paper_1512_08401_b200). There is no CPU fallback.")
     lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | C.RTLD_GLOBAL)
-    for name, (res, args) in SIGNATURES.items():
+    for name, (res, args) in list(SIGNATURES.items()) + list(DIAG_SIGNATURES.items()):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "internal.hpp"
+#include "wbx_diag.h"
 
 struct wbx_solver;
 
@@ -96,82 +97,11 @@ __global__ void delta_kernel(double* x, uint64_t i) { x[i] = 1.0; }
 
 unsigned nblocks(uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
-// Gram diagonals (precond.cpp:16-67), exact: same accumulation and first-touch order.
-void gram_host(const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
-
-// Gram diagonals: on the device (gram.cu, same operation order, bitwise equal) when a context
-// is given; the host path (also the fallback when a column's 2-hop set overflows the device
-// table) otherwise.
-// WBX_GRAM=host|device forces one path (device: fail instead of falling back).
+// Gram diagonals (precond.cpp:16-67) on the device (gram.cu): the reference's exact
+// accumulation and first-touch order, bitwise; no host path.
 void gram(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2) {
-    const char* e = std::getenv("WBX_GRAM");
-    const std::string mode = e ? e : "";
-    if (ctx && mode != "host") {
-        if (wbx::gram_device(ctx, op, cap_factor, diagM, diagM2)) return;
-        if (mode == "device") wbx::fail(WBX_TOO_LARGE, "gram_diagonals: a column's 2-hop set exceeds the device table");
-    }
-    gram_host(op, cap_factor, diagM, diagM2);
-}
-
-void gram_host(const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2) {
-    const uint64_t n = op->n, nnz = op->nnz;
-    const auto& rp = op->h_rowptr;
-    const auto& cl = op->h_col;
-    const auto& vl = op->h_val;
-    std::vector<uint64_t> toff(n + 1, 0);
-    for (uint64_t k = 0; k < nnz; ++k) ++toff[cl[k] + 1];
-    for (uint64_t i = 0; i < n; ++i) toff[i + 1] += toff[i];
-    std::vector<uint32_t> trow(nnz);
-    std::vector<double> tval(nnz);
-    {
-        std::vector<uint64_t> cur(toff.begin(), toff.end() - 1);
-        for (uint64_t r = 0; r < n; ++r)
-            for (uint64_t k = rp[r]; k < rp[r + 1]; ++k) {
-                const uint64_t pos = cur[cl[k]]++;
-                trow[pos] = static_cast<uint32_t>(r);
-                tval[pos] = vl[k];
-            }
-    }
-    for (uint64_t i = 0; i < n; ++i) {
-        double s = 0.0;
-        for (uint64_t k = toff[i]; k < toff[i + 1]; ++k) s += tval[k] * tval[k];
-        diagM[i] = s;
-    }
-    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    std::vector<uint64_t> counts(nth, 0);
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < nth; ++t) {
-        pool.emplace_back([&, t] {
-            std::vector<double> acc(n, 0.0);
-            std::vector<uint32_t> touched;
-            uint64_t cnt = 0;
-            for (uint64_t i = t; i < n; i += nth) {
-                touched.clear();
-                for (uint64_t k = toff[i]; k < toff[i + 1]; ++k) {
-                    const uint32_t row = trow[k];
-                    const double a = tval[k];
-                    for (uint64_t j = rp[row]; j < rp[row + 1]; ++j) {
-                        const uint32_t c = cl[j];
-                        if (acc[c] == 0.0) touched.push_back(c);
-                        acc[c] += a * vl[j];
-                    }
-                }
-                double s = 0.0;
-                for (uint32_t c : touched) {
-                    s += acc[c] * acc[c];
-                    acc[c] = 0.0;
-                }
-                diagM2[i] = s;
-                cnt += touched.size();
-            }
-            counts[t] = cnt;
-        });
-    }
-    for (auto& th : pool) th.join();
-    uint64_t total = 0;
-    for (auto c : counts) total += c;
-    const uint64_t cap = cap_factor * std::max<uint64_t>(nnz, 1);
-    if (total > cap) wbx::fail(WBX_MEMORY_GUARD, "gram_diagonals: nnz(M) exceeds the configured cap");
+    need(ctx, "ctx");
+    wbx::gram_device(ctx, op, cap_factor, diagM, diagM2);
 }
 
 }  // namespace
@@ -413,7 +343,7 @@ int wbx_spmv(wbx_ctx* ctx, const wbx_op* op, int transpose, const double* x, dou
         const uint64_t n = op->n;
         wbx::DevBuf<double> dx(n), dy(n);
         dx.upload(x, n, ctx->stream);
-        wbx::spmv_full_fp64(const_cast<wbx_op*>(op), transpose, dx.p, dy.p, ctx->stream);
+        wbx::spmv_full_fp64(ctx, op, transpose, dx.p, dy.p);
         WBX_CUDA(cudaMemcpyAsync(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         WBX_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -425,11 +355,9 @@ int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, c
         need(ctx, "ctx");
         need(op, "op");
         if (precision == WBX_FP64)
-            wbx::spmv_full_fp64(const_cast<wbx_op*>(op), transpose, static_cast<const double*>(x_dev),
-                                static_cast<double*>(y_dev), ctx->stream);
+            wbx::spmv_full_fp64(ctx, op, transpose, static_cast<const double*>(x_dev), static_cast<double*>(y_dev));
         else
-            wbx::spmv_full_fp32(const_cast<wbx_op*>(op), transpose, static_cast<const float*>(x_dev),
-                                static_cast<float*>(y_dev), ctx->stream);
+            wbx::spmv_full_fp32(ctx, op, transpose, static_cast<const float*>(x_dev), static_cast<float*>(y_dev));
     });
 }
 
@@ -451,6 +379,22 @@ int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int prec
     });
 }
 
+int wbx_diag_spmv_compact_mode(wbx_ctx* ctx, const wbx_op* op, int transpose, int mode, const float* x_dev,
+                               float* y_dev) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(op, "op");
+        if (mode < 0 || mode > 7) wbx::fail(WBX_BAD_SPEC, "unknown SpMV kernel mode");
+        if (!(op->A.seg_ok && op->T.seg_ok)) wbx::fail(WBX_TOO_LARGE, "fp32 layout unavailable");
+        wbx::spmv_compact<float>(ctx, transpose ? op->T : op->A, x_dev, y_dev, ctx->stream, mode);
+    });
+}
+
+int wbx_diag_set_spmv_pf(long long bytes) {
+    wbx::set_spmv_pf_bytes(bytes);
+    return WBX_OK;
+}
+
 int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0, double* g) {
     return guard([&] {
         need(ctx, "ctx");
@@ -462,10 +406,10 @@ int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const d
         wbx::DevBuf<double> dx(n), dx0(n), dr(n), dg(n);
         dx.upload(x, n, ctx->stream);
         dx0.upload(x0, n, ctx->stream);
-        wbx::spmv_full_fp64(const_cast<wbx_op*>(op), 0, dx.p, dr.p, ctx->stream);
+        wbx::spmv_full_fp64(ctx, op, 0, dx.p, dr.p);
         sub_kernel<<<nblocks(n), 256, 0, ctx->stream>>>(n, dr.p, dx0.p);
         wbx::count_launch(ctx);
-        wbx::spmv_full_fp64(const_cast<wbx_op*>(op), 1, dr.p, dg.p, ctx->stream);
+        wbx::spmv_full_fp64(ctx, op, 1, dr.p, dg.p);
         WBX_CUDA(cudaMemcpyAsync(g, dg.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         WBX_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -591,7 +535,7 @@ int wbx_energy(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0
         dx.upload(x, n, ctx->stream);
         dx0.upload(x0, n, ctx->stream);
         dw.upload(w, n, ctx->stream);
-        wbx::spmv_full_fp64(const_cast<wbx_op*>(op), 0, dx.p, dr.p, ctx->stream);
+        wbx::spmv_full_fp64(ctx, op, 0, dx.p, dr.p);
         const unsigned G = 2 * ctx->num_sms;
         wbx::DevBuf<double> part(2 * G);
         energy_partials<<<G, 256, 0, ctx->stream>>>(n, dr.p, dx0.p, dx.p, dw.p, part.p);

@@ -75,6 +75,9 @@ struct wbx_ctx {
     int num_sms = 0;
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
+    // standalone SpMV: compacted input / output of the calling context
+    wbx::DevBuf<double> scratch64[2];
+    wbx::DevBuf<float> scratch32[2];
 };
 
 // Wavelet layout + filters (WaveletBasis, wavelet.hpp:68-74).
@@ -114,6 +117,15 @@ struct wbx_sell {
     // the same slices as contiguous records for TMA staging: [lane_info x32][pairs]
     wbx::DevBuf<uint64_t> rec_off;    // uint4 offset of each record
     wbx::DevBuf<uint4> rec;
+    // row-per-lane fp32 layout (the standalone SpMV, spmv.cu sell_row_kernel): the xslices
+    // of the exact layout (32 consecutive sorted rows, one per lane), element-major, packed as
+    // {val, col, val, col} pairs [np x 32 x uint4] followed, for an odd slice length L, by the
+    // last element [32 x uint2]. Row sums run in element order. No per-lane row word: rows of
+    // slice s are s*32 + lane; no segment padding (rows of a slice have ~equal length, they
+    // are sorted). rslice[s] = {uint4 offset, L}.
+    wbx::DevBuf<uint2> rslice;
+    wbx::DevBuf<uint4> rpk;
+    uint64_t rpk_u4 = 0;
 };
 
 // A compacted operator side on the host: rows in the solver's sorted order, columns as
@@ -142,8 +154,6 @@ struct wbx_op {
     std::vector<uint32_t> h_col;
     std::vector<double> h_val;
     uint64_t device_bytes = 0;
-    wbx::DevBuf<double> scratch64[2];  // standalone SpMV: compacted input / output
-    wbx::DevBuf<float> scratch32[2];
 };
 
 namespace wbx {
@@ -161,10 +171,12 @@ void make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, std::vector<wb
 void make_filters(uint32_t family, uint32_t order, double* lo, double* hi, uint32_t* len);
 
 // spmv.cu
+// mode: the fp32 SELL kernel (-1: WBX_SPMV / default row kernel; see spmv.cu spmv_mode)
 template <typename T>
-void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s);
-void spmv_full_fp64(wbx_op* op, int transpose, const double* x_dev, double* y_dev, cudaStream_t s);
-void spmv_full_fp32(wbx_op* op, int transpose, const float* x_dev, float* y_dev, cudaStream_t s);
+void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s, int mode = -1);
+void spmv_full_fp64(wbx_ctx* ctx, const wbx_op* op, int transpose, const double* x_dev, double* y_dev);
+void spmv_full_fp32(wbx_ctx* ctx, const wbx_op* op, int transpose, const float* x_dev, float* y_dev);
+void set_spmv_pf_bytes(long long bytes);  // row kernel's L2 prefetch distance (-1: default)
 
 // op_build.cu
 struct SellView;
@@ -192,8 +204,9 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, 
 struct WinView;
 WinView view_of(const WinSide& w);
 
-// gram.cu: Gram diagonals on the device; false if a column overflowed the per-warp table
-bool gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
+// gram.cu: Gram diagonals on the device (shared-memory tables, global-memory second pass for
+// columns whose 2-hop set overflows them)
+void gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

@@ -45,8 +45,62 @@ struct HostSell {
     std::vector<uint32_t> lane_info;
     std::vector<uint64_t> rec_off;  // uint4 offset of each slice record (+ total)
     std::vector<uint4> rec;
+    // row-per-lane fp32 layout over the exact layout's slices
+    std::vector<uint2> rslice;
+    std::vector<uint4> rpk;
     bool seg_ok = true;
 };
+
+// Row-per-lane fp32 layout (wbx_sell::rslice/rpk): slice s = rows 32s..32s+31 (sorted by
+// length, so the slice's rows have ~equal length and padding is ~0), element pairs
+// {val, col, val, col} element-major [np x 32 lanes], then for an odd slice length the last
+// element [32 lanes x {val, col}]. Padding elements (a lane whose row is shorter, or a lane
+// past the last row) carry value 0 and the lane's last real column (the gather then hits a
+// line the lane already touched).
+template <typename RowRange>
+void make_row_layout(HostSell& h, uint64_t nrows, RowRange& range) {
+    const uint64_t slices = (nrows + 31) / 32;
+    h.rslice.assign(slices, make_uint2(0, 0));
+    uint64_t off = 0;
+    for (uint64_t s = 0; s < slices; ++s) {
+        const uint64_t L = h.xslice_len[s];
+        if (off > 0xffffffffull) fail(WBX_TOO_LARGE, "operator stream exceeds 32-bit slice offsets");
+        h.rslice[s] = make_uint2(static_cast<uint32_t>(off), static_cast<uint32_t>(L));
+        off += (L / 2) * 32 + (L & 1) * 16;
+    }
+    h.rpk.assign(off, make_uint4(0, 0, 0, 0));
+    for (uint64_t s = 0; s < slices; ++s) {
+        const uint64_t L = h.xslice_len[s], np = L / 2, base = h.rslice[s].x;
+        uint2* tail = reinterpret_cast<uint2*>(h.rpk.data() + base + np * 32);
+        for (uint64_t lane = 0; lane < 32; ++lane) {
+            const uint64_t r = s * 32 + lane;
+            const uint64_t len = r < nrows ? range.len(r) : 0;
+            uint32_t last = 0;
+            for (uint64_t j = 0; j < L; ++j) {
+                uint32_t c = last, bits = 0;
+                if (j < len) {
+                    double v;
+                    range.get(r, j, c, v);
+                    const float vf = static_cast<float>(v);
+                    std::memcpy(&bits, &vf, 4);
+                    last = c;
+                }
+                if (j < 2 * np) {
+                    uint4& p = h.rpk[base + (j / 2) * 32 + lane];
+                    if (j % 2 == 0) {
+                        p.x = bits;
+                        p.y = c;
+                    } else {
+                        p.z = bits;
+                        p.w = c;
+                    }
+                } else {
+                    tail[lane] = make_uint2(bits, c);
+                }
+            }
+        }
+    }
+}
 
 // rows: list of row ids (in slice order); each row r has [beg[r], end[r]) in (cols, vals),
 // cols already remapped to the compacted column space.
@@ -79,6 +133,7 @@ HostSell make_sell(uint64_t nrows, RowRange range) {
                 range.get(r, j, h.col[e], h.v64[e]);
             }
         }
+    make_row_layout(h, nrows, range);
     // ---- segmented fp32 layout
     struct Seg {
         uint64_t row, beg, len;
@@ -188,7 +243,10 @@ void upload_sell(wbx_sell& d, const HostSell& h, uint64_t rows, cudaStream_t s, 
     d.lane_info.upload(h.lane_info, s);
     d.rec_off.upload(h.rec_off, s);
     d.rec.upload(h.rec, s);
-    bytes += d.rec_off.bytes() + d.rec.bytes();
+    d.rslice.upload(h.rslice, s);
+    d.rpk.upload(h.rpk, s);
+    d.rpk_u4 = h.rpk.size();
+    bytes += d.rec_off.bytes() + d.rec.bytes() + d.rslice.bytes() + d.rpk.bytes();
     bytes += d.xslice_ptr.bytes() + d.xslice_len.bytes() + d.val64.bytes() + d.col.bytes() +
              d.row_len.bytes() + d.slice_ptr.bytes() + d.slice_np.bytes() + d.pk.bytes() +
              d.lane_info.bytes();
@@ -224,6 +282,9 @@ SellView view_of(const wbx_sell& m) {
     v.lane_info = m.lane_info.p;
     v.rec = m.rec.p;
     v.rec_off = m.rec_off.p;
+    v.rslice = m.rslice.p;
+    v.rpk = m.rpk.p;
+    v.rpk_u4 = m.rpk_u4;
     v.rows = static_cast<uint32_t>(m.rows);
     v.xslices = static_cast<uint32_t>(m.xslices);
     v.slices = static_cast<uint32_t>(m.slices);

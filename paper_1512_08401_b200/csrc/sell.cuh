@@ -30,6 +30,10 @@ struct SellView {
     const uint32_t* lane_info;
     const uint4* rec;          // slice records [lane_info x32][pairs] (TMA staging)
     const uint64_t* rec_off;   // uint4 offset of each record
+    // row-per-lane fp32 layout (wbx_sell::rslice / rpk)
+    const uint2* rslice;
+    const uint4* rpk;
+    uint64_t rpk_u4;
     uint32_t rows, xslices, slices;
 };
 

@@ -2479,10 +2479,30 @@ int wbx_solver_phase_ms(const wbx_solver* s, float* tau_ms, float* iters_ms) {
 int wbx_solver_tau_stats(const wbx_solver* s, double* tau, uint32_t* ref_iters, uint32_t* product_pairs) {
     if (!s || !tau || !ref_iters || !product_pairs) return WBX_INVALID_ARGUMENT;
     double out[wbx::OUT_COUNT];
-    if (cudaMemcpy(out, s->out.p, sizeof out, cudaMemcpyDeviceToHost) != cudaSuccess) return WBX_CUDA_ERROR;
+    // ordered after the solver kernels on the context's (non-blocking) stream
+    if (cudaMemcpyAsync(out, s->out.p, sizeof out, cudaMemcpyDeviceToHost, s->ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+        return WBX_CUDA_ERROR;
     *tau = out[wbx::OUT_TAU];
     *ref_iters = static_cast<uint32_t>(out[wbx::OUT_TAU_ITERS]);
     *product_pairs = static_cast<uint32_t>(out[wbx::OUT_TAU_STEPS]);
+    return WBX_OK;
+}
+
+int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
+    if (!s || !buf || len == 0) return WBX_INVALID_ARGUMENT;
+    const bool fp64 = s->cfg.precision == WBX_FP64;
+    const bool track = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
+    const char* tau = s->cfg.tau > 0.0 ? "set_tau_kernel"
+                      : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
+                      : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
+                                                   : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
+    const char* it = (s->win && !track && s->batch == 1) ? "fista_win_kernel"
+                     : s->batch == 4                      ? "fista_batch_kernel<4>"
+                     : s->batch == 8                      ? "fista_batch_kernel<8>"
+                     : fp64                               ? "fista_kernel<double>"
+                                                          : "fista_kernel<float>";
+    std::snprintf(buf, len, "%s %s", tau, it);
     return WBX_OK;
 }
 

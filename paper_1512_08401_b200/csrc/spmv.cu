@@ -88,6 +88,68 @@ __global__ void __launch_bounds__(kBlock, MINB) sell_f32_part_kernel(SellView M,
     if (r != kNoRow) y[r] = acc;
 }
 
+// Row-per-lane fp32 SpMV (the default standalone kernel): slice s = the 32 consecutive
+// sorted rows 32s..32s+31, one per lane; the lane walks its row in element order in parts
+// of H {val, col, val, col} pairs (16-B loads, 512 B per warp instruction), then the odd
+// last element. Rows of a slice have ~equal length (the compacted rows are sorted by
+// length), so the stream carries no segment padding and no per-lane row word: 8 B per
+// nonzero plus 8 B per 32 rows. The operator stream is loaded EVICT_FIRST (read once;
+// it must not push x out of L2), and each warp issues a bulk L2 prefetch of the stream
+// window PF bytes ahead of its own slice (the ranges tile the stream, so every byte is
+// prefetched once and the prefetch front runs PF bytes ahead of the compute front):
+// HBM requests are in flight without holding registers or shared memory.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int H>
+__global__ void __launch_bounds__(kBlock, 8) sell_row_kernel(SellView M, const float* __restrict__ x,
+                                                             float* __restrict__ y, uint64_t pf_u4) {
+    const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= M.xslices) return;
+    const uint2 meta = M.rslice[s];
+    const uint32_t L = meta.y, np = L >> 1;
+    if (pf_u4 != 0 && lane == 0) {
+        const uint64_t a = uint64_t(meta.x) + pf_u4;
+        uint64_t b = uint64_t(meta.x) + np * 32u + (L & 1u) * 16u + pf_u4;
+        if (b > M.rpk_u4) b = M.rpk_u4;
+        if (a < b) prefetch_l2_bulk(M.rpk + a, static_cast<uint32_t>((b - a) * 16u));
+    }
+    const uint4* p = M.rpk + meta.x + lane;
+    const uint64_t pol = l2_evict_first_policy();
+    float acc = 0.f;
+    for (uint32_t h = 0; h < np; h += H) {
+        uint4 e[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) e[j] = h + j < np ? ld_stream(p + (h + j) * kWarp, pol) : make_uint4(0, 0, 0, 0);
+        float g[2 * H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            g[2 * j] = h + j < np ? x[e[j].y] : 0.f;
+            g[2 * j + 1] = h + j < np ? x[e[j].w] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            if (h + j < np) {
+                acc = fmaf(__uint_as_float(e[j].x), g[2 * j], acc);
+                acc = fmaf(__uint_as_float(e[j].z), g[2 * j + 1], acc);
+            }
+        }
+    }
+    if (L & 1u) {
+        const uint2 t = ld_stream(reinterpret_cast<const uint2*>(M.rpk + meta.x + np * 32u) + lane, pol);
+        acc = fmaf(__uint_as_float(t.x), x[t.y], acc);
+    }
+    const uint32_t r = s * kWarp + lane;
+    if (r < M.rows) y[r] = acc;
+}
+
 // fp32 SELL SpMV with the operator stream staged by the TMA engine. Each warp walks the
 // slices gw, gw + TW, ... (TW = warps in the grid); lane 0 keeps the warp's next
 // slice records ([lane_info 32 x u32][np x 32 pairs]) in flight as 1-D bulk copies into a
@@ -216,7 +278,9 @@ int spmv_mode() {
         if (e && std::strcmp(e, "tma3") == 0) return 3;
         if (e && std::strcmp(e, "reg") == 0) return 0;
         if (e && std::strcmp(e, "half") == 0) return 4;
-        return 5;
+        if (e && std::strcmp(e, "quarter") == 0) return 5;
+        if (e && std::strcmp(e, "row4") == 0) return 7;
+        return 6;
     }();
     return mode;
 }
@@ -236,8 +300,28 @@ void launch_tma(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaS
     sell_f32_tma_kernel<NS, KS, WARPS><<<grid, WARPS * 32, smem, s>>>(v, x, y);
 }
 
-void launch_sell_f32(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s) {
-    const int mode = spmv_mode();
+// L2 prefetch distance of the row kernel (bytes ahead in the operator stream; WBX_SPMV_PF,
+// 0 disables)
+long long g_spmv_pf_bytes = -1;  // wbx_diag_set_spmv_pf (sweeps); -1: WBX_SPMV_PF or the default
+
+uint64_t spmv_pf_u4() {
+    static const uint64_t pf = [] {
+        const char* e = std::getenv("WBX_SPMV_PF");
+        const long long b = e ? std::atoll(e) : (16ll << 20);
+        return static_cast<uint64_t>(b > 0 ? b : 0) / 16u;
+    }();
+    return g_spmv_pf_bytes >= 0 ? static_cast<uint64_t>(g_spmv_pf_bytes) / 16u : pf;
+}
+
+void launch_sell_f32(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s, int mode) {
+    if (mode == 6 || mode == 7) {
+        const unsigned rb = static_cast<unsigned>((uint64_t(v.xslices) * 32 + kBlock - 1) / kBlock);
+        if (mode == 6)
+            sell_row_kernel<2><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
+        else
+            sell_row_kernel<4><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
+        return;
+    }
     const unsigned blocks = static_cast<unsigned>((uint64_t(v.slices) * 32 + kBlock - 1) / kBlock);
     if (mode == 4)
         sell_f32_part_kernel<4, 6><<<blocks, kBlock, 0, s>>>(v, x, y);
@@ -257,24 +341,25 @@ inline unsigned blocks_for(uint64_t threads) {
     return static_cast<unsigned>((threads + kBlock - 1) / kBlock);
 }
 
+// compacted scratch of the CALLING context (calls on one context are serialised; two
+// contexts sharing an operator never share scratch)
 template <typename T>
-DevBuf<T>& scratch_of(wbx_op* op, int which, uint64_t count) {
-    DevBuf<T>& b = sizeof(T) == 8 ? reinterpret_cast<DevBuf<T>&>(op->scratch64[which])
-                                  : reinterpret_cast<DevBuf<T>&>(op->scratch32[which]);
+DevBuf<T>& scratch_of(wbx_ctx* ctx, int which, uint64_t count) {
+    DevBuf<T>& b = sizeof(T) == 8 ? reinterpret_cast<DevBuf<T>&>(ctx->scratch64[which])
+                                  : reinterpret_cast<DevBuf<T>&>(ctx->scratch32[which]);
     if (b.n < count) b.alloc(count);
     return b;
 }
 
 template <typename T>
-void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
+void full_spmv(wbx_ctx* ctx, const wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
     const wbx_sell& M = transpose ? op->T : op->A;
     const uint32_t* in_idx = transpose ? op->R_glob.p : op->C_glob.p;   // gathered inputs
     const uint32_t* out_idx = transpose ? op->C_glob.p : op->R_glob.p;  // scattered outputs
     const uint32_t m_in = static_cast<uint32_t>(transpose ? op->nR : op->nC);
     const uint32_t m_out = static_cast<uint32_t>(M.rows);
-    // compacted scratch cached on the operator (calls on one context are serialised)
-    DevBuf<T>& xin = scratch_of<T>(op, 0, m_in > 0 ? m_in : 1);
-    DevBuf<T>& yout = scratch_of<T>(op, 1, m_out > 0 ? m_out : 1);
+    DevBuf<T>& xin = scratch_of<T>(ctx, 0, m_in > 0 ? m_in : 1);
+    DevBuf<T>& yout = scratch_of<T>(ctx, 1, m_out > 0 ? m_out : 1);
     WBX_CUDA(cudaMemsetAsync(y, 0, op->n * sizeof(T), s));
     if (m_out > 0) {
         gather_kernel<T><<<blocks_for(m_in), kBlock, 0, s>>>(x, in_idx, m_in, xin.p);
@@ -282,40 +367,42 @@ void full_spmv(wbx_op* op, int transpose, const T* x, T* y, cudaStream_t s) {
         if constexpr (sizeof(T) == 8)
             sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, xin.p, yout.p);
         else
-            launch_sell_f32(op->ctx, v, xin.p, yout.p, s);
+            launch_sell_f32(ctx, v, xin.p, yout.p, s, spmv_mode());
         scatter_kernel<T><<<blocks_for(m_out), kBlock, 0, s>>>(yout.p, out_idx, m_out, y);
-        count_launch(op->ctx, 3);
+        count_launch(ctx, 3);
         WBX_CUDA(cudaGetLastError());
     }
 }
 
 }  // namespace
 
-void spmv_full_fp64(wbx_op* op, int transpose, const double* x_dev, double* y_dev, cudaStream_t s) {
-    full_spmv<double>(op, transpose, x_dev, y_dev, s);
+void set_spmv_pf_bytes(long long b) { g_spmv_pf_bytes = b; }
+
+void spmv_full_fp64(wbx_ctx* ctx, const wbx_op* op, int transpose, const double* x_dev, double* y_dev) {
+    full_spmv<double>(ctx, op, transpose, x_dev, y_dev, ctx->stream);
 }
 
-void spmv_full_fp32(wbx_op* op, int transpose, const float* x_dev, float* y_dev, cudaStream_t s) {
+void spmv_full_fp32(wbx_ctx* ctx, const wbx_op* op, int transpose, const float* x_dev, float* y_dev) {
     if (!(op->A.seg_ok && op->T.seg_ok))
         fail(WBX_TOO_LARGE, "operator rows longer than 496 nonzeros: fp32 layout unavailable, use precision 64");
-    full_spmv<float>(op, transpose, x_dev, y_dev, s);
+    full_spmv<float>(ctx, op, transpose, x_dev, y_dev, ctx->stream);
 }
 
 // Compacted-space SpMV used by the kernel benchmark (bench.py --kernel spmv):
 // y[R] = A x[C] with both vectors already compacted.
 template <typename T>
-void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s) {
+void spmv_compact(wbx_ctx* ctx, const wbx_sell& M, const T* x, T* y, cudaStream_t s, int mode) {
     if (M.rows == 0) return;
     const SellView v = view_of(M);
     if constexpr (sizeof(T) == 8)
         sell_f64_kernel<<<blocks_for(uint64_t(v.xslices) * 32), kBlock, 0, s>>>(v, x, y);
     else
-        launch_sell_f32(ctx, v, x, y, s);
+        launch_sell_f32(ctx, v, x, y, s, mode < 0 ? spmv_mode() : mode);
     count_launch(ctx);
     WBX_CUDA(cudaGetLastError());
 }
 
-template void spmv_compact<float>(wbx_ctx*, const wbx_sell&, const float*, float*, cudaStream_t);
-template void spmv_compact<double>(wbx_ctx*, const wbx_sell&, const double*, double*, cudaStream_t);
+template void spmv_compact<float>(wbx_ctx*, const wbx_sell&, const float*, float*, cudaStream_t, int);
+template void spmv_compact<double>(wbx_ctx*, const wbx_sell&, const double*, double*, cudaStream_t, int);
 
 }  // namespace wbx

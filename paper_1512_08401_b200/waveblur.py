@@ -227,7 +227,7 @@ class WaveletBasis:  # wavelet.hpp:68-74, plus its device residency (wbx_basis)
         self.filters = filters
         self.layout = layout
         self._ctx = ctx
-        self._handle = None
+        self._handles = {}  # Context -> native handle
 
     def dims(self):
         return self.layout.dims
@@ -236,22 +236,27 @@ class WaveletBasis:  # wavelet.hpp:68-74, plus its device residency (wbx_basis)
         return self.layout.J
 
     def device(self, ctx: Optional[Context] = None):
+        """The native basis on `ctx`. One handle per context, created on first use and kept
+        until this object dies: a solver built on a handle can never see it freed (a later
+        call on another context creates a second handle instead of replacing the first)."""
         ctx = ctx or self._ctx or default_context()
-        if self._handle is None or self._ctx is not ctx:
+        h = self._handles.get(ctx)
+        if h is None:
             d = np.array(self.layout.dims, dtype=np.uint64)
             h = C.c_void_p()
             _check(lib.wbx_basis_create(ctx.handle, int(self.filters.family), self.filters.order,
                                         len(self.layout.dims), _u64ptr(d), self.layout.J, C.byref(h)))
-            self._release()
-            self._handle, self._ctx = h, ctx
-        return self._handle
+            self._handles[ctx] = h
+            if self._ctx is None:
+                self._ctx = ctx
+        return h
 
     def _release(self):
         if lib is None:  # interpreter shutdown: the library is already gone
             return
-        if self._handle is not None:
-            lib.wbx_basis_destroy(self._handle)
-            self._handle = None
+        for h in self._handles.values():
+            lib.wbx_basis_destroy(h)
+        self._handles.clear()
 
     def __del__(self):
         if lib is None:  # interpreter shutdown: the library is already gone
@@ -322,23 +327,27 @@ class SparseOperator:
         self.layout = layout
         self.family = FilterFamily(family)
         self.order = int(order)
-        self._dev = None
+        self._devs = {}  # Context -> native handle
         self._ctx = None
 
     def nnz(self) -> int:
         return int(self.values.size)
 
     def device(self, ctx: Optional[Context] = None):
-        ctx = ctx or default_context()
-        if self._dev is None or self._ctx is not ctx:
+        """The device layouts on `ctx` (wbx_op_create). One handle per context, kept until
+        this object dies, so solvers and Deblurrers built on a handle never see it freed."""
+        ctx = ctx or self._ctx or default_context()
+        h = self._devs.get(ctx)
+        if h is None:
             if self.row_offsets.size != self.n + 1:
                 raise ShapeMismatch("row_offsets must have n+1 entries")
             h = C.c_void_p()
             _check(lib.wbx_op_create(ctx.handle, self.n, _u64ptr(self.row_offsets),
                                      _u32ptr(self.col_indices), _dptr(self.values), C.byref(h)))
-            self._release()
-            self._dev, self._ctx = h, ctx
-        return self._dev
+            self._devs[ctx] = h
+            if self._ctx is None:
+                self._ctx = ctx
+        return h
 
     def info(self, ctx: Optional[Context] = None) -> N.wbx_op_info:
         inf = N.wbx_op_info()
@@ -348,9 +357,9 @@ class SparseOperator:
     def _release(self):
         if lib is None:  # interpreter shutdown: the library is already gone
             return
-        if self._dev is not None:
-            lib.wbx_op_destroy(self._dev)
-            self._dev = None
+        for h in self._devs.values():
+            lib.wbx_op_destroy(h)
+        self._devs.clear()
 
     def __del__(self):
         if lib is None:  # interpreter shutdown: the library is already gone
@@ -1029,6 +1038,12 @@ class Deblurrer:
         t, i = C.c_float(), C.c_float()
         _check(lib.wbx_solver_phase_ms(self.handle, C.byref(t), C.byref(i)))
         return float(t.value), float(i.value)
+
+    def kernels(self):
+        """(step-estimate kernel, iteration kernel) names of the engine this solver runs."""
+        buf = C.create_string_buffer(256)
+        _check(lib.wbx_solver_kernels(self.handle, buf, 256))
+        return tuple(buf.value.decode().split(" ", 1))
 
     def tau_stats(self):
         """(tau, the reference's power-iteration count, operator product pairs spent) of the

@@ -174,12 +174,13 @@ def test_prox_bitwise_vs_oracle():
     assert np.array_equal(z, O.prox(z0, 0.3, w, 0.7, p))
 
 
-@pytest.mark.parametrize("gram", ["device", "host"])
+@pytest.mark.parametrize("cap", ["2048", "32"])
 @pytest.mark.parametrize("name", ["c1_db4_256", "s64_sym6_spai", "s128_1d_sym6"])
-def test_preconditioner_bitwise_vs_reference(golden, monkeypatch, name, gram):
-    """Gram diagonals on the device (no host fallback allowed) and on the host: SPAI and
-    the Gram diagonals bitwise equal to the reference / oracle."""
-    monkeypatch.setenv("WBX_GRAM", gram)
+def test_preconditioner_bitwise_vs_reference(golden, monkeypatch, name, cap):
+    """Gram diagonals on the device (there is no host path): SPAI and the Gram diagonals
+    bitwise equal to the reference / oracle, with the default shared-memory tables and with
+    32-slot tables, which sends most columns through the global-memory second pass."""
+    monkeypatch.setenv("WBX_GRAM_CAP", cap)
     g = golden(name)
     op = g.operator()
     P = precond_of(g, op)
