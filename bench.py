@@ -95,6 +95,7 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._stop = threading.Event()
+        self._ready = threading.Event()   # set after the first sample (NVML init is slow)
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
@@ -106,13 +107,16 @@ class ClockSampler:
             get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
             bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-            while not self._stop.is_set():
+            while True:  # at least one sample, and one more after the timed region ends
+                stop = self._stop.is_set()
                 sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                 r = get_reasons(h)
                 self.samples.append([str(self.device), str(sm), str(mx), ""] +
                                     ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.005)
-            return
+                self._ready.set()
+                if stop:
+                    return
+                self._stop.wait(0.002)
         except Exception:
             pass
         while not self._stop.is_set():
@@ -124,10 +128,12 @@ class ClockSampler:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t.start()
+        self._ready.wait(timeout=30)  # sampling is live before the timed region starts
         return self
 
     def __exit__(self, *exc):
@@ -445,6 +451,26 @@ def extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, tau, flush)
     out["c2_fp64_bitwise"] = {"ms_per_deblur": round(_time_dev(d64, torch, stream, flush, u0_dev, out_dev, reps=3), 3),
                               "kernels": list(d64.kernels())}
     del d64
+    # the reference's own API call fista(problem, P, cfg) with its per-iteration energies (what
+    # the drop-in binding forwards: wbx_pgd with track_energy, host fp64 vectors in and out,
+    # tau inside), wall time; its iteration kernel
+    x0 = W.analyze(u0, basis, ctx).values
+    prob = W.DeblurProblem(W.SparseThetaOp(op, ctx), x0, w, 1e-4)
+    fcfg = W.SolverConfig(max_iters=ITERS, precision=32, track_energy=True)
+    W.fista(prob, P, fcfg, ctx)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rep = W.fista(prob, P, fcfg, ctx)
+        ts.append(1e3 * (time.perf_counter() - t0))
+    dt = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=True), ctx)
+    out["c2_fista_api_tracked"] = {"ms_wall": round(float(np.median(ts)), 3), "iters_used": int(rep.iters_used),
+                                   "energies": len(rep.energies), "kernels": list(dt.kernels()),
+                                   "ms_deblur_dev_tracked": round(_time_dev(dt, torch, stream, flush, u0_dev,
+                                                                            out_dev, reps=3), 4),
+                                   "api": "waveblur.fista -> wbx_pgd (host fp64 x0/x_final, energies every "
+                                          "iteration, tau inside)"}
+    del dt
     # C3: 1024^2 spatially varying blur (sigma 2.5 -> 7.5 px down the image)
     lad = W.SigmaLadder.from_npz(np.load(ROOT / "tests" / "golden" / "c3_ladder_1024.npz"))
     opv = W.theta_varying(lad, 2.5, 7.5)

@@ -20,12 +20,12 @@ int wbx_diag_stream_gbs(int device, int mode, uint64_t bytes, int reps, int chun
 int wbx_diag_slice_profile(double* out);
 /* The fp32 SELL kernel of wbx_spmv_compact_dev selected explicitly (tests compare the
  * variants; WBX_SPMV selects the default once per process): mode 0 reg, 1 tma1, 2 tma2,
- * 3 tma3, 4 half, 5 quarter (segmented layout, one fma order), 6 row (default), 7 row4
- * (row-per-lane layout, element order). Device pointers, compacted spaces, async. */
+ * 3 tma3, 4 half, 5 quarter (segmented layout, one fma order), 6 row2, 7 row (default),
+ * 8 row8 (row-per-lane layout, element order). Device pointers, compacted spaces, async. */
 struct wbx_ctx;
 struct wbx_op;
 /* L2 prefetch distance (bytes ahead in the operator stream) of the row kernel; -1 restores
- * the default (WBX_SPMV_PF or 16 MiB), 0 disables the prefetch. */
+ * the default (WBX_SPMV_PF, else 0 = no prefetch: measured slower on B200). */
 int wbx_diag_set_spmv_pf(long long bytes);
 int wbx_diag_spmv_compact_mode(struct wbx_ctx* ctx, const struct wbx_op* op, int transpose, int mode,
                                const float* x_dev, float* y_dev);

@@ -3,13 +3,16 @@
 // Defines the reference's hot-path functions (wavelet.hpp:88,91; theta.hpp:83-89;
 // precond.hpp:26-34; solver.hpp:86-105; SparseThetaOp::apply/apply_adjoint) on top of the
 // C ABI in include/wbx.h. The reference's CPU definitions stay in the library under a
-// `*_host` name; operators that are not a SparseThetaOp (ExactThetaOp,
-// user ThetaOps) keep running there. WBX_BACKEND_PRECISION=32 selects the fp32 hot path;
-// the default is the fp64 mode, bitwise equal to the reference.
+// `*_host` name. SparseThetaOp and ExactThetaOp (solver.cpp:11-31) run on
+// the device (ExactThetaOp::apply/apply_adjoint/ops_per_pixel are defined here, so the exact
+// operator's FFT route, its estimate_step and its fista/ista run through wbx_exact_*); only
+// user-defined ThetaOps keep the host loop. WBX_BACKEND_PRECISION=32 selects the fp32 hot
+// path; the default is the fp64 mode, bitwise equal to the reference.
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <list>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <vector>
@@ -129,16 +132,70 @@ const SparseOperator* sparse_of(const ThetaOp* op) {
     return s ? &s->sparse() : nullptr;
 }
 
+// ExactThetaOp keeps its PSF and basis private (solver.hpp:41-52); its member functions,
+// defined below, register them here so that the free functions (estimate_step, fista) can
+// route an exact operator to the device.
+struct ExactParts {
+    const Psf* psf;
+    const WaveletBasis* basis;
+};
+std::map<const ExactThetaOp*, ExactParts>& exact_registry() {
+    static std::map<const ExactThetaOp*, ExactParts> m;
+    return m;
+}
+
+// the device exact operator of (PSF kernel, basis), cached by content (building it plans
+// the FFTs and uploads the kernel spectrum)
+wbx_exact_op* device_exact(const Psf& psf, const WaveletBasis& b) {
+    const Image& k = psf.kernel;
+    if (k.dims != b.dims()) throw ShapeMismatch("ExactThetaOp: PSF and basis dims differ");
+    uint64_t key = 0xcbf29ce484222325ULL;
+    mix(key, k.v.data(), k.v.size() * sizeof(double));
+    const auto fam = static_cast<uint32_t>(b.filters.family);
+    const uint32_t meta[3] = {fam, static_cast<uint32_t>(b.filters.order), static_cast<uint32_t>(b.levels())};
+    mix(key, meta, sizeof meta);
+    for (std::size_t d : b.dims()) {
+        const uint64_t dd = d;
+        mix(key, &dd, sizeof dd);
+    }
+    struct Entry {
+        uint64_t key;
+        wbx_exact_op* e;
+    };
+    static std::list<Entry> cache;
+    for (auto it = cache.begin(); it != cache.end(); ++it)
+        if (it->key == key) {
+            cache.splice(cache.begin(), cache, it);
+            return cache.front().e;
+        }
+    wbx_exact_op* e = nullptr;
+    check(wbx_exact_op_create(ctx(), device_basis(b), k.v.data(), &e));
+    cache.push_front({key, e});
+    if (cache.size() > 4) {
+        wbx_exact_op_destroy(cache.back().e);
+        cache.pop_back();
+    }
+    return e;
+}
+
+const ExactParts* exact_of(const ThetaOp* op) {
+    const auto* e = dynamic_cast<const ExactThetaOp*>(op);
+    if (!e) return nullptr;
+    e->ops_per_pixel();  // (re)registers this operator's PSF and basis
+    return &exact_registry().at(e);
+}
+
 void require_len(std::size_t got, std::size_t want, const char* what) {
     if (got != want) throw ShapeMismatch(std::string(what) + ": vector length mismatch");
 }
 
 SolveReport pgd(const DeblurProblem& p, const DiagonalPreconditioner& P, const SolverConfig& c, int accelerate) {
     const SparseOperator* s = sparse_of(p.op);
-    if (!s) return accelerate ? fista_host(p, P, c) : ista_host(p, P, c);
-    require_len(p.x0.size(), s->n, "run_pgd");
-    require_len(p.weights.size(), s->n, "run_pgd");
-    require_len(P.p.size(), s->n, "run_pgd");
+    const ExactParts* ex = s ? nullptr : exact_of(p.op);
+    if (!s && !ex) return accelerate ? fista_host(p, P, c) : ista_host(p, P, c);
+    const std::size_t n = p.op->dim();
+    if (p.x0.size() != n || p.weights.size() != n || P.p.size() != n)
+        throw ShapeMismatch("solver: inconsistent problem dimensions");  // solver.cpp:106-107
     std::lock_guard<std::recursive_mutex> g(mu);
     wbx_solver_cfg cfg;
     wbx_solver_cfg_default(&cfg);
@@ -151,19 +208,25 @@ SolveReport pgd(const DeblurProblem& p, const DiagonalPreconditioner& P, const S
     cfg.track_energy = 1;  // SolveReport always carries E(x_k)
     cfg.precision = precision();
     SolveReport r;
-    r.x_final.resize(s->n);
+    r.x_final.resize(n);
     r.energies.resize(c.max_iters);
     std::vector<uint64_t> supp(c.max_iters);
     wbx_report rep{};
     rep.energies = r.energies.data();
     rep.support_sizes = supp.data();
-    check(wbx_pgd(ctx(), device_op(*s), p.x0.data(), p.weights.data(), p.lambda, P.p.data(), &cfg, accelerate,
-                  r.x_final.data(), &rep));
+    if (s) {
+        check(wbx_pgd(ctx(), device_op(*s), p.x0.data(), p.weights.data(), p.lambda, P.p.data(), &cfg, accelerate,
+                      r.x_final.data(), &rep));
+        r.ops_per_pixel_per_iter = rep.ops_per_pixel_per_iter;
+    } else {  // the exact FFT operator: fp64, the reference's expressions (exact_op.cu)
+        check(wbx_pgd_exact(device_exact(*ex->psf, *ex->basis), p.x0.data(), p.weights.data(), p.lambda,
+                            P.p.data(), &cfg, accelerate, r.x_final.data(), &rep));
+        r.ops_per_pixel_per_iter = p.op->ops_per_pixel();
+    }
     r.iters_used = rep.iters_used;
     r.energies.resize(rep.iters_used);
     if (c.track_support) r.support_sizes.assign(supp.begin(), supp.begin() + rep.iters_used);
     r.wall_time_s = rep.wall_time_s;
-    r.ops_per_pixel_per_iter = rep.ops_per_pixel_per_iter;
     r.initial_energy = rep.initial_energy;
     return r;
 }
@@ -222,6 +285,30 @@ std::vector<double> SparseThetaOp::apply_adjoint(const std::vector<double>& x) c
     return spmv_t(sparse(), x);
 }
 
+// ExactThetaOp (solver.cpp:21-31): analyze(convolve(synthesize(x), psf)) and the adjoint
+// with the conjugate kernel spectrum, on the device in the reference's arithmetic (bitwise)
+double ExactThetaOp::ops_per_pixel() const {
+    std::lock_guard<std::recursive_mutex> g(mu);
+    exact_registry()[this] = ExactParts{&psf_, basis_};
+    return exact_ops_per_pixel(*basis_);
+}
+
+std::vector<double> ExactThetaOp::apply(const std::vector<double>& x) const {
+    require_len(x.size(), basis_->layout.total(), "ExactThetaOp::apply");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> y(x.size());
+    check(wbx_exact_apply(device_exact(psf_, *basis_), 0, x.data(), y.data()));
+    return y;
+}
+
+std::vector<double> ExactThetaOp::apply_adjoint(const std::vector<double>& x) const {
+    require_len(x.size(), basis_->layout.total(), "ExactThetaOp::apply_adjoint");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    std::vector<double> y(x.size());
+    check(wbx_exact_apply(device_exact(psf_, *basis_), 1, x.data(), y.data()));
+    return y;
+}
+
 GramDiagonals gram_diagonals(const SparseOperator& op, std::size_t nnz_cap_factor) {
     std::lock_guard<std::recursive_mutex> g(mu);
     GramDiagonals d;
@@ -269,12 +356,16 @@ std::vector<double> prox_weighted_l1_P(const std::vector<double>& z0, double tau
 
 double estimate_step(const ThetaOp& op, const DiagonalPreconditioner& P, double step_safety) {
     const SparseOperator* s = sparse_of(&op);
-    if (!s) return estimate_step_host(op, P, step_safety);
-    require_len(P.p.size(), s->n, "estimate_step");
+    const ExactParts* ex = s ? nullptr : exact_of(&op);
+    if (!s && !ex) return estimate_step_host(op, P, step_safety);
+    require_len(P.p.size(), op.dim(), "estimate_step");
     std::lock_guard<std::recursive_mutex> g(mu);
     double tau = 0.0;
     uint32_t iters = 0;
-    check(wbx_estimate_step(ctx(), device_op(*s), P.p.data(), step_safety, &tau, &iters));
+    if (s)
+        check(wbx_estimate_step(ctx(), device_op(*s), P.p.data(), step_safety, &tau, &iters));
+    else
+        check(wbx_estimate_step_exact(device_exact(*ex->psf, *ex->basis), P.p.data(), step_safety, &tau, &iters));
     return tau;
 }
 

@@ -4,8 +4,9 @@
 # Emulates the maintainer's build of INTEGRATION.md §2 on an unmodified reference object:
 # the reference's CPU definitions of the functions integration/wbx_backend.cpp routes to
 # libwbx are renamed to `<name>_host` (the backend keeps calling them for operators that
-# are not a SparseThetaOp), and SparseThetaOp::apply/apply_adjoint become weak so the
-# backend's definitions (and the vtable slots) win at link time.
+# are not device operators), and SparseThetaOp::apply/apply_adjoint and
+# ExactThetaOp::apply/apply_adjoint/ops_per_pixel become weak so the backend's definitions
+# (and the vtable slots) win at link time.
 set -euo pipefail
 in=$1
 out=$2
@@ -19,7 +20,7 @@ while read -r _ kind sym; do
         prefix="_ZN8waveblur${#name}${name}"
         [[ $sym == "$prefix"* ]] || continue
         args+=(--redefine-sym "$sym=_ZN8waveblur$((${#name} + 5))${name}_host${sym#"$prefix"}")
-    elif [[ $dem =~ ^waveblur::SparseThetaOp::apply(_adjoint)?\( ]]; then
+    elif [[ $dem =~ ^waveblur::SparseThetaOp::apply(_adjoint)?\( || $dem =~ ^waveblur::ExactThetaOp::(apply|apply_adjoint|ops_per_pixel)\( ]]; then
         args+=(--weaken-symbol "$sym")
     fi
 done < <(nm --defined-only "$in")

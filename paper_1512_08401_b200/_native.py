@@ -6,6 +6,7 @@ importing this module raises, and every product entry point fails loudly.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 from pathlib import Path
@@ -167,6 +168,16 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
+
+# Interpreter exit: native objects are NOT released from __del__ any more (finalisation order is
+# arbitrary at exit, so an object could otherwise be released after the context it lives on;
+# the process exit frees the device anyway).
+_SHUTDOWN = [False]
+atexit.register(lambda: _SHUTDOWN.__setitem__(0, True))
+
+
+def alive() -> bool:
+    return not _SHUTDOWN[0]
 
 
 def last_error() -> str:

@@ -384,7 +384,7 @@ int wbx_diag_spmv_compact_mode(wbx_ctx* ctx, const wbx_op* op, int transpose, in
     return guard([&] {
         need(ctx, "ctx");
         need(op, "op");
-        if (mode < 0 || mode > 7) wbx::fail(WBX_BAD_SPEC, "unknown SpMV kernel mode");
+        if (mode < 0 || mode > 8) wbx::fail(WBX_BAD_SPEC, "unknown SpMV kernel mode");
         if (!(op->A.seg_ok && op->T.seg_ok)) wbx::fail(WBX_TOO_LARGE, "fp32 layout unavailable");
         wbx::spmv_compact<float>(ctx, transpose ? op->T : op->A, x_dev, y_dev, ctx->stream, mode);
     });

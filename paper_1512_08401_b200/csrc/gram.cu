@@ -15,6 +15,7 @@
 // same operation order.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.hpp"
@@ -26,14 +27,17 @@ constexpr int kGramWarps = 4;            // warps per CTA
 constexpr uint32_t kGramCap = 2048;      // shared-memory table slots per warp (power of two)
 constexpr uint32_t kEmpty = 0xffffffffu;
 
-// one warp's accumulator table: key / val / first-touch order, `cap` slots (power of two)
+// one warp's accumulator table: key / val / first-touch order, `cap` slots (power of two);
+// the shared-memory tables keep 16-bit order entries (14 B per slot: 2 CTAs of 4 warps per SM)
+template <typename ORD>
 struct GramTab {
     uint32_t* key;
     double* val;
-    uint32_t* order;
+    ORD* order;
     uint32_t cap;
 };
 
+template <typename ORD>
 __global__ void __launch_bounds__(kGramWarps * 32) gram_kernel(uint64_t ncols, const uint32_t* __restrict__ cols,
                                                               const uint64_t* __restrict__ rp,
                                                               const uint32_t* __restrict__ cl,
@@ -49,17 +53,17 @@ __global__ void __launch_bounds__(kGramWarps * 32) gram_kernel(uint64_t ncols, c
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kGramWarps + warp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kGramWarps;
-    GramTab S;
-    if (gkey == nullptr) {  // shared-memory tables: [key x cap][val x cap][order x cap] per warp
-        unsigned char* b = smem_raw + static_cast<size_t>(warp) * smem_cap * 16u;
+    GramTab<ORD> S;
+    if (gkey == nullptr) {  // shared-memory tables: [val x cap][key x cap][order x cap] per warp
+        unsigned char* b = smem_raw + static_cast<size_t>(warp) * smem_cap * (12u + sizeof(ORD));
         S.val = reinterpret_cast<double*>(b);
         S.key = reinterpret_cast<uint32_t*>(b + static_cast<size_t>(smem_cap) * 8u);
-        S.order = S.key + smem_cap;
+        S.order = reinterpret_cast<ORD*>(S.key + smem_cap);
         S.cap = smem_cap;
     } else {  // second pass: this warp's slice of the global tables
         S.key = gkey + gw * gcap;
         S.val = gval + gw * gcap;
-        S.order = gorder + gw * gcap;
+        S.order = reinterpret_cast<ORD*>(gorder) + gw * gcap;
         S.cap = gcap;
     }
     for (uint32_t t = lane; t < S.cap; t += 32) {
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(kGramWarps * 32) gram_kernel(uint64_t ncols, c
                 }
                 // first touches appended in lane (= ascending column) order
                 const unsigned fm = __ballot_sync(0xffffffffu, act && fresh);
-                if (act && fresh) S.order[nlist + __popc(fm & ((1u << lane) - 1u))] = slot;
+                if (act && fresh) S.order[nlist + __popc(fm & ((1u << lane) - 1u))] = static_cast<ORD>(slot);
                 nlist += __popc(fm);
                 if (act) {
                     const double old = S.val[slot];
@@ -202,11 +206,11 @@ void gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* di
         const long v = std::atol(e);
         if (v >= 32 && v <= static_cast<long>(kGramCap) && (v & (v - 1)) == 0) cap = static_cast<uint32_t>(v);
     }
-    const unsigned smem = kGramWarps * cap * 16u;
-    WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(gram_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kGramWarps * kGramCap * 16u)));
+    const unsigned smem = kGramWarps * cap * 14u;
+    WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(gram_kernel<uint16_t>),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGramWarps * kGramCap * 14u)));
     const unsigned grid = 2u * static_cast<unsigned>(ctx->num_sms);
-    gram_kernel<<<grid, kGramWarps * 32, smem, st>>>(n, nullptr, d_rp.p, d_cl.p, d_vl.p, d_toff.p, d_trow.p, d_tval.p,
+    gram_kernel<uint16_t><<<grid, kGramWarps * 32, smem, st>>>(n, nullptr, d_rp.p, d_cl.p, d_vl.p, d_toff.p, d_trow.p, d_tval.p,
                                                      d_m.p, d_m2.p, d_cnt.p, cap, nullptr, nullptr, nullptr, 0, d_ovf.p,
                                                      d_novf.p);
     count_launch(ctx);
@@ -236,7 +240,10 @@ void gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* di
         const uint64_t tw = uint64_t(g2) * kGramWarps;
         DevBuf<uint32_t> gkey(tw * gcap), gorder(tw * gcap);
         DevBuf<double> gval(tw * gcap);
-        gram_kernel<<<g2, kGramWarps * 32, 0, st>>>(novf, d_ovf.p, d_rp.p, d_cl.p, d_vl.p, d_toff.p, d_trow.p, d_tval.p,
+        if (std::getenv("WBX_VERBOSE"))
+            std::fprintf(stderr, "wbx gram: %u columns overflow the shared tables; global pass, %llu-slot tables\n",
+                         novf, static_cast<unsigned long long>(gcap));
+        gram_kernel<uint32_t><<<g2, kGramWarps * 32, 0, st>>>(novf, d_ovf.p, d_rp.p, d_cl.p, d_vl.p, d_toff.p, d_trow.p, d_tval.p,
                                                     d_m.p, d_m2.p, d_cnt.p, 0, gkey.p, gval.p, gorder.p,
                                                     static_cast<uint32_t>(gcap), d_ovf.p, d_novf.p);
         count_launch(ctx);

@@ -5,6 +5,9 @@
 
 #include <cstdint>
 #include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -66,6 +69,22 @@ struct DevBuf {
         if (n < h.size()) alloc(h.size());
         upload(h.data(), h.size(), s);
     }
+};
+
+// winlayout.cu: per-CTA window layout of one operator side (win.cuh)
+struct WinSide {
+    uint32_t G = 0, max_u = 0, max_win = 0, max_rows = 0, max_slices = 0, max_dict = 0;
+    uint32_t src_len = 0;  // length of the gathered vector (set by the solver)
+    DevBuf<uint32_t> u_off, u_idx, s_off, r_off, d_off;
+    DevBuf<uint16_t> u_slot;
+    DevBuf<uint4> s_tab, rec;
+    DevBuf<float> d_val;
+    uint64_t bytes = 0;
+};
+// both sides for one grid size G; ok == false when a window exceeds 16-bit local indices
+struct WinPair {
+    WinSide A, T;
+    bool ok = false;
 };
 
 }  // namespace wbx
@@ -154,6 +173,10 @@ struct wbx_op {
     std::vector<uint32_t> h_col;
     std::vector<double> h_val;
     uint64_t device_bytes = 0;
+    // window layouts per solver grid size, built once per operator and shared by every solver
+    // on it (a host loop calling fista() on one operator pays the layout build once)
+    mutable std::mutex win_mu;
+    mutable std::map<uint32_t, std::shared_ptr<wbx::WinPair>> win_cache;
 };
 
 namespace wbx {
@@ -190,16 +213,7 @@ void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint
                 const std::function<void(uint64_t, uint64_t, uint32_t&, double&)>& get, cudaStream_t s,
                 uint64_t& bytes);
 
-// winlayout.cu: per-CTA window layout of one operator side (win.cuh)
-struct WinSide {
-    uint32_t G = 0, max_u = 0, max_win = 0, max_rows = 0, max_slices = 0, max_dict = 0;
-    uint32_t src_len = 0;  // length of the gathered vector (set by the solver)
-    DevBuf<uint32_t> u_off, u_idx, s_off, r_off, d_off;
-    DevBuf<uint16_t> u_slot;
-    DevBuf<uint4> s_tab, rec;
-    DevBuf<float> d_val;
-    uint64_t bytes = 0;
-};
+// winlayout.cu: per-CTA window layout of one operator side (WinSide, above)
 void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side);  // side 'A' or 'T'
 struct WinView;
 WinView view_of(const WinSide& w);

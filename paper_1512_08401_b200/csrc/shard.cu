@@ -661,8 +661,9 @@ int wbx_shard_setup(wbx_shard* s, const double* p, const double* w, double lambd
         s->thr.alloc(nC);
         s->wv.alloc(nC);
         s->x0R.alloc(std::max<uint64_t>(1, s->rhi - s->rlo));
-        s->part.alloc(2 * std::max<uint64_t>(wbx::blocks_for(uint64_t(s->T.slices) * 32),
-                                             2 * static_cast<uint64_t>(s->ctx->num_sms)));
+        // per-block partials of the reductions: every launch's grid is capped at 8 CTAs per SM
+        // (power / Lanczos phases on either side) or is 2 per SM (init)
+        s->part.alloc(2 * 8 * static_cast<uint64_t>(s->ctx->num_sms));
         s->lambda = lambda;
         s->max_iters = max_iters;
         WBX_CUDA(cudaStreamSynchronize(st));

@@ -1256,6 +1256,168 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(Sol
     for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
 }
 
+// Sum of three sets of G per-CTA partials in a fixed order (identical in every CTA); all threads.
+__device__ __forceinline__ void cta_sum3(const double* p0, const double* p1, const double* p2, unsigned G,
+                                         double* red3, double (&out)[3]) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (unsigned i = threadIdx.x; i < G; i += kWinBlock) {
+        s0 += p0[i];
+        s1 += p1[i];
+        s2 += p2[i];
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((threadIdx.x & 31) == 0) {
+        red3[3 * (threadIdx.x >> 5) + 0] = s0;
+        red3[3 * (threadIdx.x >> 5) + 1] = s1;
+        red3[3 * (threadIdx.x >> 5) + 2] = s2;
+    }
+    __syncthreads();
+    out[0] = out[1] = out[2] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kWinWarps; ++k) {
+        out[0] += red3[3 * k + 0];
+        out[1] += red3[3 * k + 1];
+        out[2] += red3[3 * k + 2];
+    }
+    __syncthreads();
+}
+
+// block partial (fixed tree) of v -> dst[blockIdx.x]; all threads
+__device__ __forceinline__ void win_block_partial(double v, double* dst, double* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < kWinWarps; ++k) t += red[k];
+        dst[blockIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// FISTA / ISTA on the window engine WITH the reference's per-iteration bookkeeping
+// (run_pgd, solver.cpp:118-150): E(x_0), E(x_k) and the support size every iteration, the
+// NonFiniteEnergy check and the ref_energy stopping rule — still two operator products per
+// iteration. The reference spends a third SpMV on energy(x_k) (Theta x_k, solver.cpp:44-55);
+// here Theta x_k comes by linearity from the phase-A product of the next iteration:
+//   y_k = x_k + beta_k (x_k - x_k-1)  =>  Theta x_k = (Theta y_k + beta_k Theta x_k-1) / (1 + beta_k),
+// kept per own row of Theta in shared memory (u, next to x0). So E(x_k) is complete after phase
+// A of iteration k+1 (one phase later): the stopping decision is taken there, before phase T
+// overwrites x_k (x_prev in the CTA state). Every CTA sums the same per-CTA partials in the
+// same order, so all take the same decision without further communication.
+// Decoupled coordinates (empty Theta column) are tracked by decoupled_kernel (dec_reg/dec_supp).
+template <bool DICT>
+__global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_track_kernel(SolveArgs a) {
+    __shared__ double smem[kWinWarps + 1];
+    __shared__ double red[3 * kWinWarps];
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    const uint64_t gthread = static_cast<uint64_t>(blockIdx.x) * kWinBlock + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
+    const unsigned G = gridDim.x;
+    const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
+    Epoch epoch{epoch0, epoch0};
+    float* yC = static_cast<float*>(a.yC);
+    float* res = static_cast<float*>(a.res);
+    const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
+    const WinSmem ws = win_smem_init<8, 16>(dsmem, a);
+    float* win = static_cast<float*>(ws.win);
+    float2* ra = static_cast<float2*>(ws.ownA);  // {x0, Theta x_k-1} of the CTA's Theta rows
+    float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) {
+        const uint32_t c = ws.rT0 + i;
+        const float v = static_cast<float>(a.x0_full[a.C_glob[c]]);
+        yC[c] = v;
+        cs[i] = make_float4(v, v, static_cast<float>(tau / a.pC[c]),
+                            static_cast<float>(thr_exact(tau, a.lambda, a.wC[c], a.pC[c])));
+    }
+    for (uint32_t i = threadIdx.x; i < ws.nrA; i += kWinBlock)
+        ra[i] = make_float2(static_cast<float>(a.x0_full[a.R_glob[ws.rA0 + i]]), 0.f);
+    // constant parts of the energy: sum of x0^2 over rows outside R (Theta x is 0 there) and
+    // lambda-free sum of w |x0| over every coordinate (E(x_0))
+    double e0s[2] = {0.0, 0.0};
+    for (uint64_t i = gthread; i < a.n; i += nthreads) {
+        const double x0 = a.x0_full[i];
+        if (!bit_set(a.isR, i)) e0s[0] += x0 * x0;
+        e0s[1] += a.w_full[i] * fabs(x0);
+    }
+    grid_sync_reduce<2, kWinBlock>(a.sync, epoch, e0s, smem);  // (also: yC complete)
+    const double quad_nonR = e0s[0];
+    double stop_gap = 0.0;
+    // per-CTA partials, after the barrier-reduction slots (which other CTAs may still be reading
+    // when a fast CTA starts phase A): [G] quadratic part of phase A; [2][G] w|x| and support of
+    // phase T, double-buffered by iteration parity (read after the next A barrier)
+    double* const tp = a.sync.part + static_cast<uint64_t>(2 * kRedSlots) * G;
+    double* const q_part = tp;
+    auto reg_part = [&](int k) { return tp + static_cast<uint64_t>(1 + 2 * (k & 1)) * G; };
+    auto sup_part = [&](int k) { return tp + static_cast<uint64_t>(2 + 2 * (k & 1)) * G; };
+    WinProf pf;
+    int used = 0;
+    for (int k = 1;; ++k) {
+        // phase A of iteration k: res = Theta y_k-1 - x0; Theta x_k-1 by linearity
+        const float bp = k >= 2 ? a.beta32[k - 2] : 0.f;  // beta_k-1
+        const float inv = 1.f / (1.f + bp);
+        double q = 0.0;
+        win_phase<float, float, DICT>(a.wA, ws.uA, ws.usA, ws.nuA, ws.sA, ws.nsA, ws.dA, yC, win,
+                                      [&](uint32_t r, float acc) {
+                                          float2& st = ra[r - ws.rA0];
+                                          res[r] = acc - st.x;
+                                          const float u = k == 1 ? acc : fmaf(bp, st.y, acc) * inv;
+                                          st.y = u;
+                                          const double d = static_cast<double>(u) - static_cast<double>(st.x);
+                                          q += d * d;
+                                      },
+                                      pf);
+        win_block_partial(q, q_part, red);
+        grid_sync(a.sync, epoch, smem);
+        // E(x_k-1) (solver.cpp:44-55, 118, 130): quadratic part of this phase, weighted l1 and
+        // support of phase T of iteration k-1 (+ the decoupled coordinates)
+        double t[3];
+        cta_sum3(q_part, reg_part(k - 1), sup_part(k - 1), G, red, t);
+        if (k == 1) {
+            const double e0 = 0.5 * (t[0] + quad_nonR) + a.lambda * e0s[1];
+            stop_gap = a.rel_tol * e0;
+            if (gthread == 0) a.out[OUT_INITIAL_ENERGY] = e0;
+        } else {
+            const double e = 0.5 * (t[0] + quad_nonR) + a.lambda * (t[1] + a.dec_reg[k - 2]);
+            if (gthread == 0) {
+                a.energies[k - 2] = e;
+                a.supports[k - 2] = static_cast<unsigned long long>(t[2] + a.dec_supp[k - 2]);
+            }
+            used = k - 1;
+            if (!isfinite(e)) {
+                if (gthread == 0) a.out[OUT_STATUS] = 8.0;  // NonFiniteEnergy (solver.cpp:131-133)
+                break;
+            }
+            if (a.stop_on_ref && e - a.ref_energy <= stop_gap) break;  // solver.cpp:150
+        }
+        if (k > a.max_iters) break;
+        // phase T of iteration k: gradient + step + prox + momentum; sums of w|x_k|, support
+        const float beta = a.beta32[k - 1];
+        double rg = 0.0, sp = 0.0;
+        win_phase<float, float, DICT>(a.wT, ws.uT, ws.usT, ws.nuT, ws.sT, ws.nsT, ws.dT, res, win,
+                                      [&](uint32_t c, float g) {
+                                          float4& s = cs[c - ws.rT0];
+                                          const float z0 = fmaf(-s.z, g, s.x);
+                                          const float xn = Prec<float>::prox(z0, s.w);
+                                          const float yn = fmaf(beta, xn - s.y, xn);
+                                          s.x = yn;
+                                          s.y = xn;
+                                          yC[c] = yn;
+                                          rg += a.wC[c] * fabs(static_cast<double>(xn));
+                                          sp += xn != 0.f ? 1.0 : 0.0;
+                                      },
+                                      pf);
+        win_block_partial(rg, reg_part(k), red);
+        win_block_partial(sp, sup_part(k), red);
+        grid_sync(a.sync, epoch, smem);
+    }
+    pf.flush();
+    if (gthread == 0) a.out[OUT_ITERS_USED] = used;
+    for (uint32_t i = threadIdx.x; i < ws.nrT; i += kWinBlock) a.x_full[a.C_glob[ws.rT0 + i]] = static_cast<double>(cs[i].y);
+}
+
 // estimate_step on the window engine: fp64 accumulation, own state and reductions; fp32
 // operator values; vector windows in WINT (float: the gathered u and t entries are rounded
 // to fp32, the products are exact in fp64; double: fp64 windows, WBX_TAU_WINDOW=64)
@@ -1923,10 +2085,12 @@ struct wbx_solver {
     int nslots = 3;  // TMA slots in flight per warp
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
     bool win = false, win_dict = false, tau_win64 = false, tau_lanczos = false;
+    bool win_track = false;  // tracked solves (energies / supports / ref_energy) on the window engine
+    unsigned win_smem_track = 0;
     int grid_tau_lz = 0;
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
-    wbx::WinSide wA, wT;
+    std::shared_ptr<wbx::WinPair> wp;  // window layouts (owned by the operator's cache)
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
     cudaStream_t copy_stream = nullptr;  // host->device image copies overlapping the step estimate
@@ -2029,8 +2193,8 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.lz_every = env_int("WBX_LZ_EVERY", 4, 1, kLzCap);
     a.lz_gap = env_int("WBX_LZ_GAP", 4, 1, kLzCap);
     if (s->win) {
-        a.wA = view_of(s->wA);
-        a.wT = view_of(s->wT);
+        a.wA = view_of(s->wp->A);
+        a.wT = view_of(s->wp->T);
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
@@ -2125,10 +2289,37 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         reduce_rows_kernel<<<(K + 127) / 128, 128, 0, st>>>(s->wsup.p, nwarps, K, s->dec_supp.p);
         count_launch(ctx, 3);
     }
-    launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
+    if (s->win_track) {  // the window engine with energy / support tracking
+        const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_track_kernel<true>)
+                                    : reinterpret_cast<const void*>(fista_win_track_kernel<false>);
+        launch_coop_smem(k, s->grid_win, s->win_smem_track, a, st, kWinBlock);
+    } else {
+        launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
+    }
     decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, 0, nullptr, nullptr, s->out.p);
     count_launch(ctx, 2);
     WBX_CUDA(cudaGetLastError());
+}
+
+// The operator's window layouts for grid size G, built on first use and cached on the operator
+std::shared_ptr<WinPair> win_layout(const wbx_op* op, uint32_t G, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(op->win_mu);
+    auto it = op->win_cache.find(G);
+    if (it != op->win_cache.end()) return it->second;
+    auto p = std::make_shared<WinPair>();
+    try {
+        build_win(p->A, op->hA, G, st, 'A');
+        build_win(p->T, op->hT, G, st, 'T');
+        p->A.src_len = static_cast<uint32_t>(op->nC);  // A rows gather C-space vectors
+        p->T.src_len = static_cast<uint32_t>(op->nR);
+        WBX_CUDA(cudaStreamSynchronize(st));  // usable from any stream of the device
+        p->ok = true;
+    } catch (const Error& e) {
+        if (e.status != WBX_TOO_LARGE) throw;
+        p = std::make_shared<WinPair>();  // not representable at this G (ok == false)
+    }
+    op->win_cache[G] = p;
+    return p;
 }
 
 template <typename T>
@@ -2157,16 +2348,10 @@ void alloc_state(wbx_solver* s) {
     if (sizeof(T) == 4 && !(eng && std::string(eng) == "stream")) {  // batches use it for tau
         for (int bps = kWinMinBlocks; bps >= 1 && !s->win; --bps) {
             const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
-            try {
-                build_win(s->wA, s->op->hA, G, s->ctx->stream, 'A');
-                build_win(s->wT, s->op->hT, G, s->ctx->stream, 'T');
-                s->wA.src_len = static_cast<uint32_t>(s->op->nC);  // A rows gather C-space vectors
-                s->wT.src_len = static_cast<uint32_t>(s->op->nR);
-            } catch (const Error&) {
-                continue;  // a window exceeded 16-bit local indices
-            }
-            const WinView vA = view_of(s->wA), vT = view_of(s->wT);
-            const unsigned mu = std::max(s->wA.max_win, s->wT.max_win);
+            s->wp = win_layout(s->op, G, s->ctx->stream);
+            if (!s->wp->ok) continue;  // a window exceeded 16-bit local indices
+            const WinView vA = view_of(s->wp->A), vT = view_of(s->wp->T);
+            const unsigned mu = std::max(s->wp->A.max_win, s->wp->T.max_win);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
             s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
             // tau by Lanczos + the power iteration on the tridiagonal (tau_lanczos_win_kernel);
@@ -2200,14 +2385,26 @@ void alloc_state(wbx_solver* s) {
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
+            // the tracked variant keeps Theta x_k-1 next to x0 per own row (+4 B per row)
+            s->win_smem_track = win_smem_head<8, 16>(vA, vT) + mu * 4u;
+            if (s->win_smem_track <= limit && !(std::getenv("WBX_TRACK_ENGINE") &&
+                                                std::string(std::getenv("WBX_TRACK_ENGINE")) == "stream")) {
+                const void* kk = s->win_dict ? reinterpret_cast<const void*>(fista_win_track_kernel<true>)
+                                             : reinterpret_cast<const void*>(fista_win_track_kernel<false>);
+                WBX_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(s->win_smem_track)));
+                int pk = 0;
+                WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pk, kk, kWinBlock, s->win_smem_track));
+                s->win_track = pk >= bps;
+            }
             if (std::getenv("WBX_VERBOSE"))
                 std::fprintf(stderr,
                              "wbx window engine: G=%u max_u A/T=%u/%u max_rows A/T=%u/%u max_slices A/T=%u/%u "
                              "dict floats A/T=%u/%u rec bytes A/T=%llu/%llu smem fista/tau=%u/%u\n",
-                             G, s->wA.max_u, s->wT.max_u, s->wA.max_rows, s->wT.max_rows, s->wA.max_slices,
-                             s->wT.max_slices, s->wA.max_dict, s->wT.max_dict,
-                             static_cast<unsigned long long>(s->wA.rec.bytes()),
-                             static_cast<unsigned long long>(s->wT.rec.bytes()), s->win_smem_fista, s->win_smem_tau);
+                             G, s->wp->A.max_u, s->wp->T.max_u, s->wp->A.max_rows, s->wp->T.max_rows,
+                             s->wp->A.max_slices, s->wp->T.max_slices, s->wp->A.max_dict, s->wp->T.max_dict,
+                             static_cast<unsigned long long>(s->wp->A.rec.bytes()),
+                             static_cast<unsigned long long>(s->wp->T.rec.bytes()), s->win_smem_fista, s->win_smem_tau);
         }
     }
     if (!s->win)  // stream engine: Lanczos tau unless WBX_TAU=power (the window attempts may have reset it)
@@ -2259,10 +2456,10 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     s->uC.alloc(nC ? nC : 1);
     s->t64.alloc(op->nR ? op->nR : 1);
     s->out.alloc(OUT_COUNT);
-    const uint64_t gmax = static_cast<uint64_t>(std::max(s->grid_fista, s->grid_tau));
+    const uint64_t gmax = static_cast<uint64_t>(std::max({s->grid_fista, s->grid_tau, s->grid_tau_lz, s->grid_win}));
     s->gen.alloc(64);
     s->arrive.alloc(gmax);
-    s->part.alloc(2 * kRedSlots * gmax);
+    s->part.alloc((2 * kRedSlots + 5) * gmax);  // barrier reductions + tracked window solve partials
     s->red.alloc(kRedSlots);
     WBX_CUDA(cudaMemsetAsync(s->gen.p, 0, s->gen.bytes(), st));
     WBX_CUDA(cudaMemsetAsync(s->arrive.p, 0, s->arrive.bytes(), st));
@@ -2498,6 +2695,7 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
     const char* it = (s->win && !track && s->batch == 1) ? "fista_win_kernel"
+                     : (s->win_track && track && s->batch == 1) ? "fista_win_track_kernel"
                      : s->batch == 4                      ? "fista_batch_kernel<4>"
                      : s->batch == 8                      ? "fista_batch_kernel<8>"
                      : fp64                               ? "fista_kernel<double>"

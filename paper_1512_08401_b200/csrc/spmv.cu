@@ -107,8 +107,8 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <int H>
-__global__ void __launch_bounds__(kBlock, 8) sell_row_kernel(SellView M, const float* __restrict__ x,
+template <int H, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) sell_row_kernel(SellView M, const float* __restrict__ x,
                                                              float* __restrict__ y, uint64_t pf_u4) {
     const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -266,10 +266,12 @@ __global__ void __launch_bounds__(WARPS * 32) sell_f32_tma_kernel(SellView M, co
     }
 }
 
-// WBX_SPMV=quarter (default: sell_f32_part_kernel<2>, 32 registers, 64 warps/SM) | half
-// (<4>) | reg (sell_f32_kernel, all 8 pairs at once) | tma1 | tma2 | tma3 (TMA-staged
-// variants). 4096^2 fp32 forward: quarter 97 us, half 100 us, reg 118 us, tma1 137 us, tma2 158 us, tma3 132 us (tools/spmv_roofline.py,
-// profiles/r01_spmv_roofline.md)
+// WBX_SPMV: row (default, sell_row_kernel<4>: row-per-lane layout, 4 pairs per step, 32
+// registers, 64 warps/SM) | row2 | row8 (2 / 8 pairs per step) | quarter | half | reg (segmented
+// layout: sell_f32_part_kernel<2>, <4>, sell_f32_kernel) | tma1 | tma2 | tma3 (TMA-staged
+// segmented variants). 4096^2 fp32 forward, L2 flushed: row 75.8 us (0.84 of HBM), row2 77.8,
+// quarter 97, half 100, reg 118, tma1 137, tma2 158, tma3 132 us (tools/spmv_sweep.py,
+// profiles/r02_spmv_roofline.md, profiles/r01_spmv_roofline.md)
 int spmv_mode() {
     static const int mode = [] {
         const char* e = std::getenv("WBX_SPMV");
@@ -279,8 +281,9 @@ int spmv_mode() {
         if (e && std::strcmp(e, "reg") == 0) return 0;
         if (e && std::strcmp(e, "half") == 0) return 4;
         if (e && std::strcmp(e, "quarter") == 0) return 5;
-        if (e && std::strcmp(e, "row4") == 0) return 7;
-        return 6;
+        if (e && std::strcmp(e, "row2") == 0) return 6;
+        if (e && std::strcmp(e, "row8") == 0) return 8;
+        return 7;
     }();
     return mode;
 }
@@ -307,19 +310,21 @@ long long g_spmv_pf_bytes = -1;  // wbx_diag_set_spmv_pf (sweeps); -1: WBX_SPMV_
 uint64_t spmv_pf_u4() {
     static const uint64_t pf = [] {
         const char* e = std::getenv("WBX_SPMV_PF");
-        const long long b = e ? std::atoll(e) : (16ll << 20);
+        const long long b = e ? std::atoll(e) : 0ll;  // measured: the prefetch costs 13-20 % (r02 sweep)
         return static_cast<uint64_t>(b > 0 ? b : 0) / 16u;
     }();
     return g_spmv_pf_bytes >= 0 ? static_cast<uint64_t>(g_spmv_pf_bytes) / 16u : pf;
 }
 
 void launch_sell_f32(wbx_ctx* ctx, const SellView& v, const float* x, float* y, cudaStream_t s, int mode) {
-    if (mode == 6 || mode == 7) {
+    if (mode >= 6) {
         const unsigned rb = static_cast<unsigned>((uint64_t(v.xslices) * 32 + kBlock - 1) / kBlock);
         if (mode == 6)
-            sell_row_kernel<2><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
+            sell_row_kernel<2, 8><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
+        else if (mode == 7)
+            sell_row_kernel<4, 8><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
         else
-            sell_row_kernel<4><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
+            sell_row_kernel<8, 4><<<rb, kBlock, 0, s>>>(v, x, y, spmv_pf_u4());
         return;
     }
     const unsigned blocks = static_cast<unsigned>((uint64_t(v.slices) * 32 + kBlock - 1) / kBlock);

@@ -48,7 +48,7 @@ class _Shard:
         self.world, self.rank, self.rlo, self.rhi, self.clo, self.chi, self.maxR, self.maxC = (int(v) for v in info)
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         if getattr(self, "h", None):
             lib.wbx_shard_destroy(self.h)

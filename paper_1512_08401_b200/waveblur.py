@@ -120,7 +120,7 @@ class Context:
         return int(lib.wbx_ctx_launch_count(self.handle))
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         if getattr(self, "handle", None):
             lib.wbx_ctx_destroy(self.handle)
@@ -252,14 +252,14 @@ class WaveletBasis:  # wavelet.hpp:68-74, plus its device residency (wbx_basis)
         return h
 
     def _release(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         for h in self._handles.values():
             lib.wbx_basis_destroy(h)
         self._handles.clear()
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         self._release()
 
@@ -355,14 +355,14 @@ class SparseOperator:
         return inf
 
     def _release(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         for h in self._devs.values():
             lib.wbx_op_destroy(h)
         self._devs.clear()
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         self._release()
 
@@ -596,7 +596,7 @@ class StencilOperator:
                                         C.c_void_p(y_ptr)))
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         if getattr(self, "handle", None):
             lib.wbx_stencil_destroy(self.handle)
@@ -820,7 +820,7 @@ class ExactThetaOp:
         return self.n
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         if getattr(self, "handle", None):
             lib.wbx_exact_op_destroy(self.handle)
@@ -1053,7 +1053,7 @@ class Deblurrer:
         return float(t.value), int(it.value), int(pp.value)
 
     def __del__(self):
-        if lib is None:  # interpreter shutdown: the library is already gone
+        if lib is None or N is None or not N.alive():  # interpreter exit: leave it to the process
             return
         if getattr(self, "handle", None):
             lib.wbx_solver_destroy(self.handle)

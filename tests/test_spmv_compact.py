@@ -7,7 +7,7 @@ tools/spmv_roofline.py measures).
   once per process), against the oracle's fp64 spmv (oracle/wbx_oracle.c, pinned bitwise to the
   reference): |y - y_ref| <= 1e-6 * max|y_ref| (fp32 values and vector entries, fp32 sums);
 * variants sharing a summation order are bitwise equal: the segmented kernels (reg, tma1-3,
-  half, quarter) among themselves, the row-per-lane kernels (row, row4) among themselves."""
+  half, quarter) among themselves, the row-per-lane kernels (row, row2, row8) among themselves."""
 import ctypes as C
 
 import numpy as np
@@ -19,9 +19,9 @@ from paper_1512_08401_b200 import waveblur as W
 
 pytestmark = pytest.mark.gpu
 
-MODES = {"reg": 0, "tma1": 1, "tma2": 2, "tma3": 3, "half": 4, "quarter": 5, "row": 6, "row4": 7}
+MODES = {"reg": 0, "tma1": 1, "tma2": 2, "tma3": 3, "half": 4, "quarter": 5, "row2": 6, "row": 7, "row8": 8}
 SEGMENTED = ("reg", "tma1", "tma2", "tma3", "half", "quarter")
-ROW = ("row", "row4")
+ROW = ("row", "row2", "row8")
 
 
 def compacted_spaces(op):
@@ -103,13 +103,13 @@ def test_fp32_kernels_vs_oracle_and_each_other(golden, name):
             assert err <= 1e-6, (name, m, transpose, err)
         for m in SEGMENTED[1:]:
             assert np.array_equal(out[m], out[SEGMENTED[0]]), (name, m, transpose)
-        assert np.array_equal(out["row4"], out["row"]), (name, transpose)
+        assert np.array_equal(out["row2"], out["row"]) and np.array_equal(out["row8"], out["row"]), (name, transpose)
 
 
 def test_fp32_row_kernel_at_4096_vs_oracle():
     """The operator tools/spmv_roofline.py measures (C2's Theta_K carried to 4096^2, 50 M
     nonzeros, HBM-streamed): the default row kernel, forward and adjoint, against the
-    oracle's fp64 spmv on a sample of rows (1e-6 of max|y|) and bitwise against row4."""
+    oracle's fp64 spmv on a sample of rows (1e-6 of max|y|) and bitwise against row2 / row8."""
     import torch
     from pathlib import Path
     z = np.load(Path(__file__).resolve().parent / "golden" / "c2_db4_1024.npz")
@@ -127,7 +127,8 @@ def test_fp32_row_kernel_at_4096_vs_oracle():
     x = rng.standard_normal(op.n).astype(np.float32).astype(np.float64)
     xc = torch.from_numpy(x[Cc].astype(np.float32)).to(dev)
     y = run_mode(ctx, h, False, MODES["row"], xc, R.size)
-    assert np.array_equal(y, run_mode(ctx, h, False, MODES["row4"], xc, R.size))
+    assert np.array_equal(y, run_mode(ctx, h, False, MODES["row2"], xc, R.size))
+    assert np.array_equal(y, run_mode(ctx, h, False, MODES["row8"], xc, R.size))
     sample = rng.choice(R.size, 20000, replace=False)
     ref = np.array([vals[rp[r]:rp[r + 1]] @ x[cols[rp[r]:rp[r + 1]]] for r in R[sample]])
     assert np.abs(y[sample] - ref).max() <= 1e-6 * np.abs(ref).max()

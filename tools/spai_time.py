@@ -7,7 +7,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_1512_08401_b200 import waveblur as W  # noqa: E402
 
-op, basis, u0, meta = bench.make_inputs()
+op, basis, u0 = bench.make_inputs()
 ctx = W.Context(0)
 op.device(ctx)
 for _ in range(3):

@@ -17,10 +17,10 @@ import torch  # noqa: E402
 from paper_1512_08401_b200 import _native as N  # noqa: E402
 from paper_1512_08401_b200 import waveblur as W  # noqa: E402
 
-MODES = {"reg": 0, "tma1": 1, "tma2": 2, "tma3": 3, "half": 4, "quarter": 5, "row": 6, "row4": 7}
+MODES = {"reg": 0, "tma1": 1, "tma2": 2, "tma3": 3, "half": 4, "quarter": 5, "row2": 6, "row": 7, "row8": 8}
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-modes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["quarter", "row", "row4"]
+modes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["quarter", "row2", "row", "row8"]
 pfs = [float(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0, 4, 16, 64]
 z = np.load(ROOT / "tests" / "golden" / "c2_db4_1024.npz")
 gl = W.GeneratorList((1024, 1024), 4, W.FilterFamily.Daubechies, 4, z["gen_block"].astype(np.uint32),
