@@ -174,6 +174,34 @@ int wbx_theta_conv_topk(wbx_ctx* ctx, wbx_basis* basis, const double* psf, const
  * generate_psf(GaussianSpec{sigma}) (host). */
 int wbx_psf_gaussian(uint32_t ndim, const uint64_t* dims, double sigma, double* kernel);
 
+/* ---------------------------------------------------------------- PSFs, convolution, degrade
+ * generate_psf (operators.cpp:298-318; PsfSpec, operators.hpp:15-36): the kernel image on the
+ * full grid (centred at index 0, wrap-around, unit mass), same expressions as the reference
+ * (bitwise). params by kind: GAUSSIAN {sigma}, SKEWED {sigma}, MOTION {points, sigma1, sigma2,
+ * seed} (MotionSpec defaults 5, 8, 1, 0), AIRY {scale}, DEFOCUS {radius}. ctx: needed by MOTION
+ * (its Gaussian post-smoothing is a device FFT convolution), may be NULL otherwise.
+ * BadSpec on bad parameters, ShapeMismatch on non-dyadic dims (Image::require_dyadic). */
+typedef enum {
+    WBX_PSF_GAUSSIAN = 0,
+    WBX_PSF_SKEWED = 1,
+    WBX_PSF_MOTION = 2,
+    WBX_PSF_AIRY = 3,
+    WBX_PSF_DEFOCUS = 4
+} wbx_psf_kind;
+int wbx_generate_psf(wbx_ctx* ctx, uint32_t kind, const double* params, uint32_t ndim, const uint64_t* dims,
+                     double* kernel);
+/* convolve / apply_adjoint (operators.cpp:320-326, convolve_spectral :20-77): circular
+ * convolution with the kernel image (adjoint: with h~[i] = h[-i]) through the device FFT, in
+ * the oracle build's FFT arithmetic. Host images, synchronous. */
+int wbx_convolve(wbx_ctx* ctx, uint32_t ndim, const uint64_t* dims, const double* kernel, const double* u,
+                 int adjoint, double* out);
+/* add_noise (operators.cpp:344-356): u + sigma * N(0,1), per-index Box-Muller on
+ * CounterRng(seed) draws 2i, 2i+1; on the device. degrade (operators.cpp:385-387) =
+ * add_noise(convolve(u, psf), noise_sigma, seed). */
+int wbx_add_noise(wbx_ctx* ctx, uint64_t n, const double* u, double sigma, uint64_t seed, double* out);
+int wbx_degrade(wbx_ctx* ctx, uint32_t ndim, const uint64_t* dims, const double* kernel, const double* u,
+                double noise_sigma, uint64_t seed, double* out);
+
 /* Spatially varying Theta_K (BASELINE configs C3/C4; the reference has no 2-D spatially
  * varying operator): column mu = the column of the stationary operator whose
  * Gaussian sigma matches the spatial row of psi_mu, sigma varying linearly from

@@ -1,8 +1,9 @@
 // proj/src/wbx_backend.cpp — route the hot path of waveblur to libwbx.so (B200).
 //
 // Defines the reference's hot-path functions (wavelet.hpp:88,91; theta.hpp:83-89;
-// precond.hpp:26-34; solver.hpp:86-105; SparseThetaOp::apply/apply_adjoint) on top of the
-// C ABI in include/wbx.h. The reference's CPU definitions stay in the library under a
+// precond.hpp:26-34; solver.hpp:86-105; SparseThetaOp::apply/apply_adjoint) and the PSF side
+// (operators.hpp:44-77: generate_psf, convolve, apply_adjoint, add_noise, degrade) on top of
+// the C ABI in include/wbx.h. The reference's CPU definitions stay in the library under a
 // `*_host` name. SparseThetaOp and ExactThetaOp (solver.cpp:11-31) run on
 // the device (ExactThetaOp::apply/apply_adjoint/ops_per_pixel are defined here, so the exact
 // operator's FFT route, its estimate_step and its fista/ista run through wbx_exact_*); only
@@ -15,8 +16,11 @@
 #include <map>
 #include <mutex>
 #include <stdexcept>
+#include <type_traits>
+#include <variant>
 #include <vector>
 
+#include "waveblur/operators.hpp"
 #include "waveblur/precond.hpp"
 #include "waveblur/solver.hpp"
 #include "waveblur/theta.hpp"
@@ -277,6 +281,80 @@ std::vector<double> approx_gradient(const SparseOperator& op, const std::vector<
     std::vector<double> y(op.n);
     check(wbx_approx_gradient(ctx(), device_op(op), x.data(), x0.data(), y.data()));
     return y;
+}
+
+// ---- PSFs and the FFT convolution (operators.cpp:98-387)
+Psf generate_psf(const PsfSpec& spec, const std::vector<std::size_t>& dims) {
+    double params[4] = {0.0, 0.0, 0.0, 0.0};
+    uint32_t kind = WBX_PSF_GAUSSIAN;
+    std::visit(
+        [&](const auto& sp) {
+            using T = std::decay_t<decltype(sp)>;
+            if constexpr (std::is_same_v<T, GaussianSpec>) {
+                params[0] = sp.sigma;
+            } else if constexpr (std::is_same_v<T, SkewedGaussianSpec>) {
+                kind = WBX_PSF_SKEWED;
+                params[0] = sp.sigma;
+            } else if constexpr (std::is_same_v<T, MotionSpec>) {
+                kind = WBX_PSF_MOTION;
+                params[0] = sp.points;
+                params[1] = sp.sigma1;
+                params[2] = sp.sigma2;
+                params[3] = static_cast<double>(sp.seed);
+                if (sp.seed >= (1ULL << 53)) throw BadSpec("motion blur: seed must be < 2^53 here");
+            } else if constexpr (std::is_same_v<T, AirySpec>) {
+                kind = WBX_PSF_AIRY;
+                params[0] = sp.scale;
+            } else {
+                kind = WBX_PSF_DEFOCUS;
+                params[0] = sp.radius;
+            }
+        },
+        spec);
+    Image tmp(dims);
+    tmp.require_dyadic();
+    std::lock_guard<std::recursive_mutex> g(mu);
+    const std::vector<uint64_t> d(dims.begin(), dims.end());
+    check(wbx_generate_psf(kind == WBX_PSF_MOTION ? ctx() : nullptr, kind, params,
+                           static_cast<uint32_t>(d.size()), d.data(), tmp.v.data()));
+    return Psf{std::move(tmp), spec};
+}
+
+namespace {
+Image conv(const Image& u, const Psf& psf, int adjoint) {
+    if (u.dims != psf.kernel.dims) throw ShapeMismatch("convolve: image/kernel dims differ");
+    u.require_dyadic();
+    std::lock_guard<std::recursive_mutex> g(mu);
+    Image out(u.dims);
+    const std::vector<uint64_t> d(u.dims.begin(), u.dims.end());
+    check(wbx_convolve(ctx(), static_cast<uint32_t>(d.size()), d.data(), psf.kernel.v.data(), u.v.data(), adjoint,
+                       out.v.data()));
+    return out;
+}
+}  // namespace
+
+Image convolve(const Image& u, const Psf& psf) { return conv(u, psf, 0); }
+
+Image apply_adjoint(const Image& u, const Psf& psf) { return conv(u, psf, 1); }
+
+Image add_noise(const Image& u, double sigma, std::uint64_t seed) {
+    if (sigma < 0.0) throw BadSpec("noise sigma must be >= 0");
+    std::lock_guard<std::recursive_mutex> g(mu);
+    Image out(u.dims);
+    check(wbx_add_noise(ctx(), u.size(), u.v.data(), sigma, seed, out.v.data()));
+    return out;
+}
+
+Image degrade(const Image& u, const DegradationModel& model) {
+    if (u.dims != model.psf.kernel.dims) throw ShapeMismatch("convolve: image/kernel dims differ");
+    if (model.noise_sigma < 0.0) throw BadSpec("noise sigma must be >= 0");
+    u.require_dyadic();
+    std::lock_guard<std::recursive_mutex> g(mu);
+    Image out(u.dims);
+    const std::vector<uint64_t> d(u.dims.begin(), u.dims.end());
+    check(wbx_degrade(ctx(), static_cast<uint32_t>(d.size()), d.data(), model.psf.kernel.v.data(), u.v.data(),
+                      model.noise_sigma, model.seed, out.v.data()));
+    return out;
 }
 
 std::vector<double> SparseThetaOp::apply(const std::vector<double>& x) const { return spmv(sparse(), x); }

@@ -10,7 +10,7 @@
 set -euo pipefail
 in=$1
 out=$2
-routed='analyze|synthesize|spmv|spmv_t|approx_gradient|energy|prox_weighted_l1_P|estimate_step|ista|fista|gram_diagonals|jacobi|spai'
+routed='analyze|synthesize|spmv|spmv_t|approx_gradient|energy|prox_weighted_l1_P|estimate_step|ista|fista|gram_diagonals|jacobi|spai|generate_psf|convolve|apply_adjoint|add_noise|degrade'
 args=()
 while read -r _ kind sym; do
     case $kind in T | W) ;; *) continue ;; esac

@@ -17,6 +17,7 @@ LIB_PATH = Path(os.environ.get("WBX_LIB") or Path(__file__).resolve().parent / "
 WBX_OK = 0
 WBX_FP32 = 32
 WBX_FP64 = 64
+WBX_PSF_GAUSSIAN, WBX_PSF_SKEWED, WBX_PSF_MOTION, WBX_PSF_AIRY, WBX_PSF_DEFOCUS = range(5)
 
 
 class wbx_band(C.Structure):
@@ -91,6 +92,10 @@ SIGNATURES = {
                                 C.POINTER(wbx_report)]),
     "wbx_theta_conv_topk": (C.c_int, [_P, _P, _D, _D, C.c_uint64, C.c_uint64, _U32, _U32, _U64, _D, _U64]),
     "wbx_psf_gaussian": (C.c_int, [C.c_uint32, _U64, C.c_double, _D]),
+    "wbx_generate_psf": (C.c_int, [_P, C.c_uint32, _D, C.c_uint32, _U64, _D]),
+    "wbx_convolve": (C.c_int, [_P, C.c_uint32, _U64, _D, _D, C.c_int, _D]),
+    "wbx_add_noise": (C.c_int, [_P, C.c_uint64, _D, C.c_double, C.c_uint64, _D]),
+    "wbx_degrade": (C.c_int, [_P, C.c_uint32, _U64, _D, _D, C.c_double, C.c_uint64, _D]),
     "wbx_theta_expand": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                    _U64, _U64, _U32, _D]),
     "wbx_theta_varying": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint32, _D, _U64, _U32, _U32, _U64, _D,

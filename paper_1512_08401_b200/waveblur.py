@@ -547,6 +547,140 @@ def gaussian_psf_kernel(dims, sigma: float) -> np.ndarray:
     return k.reshape(dims)
 
 
+# ----------------------------------------------------------------------------- PSFs (operators.hpp:15-77)
+@dataclass
+class GaussianSpec:
+    sigma: float
+
+
+@dataclass
+class SkewedGaussianSpec:
+    sigma: float
+
+
+@dataclass
+class MotionSpec:
+    points: int = 5
+    sigma1: float = 8.0  # std-dev of the control point cloud
+    sigma2: float = 1.0  # post-smoothing Gaussian
+    seed: int = 0
+
+
+@dataclass
+class AirySpec:
+    scale: float
+
+
+@dataclass
+class DefocusSpec:
+    radius: float
+
+
+def psf_spec_string(spec) -> str:
+    """psf_spec_string (operators.cpp:276-296)."""
+    g = lambda v: f"{v:g}"  # noqa: E731  (std::ostream default format)
+    if isinstance(spec, GaussianSpec):
+        return f"gaussian:{g(spec.sigma)}"
+    if isinstance(spec, SkewedGaussianSpec):
+        return f"skewed:{g(spec.sigma)}"
+    if isinstance(spec, MotionSpec):
+        return f"motion:{spec.points}:{g(spec.sigma1)}:{g(spec.sigma2)}:{spec.seed}"
+    if isinstance(spec, AirySpec):
+        return f"airy:{g(spec.scale)}"
+    return f"defocus:{g(spec.radius)}"
+
+
+@dataclass
+class Psf:  # operators.hpp:38-42
+    kernel: np.ndarray
+    spec: object
+
+
+def _psf_params(spec):
+    if isinstance(spec, GaussianSpec):
+        return N.WBX_PSF_GAUSSIAN, [spec.sigma]
+    if isinstance(spec, SkewedGaussianSpec):
+        return N.WBX_PSF_SKEWED, [spec.sigma]
+    if isinstance(spec, MotionSpec):
+        return N.WBX_PSF_MOTION, [float(spec.points), spec.sigma1, spec.sigma2, float(spec.seed)]
+    if isinstance(spec, AirySpec):
+        return N.WBX_PSF_AIRY, [spec.scale]
+    if isinstance(spec, DefocusSpec):
+        return N.WBX_PSF_DEFOCUS, [spec.radius]
+    raise BadSpec("unknown PSF spec")
+
+
+def generate_psf(spec, dims, ctx: Optional[Context] = None) -> Psf:
+    """generate_psf (operators.cpp:298-318): the kernel image (centred at 0, wrap-around, unit
+    mass). Motion kernels smooth on the device (their context: ctx or the default)."""
+    kind, params = _psf_params(spec)
+    dims = tuple(int(d) for d in dims)
+    if kind == N.WBX_PSF_MOTION and spec.seed >= 2 ** 53:
+        raise BadSpec("motion seed must be < 2^53")
+    d = np.array(dims, dtype=np.uint64)
+    k = np.zeros(int(np.prod(dims)) if dims else 1, dtype=np.float64)
+    c = (ctx or default_context()) if kind == N.WBX_PSF_MOTION else ctx
+    _check(lib.wbx_generate_psf(c.handle if c else None, kind, _dptr(np.array(params, dtype=np.float64)), len(dims),
+                                _u64ptr(d), _dptr(k)))
+    return Psf(k.reshape(dims), spec)
+
+
+def _kernel_of(psf) -> np.ndarray:
+    return np.ascontiguousarray(psf.kernel if isinstance(psf, Psf) else psf, dtype=np.float64)
+
+
+def _conv(u, psf, adjoint: int, ctx) -> np.ndarray:
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    k = _kernel_of(psf)
+    if k.shape != u.shape:
+        raise ShapeMismatch("convolve: image and kernel dims differ")
+    ctx = ctx or default_context()
+    out = np.empty_like(u)
+    d = np.array(u.shape, dtype=np.uint64)
+    _check(lib.wbx_convolve(ctx.handle, u.ndim, _u64ptr(d), _dptr(k), _dptr(u), adjoint, _dptr(out)))
+    return out
+
+
+def convolve(u, psf, ctx: Optional[Context] = None) -> np.ndarray:
+    """convolve (operators.cpp:320-322): circular convolution via the device FFT."""
+    return _conv(u, psf, 0, ctx)
+
+
+def apply_adjoint_psf(u, psf, ctx: Optional[Context] = None) -> np.ndarray:
+    """apply_adjoint (operators.cpp:324-326): H* u = h~ * u, h~[i] = h[-i]."""
+    return _conv(u, psf, 1, ctx)
+
+
+def add_noise(u, sigma: float, seed: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """add_noise (operators.cpp:344-356): per-index Box-Muller, on the device."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    ctx = ctx or default_context()
+    out = np.empty_like(u)
+    _check(lib.wbx_add_noise(ctx.handle, u.size, _dptr(u), float(sigma), int(seed), _dptr(out)))
+    return out
+
+
+@dataclass
+class DegradationModel:  # operators.hpp:69-73
+    psf: Psf
+    noise_sigma: float = 0.0
+    seed: int = 0
+
+
+def degrade(u, model: DegradationModel, ctx: Optional[Context] = None) -> np.ndarray:
+    """degrade (operators.cpp:385-387) = add_noise(convolve(u, psf), sigma, seed), on the device."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    k = _kernel_of(model.psf)
+    if k.shape != u.shape:
+        raise ShapeMismatch("degrade: image and kernel dims differ")
+    ctx = ctx or default_context()
+    out = np.empty_like(u)
+    d = np.array(u.shape, dtype=np.uint64)
+    _check(lib.wbx_degrade(ctx.handle, u.ndim, _u64ptr(d), _dptr(k), _dptr(u), float(model.noise_sigma),
+                           int(model.seed), _dptr(out)))
+    return out
+
+
 def dyadic_band_weights(layout: SubbandLayout) -> np.ndarray:
     """Per-band sigma of dyadic_weights (theta.cpp:153-165): 2^(level - J)."""
     return np.array([2.0 ** (b.level - layout.J) for b in layout.bands], dtype=np.float64)

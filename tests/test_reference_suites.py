@@ -1,10 +1,11 @@
-"""The reference's own doctest suites (proj/tests/test_{wavelet,theta,precond,solver}.cpp),
+"""The reference's own doctest suites (proj/tests/test_{wavelet,operators,theta,precond,solver}.cpp),
 unmodified, with the reference's hot path routed to libwbx.so by the maintainer binding of
 INTEGRATION.md §2 (integration/wbx_backend.cpp; `make -C oracle wbx-tests` links it ahead of
 the reference objects, whose routed definitions are renamed to *_host). Every analyze /
 synthesize / spmv / spmv_t / approx_gradient / energy / prox / estimate_step / ista / fista /
-gram_diagonals / jacobi / spai call of those suites on a SparseThetaOp runs on the B200, in
-the fp64 mode, at the suites' native tolerances (bitwise where they compare bitwise).
+gram_diagonals / jacobi / spai call of those suites on a SparseThetaOp or ExactThetaOp, and every
+generate_psf / convolve / apply_adjoint / add_noise / degrade call, runs through libwbx (the B200),
+in the fp64 mode, at the suites' native tolerances (bitwise where they compare bitwise).
 
 The binaries are built in the build container (they compile the reference's test sources
 from /root/reference) and travel prebuilt under oracle/_ref/."""
@@ -16,7 +17,7 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 REF = ROOT / "oracle" / "_ref"
-SUITES = ["wavelet", "theta", "precond", "solver"]
+SUITES = ["wavelet", "operators", "theta", "precond", "solver"]
 
 pytestmark = pytest.mark.gpu
 
