@@ -148,6 +148,26 @@ int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, c
  * used to measure the SpMV against the HBM roofline (tools/spmv_roofline.py). */
 int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision,
                          const void* x_dev, void* y_dev);
+/* write_operator / read_operator (theta.cpp:413-490): the reference's WTHETA01 file, same
+ * bytes, same validation (WBX_IO_ERROR with the reference's messages; bad layouts raise what
+ * make_layout raises). read: the arrays are allocated by the library (malloc; wbx_free);
+ * dims must hold 2 entries. */
+int wbx_write_operator(const char* path, uint32_t ndim, const uint64_t* dims, uint32_t J, uint32_t family,
+                       uint32_t order, uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
+                       const double* values);
+int wbx_read_operator(const char* path, uint32_t* ndim, uint64_t* dims, uint32_t* J, uint32_t* family,
+                      uint32_t* order, uint64_t* n, uint64_t* nnz, uint64_t** row_offsets,
+                      uint32_t** col_indices, double** values);
+/* Device-ready operator cache (WBXOP001; no reference counterpart): everything
+ * wbx_op_create built (compacted orders, exact fp64 SELL, fp32 layouts of Theta and Theta^T)
+ * plus the window layouts solvers built since, and optionally the operator's preconditioner p
+ * (n doubles, may be NULL) and step tau (0 = none). wbx_op_load uploads them without
+ * recomputing anything; p (n doubles) / has_p / tau may be NULL. */
+int wbx_op_save(const wbx_op* op, const char* path, const double* p, double tau);
+int wbx_op_load(wbx_ctx* ctx, const char* path, wbx_op** out, double* p, int* has_p, double* tau);
+/* The operator's CSR (SparseThetaOp::sparse(), solver.hpp:33): row_offsets n + 1, columns and
+ * values nnz (wbx_op_get_info) entries, caller-allocated. */
+int wbx_op_get_csr(const wbx_op* op, uint64_t* row_offsets, uint32_t* col_indices, double* values);
 /* approx_gradient (theta.cpp:358-365): Theta^T (Theta x - x0) */
 int wbx_approx_gradient(wbx_ctx* ctx, const wbx_op* op, const double* x, const double* x0,
                         double* g);

@@ -78,6 +78,13 @@ SIGNATURES = {
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_spmv_compact_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
+    "wbx_write_operator": (C.c_int, [C.c_char_p, C.c_uint32, _U64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                     _U64, _U32, _D]),
+    "wbx_read_operator": (C.c_int, [C.c_char_p, _U32, _U64, _U32, _U32, _U32, _U64, _U64, C.POINTER(_U64),
+                                    C.POINTER(_U32), C.POINTER(_D)]),
+    "wbx_op_save": (C.c_int, [_P, C.c_char_p, _D, C.c_double]),
+    "wbx_op_get_csr": (C.c_int, [_P, _U64, _U32, _D]),
+    "wbx_op_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_P), _D, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "wbx_approx_gradient": (C.c_int, [_P, _P, _D, _D, _D]),
     "wbx_stencil_create": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                      C.POINTER(C.c_void_p)]),

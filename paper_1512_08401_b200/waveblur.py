@@ -421,77 +421,78 @@ def transpose(op: SparseOperator) -> SparseOperator:
                           op.family, op.order)
 
 
-_MAGIC = b"WTHETA01"
-
-
 def write_operator(op: SparseOperator, path: str) -> None:
-    """Bit-exact WTHETA01 file (theta.cpp:428-443)."""
+    """write_operator (theta.cpp:428-443): the bit-exact WTHETA01 file, through the C ABI."""
     if op.layout is None:
         raise IoError("operator has no layout")
-    try:
-        with open(path, "wb") as f:
-            f.write(_MAGIC)
-            dims = op.layout.dims
-            f.write(struct.pack("<I", len(dims)))
-            for s in dims:
-                f.write(struct.pack("<I", s))
-            f.write(struct.pack("<IIII", op.layout.J, int(op.family), op.order, op.nnz()))
-            f.write(op.row_offsets.astype("<u8").tobytes())
-            f.write(op.col_indices.astype("<u4").tobytes())
-            f.write(op.values.astype("<f8").tobytes())
-    except OSError as e:
-        raise IoError(f"cannot write operator file {path}: {e}") from e
+    d = np.array(op.layout.dims, dtype=np.uint64)
+    _check(lib.wbx_write_operator(str(path).encode(), len(op.layout.dims), _u64ptr(d), op.layout.J, int(op.family),
+                                  op.order, op.n, _u64ptr(op.row_offsets), _u32ptr(op.col_indices),
+                                  _dptr(op.values)))
 
 
 def read_operator(path: str) -> SparseOperator:
-    """WTHETA01 reader with the reference's validation (theta.cpp:445-490)."""
+    """read_operator (theta.cpp:445-490) with the reference's validation, through the C ABI."""
+    nd, J, fam, order = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    dims = np.zeros(2, dtype=np.uint64)
+    n, nnz = C.c_uint64(), C.c_uint64()
+    ro, ci, va = _U64P(), _U32P(), _DP()
+    _check(lib.wbx_read_operator(str(path).encode(), C.byref(nd), _u64ptr(dims), C.byref(J), C.byref(fam),
+                                 C.byref(order), C.byref(n), C.byref(nnz), C.byref(ro), C.byref(ci), C.byref(va)))
     try:
-        data = open(path, "rb").read()
-    except OSError as e:
-        raise IoError(f"cannot open operator file {path}") from e
-    if len(data) < 8:
-        raise IoError("operator file truncated")
-    if data[:8] != _MAGIC:
-        raise IoError(f"{path}: not a WTHETA01 operator file")
-    pos = 8
+        k = int(nnz.value)
+        row_offsets = np.ctypeslib.as_array(ro, shape=(n.value + 1,)).copy()
+        cols = np.ctypeslib.as_array(ci, shape=(max(k, 1),))[:k].copy()
+        vals = np.ctypeslib.as_array(va, shape=(max(k, 1),))[:k].copy()
+    finally:
+        lib.wbx_free(ro)
+        lib.wbx_free(ci)
+        lib.wbx_free(va)
+    layout = make_layout([int(v) for v in dims[: nd.value]], J.value)
+    return SparseOperator(int(n.value), row_offsets, cols, vals, layout, FilterFamily(fam.value), order.value)
 
-    def u32():
-        nonlocal pos
-        if pos + 4 > len(data):
-            raise IoError("operator file truncated")
-        v = struct.unpack_from("<I", data, pos)[0]
-        pos += 4
-        return v
 
-    d = u32()
-    if d < 1 or d > 2:
-        raise IoError(f"{path}: bad dimension count")
-    dims = [u32() for _ in range(d)]
-    J, family, order, nnz = u32(), u32(), u32(), u32()
-    if family > 2:
-        raise IoError(f"{path}: bad filter family id")
-    layout = make_layout(dims, J)
-    n = layout.total()
-    need = 8 * (n + 1) + 4 * nnz + 8 * nnz
-    if pos + need > len(data):
-        raise IoError("operator file truncated")
-    ro = np.frombuffer(data, "<u8", n + 1, pos).astype(np.uint64)
-    pos += 8 * (n + 1)
-    ci = np.frombuffer(data, "<u4", nnz, pos).astype(np.uint32)
-    pos += 4 * nnz
-    va = np.frombuffer(data, "<f8", nnz, pos).astype(np.float64)
-    if ro[0] != 0 or ro[n] != nnz:
-        raise IoError(f"{path}: inconsistent row offsets")
-    if np.any(np.diff(ro.astype(np.int64)) < 0):
-        raise IoError(f"{path}: row offsets not nondecreasing")
-    if nnz and np.any(ci >= n):
-        raise IoError(f"{path}: column index out of range")
-    if nnz > 1:
-        rows = np.repeat(np.arange(n), np.diff(ro.astype(np.int64)))
-        same = rows[1:] == rows[:-1]
-        if np.any(same & (ci[1:].astype(np.int64) <= ci[:-1].astype(np.int64))):
-            raise IoError(f"{path}: columns not strictly increasing in a row")
-    return SparseOperator(n, ro, ci, va, layout, FilterFamily(family), order)
+_U64P = lambda: C.POINTER(C.c_uint64)()  # noqa: E731
+_U32P = lambda: C.POINTER(C.c_uint32)()  # noqa: E731
+_DP = lambda: C.POINTER(C.c_double)()  # noqa: E731
+
+
+def save_device_operator(op: SparseOperator, path: str, P: Optional["DiagonalPreconditioner"] = None,
+                         tau: float = 0.0, ctx: Optional[Context] = None) -> None:
+    """Device-ready operator cache (WBXOP001, include/wbx.h wbx_op_save): the device layouts
+    (and the window layouts solvers built on `ctx`), optionally P and tau."""
+    p = _f64(P.p, op.n, "preconditioner") if P is not None else None
+    _check(lib.wbx_op_save(op.device(ctx), str(path).encode(), _dptr(p) if p is not None else None, float(tau)))
+
+
+def load_device_operator(path: str, ctx: Optional[Context] = None, layout: Optional[SubbandLayout] = None):
+    """wbx_op_load: (SparseOperator with its device handle bound to ctx, P or None, tau)."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    inf = N.wbx_op_info()
+    # the element count is needed for p before loading: read it from the header
+    with open(path, "rb") as f:
+        head = f.read(20)
+    if len(head) < 20 or head[:8] != b"WBXOP001":
+        raise IoError(f"{path}: not a WBXOP001 device operator cache")
+    n = struct.unpack_from("<Q", head, 12)[0]
+    p = np.empty(n)
+    has_p, tau = C.c_int(), C.c_double()
+    _check(lib.wbx_op_load(ctx.handle, str(path).encode(), C.byref(h), _dptr(p), C.byref(has_p), C.byref(tau)))
+    try:
+        _check(lib.wbx_op_get_info(h, C.byref(inf)))
+        ro = np.empty(int(inf.n) + 1, dtype=np.uint64)
+        ci = np.empty(max(int(inf.nnz), 1), dtype=np.uint32)
+        va = np.empty(max(int(inf.nnz), 1), dtype=np.float64)
+        _check(lib.wbx_op_get_csr(h, _u64ptr(ro), _u32ptr(ci), _dptr(va)))
+    except Exception:
+        lib.wbx_op_destroy(h)
+        raise
+    k = int(inf.nnz)
+    op = SparseOperator(int(inf.n), ro, ci[:k], va[:k], layout)
+    op._devs[ctx] = h  # the loaded device layouts ARE this operator's handle on ctx
+    op._ctx = ctx
+    return op, (DiagonalPreconditioner(p, PrecondKind.Spai) if has_p.value else None), float(tau.value)
 
 
 @dataclass
