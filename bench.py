@@ -495,25 +495,16 @@ def extra_workloads(W, torch, ctx, stream, dev, op, basis, P, w, u0, tau, flush)
     return out
 
 
-class _SingleGpu:
-    """ShardedDeblurrer-like facade over the single-GPU Deblurrer (C4 at one GPU)."""
-
-    def __init__(self, d):
-        self.d = d
-        self.tau_iters = 0
-
-    def deblur_dev(self, u0_ptr, u_ptr):
-        self.d.deblur_dev(u0_ptr, u_ptr, clamp=True)
-
-
 def run_c4(args, rank, world, local_rank):
     """BASELINE config C4: one size^2 spatially varying deblur (sigma 2.5 -> 7.5 px), Theta_K
-    row-sharded over `world` GPUs; NCCL all-gathers of the padded y / res slices over NVLink
-    after every phase (strong scaling: total work fixed)."""
+    row-sharded over `world` GPUs by the library's sharded solver (wbx_sharded: per-rank phase
+    kernels, NCCL all-gathers of the padded y / res slices over NVLink inside libwbx, the FISTA
+    iterations as one CUDA graph); strong scaling (total work fixed). At one GPU the same
+    engine runs world 1; the single-GPU persistent solver (Deblurrer) is reported beside it."""
     import torch
     from paper_1512_08401_b200 import synthetic as S
     from paper_1512_08401_b200 import waveblur as W
-    from paper_1512_08401_b200.sharded import ShardedDeblurrer, TorchExchange
+    from paper_1512_08401_b200.sharded import ShardedDeblurrer, nccl_comm
     size = args.size
     dims = (size, size)
     dev = torch.device("cuda", local_rank)
@@ -531,43 +522,50 @@ def run_c4(args, rank, world, local_rank):
     P = W.spai(op, ctx)
     w = W.scale_weights(basis.layout)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    comm = None
     if world > 1:
         import torch.distributed as dist
-        ex = TorchExchange(torch, dist, stream)
-        sh = ShardedDeblurrer(torch, ctx, op, basis, P, w, 1e-4, ITERS, world, [rank], ex)
-        path = f"Theta row-sharded x{world}, NCCL all-gather of y/res"
-    else:  # one GPU: nothing to shard, the single-GPU persistent solver
-        sh = _SingleGpu(W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False), ctx))
-        path = "single GPU (persistent solver, no sharding)"
+        comm = nccl_comm(torch, dist, ctx)
+    sh = ShardedDeblurrer(ctx, op, basis, P, w, 1e-4, ITERS, world, [rank], comm=comm)
     with torch.cuda.stream(stream):
         u0_dev = torch.from_numpy(u0.ravel().copy()).to(dev)
         out = torch.empty_like(u0_dev)
     setup_s = time.perf_counter() - t_setup
-    for _ in range(max(1, args.warmup)):
-        sh.deblur_dev(u0_dev.data_ptr(), out.data_ptr())
-    ctx.synchronize()
+
+    def timed(fn, steps):
+        for _ in range(max(1, args.warmup)):
+            fn()
+        ctx.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+        for _ in range(steps):
+            fn()
+        with torch.cuda.stream(stream):
+            b.record(stream)
+        b.synchronize()
+        return _max_over_ranks(a.elapsed_time(b) / steps, world, dev)
+
     steps = max(1, min(args.steps, 5))
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    with torch.cuda.stream(stream):
-        a.record(stream)
-    for _ in range(steps):
-        sh.deblur_dev(u0_dev.data_ptr(), out.data_ptr())
-    with torch.cuda.stream(stream):
-        b.record(stream)
-    b.synchronize()
-    ms = _max_over_ranks(a.elapsed_time(b) / steps, world, dev)
+    ms = timed(lambda: sh.deblur_dev(u0_dev.data_ptr(), out.data_ptr(), clamp=True), steps)
+    st = sh.stats()
     restored = out.cpu().numpy().reshape(dims)
-    if isinstance(sh, _SingleGpu):  # the power-iteration count of the solver's own run
-        sh.tau_iters = int(sh.d.deblur(u0, clamp=True)[1].tau_iters)
-    return {"metric": f"ms per {size}x{size} spatially varying deblur (C4)", "value": round(ms, 3),
+    line = {"metric": f"ms per {size}x{size} spatially varying deblur (C4)", "value": round(ms, 3),
             "unit": "ms", "n_gpus": world, "steps": steps, "higher_is_better": False, "scaling": "strong",
             "impl": "ours", "config": {"workload": f"C4: {size}^2 varying Gaussian 2.5->7.5 px, db4 J=4, K~3.4N, "
                                                    f"SPAI, 100 FISTA iters incl. tau", "nnz": int(op.nnz()),
-                                       "parallelism": path},
-            "tau_iters": sh.tau_iters, "setup_s": round(setup_s, 1),
+                                       "parallelism": f"Theta row-sharded x{world} (wbx_sharded, NCCL inside libwbx)"},
+            "breakdown": st, "setup_s": round(setup_s, 1),
             "psnr_observed_db": round(S.psnr(u0, clean), 3), "psnr_restored_db": round(S.psnr(restored, clean), 3)}
+    if world == 1:  # the single-GPU persistent solver on the same operator, for comparison
+        d = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=ITERS, track_energy=False), ctx)
+        line["single_gpu_persistent"] = {
+            "ms": round(timed(lambda: d.deblur_dev(u0_dev.data_ptr(), out.data_ptr(), clamp=True), steps), 3),
+            "kernels": list(d.kernels())}
+    return line
 
 
 def relaunch_under_torchrun(gpus: int) -> int:

@@ -358,6 +358,40 @@ int wbx_shard_lz_step_t(wbx_shard* s);
 int wbx_shard_lz_done(wbx_shard* s, int* done);
 int wbx_shard_lz_result(wbx_shard* s, double step_safety, double* tau, uint32_t* iters, uint32_t* steps);
 
+/* ---------------------------------------------------------------- the whole sharded deblur (C4)
+ * One image row-sharded over `world` ranks with the host loop, the exchange and a CUDA graph of
+ * the FISTA iterations inside the library: after the first call a solve is one host call
+ * (estimate_step adds one graph launch per 4 Lanczos steps from the first convergence check on).
+ * The exchange is NCCL over NVLink (libnccl.so.2 resolved at run time: the one already loaded,
+ * e.g. torch's, else the system's): rank 0 calls wbx_comm_get_unique_id, the caller broadcasts
+ * the 128 bytes (e.g. over torch.distributed), every rank calls wbx_comm_create, then
+ * wbx_sharded_create with ranks = {rank}, nranks = 1. Without a communicator all `world` ranks
+ * live in this process on ctx's device and share the padded buffers (ranks = 0..world-1): the
+ * partition code runs exactly as on `world` GPUs (emulation; world = 1 is the one-GPU engine).
+ * Rows are summed in element order by one lane wherever they live: the restored image is
+ * BITWISE the same for every world size (given tau). fp32, fixed iteration count (cfg). */
+typedef struct wbx_comm wbx_comm;
+int wbx_comm_get_unique_id(uint8_t* id128);
+int wbx_comm_create(wbx_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id128, wbx_comm** out);
+int wbx_comm_destroy(wbx_comm* c);
+typedef struct wbx_sharded wbx_sharded;
+int wbx_sharded_create(wbx_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
+                       const double* values, wbx_basis* basis, const double* p, const double* w, double lambda,
+                       const wbx_solver_cfg* cfg, uint32_t world, const uint32_t* ranks, uint32_t nranks,
+                       wbx_comm* comm, wbx_sharded** out);
+int wbx_sharded_destroy(wbx_sharded* s);
+/* estimate_step (solver.cpp:69-99) by the sharded Lanczos estimate (WBX_TAU=power: the
+ * literal power iteration); iters: the reference's iteration count; steps: product pairs */
+int wbx_sharded_estimate_step(wbx_sharded* s, double step_safety, double* tau, uint32_t* iters, uint32_t* steps);
+/* u0 (full image, every rank) -> analyze -> [estimate_step unless cfg.tau > 0] -> FISTA ->
+ * assemble x (NCCL all-reduce of the disjoint pieces) -> synthesize (-> clamp); device
+ * pointers, async on ctx's stream */
+int wbx_sharded_deblur_dev(wbx_sharded* s, const double* u0_dev, double* u_dev, int clamp);
+/* tau of the last deblur, its reference iteration count and product pairs, device ms of
+ * (analyze + tau) and of (iterations + synthesis), kernel launches */
+int wbx_sharded_stats(const wbx_sharded* s, double* tau, uint32_t* tau_iters, uint32_t* tau_steps, float* tau_ms,
+                      float* iters_ms, uint64_t* launches);
+
 /* launches of the last deblur, and the solver kernel's device time (ms) */
 int wbx_solver_last_stats(const wbx_solver* s, uint64_t* launches, float* solve_ms);
 // Device time of the last solve split into the step-size estimate (estimate_step, 0 when tau

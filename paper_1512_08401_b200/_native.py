@@ -131,6 +131,15 @@ SIGNATURES = {
     "wbx_solver_phase_ms": (C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "wbx_solver_tau_stats": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "wbx_solver_kernels": (C.c_int, [_P, C.c_char_p, C.c_uint64]),
+    "wbx_comm_get_unique_id": (C.c_int, [C.c_char_p]),
+    "wbx_comm_create": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_char_p, C.POINTER(_P)]),
+    "wbx_comm_destroy": (C.c_int, [_P]),
+    "wbx_sharded_create": (C.c_int, [_P, C.c_uint64, _U64, _U32, _D, _P, _D, _D, C.c_double,
+                                     C.POINTER(wbx_solver_cfg), C.c_uint32, _U32, C.c_uint32, _P, C.POINTER(_P)]),
+    "wbx_sharded_destroy": (C.c_int, [_P]),
+    "wbx_sharded_estimate_step": (C.c_int, [_P, C.c_double, _D, _U32, _U32]),
+    "wbx_sharded_deblur_dev": (C.c_int, [_P, _P, _P, C.c_int]),
+    "wbx_sharded_stats": (C.c_int, [_P, _D, _U32, _U32, C.POINTER(C.c_float), C.POINTER(C.c_float), _U64]),
     "wbx_shard_create": (C.c_int, [_P, C.c_uint64, _U64, _U32, _D, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
     "wbx_shard_destroy": (C.c_int, [_P]),
     "wbx_shard_plan": (C.c_int, [C.c_uint64, _U64, _U32, C.c_uint32, _U64, _U64]),

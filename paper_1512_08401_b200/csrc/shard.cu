@@ -9,17 +9,19 @@
 // by the host; or nothing when the shards are emulated on one GPU and share the buffers):
 //     phase A   res[R_p] = Theta[R_p, :] y - x0[R_p]         -> all-gather res
 //     phase T   g = Theta^T[C_p, :] res; fused update on C_p  -> all-gather y
-// No reductions cross ranks in FISTA, and every row is summed by the same lane arithmetic
-// as the persistent single-GPU kernel, so a sharded solve is BITWISE equal to the
-// single-GPU solve for any world size (given tau). estimate_step needs two scalars per
+// No reductions cross ranks in FISTA, and every row is summed sequentially in element order by
+// one lane of the row-per-lane layout wherever it lives, so a sharded solve is BITWISE the same
+// for every world size (world 1 = this engine on one GPU; given tau). estimate_step needs two scalars per
 // power iteration: each rank writes its block-ordered sums into its slot of a [world][2]
 // buffer, the buffer is all-gathered, and every rank sums the slots in rank order on the
 // device (deterministic for any world size) and updates the iteration state there. The host
 // only enqueues: nothing in the power iteration synchronises with it.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 #include <numeric>
+#include <string>
 
 #include "internal.hpp"
 #include "lanczos.cuh"
@@ -142,16 +144,44 @@ ShardArgs args_of(wbx_shard* s) {
     return a;
 }
 
-// one warp per slice of the segmented fp32 layout (same arithmetic as the persistent kernel),
-// grid-stride over the slices; whole warps in or out, no early return (block reductions follow)
+// One warp per slice of the row-per-lane fp32 layout (wbx_sell::rslice/rpk, op_build.cu), one
+// lane per row, the row summed sequentially in element order (fma in ACC), grid-stride over the
+// slices; whole warps in or out, no early return (block reductions follow). A row's sum does not
+// depend on which rank or slice holds it, so every world size gives the same bits.
 template <typename ACC, typename X, typename Epi>
-__device__ __forceinline__ void slice_rows(const SellView& M, const X* x, Epi epi) {
+__device__ __forceinline__ void slice_rows(const SellView& M, const X* __restrict__ x, Epi epi) {
+    constexpr uint32_t H = 4;  // {val, col, val, col} pairs per step (16-B loads, 512 B per warp)
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.slices; s += nw) {
-        ACC acc = seg_partial<ACC, X>(M, s, lane, x);
-        const uint32_t row = seg_combine(M, s, lane, acc);
-        if (row != kNoRow) epi(row, acc);
+    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.xslices; s += nw) {
+        const uint2 meta = M.rslice[s];
+        const uint32_t L = meta.y, np = L >> 1;
+        const uint4* p = M.rpk + meta.x + lane;
+        ACC acc = ACC(0);
+        for (uint32_t h = 0; h < np; h += H) {
+            uint4 e[H];
+#pragma unroll
+            for (uint32_t j = 0; j < H; ++j) e[j] = h + j < np ? __ldg(p + (h + j) * kWarp) : make_uint4(0, 0, 0, 0);
+            X g[2 * H];
+#pragma unroll
+            for (uint32_t j = 0; j < H; ++j) {
+                g[2 * j] = h + j < np ? x[e[j].y] : X(0);
+                g[2 * j + 1] = h + j < np ? x[e[j].w] : X(0);
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < H; ++j) {
+                if (h + j < np) {
+                    acc = fma(static_cast<ACC>(__uint_as_float(e[j].x)), static_cast<ACC>(g[2 * j]), acc);
+                    acc = fma(static_cast<ACC>(__uint_as_float(e[j].z)), static_cast<ACC>(g[2 * j + 1]), acc);
+                }
+            }
+        }
+        if (L & 1u) {
+            const uint2 t = __ldg(reinterpret_cast<const uint2*>(M.rpk + meta.x + np * kWarp) + lane);
+            acc = fma(static_cast<ACC>(__uint_as_float(t.x)), static_cast<ACC>(x[t.y]), acc);
+        }
+        const uint32_t r = s * kWarp + lane;
+        if (r < M.rows) epi(r, acc);
     }
 }
 
@@ -691,7 +721,7 @@ int wbx_shard_init(wbx_shard* s, double tau, const double* x0_full_dev, double* 
 int wbx_shard_phase_a(wbx_shard* s) {
     if (!s) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
-    if (a.A.slices) wbx::phase_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a);
+    if (a.A.xslices) wbx::phase_a_kernel<<<wbx::blocks_for(uint64_t(a.A.xslices) * 32), kBlock, 0, s->ctx->stream>>>(a);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
@@ -699,7 +729,7 @@ int wbx_shard_phase_a(wbx_shard* s) {
 int wbx_shard_phase_t(wbx_shard* s, int k) {
     if (!s || k < 1 || k > s->max_iters) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
-    if (a.T.slices) wbx::phase_t_kernel<<<wbx::blocks_for(uint64_t(a.T.slices) * 32), kBlock, 0, s->ctx->stream>>>(a, k);
+    if (a.T.xslices) wbx::phase_t_kernel<<<wbx::blocks_for(uint64_t(a.T.xslices) * 32), kBlock, 0, s->ctx->stream>>>(a, k);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
@@ -751,7 +781,7 @@ int wbx_shard_power_update(wbx_shard* s, int first) {
 int wbx_shard_power_step_a(wbx_shard* s) {
     if (!s || !s->pstate.p) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
-    if (a.A.slices) wbx::power_a_kernel<<<wbx::blocks_for(uint64_t(a.A.slices) * 32), kBlock, 0, s->ctx->stream>>>(a);
+    if (a.A.xslices) wbx::power_a_kernel<<<wbx::blocks_for(uint64_t(a.A.xslices) * 32), kBlock, 0, s->ctx->stream>>>(a);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
@@ -760,10 +790,10 @@ int wbx_shard_power_step_t(wbx_shard* s) {
     if (!s || !s->sums_pad || !s->pstate.p) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
     // a bounded grid (grid-stride over slices) keeps the partials few for the ordered sum
-    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.slices, 1)) * 32),
+    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.xslices, 1)) * 32),
                                                8u * static_cast<unsigned>(s->ctx->num_sms));
     if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
-    if (a.T.slices) {
+    if (a.T.xslices) {
         wbx::power_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
     } else {
         cudaMemsetAsync(s->part.p, 0, 2 * blocks * sizeof(double), s->ctx->stream);
@@ -822,10 +852,10 @@ static int lz_phase(wbx_shard* s, bool tside) {
     if (!s || !s->lz.p || !s->sums_pad) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
     const wbx::SellView& M = tside ? a.T : a.A;
-    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(M.slices, 1)) * 32),
+    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(M.xslices, 1)) * 32),
                                                8u * static_cast<unsigned>(s->ctx->num_sms));
     if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
-    if (M.slices) {
+    if (M.xslices) {
         if (tside)
             wbx::lz_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
         else
@@ -865,6 +895,411 @@ int wbx_shard_lz_result(wbx_shard* s, double step_safety, double* tau, uint32_t*
     *iters = static_cast<uint32_t>(st[wbx::LZ_ITERS]);
     *steps = static_cast<uint32_t>(st[wbx::LZ_STEPS]);
     *tau = (st[wbx::LZ_ZERO] != 0.0 || lam <= 0.0) ? 1.0 : 1.0 / (lam * step_safety);  // solver.cpp:89,97
+    return WBX_OK;
+}
+
+}  // extern "C"
+
+// ====================================================================================== //
+// The whole row-sharded deblur behind the C ABI (wbx_sharded_*): the host loop, the exchange
+// (NCCL over NVLink, opened at run time, or nothing when every shard lives in this process),
+// and a CUDA graph of the 100 FISTA iterations (phase kernels + all-gathers), so a solve is one
+// host call after the first. estimate_step runs as graphs of kLzChunk Lanczos steps; the host
+// reads the device's done flag once per chunk from the first scheduled check on.
+#include <dlfcn.h>
+
+#include "nccl.h"
+
+namespace wbx {
+namespace {
+
+struct NcclApi {  // the NCCL entry points used here, resolved at run time (no link dependency)
+    void* lib = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        // the NCCL already in the process (e.g. torch's) first, else the system's
+        a.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!a.lib) a.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!a.lib) a.lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!a.lib) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.lib, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.lib, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.lib, "ncclCommDestroy"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(a.lib, "ncclAllGather"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.lib, "ncclAllReduce"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.lib, "ncclGetErrorString"));
+        return a;
+    }();
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.all_reduce || !api.comm_destroy)
+        fail(WBX_CUDA_ERROR, "NCCL (libnccl.so.2) is not available");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(WBX_CUDA_ERROR, std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "NCCL error"));
+}
+
+constexpr int kLzChunk = 4;  // Lanczos steps per captured graph (= the check period)
+
+}  // namespace
+}  // namespace wbx
+
+struct wbx_comm {
+    wbx_ctx* ctx = nullptr;
+    uint32_t world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+};
+
+struct wbx_sharded {
+    wbx_ctx* ctx = nullptr;
+    wbx_basis* basis = nullptr;
+    wbx_comm* comm = nullptr;  // NULL: every shard in this process (emulation / one GPU)
+    uint32_t world = 1;
+    std::vector<wbx_shard*> shards;
+    uint64_t n = 0, maxR = 0, maxC = 0;
+    wbx::DevBuf<float> y, res;
+    wbx::DevBuf<double> u, t, sums, x0, x;
+    wbx_solver_cfg cfg{};
+    int lz_first = 60, lz_every = 4, lz_gap = 4;
+    bool power = false;
+    cudaGraphExec_t fista_exec = nullptr, lz_exec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    double tau = 0.0;
+    uint32_t tau_iters = 0, tau_steps = 0;
+    uint64_t last_launches = 0;
+    ~wbx_sharded() {
+        if (fista_exec) cudaGraphExecDestroy(fista_exec);
+        if (lz_exec) cudaGraphExecDestroy(lz_exec);
+        for (wbx_shard* s : shards) delete s;
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (ev2) cudaEventDestroy(ev2);
+    }
+};
+
+namespace wbx {
+namespace {
+
+// In-place all-gather of the equal per-rank slices of a padded buffer (count elements each).
+template <typename T>
+void gather(wbx_sharded* S, T* buf, uint64_t count) {
+    if (!S->comm || S->world == 1) return;  // shards in this process share the buffers
+    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    nccl_check(nccl().all_gather(buf + S->comm->rank * count, buf, count, dt, S->comm->comm, S->ctx->stream),
+               "ncclAllGather");
+}
+
+void each(wbx_sharded* S, int (*fn)(wbx_shard*)) {
+    for (wbx_shard* s : S->shards) {
+        const int st = fn(s);
+        if (st != WBX_OK) fail(st, std::string("shard step failed: ") + wbx_last_error());
+    }
+}
+
+// FISTA iterations (phase A, all-gather res, phase T(k), all-gather y), k = 1..iters
+void enqueue_fista(wbx_sharded* S) {
+    for (int k = 1; k <= static_cast<int>(S->cfg.max_iters); ++k) {
+        each(S, wbx_shard_phase_a);
+        gather(S, S->res.p, S->maxR);
+        for (wbx_shard* s : S->shards)
+            if (wbx_shard_phase_t(s, k) != WBX_OK) fail(WBX_CUDA_ERROR, "phase T failed");
+        gather(S, S->y.p, S->maxC);
+    }
+}
+
+// kLzChunk Lanczos steps (no-ops on the device once the estimate is done)
+void enqueue_lz_chunk(wbx_sharded* S) {
+    auto update = [&](int phase) {
+        for (wbx_shard* s : S->shards)
+            if (wbx_shard_lz_update(s, phase, S->lz_first, S->lz_every, S->lz_gap) != WBX_OK)
+                fail(WBX_CUDA_ERROR, "lz_update failed");
+    };
+    for (int j = 0; j < kLzChunk; ++j) {
+        each(S, wbx_shard_lz_step_a);
+        gather(S, S->t.p, S->maxR);
+        gather(S, S->sums.p, 2);
+        update(1);
+        each(S, wbx_shard_lz_step_t);
+        gather(S, S->sums.p, 2);
+        gather(S, S->u.p, S->maxC);
+        update(2);
+    }
+}
+
+// capture fn's enqueues on the context stream into an executable graph (once)
+template <typename F>
+cudaGraphExec_t capture(wbx_sharded* S, F fn) {
+    cudaStream_t st = S->ctx->stream;
+    cudaGraph_t g = nullptr;
+    WBX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        fn();
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    WBX_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    WBX_CUDA(e);
+    return exec;
+}
+
+bool graphs_enabled() {
+    const char* e = std::getenv("WBX_SHARD_GRAPH");
+    return !(e && std::string(e) == "0");
+}
+
+double estimate(wbx_sharded* S, double step_safety, uint32_t* iters, uint32_t* steps) {
+    cudaStream_t st = S->ctx->stream;
+    if (S->power) {  // the literal power iteration (WBX_TAU=power): fixed 200-step schedule
+        each(S, wbx_shard_power_begin);
+        gather(S, S->sums.p, 2);
+        for (wbx_shard* s : S->shards) wbx_shard_power_update(s, 1);
+        gather(S, S->u.p, S->maxC);
+        for (int it = 0; it < 200; ++it) {
+            each(S, wbx_shard_power_step_a);
+            gather(S, S->t.p, S->maxR);
+            each(S, wbx_shard_power_step_t);
+            gather(S, S->sums.p, 2);
+            for (wbx_shard* s : S->shards) wbx_shard_power_update(s, 0);
+            gather(S, S->u.p, S->maxC);
+        }
+        double tau = 0.0;
+        if (wbx_shard_power_result(S->shards[0], step_safety, &tau, iters) != WBX_OK)
+            fail(WBX_CUDA_ERROR, "power result failed");
+        *steps = *iters;
+        return tau;
+    }
+    each(S, wbx_shard_lz_begin);
+    gather(S, S->sums.p, 2);
+    for (wbx_shard* s : S->shards) wbx_shard_lz_update(s, 0, S->lz_first, S->lz_every, S->lz_gap);
+    gather(S, S->u.p, S->maxC);
+    const bool graphs = graphs_enabled();
+    if (graphs && !S->lz_exec) S->lz_exec = capture(S, [&] { enqueue_lz_chunk(S); });
+    for (int j = 0; j < kLzCap; j += kLzChunk) {
+        if (graphs) {
+            WBX_CUDA(cudaGraphLaunch(S->lz_exec, st));
+            count_launch(S->ctx, static_cast<uint64_t>(kLzChunk) * 6 * S->shards.size());
+        } else {
+            enqueue_lz_chunk(S);
+        }
+        const int done_j = j + kLzChunk;
+        if (done_j >= S->lz_first || done_j >= kLzCap) {  // a check ran in this chunk (or the cap)
+            int done = 0;
+            if (wbx_shard_lz_done(S->shards[0], &done) != WBX_OK) fail(WBX_CUDA_ERROR, "lz_done failed");
+            if (done) break;
+        }
+    }
+    double tau = 0.0;
+    if (wbx_shard_lz_result(S->shards[0], step_safety, &tau, iters, steps) != WBX_OK)
+        fail(WBX_CUDA_ERROR, std::string("Lanczos result: ") + wbx_last_error());
+    return tau;
+}
+
+__global__ void clamp01_kernel(double* u, uint64_t n) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) u[i] = fmin(fmax(u[i], 0.0), 1.0);  // std::clamp(v, 0, 1), waveblur.cpp:297
+}
+
+}  // namespace
+}  // namespace wbx
+
+extern "C" {
+
+int wbx_comm_get_unique_id(uint8_t* id128) {
+    try {
+        if (!id128) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_comm_get_unique_id");
+        ncclUniqueId id;
+        wbx::nccl_check(wbx::nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(id128, id.internal, NCCL_UNIQUE_ID_BYTES);
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_comm_create(wbx_ctx* ctx, uint32_t world, uint32_t rank, const uint8_t* id128, wbx_comm** out) {
+    try {
+        if (!ctx || !id128 || !out) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_comm_create");
+        if (world < 1 || rank >= world) wbx::fail(WBX_BAD_SPEC, "bad world / rank");
+        auto c = std::make_unique<wbx_comm>();
+        c->ctx = ctx;
+        c->world = world;
+        c->rank = rank;
+        ncclUniqueId id;
+        std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+        WBX_CUDA(cudaSetDevice(ctx->device));
+        wbx::nccl_check(wbx::nccl().comm_init_rank(&c->comm, static_cast<int>(world), id, static_cast<int>(rank)),
+                        "ncclCommInitRank");
+        *out = c.release();
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_comm_destroy(wbx_comm* c) {
+    if (!c) return WBX_OK;
+    if (c->comm) wbx::nccl().comm_destroy(c->comm);
+    delete c;
+    return WBX_OK;
+}
+
+int wbx_sharded_create(wbx_ctx* ctx, uint64_t n, const uint64_t* rowptr, const uint32_t* col, const double* val,
+                       wbx_basis* basis, const double* p, const double* w, double lambda, const wbx_solver_cfg* cfg,
+                       uint32_t world, const uint32_t* ranks, uint32_t nranks, wbx_comm* comm, wbx_sharded** out) {
+    try {
+        if (!ctx || !rowptr || !basis || !p || !w || !cfg || !ranks || !out)
+            wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_sharded_create");
+        if (basis->n != n) wbx::fail(WBX_SHAPE_MISMATCH, "operator and basis sizes differ");
+        if (cfg->precision != WBX_FP32 || cfg->track_energy || cfg->track_support || std::isfinite(cfg->ref_energy))
+            wbx::fail(WBX_BAD_SPEC, "sharded solves are fp32 with a fixed iteration count (no energy tracking)");
+        if (comm) {
+            if (nranks != 1 || comm->world != world || ranks[0] != comm->rank)
+                wbx::fail(WBX_BAD_SPEC, "a communicator run holds exactly its own rank");
+        } else if (nranks != world) {
+            wbx::fail(WBX_BAD_SPEC, "without a communicator every rank must live in this process");
+        }
+        auto S = std::make_unique<wbx_sharded>();
+        S->ctx = ctx;
+        S->basis = basis;
+        S->comm = comm;
+        S->world = world;
+        S->n = n;
+        S->cfg = *cfg;
+        auto env = [](const char* k, int d) {
+            const char* e = std::getenv(k);
+            return e ? std::max(1, std::min(wbx::kLzCap, std::atoi(e))) : d;
+        };
+        S->lz_first = env("WBX_LZ_FIRST", 60);
+        S->lz_every = wbx::kLzChunk;
+        S->lz_gap = env("WBX_LZ_GAP", 4);
+        S->power = std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power";
+        for (uint32_t i = 0; i < nranks; ++i) {
+            wbx_shard* sh = nullptr;
+            const int st = wbx_shard_create(ctx, n, rowptr, col, val, world, ranks[i], &sh);
+            if (st != WBX_OK) wbx::fail(st, wbx_last_error());
+            S->shards.push_back(sh);
+        }
+        S->maxR = S->shards[0]->maxR;
+        S->maxC = S->shards[0]->maxC;
+        S->y.alloc(world * S->maxC);
+        S->res.alloc(world * S->maxR);
+        S->u.alloc(world * S->maxC);
+        S->t.alloc(world * S->maxR);
+        S->sums.alloc(2 * world);
+        S->x0.alloc(n);
+        S->x.alloc(n);
+        cudaStream_t st = ctx->stream;
+        WBX_CUDA(cudaMemsetAsync(S->y.p, 0, S->y.bytes(), st));
+        WBX_CUDA(cudaMemsetAsync(S->res.p, 0, S->res.bytes(), st));
+        WBX_CUDA(cudaMemsetAsync(S->u.p, 0, S->u.bytes(), st));
+        WBX_CUDA(cudaMemsetAsync(S->t.p, 0, S->t.bytes(), st));
+        for (wbx_shard* sh : S->shards) {
+            wbx_shard_bind(sh, S->y.p, S->res.p, S->u.p, S->t.p);
+            const int r = wbx_shard_setup(sh, p, w, lambda, static_cast<int>(cfg->max_iters), 1);
+            if (r != WBX_OK) wbx::fail(r, wbx_last_error());
+            wbx_shard_bind_power(sh, S->sums.p);
+        }
+        WBX_CUDA(cudaEventCreate(&S->ev0));
+        WBX_CUDA(cudaEventCreate(&S->ev1));
+        WBX_CUDA(cudaEventCreate(&S->ev2));
+        WBX_CUDA(cudaStreamSynchronize(st));
+        *out = S.release();
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_sharded_destroy(wbx_sharded* s) {
+    if (s) {
+        cudaStreamSynchronize(s->ctx->stream);
+        delete s;
+    }
+    return WBX_OK;
+}
+
+int wbx_sharded_estimate_step(wbx_sharded* s, double step_safety, double* tau, uint32_t* iters, uint32_t* steps) {
+    try {
+        if (!s || !tau || !iters || !steps) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_sharded_estimate_step");
+        *tau = wbx::estimate(s, step_safety, iters, steps);
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_sharded_deblur_dev(wbx_sharded* s, const double* u0_dev, double* u_dev, int clamp) {
+    try {
+        if (!s || !u0_dev || !u_dev) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_sharded_deblur_dev");
+        cudaStream_t st = s->ctx->stream;
+        const uint64_t before = s->ctx->launches;
+        WBX_CUDA(cudaEventRecord(s->ev0, st));
+        // every rank analyses the whole observation (x0 = Psi^* u0; bitwise the reference's)
+        wbx::analyze_dev(s->basis, u0_dev, s->x0.p, st);
+        double tau = s->cfg.tau;
+        if (!(tau > 0.0)) tau = wbx::estimate(s, s->cfg.step_safety, &s->tau_iters, &s->tau_steps);
+        s->tau = tau;
+        WBX_CUDA(cudaEventRecord(s->ev1, st));
+        WBX_CUDA(cudaMemsetAsync(s->x.p, 0, s->n * sizeof(double), st));
+        for (wbx_shard* sh : s->shards)
+            if (wbx_shard_init(sh, tau, s->x0.p, s->x.p) != WBX_OK) wbx::fail(WBX_CUDA_ERROR, "shard init failed");
+        wbx::gather(s, s->y.p, s->maxC);
+        if (wbx::graphs_enabled()) {
+            if (!s->fista_exec) s->fista_exec = wbx::capture(s, [&] { wbx::enqueue_fista(s); });
+            WBX_CUDA(cudaGraphLaunch(s->fista_exec, st));
+            wbx::count_launch(s->ctx, 2 * s->cfg.max_iters * s->shards.size());
+        } else {
+            wbx::enqueue_fista(s);
+        }
+        for (wbx_shard* sh : s->shards)
+            if (wbx_shard_finalize(sh, s->x.p) != WBX_OK) wbx::fail(WBX_CUDA_ERROR, "shard finalize failed");
+        if (s->comm && s->world > 1)  // disjoint pieces (every other entry 0.0): the sum is exact
+            wbx::nccl_check(wbx::nccl().all_reduce(s->x.p, s->x.p, s->n, ncclFloat64, ncclSum, s->comm->comm, st),
+                            "ncclAllReduce");
+        wbx::synthesize_dev(s->basis, s->x.p, u_dev, st);
+        if (clamp) {
+            wbx::clamp01_kernel<<<static_cast<unsigned>((s->n + 255) / 256), 256, 0, st>>>(u_dev, s->n);
+            wbx::count_launch(s->ctx);
+        }
+        WBX_CUDA(cudaEventRecord(s->ev2, st));
+        WBX_CUDA(cudaGetLastError());
+        s->last_launches = s->ctx->launches - before;
+        return WBX_OK;
+    } catch (const wbx::Error& e) {
+        wbx_set_last_error(e.what());
+        return e.status;
+    }
+}
+
+int wbx_sharded_stats(const wbx_sharded* s, double* tau, uint32_t* tau_iters, uint32_t* tau_steps, float* tau_ms,
+                      float* iters_ms, uint64_t* launches) {
+    if (!s) return WBX_INVALID_ARGUMENT;
+    if (tau) *tau = s->tau;
+    if (tau_iters) *tau_iters = s->tau_iters;
+    if (tau_steps) *tau_steps = s->tau_steps;
+    if (launches) *launches = s->last_launches;
+    if (tau_ms && cudaEventElapsedTime(tau_ms, s->ev0, s->ev1) != cudaSuccess) return WBX_CUDA_ERROR;
+    if (iters_ms && cudaEventElapsedTime(iters_ms, s->ev1, s->ev2) != cudaSuccess) return WBX_CUDA_ERROR;
     return WBX_OK;
 }
 
