@@ -289,17 +289,25 @@ __global__ void power_t_kernel(ShardArgs a) {
     }
 }
 
-// this rank's sums: block partials in block order -> sums_pad[rank]
-__global__ void rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
-    if (!init && a.pstate[3] != 0.0) return;
-    if (threadIdx.x != 0) return;
+// this rank's sums: the block partials folded by one warp (lane-strided sums, then a fixed
+// shuffle tree: deterministic) -> sums_pad[rank]
+__device__ __forceinline__ void warp_rank_sums(const ShardArgs& a, unsigned blocks) {
     double s0 = 0.0, s1 = 0.0;
-    for (unsigned i = 0; i < blocks; ++i) {
+    for (unsigned i = threadIdx.x; i < blocks; i += 32) {
         s0 += a.part[2 * i];
         s1 += a.part[2 * i + 1];
     }
-    a.sums_pad[2 * a.rank] = s0;
-    a.sums_pad[2 * a.rank + 1] = s1;
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (threadIdx.x == 0) {
+        a.sums_pad[2 * a.rank] = s0;
+        a.sums_pad[2 * a.rank + 1] = s1;
+    }
+}
+
+__global__ void rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
+    if (!init && a.pstate[3] != 0.0) return;
+    warp_rank_sums(a, blocks);
 }
 
 // stopping rule of estimate_step (solver.cpp:84-95) on the all-gathered sums, rank order
@@ -410,14 +418,7 @@ __global__ void lz_t_kernel(ShardArgs a) {
 
 __global__ void lz_rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
     if (!init && a.lz[LZ_DONE] != 0.0) return;
-    if (threadIdx.x != 0) return;
-    double s0 = 0.0, s1 = 0.0;
-    for (unsigned i = 0; i < blocks; ++i) {
-        s0 += a.part[2 * i];
-        s1 += a.part[2 * i + 1];
-    }
-    a.sums_pad[2 * a.rank] = s0;
-    a.sums_pad[2 * a.rank + 1] = s1;
+    warp_rank_sums(a, blocks);
 }
 
 // on the all-gathered sums (rank order, every rank alike): phase 0 starts the estimate,
@@ -691,9 +692,12 @@ int wbx_shard_setup(wbx_shard* s, const double* p, const double* w, double lambd
         s->thr.alloc(nC);
         s->wv.alloc(nC);
         s->x0R.alloc(std::max<uint64_t>(1, s->rhi - s->rlo));
-        // per-block partials of the reductions: every launch's grid is capped at 8 CTAs per SM
-        // (power / Lanczos phases on either side) or is 2 per SM (init)
-        s->part.alloc(2 * 8 * static_cast<uint64_t>(s->ctx->num_sms));
+        // per-block partials of the reductions: the phase kernels run one warp per slice (the
+        // full grid of either side), init 2 CTAs per SM
+        const uint64_t gmax = std::max<uint64_t>({wbx::blocks_for(uint64_t(s->A.xslices) * 32),
+                                                  wbx::blocks_for(uint64_t(s->T.xslices) * 32),
+                                                  2 * static_cast<uint64_t>(s->ctx->num_sms)});
+        s->part.alloc(2 * gmax);
         s->lambda = lambda;
         s->max_iters = max_iters;
         WBX_CUDA(cudaStreamSynchronize(st));
@@ -790,8 +794,7 @@ int wbx_shard_power_step_t(wbx_shard* s) {
     if (!s || !s->sums_pad || !s->pstate.p) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
     // a bounded grid (grid-stride over slices) keeps the partials few for the ordered sum
-    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.xslices, 1)) * 32),
-                                               8u * static_cast<unsigned>(s->ctx->num_sms));
+    const unsigned blocks = wbx::blocks_for(uint64_t(std::max<uint32_t>(a.T.xslices, 1)) * 32);
     if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
     if (a.T.xslices) {
         wbx::power_t_kernel<<<blocks, kBlock, 0, s->ctx->stream>>>(a);
@@ -852,8 +855,7 @@ static int lz_phase(wbx_shard* s, bool tside) {
     if (!s || !s->lz.p || !s->sums_pad) return WBX_INVALID_ARGUMENT;
     wbx::ShardArgs a = wbx::args_of(s);
     const wbx::SellView& M = tside ? a.T : a.A;
-    const unsigned blocks = std::min<unsigned>(wbx::blocks_for(uint64_t(std::max<uint32_t>(M.xslices, 1)) * 32),
-                                               8u * static_cast<unsigned>(s->ctx->num_sms));
+    const unsigned blocks = wbx::blocks_for(uint64_t(std::max<uint32_t>(M.xslices, 1)) * 32);
     if (2ull * blocks > s->part.n) return WBX_TOO_LARGE;
     if (M.xslices) {
         if (tside)

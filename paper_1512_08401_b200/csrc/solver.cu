@@ -492,7 +492,8 @@ __device__ __forceinline__ void for_rows(const SellView& M, const Plan& plan, ui
 // is prox + momentum only. Runs K iterations per coordinate in registers and stops as
 // soon as x' == x_prev == 0 (then y == 0 forever: a fixed point).
 // mode 0: write x_K into x_full.  mode 1: per-iteration warp sums of w|x_k| and
-// [x_k != 0] into w*[(k-1) * nwarps + gwarp] (deterministic, no atomics).
+// [x_k != 0] into w*[(k-1) * nwarps + gwarp] (deterministic, no atomics). mode 2: both
+// (the iteration count is known in advance: no ref_energy rule).
 template <typename T>
 __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, uint64_t gthread,
                                uint64_t nthreads, double* wreg, double* wsup, uint64_t nwarps) {
@@ -532,6 +533,7 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
                     const bool fixed = xn == T(0) && xp == T(0);
                     y = Prec<T>::momentum(xn, xp, Prec<T>::beta(a, k));
                     xp = xn;
+                    x = xn;
                     reg = w * fabs(static_cast<double>(xn));
                     sup = xn != T(0) ? 1.0 : 0.0;
                     if (fixed) live = false;
@@ -544,6 +546,7 @@ __device__ void decoupled_pass(const SolveArgs& a, double tau, int K, int mode, 
                 }
                 if (!__any_sync(0xffffffffu, live)) break;
             }
+            if (mode == 2 && active) a.x_full[i] = static_cast<double>(x);
         }
     }
 }
@@ -2039,13 +2042,16 @@ __global__ void __launch_bounds__(kBlock) decoupled_kernel(SolveArgs a, int mode
     decoupled_pass<T>(a, tau, K, mode, gthread, nthreads, wreg, wsup, nthreads / 32);
 }
 
-// wreg/wsup [K][nwarps] -> dec_reg/dec_supp [K], fixed order
+// wreg/wsup [K][nwarps] -> dec_reg/dec_supp [K]: one warp per k, lane-strided partial sums
+// folded by a fixed shuffle tree (deterministic)
 __global__ void reduce_rows_kernel(const double* w, uint64_t nwarps, int K, double* outp) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (k >= K) return;
     double s = 0.0;
-    for (uint64_t j = 0; j < nwarps; ++j) s += w[static_cast<uint64_t>(k) * nwarps + j];
-    outp[k] = s;
+    for (uint64_t j = lane; j < nwarps; j += 32) s += w[static_cast<uint64_t>(k) * nwarps + j];
+    s = warp_sum(s);
+    if (lane == 0) outp[k] = s;
 }
 
 __global__ void set_tau_kernel(double* out, double tau) {
@@ -2097,6 +2103,14 @@ struct wbx_solver {
     bool input_pending = false;          // ev_in marks a pending copy of the input image
     uint64_t last_launches = 0;
     float last_solve_ms = 0.f;
+    // CUDA graphs of the deblur (WBX_GRAPH=0 disables): the step estimate, and analyze +
+    // iterations + synthesize (+ clamp) for the last (u0, u, clamp) pointers
+    cudaGraphExec_t g_tau = nullptr, g_rest = nullptr;
+    const double* g_u0 = nullptr;
+    double* g_u = nullptr;
+    int g_clamp = -1;
+    uint64_t g_tau_launches = 0, g_rest_launches = 0;
+    bool graphs_off = false;
 };
 
 namespace wbx {
@@ -2284,9 +2298,10 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     if (K > 0) {
         WBX_CUDA(cudaMemsetAsync(s->wreg.p, 0, s->wreg.bytes(), st));
         WBX_CUDA(cudaMemsetAsync(s->wsup.p, 0, s->wsup.bytes(), st));
-        decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, 1, s->wreg.p, s->wsup.p, s->out.p);
-        reduce_rows_kernel<<<(K + 127) / 128, 128, 0, st>>>(s->wreg.p, nwarps, K, s->dec_reg.p);
-        reduce_rows_kernel<<<(K + 127) / 128, 128, 0, st>>>(s->wsup.p, nwarps, K, s->dec_supp.p);
+        // without the ref_energy rule the iteration count is known: one pass also writes x_K
+        decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, a.stop_on_ref ? 1 : 2, s->wreg.p, s->wsup.p, s->out.p);
+        reduce_rows_kernel<<<(K * 32 + 255) / 256, 256, 0, st>>>(s->wreg.p, nwarps, K, s->dec_reg.p);
+        reduce_rows_kernel<<<(K * 32 + 255) / 256, 256, 0, st>>>(s->wsup.p, nwarps, K, s->dec_supp.p);
         count_launch(ctx, 3);
     }
     if (s->win_track) {  // the window engine with energy / support tracking
@@ -2296,8 +2311,11 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
     }
-    decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, 0, nullptr, nullptr, s->out.p);
-    count_launch(ctx, 2);
+    count_launch(ctx);
+    if (a.stop_on_ref || K == 0) {  // x_K of the decoupled coordinates at the count actually used
+        decoupled_kernel<T><<<s->dec_grid, kBlock, 0, st>>>(a, 0, nullptr, nullptr, s->out.p);
+        count_launch(ctx);
+    }
     WBX_CUDA(cudaGetLastError());
 }
 
@@ -2491,22 +2509,22 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
 // while the image is still being copied in) and the iterations, each bracketed by events.
 void solver_tau(wbx_solver* s) {
     cudaStream_t st = s->ctx->stream;
-    WBX_CUDA(cudaEventRecord(s->ev0, st));
+    WBX_CUDA(cudaEventRecordWithFlags(s->ev0, st, cudaEventRecordExternal));
     if (s->cfg.precision == WBX_FP64)
         run_tau<double>(s, s->x0full.p, s->xfull.p, st);
     else
         run_tau<float>(s, s->x0full.p, s->xfull.p, st);
-    WBX_CUDA(cudaEventRecord(s->ev_mid, st));
+    WBX_CUDA(cudaEventRecordWithFlags(s->ev_mid, st, cudaEventRecordExternal));
 }
 
 void solver_iters(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
     cudaStream_t st = s->ctx->stream;
-    WBX_CUDA(cudaEventRecord(s->ev_it0, st));
+    WBX_CUDA(cudaEventRecordWithFlags(s->ev_it0, st, cudaEventRecordExternal));
     if (s->cfg.precision == WBX_FP64)
         run_iters<double>(s, x0_full_dev, x_full_dev, st);
     else
         run_iters<float>(s, x0_full_dev, x_full_dev, st);
-    WBX_CUDA(cudaEventRecord(s->ev1, st));
+    WBX_CUDA(cudaEventRecordWithFlags(s->ev1, st, cudaEventRecordExternal));
 }
 
 void solver_run(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
@@ -2589,6 +2607,8 @@ void solver_free(wbx_solver* s) {
     if (s->ev_it0) cudaEventDestroy(s->ev_it0);
     if (s->ev_in) cudaEventDestroy(s->ev_in);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    if (s->g_tau) cudaGraphExecDestroy(s->g_tau);
+    if (s->g_rest) cudaGraphExecDestroy(s->g_rest);
     delete s;
 }
 
@@ -2602,6 +2622,47 @@ void solver_alloc_images(wbx_solver* s) {
 
 }  // namespace wbx
 
+namespace {
+
+// enqueue the image-dependent part of a deblur: analyze -> iterations -> synthesize (-> clamp)
+void deblur_rest(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp, cudaStream_t st) {
+    const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
+    for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
+    wbx::solver_iters(s, s->x0full.p, s->xfull.p);
+    for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st);
+    if (clamp) wbx::launch_clamp(s->ctx, u_dev, n * B, st);
+}
+
+// capture fn's enqueues on st into an executable graph; counts the kernels it enqueued
+template <typename F>
+cudaGraphExec_t capture_graph(wbx_solver* s, cudaStream_t st, uint64_t* launches, F fn) {
+    const uint64_t before = s->ctx->launches;
+    cudaGraph_t g = nullptr;
+    WBX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        fn();
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    WBX_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    WBX_CUDA(e);
+    *launches = s->ctx->launches - before;
+    s->ctx->launches = before;  // counted again at every replay
+    return exec;
+}
+
+bool graphs_wanted(const wbx_solver* s) {
+    static const bool off = std::getenv("WBX_GRAPH") && std::string(std::getenv("WBX_GRAPH")) == "0";
+    return !off && !s->graphs_off && !s->trace.p;
+}
+
+}  // namespace
+
 extern "C" {
 
 int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp) {
@@ -2609,16 +2670,40 @@ int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp
         if (!s || !u0_dev || !u_dev) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_deblur_dev");
         cudaStream_t st = s->ctx->stream;
         const uint64_t before = s->ctx->launches;
-        const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
-        wbx::solver_tau(s);  // image-independent: first, so a pending image copy overlaps it
-        if (s->input_pending) {
-            WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
-            s->input_pending = false;
+        if (graphs_wanted(s)) {
+            // two graphs: the image-independent step estimate first (a pending host->device
+            // image copy overlaps it), then the image-dependent rest; ~20 launches -> 2
+            try {
+                if (!s->g_tau) s->g_tau = capture_graph(s, st, &s->g_tau_launches, [&] { wbx::solver_tau(s); });
+                if (!s->g_rest || s->g_u0 != u0_dev || s->g_u != u_dev || s->g_clamp != clamp) {
+                    if (s->g_rest) cudaGraphExecDestroy(s->g_rest);
+                    s->g_rest = nullptr;
+                    s->g_rest = capture_graph(s, st, &s->g_rest_launches, [&] { deblur_rest(s, u0_dev, u_dev, clamp, st); });
+                    s->g_u0 = u0_dev;
+                    s->g_u = u_dev;
+                    s->g_clamp = clamp;
+                }
+            } catch (const wbx::Error&) {  // capture not supported here: enqueue directly from now on
+                cudaGetLastError();
+                s->graphs_off = true;
+            }
         }
-        for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
-        wbx::solver_iters(s, s->x0full.p, s->xfull.p);
-        for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st);
-        if (clamp) wbx::launch_clamp(s->ctx, u_dev, n * B, st);
+        if (graphs_wanted(s)) {
+            WBX_CUDA(cudaGraphLaunch(s->g_tau, st));
+            if (s->input_pending) {
+                WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
+                s->input_pending = false;
+            }
+            WBX_CUDA(cudaGraphLaunch(s->g_rest, st));
+            s->ctx->launches += s->g_tau_launches + s->g_rest_launches;
+        } else {
+            wbx::solver_tau(s);  // image-independent: first, so a pending image copy overlaps it
+            if (s->input_pending) {
+                WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
+                s->input_pending = false;
+            }
+            deblur_rest(s, u0_dev, u_dev, clamp, st);
+        }
         WBX_CUDA(cudaGetLastError());
         s->last_launches = s->ctx->launches - before;
         return WBX_OK;
