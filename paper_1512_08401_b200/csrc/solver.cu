@@ -2505,26 +2505,37 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     WBX_CUDA(cudaStreamSynchronize(st));
 }
 
+// Timing events: inside a captured graph they must be external event-record nodes (so the
+// replay records them); outside a capture, plain records.
+void record_event(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    WBX_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+        WBX_CUDA(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+    else
+        WBX_CUDA(cudaEventRecord(ev, st));
+}
+
 // Step estimate (independent of the image: it can run before the image is analysed, e.g.
 // while the image is still being copied in) and the iterations, each bracketed by events.
 void solver_tau(wbx_solver* s) {
     cudaStream_t st = s->ctx->stream;
-    WBX_CUDA(cudaEventRecordWithFlags(s->ev0, st, cudaEventRecordExternal));
+    record_event(s->ev0, st);
     if (s->cfg.precision == WBX_FP64)
         run_tau<double>(s, s->x0full.p, s->xfull.p, st);
     else
         run_tau<float>(s, s->x0full.p, s->xfull.p, st);
-    WBX_CUDA(cudaEventRecordWithFlags(s->ev_mid, st, cudaEventRecordExternal));
+    record_event(s->ev_mid, st);
 }
 
 void solver_iters(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
     cudaStream_t st = s->ctx->stream;
-    WBX_CUDA(cudaEventRecordWithFlags(s->ev_it0, st, cudaEventRecordExternal));
+    record_event(s->ev_it0, st);
     if (s->cfg.precision == WBX_FP64)
         run_iters<double>(s, x0_full_dev, x_full_dev, st);
     else
         run_iters<float>(s, x0_full_dev, x_full_dev, st);
-    WBX_CUDA(cudaEventRecordWithFlags(s->ev1, st, cudaEventRecordExternal));
+    record_event(s->ev1, st);
 }
 
 void solver_run(wbx_solver* s, const double* x0_full_dev, double* x_full_dev) {
