@@ -77,6 +77,7 @@ struct Sync {
     unsigned long long* trace;  // optional [trace_cap][grid][2] globaltimer stamps
     unsigned trace_cap;
     int mode;  // 0: master block releases, 1: every block polls all arrivals, 2: counter (default)
+    int groups;  // counter barrier: arrival counters (one 128-B line each; block b uses b % groups)
 };
 
 struct SolveArgs {
@@ -196,17 +197,31 @@ struct Epoch {
 // Counter barrier (mode 2): one arrival counter, zeroed by the host before each cooperative
 // launch; barrier k of the launch completes when the counter reaches k * G. Arrival is a
 // fire-and-forget reduction, and every block polls the one word directly (no master hop).
-constexpr unsigned kCounterWord = 32;  // Sync::gen[kCounterWord], its own 128-B line
+constexpr unsigned kCounterWord = 32;  // Sync::gen[kCounterWord + 32 g]: counter g, its own 128-B line
+constexpr int kMaxCounterGroups = 16;
 
+// Warp 0 of every block (all 32 lanes call it): arrive on the block's group counter, then wait
+// until every group counter has reached its share of k * G. With groups > 1 the arrivals spread
+// over several L2 lines (the same-address reductions of one counter serialise at its L2 slice);
+// lane g polls counter g, one round trip per poll round.
 __device__ __forceinline__ void counter_arrive_wait(const Sync& s, const Epoch& e) {
     unsigned* cnt = s.gen + kCounterWord;
-    asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-    const unsigned target = (e.cur - e.start) * gridDim.x;
+    const int ng = s.groups;
+    const unsigned G = gridDim.x, k = e.cur - e.start;
+    const unsigned lane = threadIdx.x & 31;
+    if (lane == 0)
+        asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + 32u * (blockIdx.x % ng))
+                     : "memory");
+    const unsigned members = G / ng + (lane < G % ng ? 1u : 0u);
+    const unsigned target = k * members;
+    bool ok;
     // acquiring polls: measured faster than relaxed polls + one acquire fence (the fence
     // costs more than the per-poll L1 invalidations)
-    while (static_cast<int>(ld_acquire(cnt) - target) < 0) {
-        if (WBX_POLL_NS) __nanosleep(WBX_POLL_NS);
-    }
+    do {
+        ok = true;
+        if (lane < static_cast<unsigned>(ng)) ok = static_cast<int>(ld_acquire(cnt + 32u * lane) - target) >= 0;
+        if (WBX_POLL_NS && !__all_sync(0xffffffffu, ok)) __nanosleep(WBX_POLL_NS);
+    } while (!__all_sync(0xffffffffu, ok));
 }
 
 // Optional phase trace (WBX_TRACE_FILE): per barrier and block, the time the block
@@ -238,7 +253,7 @@ __device__ __forceinline__ void grid_sync_reduce(const Sync& s, Epoch& epoch, do
     trace_point(s, epoch, 0);
     if (s.mode == 2) {  // counter barrier, then every block reduces the partials itself
         __syncthreads();
-        if (threadIdx.x == 0) counter_arrive_wait(s, epoch);
+        if (threadIdx.x < 32) counter_arrive_wait(s, epoch);
         __syncthreads();
         if (threadIdx.x < 32) {
 #pragma unroll
@@ -304,7 +319,7 @@ __device__ __forceinline__ void grid_sync(const Sync& s, Epoch& epoch, double* s
     __syncthreads();
     trace_point(s, epoch, 0);
     if (s.mode == 2) {
-        if (threadIdx.x == 0) counter_arrive_wait(s, epoch);
+        if (threadIdx.x < 32) counter_arrive_wait(s, epoch);
         trace_point(s, epoch, 1);
         __syncthreads();
         return;
@@ -2213,6 +2228,7 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     {
         const char* e = std::getenv("WBX_BARRIER");
         a.sync.mode = !e ? 2 : std::string(e) == "allpoll" ? 1 : std::string(e) == "master" ? 0 : 2;
+        a.sync.groups = env_int("WBX_BARRIER_GROUPS", 1, 1, kMaxCounterGroups);
     }
     return a;
 }
@@ -2231,7 +2247,7 @@ const void* tau_win_fn(bool dict, bool w64, bool lanczos = false) {
 void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st,
                       int block = kBlock) {
     if (a.sync.mode == 2)  // the counter barrier counts from zero in every launch
-        WBX_CUDA(cudaMemsetAsync(a.sync.gen + kCounterWord, 0, sizeof(unsigned), st));
+        WBX_CUDA(cudaMemsetAsync(a.sync.gen + kCounterWord, 0, 32u * kMaxCounterGroups * sizeof(unsigned), st));
     void* params[] = {&a};
     WBX_CUDA(cudaLaunchCooperativeKernel(kernel, dim3(grid), dim3(block), params, smem, st));
 }
@@ -2475,7 +2491,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     s->t64.alloc(op->nR ? op->nR : 1);
     s->out.alloc(OUT_COUNT);
     const uint64_t gmax = static_cast<uint64_t>(std::max({s->grid_fista, s->grid_tau, s->grid_tau_lz, s->grid_win}));
-    s->gen.alloc(64);
+    s->gen.alloc(kCounterWord + 32 * kMaxCounterGroups);
     s->arrive.alloc(gmax);
     s->part.alloc((2 * kRedSlots + 5) * gmax);  // barrier reductions + tracked window solve partials
     s->red.alloc(kRedSlots);
