@@ -11,7 +11,8 @@ if sys.argv[1] == "run":
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     import bench
     from paper_1512_08401_b200 import waveblur as W
-    op, basis, u0, meta = bench.make_inputs()
+    op, basis, u0 = bench.make_inputs()
+    meta = json.loads(bytes(np.load(bench.GOLDEN)["meta_json"]).decode())
     ctx = W.Context(0)
     P = W.spai(op, ctx)
     w = W.scale_weights(basis.layout)
@@ -56,4 +57,10 @@ if len(sys.argv) > 3 and sys.argv[3] == "blocks":
                      "p90": round(float(np.percentile(m, 90)), 2), "max": round(float(m.max()), 2),
                      "slowest": [int(b) for b in np.argsort(-m)[:12]],
                      "by_sm_pair": [round(float(x), 2) for x in m.reshape(-1, 2).mean(axis=1)[::16]]}
+        # systematic vs random: the spread of the per-block MEAN work time vs the mean spread
+        # within a phase (a block that is slow every phase can be rebalanced; noise cannot)
+        out[name]["mean_spread_us"] = round(float(m.max() - m.min()), 2)
+        out[name]["phase_spread_us_median"] = round(float(np.median(sl.max(axis=1) - sl.min(axis=1))), 2)
+        out[name]["corr_first_second_half"] = round(float(np.corrcoef(sl[: len(sl) // 2].mean(0),
+                                                                       sl[len(sl) // 2:].mean(0))[0, 1]), 3)
     print(json.dumps(out))
