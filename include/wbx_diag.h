@@ -29,6 +29,10 @@ struct wbx_op;
 int wbx_diag_set_spmv_pf(long long bytes);
 int wbx_diag_spmv_compact_mode(struct wbx_ctx* ctx, const struct wbx_op* op, int transpose, int mode,
                                const float* x_dev, float* y_dev);
+/* Per-CTA features of a solver's window layout (side 0: Theta rows, 1: Theta^T rows):
+ * out[G][6] = {rows, sum 1/m, sum nq/m, sum (q-1)/m, nonzeros, window entries}. */
+struct wbx_solver;
+int wbx_diag_win_features(const struct wbx_solver* s, int side, double* out, int* G);
 #ifdef __cplusplus
 }
 #endif

@@ -172,6 +172,7 @@ DIAG_SIGNATURES = {
     "wbx_diag_slice_profile": (C.c_int, [_D]),
     "wbx_diag_spmv_compact_mode": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_diag_set_spmv_pf": (C.c_int, [C.c_longlong]),
+    "wbx_diag_win_features": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int)]),
 }
 
 

@@ -34,6 +34,7 @@
 #include <cstdlib>
 
 #include "internal.hpp"
+#include "wbx_diag.h"
 #include "sell.cuh"
 #include "stream.cuh"
 #include "win.cuh"
@@ -2795,6 +2796,35 @@ int wbx_solver_tau_stats(const wbx_solver* s, double* tau, uint32_t* ref_iters, 
     *tau = out[wbx::OUT_TAU];
     *ref_iters = static_cast<uint32_t>(out[wbx::OUT_TAU_ITERS]);
     *product_pairs = static_cast<uint32_t>(out[wbx::OUT_TAU_STEPS]);
+    return WBX_OK;
+}
+
+// Per-CTA features of the window layout of one side (0 = Theta rows, 1 = Theta^T rows), for
+// fitting the balance cost model against traced phase times (tools/win_fit.py): out[G][6] =
+// {rows, sum 1/m, sum nq/m, sum (q-1)/m, nonzeros, window entries}. Returns G in *G.
+int wbx_diag_win_features(const wbx_solver* s, int side, double* out, int* G) {
+    if (!s || !out || !G || !s->win || !s->wp) return WBX_INVALID_ARGUMENT;
+    const wbx::WinSide& W = side ? s->wp->T : s->wp->A;
+    const HostCompact& M = side ? s->op->hT : s->op->hA;
+    std::vector<uint32_t> r_off(W.G + 1), u_off(W.G + 1);
+    if (cudaMemcpy(r_off.data(), W.r_off.p, r_off.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(u_off.data(), W.u_off.p, u_off.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return WBX_CUDA_ERROR;
+    for (uint32_t b = 0; b < W.G; ++b) {
+        double f[6] = {0, 0, 0, 0, 0, static_cast<double>(u_off[b + 1] - u_off[b])};
+        for (uint32_t r = r_off[b]; r < r_off[b + 1]; ++r) {
+            const uint64_t len = M.ptr[r + 1] - M.ptr[r];
+            const uint64_t q = std::max<uint64_t>(1, (len + wbx::kSegElems - 1) / wbx::kSegElems);
+            const double m = static_cast<double>(32 / q), nq = static_cast<double>((len + q - 1) / q + 3) / 4.0;
+            f[0] += 1.0;
+            f[1] += 1.0 / m;
+            f[2] += nq / m;
+            f[3] += static_cast<double>(q - 1) / m;
+            f[4] += static_cast<double>(len);
+        }
+        for (int k = 0; k < 6; ++k) out[b * 6 + k] = f[k];
+    }
+    *G = static_cast<int>(W.G);
     return WBX_OK;
 }
 

@@ -15,33 +15,56 @@ namespace {
 
 uint64_t segs_of(uint64_t len) { return std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems); }
 
-// Contiguous row ranges per CTA balanced by COST = wseg per lane segment + wnnz per nonzero
-// (a slice's time has a fixed part and a part growing with its quads and segment folds).
+// Contiguous row ranges per CTA balanced by a per-row COST. Default model (round 2, fitted by
+// least squares to per-CTA phase times measured with WBX_TRACE_FILE at C2, tools/win_fit.py):
+//   cost(row) = (a + b*nq + c*(q - 1)) / m + d*len + e
+// with q = segments of the row, m = floor(32/q) rows per slice, nq = quads per lane (the slice
+// chain: record loads, nq gathers + fmas per lane, q - 1 shuffle folds), len = nonzeros (window
+// growth, epilogue). WBX_WIN_MODEL_A/_T = "a,b,c,d,e" overrides per side; WBX_WIN_COST[_A|_T] =
+// "wseg,wnnz" selects round 1's model cost = wseg*q + wnnz*len.
 std::vector<uint64_t> balance(const HostCompact& M, uint32_t G, char side) {
     const uint64_t nrows = M.rows();
-    uint64_t wseg = 8, wnnz = 1;  // swept (tools/cost_sweep.sh): best of 4..12 per side at C2
+    double cm[5] = {0, 0, 0, 0, 0};
+    bool model = false;
+    uint64_t wseg = 8, wnnz = 1;  // round 1 (tools/cost_sweep.sh): best of 4..12 per side at C2
+    {
+        const std::string key = std::string("WBX_WIN_MODEL_") + side;
+        const char* e = std::getenv(key.c_str());
+        if (!e) e = std::getenv("WBX_WIN_MODEL");
+        if (e && std::sscanf(e, "%lf,%lf,%lf,%lf,%lf", &cm[0], &cm[1], &cm[2], &cm[3], &cm[4]) == 5) model = true;
+    }
     const std::string key = std::string("WBX_WIN_COST_") + side;  // per side, then both sides
     const char* e = std::getenv(key.c_str());
     if (!e) e = std::getenv("WBX_WIN_COST");
-    if (e) {  // diagnostics: "segment_weight,nonzero_weight"
+    if (e && !model) {  // diagnostics: "segment_weight,nonzero_weight"
         unsigned long long a = 0, b = 0;
         if (std::sscanf(e, "%llu,%llu", &a, &b) == 2) {
             wseg = a;
             wnnz = b;
         }
     }
-    auto cost = [&](uint64_t i) {
+    std::vector<double> cost(nrows);
+    for (uint64_t i = 0; i < nrows; ++i) {
         const uint64_t len = M.ptr[i + 1] - M.ptr[i];
-        return wseg * segs_of(len) + wnnz * len;
-    };
-    uint64_t total = 0;
-    for (uint64_t i = 0; i < nrows; ++i) total += cost(i);
+        const uint64_t q = segs_of(len);
+        if (model) {
+            const double m = static_cast<double>(32 / q);
+            const double nq = static_cast<double>((len + q - 1) / q + 3) / 4.0;
+            cost[i] = (cm[0] + cm[1] * nq + cm[2] * static_cast<double>(q - 1)) / m + cm[3] * static_cast<double>(len) +
+                      cm[4];
+        } else {
+            cost[i] = static_cast<double>(wseg * q + wnnz * len);
+        }
+    }
+    double total = 0.0;
+    for (uint64_t i = 0; i < nrows; ++i) total += cost[i];
     std::vector<uint64_t> rb(G + 1, nrows);
     rb[0] = 0;
-    uint64_t acc = 0, q = 1;
+    double acc = 0.0;
+    uint64_t q = 1;
     for (uint64_t i = 0; i < nrows && q < G; ++i) {
-        acc += cost(i);
-        while (q < G && acc * G >= total * q) rb[q++] = i + 1;
+        acc += cost[i];
+        while (q < G && acc * G >= total * static_cast<double>(q)) rb[q++] = i + 1;
     }
     return rb;
 }
