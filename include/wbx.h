@@ -346,9 +346,10 @@ int wbx_shard_power_step_a(wbx_shard* s);
 int wbx_shard_power_step_t(wbx_shard* s);
 /* tau = 1 / (lambda * step_safety) (1 for a zero operator) and the iteration count */
 int wbx_shard_power_result(wbx_shard* s, double step_safety, double* tau, uint32_t* iters);
-/* estimate_step by Lanczos (the fp32 hot path's estimator, solver.cu), device-resident:
- * lz_begin -> [all-gather sums] -> lz_update(0) -> repeat { lz_step_a -> [all-gather t, sums]
- * -> lz_update(1) -> lz_step_t -> [all-gather sums, u] -> lz_update(2) } -> lz_result.
+/* estimate_step by Lanczos (the fp32 hot path's estimator, solver.cu), device-resident; its
+ * cross-rank vectors are fp32 and reuse the FISTA buffers (P^-1/2 w in y_pad, t' in res_pad):
+ * lz_begin -> [all-gather sums, y] -> lz_update(0) -> repeat { lz_step_a -> [all-gather res,
+ * sums] -> lz_update(1) -> lz_step_t -> [all-gather sums, y] -> lz_update(2) } -> lz_result.
  * first / every / gap: the convergence-check schedule (60 / 4 / 4 in the solver);
  * lz_done synchronises and tells the host the estimate has finished. */
 int wbx_shard_lz_begin(wbx_shard* s);

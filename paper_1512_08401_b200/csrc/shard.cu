@@ -364,7 +364,7 @@ __global__ void lz_init_kernel(ShardArgs a, uint64_t lo, uint64_t hi) {
         const double v = rng_normal(0x5eedull, a.C_own[c]);
         a.wv[c] = v;
         a.qp[c] = 0.0;
-        a.u_pad[a.rank * a.maxC + c] = a.ispC[c] * v;
+        a.y_pad[a.rank * a.maxC + c] = static_cast<float>(a.ispC[c] * v);
         sc += v * v;
     }
     s2 = block_sum<kBlock>(s2, sm);
@@ -375,15 +375,17 @@ __global__ void lz_init_kernel(ShardArgs a, uint64_t lo, uint64_t hi) {
     }
 }
 
-// phase A_j: t' = Theta[R_p, :] P^-1/2 w_j, partial |t'|^2
+// phase A_j: t' = Theta[R_p, :] P^-1/2 w_j, partial |t'|^2. The Lanczos vectors that cross
+// ranks are fp32 (P^-1/2 w_j in y_pad, t' in res_pad: the FISTA buffers, idle during the
+// estimate), as in the single-GPU fp32 estimators; w_j, q_j-1 and every sum stay fp64.
 __global__ void lz_a_kernel(ShardArgs a) {
     if (a.lz[LZ_DONE] != 0.0) return;
     __shared__ double sm[kBlock / 32 + 1];
-    double* t = a.t_pad + a.rank * a.maxR;
+    float* t = a.res_pad + a.rank * a.maxR;
     double acc = 0.0;
-    slice_rows<double, double>(a.A, a.u_pad, [&](uint32_t r, double v) {
+    slice_rows<float, float>(a.A, a.y_pad, [&](uint32_t r, float v) {
         t[r] = v;
-        acc += v * v;
+        acc += static_cast<double>(v) * static_cast<double>(v);
     });
     acc = block_sum<kBlock>(acc, sm);
     if (threadIdx.x == 0) {
@@ -398,15 +400,16 @@ __global__ void lz_t_kernel(ShardArgs a) {
     __shared__ double sm[kBlock / 32 + 1];
     const int j = static_cast<int>(a.lz[LZ_J]);
     const double alpha = a.lz[j], beta = a.lz[kLzCap + j], rb = 1.0 / beta;
-    double* u = a.u_pad + a.rank * a.maxC;
+    float* u = a.y_pad + a.rank * a.maxC;
     double acc = 0.0;
-    slice_rows<double, double>(a.T, a.t_pad, [&](uint32_t c, double g) {
+    slice_rows<float, float>(a.T, a.res_pad, [&](uint32_t c, float gf) {
+        const double g = gf;
         const double z = a.ispC[c] * g * rb;  // (M q_j)_c
         const double q = a.wv[c] * rb;        // q_j
         const double wn = z - alpha * q - beta * a.qp[c];
         a.wv[c] = wn;
         a.qp[c] = q;
-        u[c] = a.ispC[c] * wn;
+        u[c] = static_cast<float>(a.ispC[c] * wn);
         acc += wn * wn;
     });
     acc = block_sum<kBlock>(acc, sm);
@@ -1027,14 +1030,14 @@ void enqueue_lz_chunk(wbx_sharded* S) {
             if (wbx_shard_lz_update(s, phase, S->lz_first, S->lz_every, S->lz_gap) != WBX_OK)
                 fail(WBX_CUDA_ERROR, "lz_update failed");
     };
-    for (int j = 0; j < kLzChunk; ++j) {
+    for (int j = 0; j < kLzChunk; ++j) {  // t' in res, P^-1/2 w in y (fp32)
         each(S, wbx_shard_lz_step_a);
-        gather(S, S->t.p, S->maxR);
+        gather(S, S->res.p, S->maxR);
         gather(S, S->sums.p, 2);
         update(1);
         each(S, wbx_shard_lz_step_t);
         gather(S, S->sums.p, 2);
-        gather(S, S->u.p, S->maxC);
+        gather(S, S->y.p, S->maxC);
         update(2);
     }
 }
@@ -1089,7 +1092,7 @@ double estimate(wbx_sharded* S, double step_safety, uint32_t* iters, uint32_t* s
     each(S, wbx_shard_lz_begin);
     gather(S, S->sums.p, 2);
     for (wbx_shard* s : S->shards) wbx_shard_lz_update(s, 0, S->lz_first, S->lz_every, S->lz_gap);
-    gather(S, S->u.p, S->maxC);
+    gather(S, S->y.p, S->maxC);
     const bool graphs = graphs_enabled();
     if (graphs && !S->lz_exec) S->lz_exec = capture(S, [&] { enqueue_lz_chunk(S); });
     for (int j = 0; j < kLzCap; j += kLzChunk) {
