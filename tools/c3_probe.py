@@ -1,13 +1,18 @@
-import sys, numpy as np
-sys.path.insert(0,'/root/repo')
+"""Which engine the C3 (1024^2 spatially varying) operator gets, and why (WBX_VERBOSE=1)."""
+import sys
 from pathlib import Path
-from paper_1512_08401_b200 import waveblur as W
-import bench
-lad = W.SigmaLadder.from_npz(np.load(Path('/root/repo/tests/golden/c3_ladder_1024.npz')))
-opv = W.theta_varying(lad, 2.5, 7.5)
-op, basis, u0, meta = bench.make_inputs()
-ctx=W.Context(0)
-P=W.spai(opv, ctx); w=W.scale_weights(basis.layout)
-d=W.Deblurrer(opv, basis, P, w, 1e-4, W.SolverConfig(max_iters=100, track_energy=False), ctx)
-for _ in range(3): d.deblur(u0)
-print(d.phase_ms(), d.tau_stats())
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1512_08401_b200 import waveblur as W  # noqa: E402
+
+ROOT = Path(__file__).resolve().parents[1]
+lad = W.SigmaLadder.from_npz(np.load(ROOT / "tests" / "golden" / "c3_ladder_1024.npz"))
+op = W.theta_varying(lad, 2.5, 7.5)
+ctx = W.Context(0)
+basis = W.make_basis(W.FilterFamily.Daubechies, 4, (1024, 1024), 4)
+P = W.spai(op, ctx)
+w = W.scale_weights(basis.layout)
+d = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=100, track_energy=False), ctx)
+print(d.kernels(), op.nnz(), op.info(ctx).nonempty_rows, op.info(ctx).nonempty_cols)
