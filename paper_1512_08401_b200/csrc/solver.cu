@@ -103,6 +103,7 @@ struct SolveArgs {
     // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
     WinView wA, wT;
     int lz_first, lz_every, lz_gap;  // Lanczos tau: first check, check period, compared m - gap
+    int win_lists_global;            // window index lists read from global memory (win_smem_head)
     // T-typed state
     void* yC;
     void* xpC;
@@ -1035,10 +1036,15 @@ struct WinSmem {
     uint32_t rA0, rT0, nrA, nrT;  // own row ranges
 };
 
+// lists_global: the window index lists (entries and slots) stay in global memory (L2) and are
+// read by the fill itself — for operators whose windows are too large for both lists and
+// window in shared memory (the spatially varying C3 operator at 1024^2)
 template <uint32_t OWN_A, uint32_t OWN_T>
-__host__ __device__ inline uint32_t win_smem_head(const WinView& A, const WinView& T) {
-    return win_align16(A.max_u * 4u) + win_align16(T.max_u * 4u) + win_align16(A.max_u * 2u) +
-           win_align16(T.max_u * 2u) + 16u * (A.max_slices + T.max_slices) +
+__host__ __device__ inline uint32_t win_smem_head(const WinView& A, const WinView& T, bool lists_global = false) {
+    const uint32_t lists = lists_global ? 0u
+                                        : win_align16(A.max_u * 4u) + win_align16(T.max_u * 4u) +
+                                              win_align16(A.max_u * 2u) + win_align16(T.max_u * 2u);
+    return lists + 16u * (A.max_slices + T.max_slices) +
            win_align16(A.max_dict * 4u) + win_align16(T.max_dict * 4u) + win_align16(A.max_rows * OWN_A) +
            win_align16(T.max_rows * OWN_T);
 }
@@ -1061,10 +1067,17 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
         p += bytes;
         return q;
     };
-    w.uA = reinterpret_cast<uint32_t*>(carve(win_align16(a.wA.max_u * 4u)));
-    w.uT = reinterpret_cast<uint32_t*>(carve(win_align16(a.wT.max_u * 4u)));
-    w.usA = reinterpret_cast<uint16_t*>(carve(win_align16(a.wA.max_u * 2u)));
-    w.usT = reinterpret_cast<uint16_t*>(carve(win_align16(a.wT.max_u * 2u)));
+    if (a.win_lists_global) {  // read in place by the fills (never written)
+        w.uA = const_cast<uint32_t*>(a.wA.u_idx + a.wA.u_off[b]);
+        w.uT = const_cast<uint32_t*>(a.wT.u_idx + a.wT.u_off[b]);
+        w.usA = const_cast<uint16_t*>(a.wA.u_slot + a.wA.u_off[b]);
+        w.usT = const_cast<uint16_t*>(a.wT.u_slot + a.wT.u_off[b]);
+    } else {
+        w.uA = reinterpret_cast<uint32_t*>(carve(win_align16(a.wA.max_u * 4u)));
+        w.uT = reinterpret_cast<uint32_t*>(carve(win_align16(a.wT.max_u * 4u)));
+        w.usA = reinterpret_cast<uint16_t*>(carve(win_align16(a.wA.max_u * 2u)));
+        w.usT = reinterpret_cast<uint16_t*>(carve(win_align16(a.wT.max_u * 2u)));
+    }
     w.sA = reinterpret_cast<uint4*>(carve(16u * a.wA.max_slices));
     w.sT = reinterpret_cast<uint4*>(carve(16u * a.wT.max_slices));
     w.dA = reinterpret_cast<float*>(carve(win_align16(a.wA.max_dict * 4u)));
@@ -1072,10 +1085,12 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     w.ownA = carve(win_align16(a.wA.max_rows * OWN_A));
     w.ownT = carve(win_align16(a.wT.max_rows * OWN_T));
     w.win = p;
-    for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
-    for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.usT[i] = a.wT.u_slot[a.wT.u_off[b] + i];
+    if (!a.win_lists_global) {
+        for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
+        for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
+        for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
+        for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.usT[i] = a.wT.u_slot[a.wT.u_off[b] + i];
+    }
     for (uint32_t i = threadIdx.x; i < w.nsA; i += kWinBlock) w.sA[i] = a.wA.s_tab[a.wA.s_off[b] + i];
     for (uint32_t i = threadIdx.x; i < w.nsT; i += kWinBlock) w.sT[i] = a.wT.s_tab[a.wT.s_off[b] + i];
     if (a.wA.max_dict)
@@ -2108,6 +2123,7 @@ struct wbx_solver {
     // window engine (fp32 single-image solves whose per-CTA windows fit shared memory)
     bool win = false, win_dict = false, tau_win64 = false, tau_lanczos = false;
     bool win_track = false;  // tracked solves (energies / supports / ref_energy) on the window engine
+    bool win_lists_global = false;  // window index lists in global memory (large windows)
     unsigned win_smem_track = 0;
     int grid_tau_lz = 0;
     int grid_win = 0;
@@ -2225,6 +2241,7 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     if (s->win) {
         a.wA = view_of(s->wp->A);
         a.wT = view_of(s->wp->T);
+        a.win_lists_global = s->win_lists_global ? 1 : 0;
     }
     {
         const char* e = std::getenv("WBX_BARRIER");
@@ -2381,32 +2398,39 @@ void alloc_state(wbx_solver* s) {
     // forces the fallback)
     const char* eng = std::getenv("WBX_ENGINE");
     if (sizeof(T) == 4 && !(eng && std::string(eng) == "stream")) {  // batches use it for tau
-        for (int bps = kWinMinBlocks; bps >= 1 && !s->win; --bps) {
+        // index lists in shared memory first; for windows too large for both lists and window,
+        // the lists in global memory (read by the fills) before giving up CTAs per SM
+        for (int attempt = 0; attempt < 2 * kWinMinBlocks && !s->win; ++attempt) {
+            const int bps = kWinMinBlocks - attempt / 2;
+            const bool lg = (attempt & 1) != 0;
+            if (const char* wl = std::getenv("WBX_WIN_LISTS")) {  // diagnostics: force one placement
+                if ((std::string(wl) == "smem" && lg) || (std::string(wl) == "global" && !lg)) continue;
+            }
             const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
             s->wp = win_layout(s->op, G, s->ctx->stream);
             if (!s->wp->ok) continue;  // a window exceeded 16-bit local indices
             const WinView vA = view_of(s->wp->A), vT = view_of(s->wp->T);
             const unsigned mu = std::max(s->wp->A.max_win, s->wp->T.max_win);
-            s->win_smem_fista = win_smem_head<4, 16>(vA, vT) + mu * 4u;
+            s->win_smem_fista = win_smem_head<4, 16>(vA, vT, lg) + mu * 4u;
             s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
             // tau by Lanczos + the power iteration on the tridiagonal (tau_lanczos_win_kernel);
             // WBX_TAU=power runs the literal power iteration
             // (falls back to the power iteration when its state does not fit next to the window)
             const unsigned limit = bps == 1 ? 220u * 1024u : (227u * 1024u) / bps - 2048u;
             s->tau_lanczos = !s->tau_win64 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
-            const unsigned smem_lz = win_smem_head<0, 24>(vA, vT) + win_align16(mu * 4u) + 16u * G +  // + partials
+            const unsigned smem_lz = win_smem_head<0, 24>(vA, vT, lg) + win_align16(mu * 4u) + 16u * G +  // + partials
                                      16u * kLzCap;                                                     // + alpha, beta
             if (s->tau_lanczos && smem_lz > limit) s->tau_lanczos = false;
             s->win_smem_tau = s->tau_lanczos ? smem_lz
-                                             : win_smem_head<0, 16>(vA, vT) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
+                                             : win_smem_head<0, 16>(vA, vT, lg) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
                                                    16u * G;  // + partials staging
             s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
             const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
                                          : reinterpret_cast<const void*>(fista_win_kernel<false>);
             const void* kt = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
             if (std::getenv("WBX_VERBOSE"))
-                std::fprintf(stderr, "wbx window engine: try G=%u smem fista/tau=%u/%u limit %u\n", G,
-                             s->win_smem_fista, s->win_smem_tau, limit);
+                std::fprintf(stderr, "wbx window engine: try G=%u lists %s smem fista/tau=%u/%u limit %u\n", G,
+                             lg ? "global" : "smem", s->win_smem_fista, s->win_smem_tau, limit);
             if (std::max(s->win_smem_fista, s->win_smem_tau) > limit) continue;
             WBX_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(s->win_smem_fista)));
@@ -2420,8 +2444,9 @@ void alloc_state(wbx_solver* s) {
             if (pf < bps || pt < bps) continue;
             s->grid_win = static_cast<int>(G);
             s->win = true;
+            s->win_lists_global = lg;
             // the tracked variant keeps Theta x_k-1 next to x0 per own row (+4 B per row)
-            s->win_smem_track = win_smem_head<8, 16>(vA, vT) + mu * 4u;
+            s->win_smem_track = win_smem_head<8, 16>(vA, vT, lg) + mu * 4u;
             if (s->win_smem_track <= limit && !(std::getenv("WBX_TRACK_ENGINE") &&
                                                 std::string(std::getenv("WBX_TRACK_ENGINE")) == "stream")) {
                 const void* kk = s->win_dict ? reinterpret_cast<const void*>(fista_win_track_kernel<true>)

@@ -434,7 +434,7 @@ def test_deblurrer_c2_1024_vs_oracle(golden):
 # ----------------------------------------------------------------------------- engine / format variants
 @pytest.mark.parametrize("env", [{}, {"WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"}, {"WBX_TAU_WINDOW": "64"},
                                  {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
-                                 {"WBX_WIN_COST": "16,1"}])
+                                 {"WBX_WIN_COST": "16,1"}, {"WBX_WIN_LISTS": "global"}])
 def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
     """Every solver engine / window format / placement / barrier the library can select
     (environment switches read at solver creation) meets the same parity bar on C1."""
@@ -449,3 +449,22 @@ def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
     assert rel_l2(u, g["restored"]) <= RTOL_IMAGE
     u2, _ = d.deblur(g["u0"], clamp=False)
     assert np.array_equal(u, u2)  # run-to-run deterministic
+
+
+@pytest.mark.parametrize("env", [{"WBX_WIN_FULL": "1"}, {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
+                                 {"WBX_WIN_COST": "16,1"}, {"WBX_WIN_LISTS": "global"}, {"WBX_BARRIER_GROUPS": "4"},
+                                 {"WBX_WIN_MODEL": "0.0186,0.0129,0.0024,0,0"}, {"WBX_GRAPH": "0"}])
+def test_window_layout_variants_leave_iterates_bitwise(golden, monkeypatch, env):
+    """The window engine's partition, slot placement, value format, list placement, barrier and
+    launch mode change no arithmetic: given tau, the restored image is bitwise the default's."""
+    g = golden("c1_db4_256")
+    cfg = W.SolverConfig(max_iters=50, track_energy=False, tau=g.meta["tau"])
+    op = g.operator()
+    P = W.spai(op)
+    ref = W.Deblurrer(op, basis_of(g), P, g.weights(), g.meta["lambda"], cfg).deblur(g["u0"], clamp=False)[0]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    op2 = g.operator()  # window layouts are cached per operator: a fresh one
+    d = W.Deblurrer(op2, basis_of(g), P, g.weights(), g.meta["lambda"], cfg)
+    assert d.kernels()[1] == "fista_win_kernel"
+    assert np.array_equal(d.deblur(g["u0"], clamp=False)[0], ref)
