@@ -468,3 +468,27 @@ def test_window_layout_variants_leave_iterates_bitwise(golden, monkeypatch, env)
     d = W.Deblurrer(op2, basis_of(g), P, g.weights(), g.meta["lambda"], cfg)
     assert d.kernels()[1] == "fista_win_kernel"
     assert np.array_equal(d.deblur(g["u0"], clamp=False)[0], ref)
+
+
+def test_deblur_graphs_follow_the_buffers(golden):
+    """wbx_deblur_dev runs as two CUDA graphs captured for the (u0, u, clamp) pointers of the
+    call: alternating buffers and clamp flags re-capture and give the same images as the
+    host entry point (and as launching kernel by kernel, WBX_GRAPH=0 in the variant test)."""
+    import torch
+    g = golden("c1_db4_256")
+    op = g.operator()
+    d = W.Deblurrer(op, basis_of(g), W.spai(op), g.weights(), g.meta["lambda"],
+                    W.SolverConfig(max_iters=50, track_energy=False))
+    ref, _ = d.deblur(g["u0"], clamp=True)
+    refc, _ = d.deblur(g["u0"], clamp=False)
+    dev = torch.device("cuda", 0)
+    u0 = torch.from_numpy(g["u0"].copy()).to(dev)
+    outs = [torch.empty_like(u0) for _ in range(2)]
+    for k in range(4):
+        o = outs[k % 2]
+        clamp = k < 2
+        d.deblur_dev(u0.data_ptr(), o.data_ptr(), clamp=clamp)
+        torch.cuda.synchronize()
+        assert np.array_equal(o.cpu().numpy().reshape(256, 256), ref if clamp else refc)
+        launches, _ = d.last_stats()
+        assert launches > 0
