@@ -1049,7 +1049,7 @@ __host__ __device__ inline uint32_t win_smem_head(const WinView& A, const WinVie
            win_align16(T.max_rows * OWN_T);
 }
 
-template <uint32_t OWN_A, uint32_t OWN_T>
+template <uint32_t OWN_A, uint32_t OWN_T, bool LG>
 __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const SolveArgs& a) {
     WinSmem w;
     const uint32_t b = blockIdx.x;
@@ -1067,7 +1067,7 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
         p += bytes;
         return q;
     };
-    if (a.win_lists_global) {  // read in place by the fills (never written)
+    if (LG) {  // read in place by the fills (never written)
         w.uA = const_cast<uint32_t*>(a.wA.u_idx + a.wA.u_off[b]);
         w.uT = const_cast<uint32_t*>(a.wT.u_idx + a.wT.u_off[b]);
         w.usA = const_cast<uint16_t*>(a.wA.u_slot + a.wA.u_off[b]);
@@ -1085,7 +1085,7 @@ __device__ __forceinline__ WinSmem win_smem_init(unsigned char* base, const Solv
     w.ownA = carve(win_align16(a.wA.max_rows * OWN_A));
     w.ownT = carve(win_align16(a.wT.max_rows * OWN_T));
     w.win = p;
-    if (!a.win_lists_global) {
+    if (!LG) {
         for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.uA[i] = a.wA.u_idx[a.wA.u_off[b] + i];
         for (uint32_t i = threadIdx.x; i < w.nuT; i += kWinBlock) w.uT[i] = a.wT.u_idx[a.wT.u_off[b] + i];
         for (uint32_t i = threadIdx.x; i < w.nuA; i += kWinBlock) w.usA[i] = a.wA.u_slot[a.wA.u_off[b] + i];
@@ -1229,7 +1229,7 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     __syncthreads();  // the window is refilled by the next phase
 }
 
-template <bool DICT>
+template <bool DICT, bool LG>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(SolveArgs a) {
     __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_kernel(Sol
     float* yC = static_cast<float*>(a.yC);
     float* res = static_cast<float*>(a.res);
     const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
-    const WinSmem ws = win_smem_init<4, 16>(dsmem, a);
+    const WinSmem ws = win_smem_init<4, 16, LG>(dsmem, a);
     float* win = static_cast<float*>(ws.win);
     float* x0s = static_cast<float*>(ws.ownA);   // x0 of the CTA's Theta rows
     float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
@@ -1342,7 +1342,7 @@ __device__ __forceinline__ void win_block_partial(double v, double* dst, double*
 // overwrites x_k (x_prev in the CTA state). Every CTA sums the same per-CTA partials in the
 // same order, so all take the same decision without further communication.
 // Decoupled coordinates (empty Theta column) are tracked by decoupled_kernel (dec_reg/dec_supp).
-template <bool DICT>
+template <bool DICT, bool LG>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_track_kernel(SolveArgs a) {
     __shared__ double smem[kWinWarps + 1];
     __shared__ double red[3 * kWinWarps];
@@ -1355,7 +1355,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_track_kern
     float* yC = static_cast<float*>(a.yC);
     float* res = static_cast<float*>(a.res);
     const double tau = a.tau_from_device ? a.out[OUT_TAU] : a.tau_given;
-    const WinSmem ws = win_smem_init<8, 16>(dsmem, a);
+    const WinSmem ws = win_smem_init<8, 16, LG>(dsmem, a);
     float* win = static_cast<float*>(ws.win);
     float2* ra = static_cast<float2*>(ws.ownA);  // {x0, Theta x_k-1} of the CTA's Theta rows
     float4* cs = static_cast<float4*>(ws.ownT);  // {y, x_prev, tau/p, threshold} of its coordinates
@@ -1455,7 +1455,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) fista_win_track_kern
 // estimate_step on the window engine: fp64 accumulation, own state and reductions; fp32
 // operator values; vector windows in WINT (float: the gathered u and t entries are rounded
 // to fp32, the products are exact in fp64; double: fp64 windows, WBX_TAU_WINDOW=64)
-template <bool DICT, typename WINT>
+template <bool DICT, typename WINT, bool LG>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(SolveArgs a) {
     __shared__ double smem[kWinWarps + 1];
     extern __shared__ __align__(16) unsigned char dsmem[];
@@ -1463,7 +1463,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
-    const WinSmem ws = win_smem_init<0, 16>(dsmem, a);
+    const WinSmem ws = win_smem_init<0, 16, LG>(dsmem, a);
     WINT* win = static_cast<WINT*>(ws.win);
     double2* cs = static_cast<double2*>(ws.ownT);  // {P^-1/2, w} of the CTA's coordinates
     constexpr bool W64 = sizeof(WINT) == 8;
@@ -1656,7 +1656,7 @@ __device__ __forceinline__ void cta_partial(double v, double* dst, double* red) 
     }
 }
 
-template <bool DICT>
+template <bool DICT, bool LG>
 __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kernel(SolveArgs a) {
     __shared__ double smem[kWinWarps + 1];
     __shared__ double red[kWinWarps];
@@ -1666,7 +1666,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kern
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * kWinBlock;
     const unsigned epoch0 = *reinterpret_cast<volatile unsigned*>(a.sync.gen);
     Epoch epoch{epoch0, epoch0};
-    const WinSmem ws = win_smem_init<0, 24>(dsmem, a);
+    const WinSmem ws = win_smem_init<0, 24, LG>(dsmem, a);
     float* win = static_cast<float*>(ws.win);
     struct LzRow {
         double isp, w, qp;  // P^-1/2, w_j (unnormalised), q_j-1 of one coordinate
@@ -2124,6 +2124,7 @@ struct wbx_solver {
     bool win = false, win_dict = false, tau_win64 = false, tau_lanczos = false;
     bool win_track = false;  // tracked solves (energies / supports / ref_energy) on the window engine
     bool win_lists_global = false;  // window index lists in global memory (large windows)
+    bool tau_stream_lz = false;     // window FISTA with the streamed engine's Lanczos step estimate
     unsigned win_smem_track = 0;
     int grid_tau_lz = 0;
     int grid_win = 0;
@@ -2251,15 +2252,37 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     return a;
 }
 
-const void* tau_win_fn(bool dict, bool w64, bool lanczos = false) {
+template <bool LG>
+const void* tau_win_fn_lg(bool dict, bool w64, bool lanczos) {
     if (lanczos)
-        return dict ? reinterpret_cast<const void*>(tau_lanczos_win_kernel<true>)
-                    : reinterpret_cast<const void*>(tau_lanczos_win_kernel<false>);
+        return dict ? reinterpret_cast<const void*>(tau_lanczos_win_kernel<true, LG>)
+                    : reinterpret_cast<const void*>(tau_lanczos_win_kernel<false, LG>);
     if (dict)
-        return w64 ? reinterpret_cast<const void*>(tau_win_kernel<true, double>)
-                   : reinterpret_cast<const void*>(tau_win_kernel<true, float>);
-    return w64 ? reinterpret_cast<const void*>(tau_win_kernel<false, double>)
-               : reinterpret_cast<const void*>(tau_win_kernel<false, float>);
+        return w64 ? reinterpret_cast<const void*>(tau_win_kernel<true, double, LG>)
+                   : reinterpret_cast<const void*>(tau_win_kernel<true, float, LG>);
+    return w64 ? reinterpret_cast<const void*>(tau_win_kernel<false, double, LG>)
+               : reinterpret_cast<const void*>(tau_win_kernel<false, float, LG>);
+}
+
+// the window kernels by value format (dictionary / full) and index-list placement (smem / global)
+const void* tau_win_fn(bool dict, bool w64, bool lanczos, bool lg) {
+    return lg ? tau_win_fn_lg<true>(dict, w64, lanczos) : tau_win_fn_lg<false>(dict, w64, lanczos);
+}
+
+const void* fista_win_fn(bool dict, bool lg) {
+    if (dict)
+        return lg ? reinterpret_cast<const void*>(fista_win_kernel<true, true>)
+                  : reinterpret_cast<const void*>(fista_win_kernel<true, false>);
+    return lg ? reinterpret_cast<const void*>(fista_win_kernel<false, true>)
+              : reinterpret_cast<const void*>(fista_win_kernel<false, false>);
+}
+
+const void* track_win_fn(bool dict, bool lg) {
+    if (dict)
+        return lg ? reinterpret_cast<const void*>(fista_win_track_kernel<true, true>)
+                  : reinterpret_cast<const void*>(fista_win_track_kernel<true, false>);
+    return lg ? reinterpret_cast<const void*>(fista_win_track_kernel<false, true>)
+              : reinterpret_cast<const void*>(fista_win_track_kernel<false, false>);
 }
 
 void launch_coop_smem(const void* kernel, int grid, unsigned smem, SolveArgs& a, cudaStream_t st,
@@ -2283,10 +2306,10 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
     // step: estimate_step on the device, or the given one
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
-    } else if (s->win) {
-        const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
+    } else if (s->win && !s->tau_stream_lz) {
+        const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos, s->win_lists_global);
         launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st, kWinBlock);
-    } else if (sizeof(T) == 4 && s->tau_lanczos) {
+    } else if (sizeof(T) == 4 && (s->tau_lanczos || s->tau_stream_lz)) {
         launch_coop<T>(reinterpret_cast<const void*>(tau_lanczos_kernel), s->grid_tau_lz, a, st);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(tau_kernel<T>), s->grid_tau, a, st);
@@ -2302,8 +2325,7 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
     wbx_ctx* ctx = s->ctx;
     const bool win = s->win && !a.track && s->batch == 1;
     if (win) {
-        const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
-                                    : reinterpret_cast<const void*>(fista_win_kernel<false>);
+        const void* k = fista_win_fn(s->win_dict, s->win_lists_global);
         launch_coop_smem(k, s->grid_win, s->win_smem_fista, a, st, kWinBlock);
         count_launch(ctx);
         WBX_CUDA(cudaGetLastError());
@@ -2339,8 +2361,7 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         count_launch(ctx, 3);
     }
     if (s->win_track) {  // the window engine with energy / support tracking
-        const void* k = s->win_dict ? reinterpret_cast<const void*>(fista_win_track_kernel<true>)
-                                    : reinterpret_cast<const void*>(fista_win_track_kernel<false>);
+        const void* k = track_win_fn(s->win_dict, s->win_lists_global);
         launch_coop_smem(k, s->grid_win, s->win_smem_track, a, st, kWinBlock);
     } else {
         launch_coop<T>(reinterpret_cast<const void*>(fista_kernel<T>), s->grid_fista, a, st);
@@ -2420,14 +2441,16 @@ void alloc_state(wbx_solver* s) {
             s->tau_lanczos = !s->tau_win64 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
             const unsigned smem_lz = win_smem_head<0, 24>(vA, vT, lg) + win_align16(mu * 4u) + 16u * G +  // + partials
                                      16u * kLzCap;                                                     // + alpha, beta
+            // the Lanczos state does not fit next to the window: the streamed engine's Lanczos
+            // estimate (60-odd steps) rather than the window power iteration (200)
+            s->tau_stream_lz = s->tau_lanczos && smem_lz > limit;
             if (s->tau_lanczos && smem_lz > limit) s->tau_lanczos = false;
             s->win_smem_tau = s->tau_lanczos ? smem_lz
                                              : win_smem_head<0, 16>(vA, vT, lg) + win_align16(mu * (s->tau_win64 ? 8u : 4u)) +
                                                    16u * G;  // + partials staging
             s->win_dict = vA.max_dict > 0 && vT.max_dict > 0;
-            const void* kf = s->win_dict ? reinterpret_cast<const void*>(fista_win_kernel<true>)
-                                         : reinterpret_cast<const void*>(fista_win_kernel<false>);
-            const void* kt = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos);
+            const void* kf = fista_win_fn(s->win_dict, lg);
+            const void* kt = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos, lg);
             if (std::getenv("WBX_VERBOSE"))
                 std::fprintf(stderr, "wbx window engine: try G=%u lists %s smem fista/tau=%u/%u limit %u\n", G,
                              lg ? "global" : "smem", s->win_smem_fista, s->win_smem_tau, limit);
@@ -2449,8 +2472,7 @@ void alloc_state(wbx_solver* s) {
             s->win_smem_track = win_smem_head<8, 16>(vA, vT, lg) + mu * 4u;
             if (s->win_smem_track <= limit && !(std::getenv("WBX_TRACK_ENGINE") &&
                                                 std::string(std::getenv("WBX_TRACK_ENGINE")) == "stream")) {
-                const void* kk = s->win_dict ? reinterpret_cast<const void*>(fista_win_track_kernel<true>)
-                                             : reinterpret_cast<const void*>(fista_win_track_kernel<false>);
+                const void* kk = track_win_fn(s->win_dict, lg);
                 WBX_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(s->win_smem_track)));
                 int pk = 0;
@@ -2613,7 +2635,8 @@ void solver_report(wbx_solver* s, wbx_report* rep) {
     if (out[OUT_STATUS] == 8.0) fail(WBX_NONFINITE_ENERGY, "solver diverged (non-finite energy)");
     if (std::getenv("WBX_VERBOSE"))
         std::fprintf(stderr, "wbx tau: %.17g after %g reference iterations, %g operator product pairs (%s)\n",
-                     out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_TAU_STEPS], s->tau_lanczos ? "lanczos" : "power");
+                     out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_TAU_STEPS],
+                     (s->tau_lanczos || s->tau_stream_lz) ? "lanczos" : "power");
     if (rep == nullptr) return;
     rep->iters_used = static_cast<uint64_t>(out[OUT_ITERS_USED]);
     rep->tau = out[OUT_TAU];
@@ -2858,6 +2881,7 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
     const bool fp64 = s->cfg.precision == WBX_FP64;
     const bool track = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
     const char* tau = s->cfg.tau > 0.0 ? "set_tau_kernel"
+                      : s->tau_stream_lz ? "tau_lanczos_kernel"
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
