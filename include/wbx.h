@@ -148,6 +148,13 @@ int wbx_spmv_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision, c
  * used to measure the SpMV against the HBM roofline (tools/spmv_roofline.py). */
 int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int precision,
                          const void* x_dev, void* y_dev);
+/* Attach the kept generator groups (wbx_theta_expand format) of a stationary Theta_K to its
+ * operator; they must expand to the operator's CSR exactly (WBX_BAD_SPEC otherwise). Solvers on
+ * the operator may then run the stencil engine (no index stream: every entry of a circulant
+ * block is an affine function of its output position; csrc/stencil_engine.cuh). */
+int wbx_op_set_generators(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
+                          const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
+                          const double* values);
 /* write_operator / read_operator (theta.cpp:413-490): the reference's WTHETA01 file, same
  * bytes, same validation (WBX_IO_ERROR with the reference's messages; bad layouts raise what
  * make_layout raises). read: the arrays are allocated by the library (malloc; wbx_free);

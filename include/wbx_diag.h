@@ -31,6 +31,11 @@ int wbx_diag_spmv_compact_mode(struct wbx_ctx* ctx, const struct wbx_op* op, int
                                const float* x_dev, float* y_dev);
 /* Per-CTA features of a solver's window layout (side 0: Theta rows, 1: Theta^T rows):
  * out[G][6] = {rows, sum 1/m, sum nq/m, sum (q-1)/m, nonzeros, window entries}. */
+/* Host execution of the stencil engine's plan (grid G) for an operator given by its kept
+ * generator groups: y = Theta x (phase 0) / Theta^T x (phase 1), full-length fp64 vectors. */
+int wbx_diag_stencil_apply_host(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
+                                const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
+                                const double* values, int phase, uint32_t G, const double* x, double* y);
 struct wbx_solver;
 int wbx_diag_win_features(const struct wbx_solver* s, int side, double* out, int* G);
 #ifdef __cplusplus

@@ -78,6 +78,7 @@ SIGNATURES = {
     "wbx_spmv": (C.c_int, [_P, _P, C.c_int, _D, _D]),
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_spmv_compact_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
+    "wbx_op_set_generators": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D]),
     "wbx_write_operator": (C.c_int, [C.c_char_p, C.c_uint32, _U64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                      _U64, _U32, _D]),
     "wbx_read_operator": (C.c_int, [C.c_char_p, _U32, _U64, _U32, _U32, _U32, _U64, _U64, C.POINTER(_U64),
@@ -172,6 +173,8 @@ DIAG_SIGNATURES = {
     "wbx_diag_slice_profile": (C.c_int, [_D]),
     "wbx_diag_spmv_compact_mode": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_diag_set_spmv_pf": (C.c_int, [C.c_longlong]),
+    "wbx_diag_stencil_apply_host": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
+                                              C.c_int, C.c_uint32, _D, _D]),
     "wbx_diag_win_features": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int)]),
 }
 

@@ -81,6 +81,8 @@ struct WinSide {
     DevBuf<float> d_val;
     uint64_t bytes = 0;
 };
+struct StencilPlan;  // stencil_plan.cu
+
 // both sides for one grid size G; ok == false when a window exceeds 16-bit local indices
 struct WinPair {
     WinSide A, T;
@@ -177,6 +179,15 @@ struct wbx_op {
     // on it (a host loop calling fista() on one operator pays the layout build once)
     mutable std::mutex win_mu;
     mutable std::map<uint32_t, std::shared_ptr<wbx::WinPair>> win_cache;
+    // the operator as the reference's kept generator groups (stationary Theta_K), when the
+    // caller attached them (wbx_op_set_generators, checked against the CSR): the stencil engine
+    bool has_gens = false;
+    uint32_t g_ndim = 0;
+    std::vector<wbx_band> g_bands;
+    std::vector<uint32_t> g_block, g_index;
+    std::vector<uint64_t> g_count;
+    std::vector<double> g_val;
+    mutable std::map<uint64_t, std::shared_ptr<wbx::StencilPlan>> st_cache;  // by (CTA warps, G)
 };
 
 namespace wbx {
@@ -221,6 +232,19 @@ WinView view_of(const WinSide& w);
 // gram.cu: Gram diagonals on the device (shared-memory tables, global-memory second pass for
 // columns whose 2-hop set overflows them)
 void gram_device(wbx_ctx* ctx, const wbx_op* op, uint64_t cap_factor, double* diagM, double* diagM2);
+
+// stencil_plan.cu: the stencil engine's plan for grid G (ok == false when it does not apply)
+std::shared_ptr<StencilPlan> build_stencil_plan(const std::vector<wbx_band>& bands, uint32_t ndim, uint64_t n,
+                                                const std::vector<uint32_t>& gblock, const std::vector<uint32_t>& gidx,
+                                                const std::vector<uint64_t>& gcount, const std::vector<double>& gval,
+                                                uint32_t G, uint32_t cta_warps, uint32_t smem_budget_floats);
+void upload_stencil_plan(StencilPlan& p, cudaStream_t st);
+bool stencil_plan_ok(const StencilPlan& p, std::string* why);
+void stencil_apply_host(const StencilPlan& p, int ph, const double* src, double* out);
+struct StencilView;
+StencilView view_of(const StencilPlan& p);
+// the operator's plan for grid G (built from its generator groups, uploaded, cached on it)
+std::shared_ptr<StencilPlan> stencil_plan_for(const wbx_op* op, uint32_t G, uint32_t cta_warps, cudaStream_t st);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

@@ -39,6 +39,7 @@
 #include "stream.cuh"
 #include "win.cuh"
 #include "lanczos.cuh"
+#include "stencil_engine.cuh"
 
 extern "C" void wbx_set_last_error(const char* msg);
 
@@ -104,6 +105,11 @@ struct SolveArgs {
     WinView wA, wT;
     int lz_first, lz_every, lz_gap;  // Lanczos tau: first check, check period, compared m - gap
     int win_lists_global;            // window index lists read from global memory (win_smem_head)
+    // stencil engine (stencil_engine.cuh): the plan and its fp32 source vectors
+    StencilView st;
+    int st_fill;  // window fill: 0 bulk copies (TMA), 1 cp.async 16 B per warp row (WBX_ST_FILL)
+    float* yF;
+    float* resF;
     // T-typed state
     void* yC;
     void* xpC;
@@ -2061,6 +2067,8 @@ __global__ void __launch_bounds__(kBlock, WBX_FISTA_MINB) fista_batch_kernel(Sol
     }
 }
 
+#include "stencil_kernel.cuh"
+
 // Decoupled pass as its own kernel (tracking mode: per-iteration sums, then the final
 // write with the iteration count the solve actually used).
 template <typename T>
@@ -2130,6 +2138,12 @@ struct wbx_solver {
     int grid_win = 0;
     unsigned win_smem_fista = 0, win_smem_tau = 0;
     std::shared_ptr<wbx::WinPair> wp;  // window layouts (owned by the operator's cache)
+    // stencil engine (stationary operators with their generator groups attached)
+    bool stencil = false;
+    int grid_st = 0;
+    unsigned st_smem = 0;
+    std::shared_ptr<wbx::StencilPlan> sp;  // owned by the operator's cache
+    wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
     cudaStream_t copy_stream = nullptr;  // host->device image copies overlapping the step estimate
@@ -2244,6 +2258,12 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
         a.wT = view_of(s->wp->T);
         a.win_lists_global = s->win_lists_global ? 1 : 0;
     }
+    if (s->stencil) {
+        a.st = view_of(*s->sp);
+        a.st_fill = env_int("WBX_ST_FILL", 0, 0, 2);
+        a.yF = s->yF.p;
+        a.resF = s->resF.p;
+    }
     {
         const char* e = std::getenv("WBX_BARRIER");
         a.sync.mode = !e ? 2 : std::string(e) == "allpoll" ? 1 : std::string(e) == "master" ? 0 : 2;
@@ -2323,6 +2343,13 @@ template <typename T>
 void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
+    if (s->stencil && !a.track && s->batch == 1) {
+        a.isC = a.st.coupled;  // the decoupled pass: coordinates outside the Theta^T output bands
+        launch_coop_smem(reinterpret_cast<const void*>(fista_stencil_kernel), s->grid_st, s->st_smem, a, st, kStBlock);
+        count_launch(ctx);
+        WBX_CUDA(cudaGetLastError());
+        return;
+    }
     const bool win = s->win && !a.track && s->batch == 1;
     if (win) {
         const void* k = fista_win_fn(s->win_dict, s->win_lists_global);
@@ -2491,6 +2518,37 @@ void alloc_state(wbx_solver* s) {
     }
     if (!s->win)  // stream engine: Lanczos tau unless WBX_TAU=power (the window attempts may have reset it)
         s->tau_lanczos = sizeof(T) == 4 && !(std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power");
+    // stencil engine for the FISTA iterations (fp32 single images; the operator carries its
+    // generator groups): 2 then 1 CTA per SM
+    const char* se = std::getenv("WBX_STENCIL");
+    if (sizeof(T) == 4 && s->batch == 1 && s->op->has_gens && se && std::string(se) != "0" &&
+        !(eng && std::string(eng) == "stream")) {
+        for (int bps = 1; bps >= 1 && !s->stencil; --bps) {
+            const uint32_t G = static_cast<uint32_t>(bps * s->ctx->num_sms);
+            auto sp = stencil_plan_for(s->op, G, kStWarps, s->ctx->stream);
+            std::string why;
+            if (!stencil_plan_ok(*sp, &why)) {
+                if (std::getenv("WBX_VERBOSE")) std::fprintf(stderr, "wbx stencil engine: G=%u: %s\n", G, why.c_str());
+                continue;
+            }
+            const unsigned smem = st_smem_layout(view_of(*sp)).total;
+            const unsigned limit = bps == 1 ? 220u * 1024u : (227u * 1024u) / bps - 2048u;
+            if (std::getenv("WBX_VERBOSE"))
+                std::fprintf(stderr, "wbx stencil engine: G=%u smem %u limit %u\n", G, smem, limit);
+            if (smem > limit) continue;
+            const void* k = reinterpret_cast<const void*>(fista_stencil_kernel);
+            WBX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            int occ = 0;
+            WBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kStBlock, smem));
+            if (occ < bps) continue;
+            s->stencil = true;
+            s->sp = sp;
+            s->grid_st = static_cast<int>(G);
+            s->st_smem = smem;
+            s->yF.alloc(s->op->n);    // y (phase A source), natural layout
+            s->resF.alloc(s->op->n);  // residual (phase T source)
+        }
+    }
 }
 
 }  // namespace
@@ -2538,7 +2596,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     s->uC.alloc(nC ? nC : 1);
     s->t64.alloc(op->nR ? op->nR : 1);
     s->out.alloc(OUT_COUNT);
-    const uint64_t gmax = static_cast<uint64_t>(std::max({s->grid_fista, s->grid_tau, s->grid_tau_lz, s->grid_win}));
+    const uint64_t gmax = static_cast<uint64_t>(std::max({s->grid_fista, s->grid_tau, s->grid_tau_lz, s->grid_win, s->grid_st}));
     s->gen.alloc(kCounterWord + 32 * kMaxCounterGroups);
     s->arrive.alloc(gmax);
     s->part.alloc((2 * kRedSlots + 5) * gmax);  // barrier reductions + tracked window solve partials
@@ -2885,7 +2943,8 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
-    const char* it = (s->win && !track && s->batch == 1) ? "fista_win_kernel"
+    const char* it = (s->stencil && !track && s->batch == 1) ? "fista_stencil_kernel"
+                     : (s->win && !track && s->batch == 1) ? "fista_win_kernel"
                      : (s->win_track && track && s->batch == 1) ? "fista_win_track_kernel"
                      : s->batch == 4                      ? "fista_batch_kernel<4>"
                      : s->batch == 8                      ? "fista_batch_kernel<8>"

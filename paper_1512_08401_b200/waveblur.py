@@ -344,6 +344,14 @@ class SparseOperator:
             h = C.c_void_p()
             _check(lib.wbx_op_create(ctx.handle, self.n, _u64ptr(self.row_offsets),
                                      _u32ptr(self.col_indices), _dptr(self.values), C.byref(h)))
+            gl = getattr(self, "generators", None)
+            if gl is not None:
+                d = np.array(gl.dims, dtype=np.uint64)
+                st = lib.wbx_op_set_generators(h, len(gl.dims), _u64ptr(d), gl.J, gl.blocks.size, _u32ptr(gl.blocks),
+                                               _u32ptr(gl.gen_index), _u64ptr(gl.counts), _dptr(gl.values))
+                if st != N.WBX_OK:
+                    lib.wbx_op_destroy(h)
+                    _check(st)
             self._devs[ctx] = h
             if self._ctx is None:
                 self._ctx = ctx
@@ -536,7 +544,9 @@ def theta_from_generators(gl: GeneratorList) -> SparseOperator:
     ci = np.zeros(max(nnz.value, 1), dtype=np.uint32)
     va = np.zeros(max(nnz.value, 1), dtype=np.float64)
     _check(lib.wbx_theta_expand(*args, _u64ptr(ro), _u32ptr(ci), _dptr(va)))
-    return SparseOperator(n, ro, ci[: nnz.value], va[: nnz.value], layout, gl.family, gl.order)
+    op = SparseOperator(n, ro, ci[: nnz.value], va[: nnz.value], layout, gl.family, gl.order)
+    op.generators = gl  # the compressed form: attached to the device operator (stencil engine)
+    return op
 
 
 def gaussian_psf_kernel(dims, sigma: float) -> np.ndarray:
