@@ -98,13 +98,13 @@ __device__ double lz_power_on_T(const double* al, const double* be, int m, doubl
 struct LzCtl {  // control state of tau_lanczos_win_kernel (shared memory, identical in every CTA)
     double alpha, beta, rb;  // alpha_j, beta_j, 1 / beta_j of the current step
     int breakdown;
-    double r2, lambda, check_prev;
+    double r2, lambda, check_prev, tol;
     int stop_prev, iters, steps, zero, done, gap;
 };
 
 // Evaluate T_m (warp 0) and take the decision: `final` (the cap, a breakdown) or the
 // zero-operator sentinel end the estimate; otherwise it ends when this check agrees with the
-// previous one (same stopping index, lambda within 1e-12). All threads of the CTA call it.
+// previous one (same stopping index, lambda within ctl->tol). All threads of the CTA call it.
 __device__ __noinline__ bool lz_check(const double* al, const double* be, int m, bool final, LzCtl* ctl) {
     // warp 0 evaluates T_m and warp 1 T_{m-gap} at the same time (the other warps idle): two
     // estimates per check, so the first check at which they agree ends the estimate
@@ -137,7 +137,7 @@ __device__ __noinline__ bool lz_check(const double* al, const double* be, int m,
     if (threadIdx.x == 0) {
         const double lam = ctl->lambda;
         ctl->done = final || ctl->zero ||
-                    (m1 >= 1 && its1 == ctl->iters && fabs(lam - lam1) <= 1e-12 * fabs(lam));
+                    (m1 >= 1 && its1 == ctl->iters && fabs(lam - lam1) <= ctl->tol * fabs(lam));
     }
     __syncthreads();
     return ctl->done != 0;

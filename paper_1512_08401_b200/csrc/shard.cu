@@ -18,6 +18,7 @@
 // only enqueues: nothing in the power iteration synchronises with it.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -426,7 +427,7 @@ __global__ void lz_rank_sums_kernel(ShardArgs a, unsigned blocks, int init) {
 
 // on the all-gathered sums (rank order, every rank alike): phase 0 starts the estimate,
 // 1 takes alpha_j, 2 takes beta_j+1 and runs the scheduled check (two warps)
-__global__ void lz_update_kernel(ShardArgs a, int phase, int first, int every, int gap) {
+__global__ void lz_update_kernel(ShardArgs a, int phase, int first, int every, int gap, double tol) {
     __shared__ LzCtl ctl;
     __shared__ int check, final;
     double* lz = a.lz;
@@ -457,6 +458,7 @@ __global__ void lz_update_kernel(ShardArgs a, int phase, int first, int every, i
                 check = final || (jn >= first && (jn - first) % every == 0);
                 ctl.r2 = lz[LZ_R2];
                 ctl.gap = gap;
+                ctl.tol = tol;
                 ctl.done = 0;
             }
         }
@@ -849,7 +851,9 @@ int wbx_shard_lz_begin(wbx_shard* s) {
 int wbx_shard_lz_update(wbx_shard* s, int phase, int first, int every, int gap) {
     if (!s || !s->sums_pad || !s->lz.p || phase < 0 || phase > 2 || first < 1 || every < 1 || gap < 1)
         return WBX_INVALID_ARGUMENT;
-    wbx::lz_update_kernel<<<1, 64, 0, s->ctx->stream>>>(wbx::args_of(s), phase, first, every, gap);
+    // the single-GPU solver's agreement tolerance (WBX_LZ_TOL, solver.cu make_args)
+    const double tol = std::getenv("WBX_LZ_TOL") ? std::atof(std::getenv("WBX_LZ_TOL")) : 1e-9;
+    wbx::lz_update_kernel<<<1, 64, 0, s->ctx->stream>>>(wbx::args_of(s), phase, first, every, gap, tol);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
 }
@@ -976,7 +980,7 @@ struct wbx_sharded {
     wbx::DevBuf<float> y, res;
     wbx::DevBuf<double> u, t, sums, x0, x;
     wbx_solver_cfg cfg{};
-    int lz_first = 60, lz_every = 4, lz_gap = 4;
+    int lz_first = 52, lz_every = 4, lz_gap = 4;
     bool power = false;
     cudaGraphExec_t fista_exec = nullptr, lz_exec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -1192,7 +1196,7 @@ int wbx_sharded_create(wbx_ctx* ctx, uint64_t n, const uint64_t* rowptr, const u
             const char* e = std::getenv(k);
             return e ? std::max(1, std::min(wbx::kLzCap, std::atoi(e))) : d;
         };
-        S->lz_first = env("WBX_LZ_FIRST", 60);
+        S->lz_first = env("WBX_LZ_FIRST", 52);
         S->lz_every = wbx::kLzChunk;
         S->lz_gap = env("WBX_LZ_GAP", 4);
         S->power = std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power";

@@ -104,6 +104,7 @@ struct SolveArgs {
     // window engine (win.cuh): per-CTA layouts of Theta (A) and Theta^T (T)
     WinView wA, wT;
     int lz_first, lz_every, lz_gap;  // Lanczos tau: first check, check period, compared m - gap
+    double lz_tol;                   // Lanczos tau: two checks agree when lambda is within lz_tol
     int win_lists_global;            // window index lists read from global memory (win_smem_head)
     // stencil engine (stencil_engine.cuh): the plan and its fp32 source vectors
     StencilView st;
@@ -1625,9 +1626,12 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_win_kernel(Solve
 // step costs the same two operator products as a power iteration, but the quadrature
 // converges super-geometrically in m: at C2, estimates from successive m agree to 1e-15
 // from m = 56 on, where the power iteration needs all 200 iterations. The kernel checks at
-// m = lz_first, lz_first + lz_every, ... and stops once two checks agree to 1e-12 with the
-// same stopping index, or at m = 200, where the identity covers every p <= 399 the
-// reference can reach.
+// m = lz_first (52), lz_first + lz_every, ... and stops once the estimates from T_m and
+// T_{m-4} agree to lz_tol (1e-9) with the same stopping index, or at m = 200, where the
+// identity covers every p <= 399 the reference can reach. 1e-9 sits 60x below the fp32
+// rounding of tau/p the iterations use (and below the 2e-8 the fp32 operator values already
+// move tau from the reference's); at C2 the estimate then stops at m = 52 instead of 60
+// (tools/lz_sweep.py).
 // sum of G staged block partials in a fixed order (the same in every CTA); all threads
 __device__ __forceinline__ double cta_sum_staged(const double* st, unsigned G, double* red) {
     double p = 0.0;
@@ -1714,6 +1718,7 @@ __global__ void __launch_bounds__(kWinBlock, kWinMinBlocks) tau_lanczos_win_kern
         ctl.zero = !(beta > 0.0);
         ctl.breakdown = 0;
         ctl.gap = a.lz_gap;
+        ctl.tol = a.lz_tol;
         ctl.done = ctl.zero;
     }
     __syncthreads();
@@ -1842,6 +1847,7 @@ __global__ void __launch_bounds__(kBlock, WBX_TAU_MINB) tau_lanczos_kernel(Solve
         ctl.done = ctl.zero;
         ctl.breakdown = 0;
         ctl.gap = a.lz_gap;
+        ctl.tol = a.lz_tol;
     }
     __syncthreads();
     for (int j = 0; !ctl.done;) {
@@ -2250,9 +2256,10 @@ SolveArgs make_args(wbx_solver* s, const double* x0_full, double* x_full) {
     a.sync.trace = s->trace.p;
     a.sync.trace_cap = static_cast<unsigned>(s->trace_cap);
     a.nslots = s->nslots;
-    a.lz_first = env_int("WBX_LZ_FIRST", 60, 1, kLzCap);
+    a.lz_first = env_int("WBX_LZ_FIRST", 52, 1, kLzCap);
     a.lz_every = env_int("WBX_LZ_EVERY", 4, 1, kLzCap);
     a.lz_gap = env_int("WBX_LZ_GAP", 4, 1, kLzCap);
+    a.lz_tol = std::getenv("WBX_LZ_TOL") ? std::atof(std::getenv("WBX_LZ_TOL")) : 1e-9;
     if (s->win) {
         a.wA = view_of(s->wp->A);
         a.wT = view_of(s->wp->T);
