@@ -75,6 +75,7 @@ struct DevBuf {
 struct WinSide {
     uint32_t G = 0, max_u = 0, max_win = 0, max_rows = 0, max_slices = 0, max_dict = 0;
     uint32_t src_len = 0;  // length of the gathered vector (set by the solver)
+    bool chunk = false;    // chunk layout (win.cuh WinView::chunk)
     DevBuf<uint32_t> u_off, u_idx, s_off, r_off, d_off;
     DevBuf<uint16_t> u_slot;
     DevBuf<uint4> s_tab, rec;
@@ -225,7 +226,8 @@ void build_sell(wbx_sell& out, uint64_t nrows, const std::function<uint64_t(uint
                 uint64_t& bytes);
 
 // winlayout.cu: per-CTA window layout of one operator side (WinSide, above)
-void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side);  // side 'A' or 'T'
+// side 'A' or 'T'; chunk: the chunk layout (fp32 sources, 16-byte window copies)
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side, bool chunk);
 struct WinView;
 WinView view_of(const WinSide& w);
 

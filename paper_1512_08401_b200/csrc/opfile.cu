@@ -141,7 +141,9 @@ void get_compact(File& f, HostCompact& h, uint64_t cap) {
 }
 
 void put_win(File& f, const WinSide& w) {
-    const uint32_t hdr[7] = {w.G, w.max_u, w.max_win, w.max_rows, w.max_slices, w.max_dict, w.src_len};
+    // src_len < 2^31; its top bit carries the chunk-layout flag
+    const uint32_t hdr[7] = {w.G, w.max_u, w.max_win, w.max_rows, w.max_slices, w.max_dict,
+                             w.src_len | (w.chunk ? 0x80000000u : 0u)};
     f.write(hdr, sizeof hdr);
     f.put64(w.bytes);
     put_dev(f, w.u_off);
@@ -163,7 +165,8 @@ void get_win(File& f, WinSide& w, uint64_t cap, cudaStream_t s) {
     w.max_rows = hdr[3];
     w.max_slices = hdr[4];
     w.max_dict = hdr[5];
-    w.src_len = hdr[6];
+    w.src_len = hdr[6] & 0x7fffffffu;
+    w.chunk = (hdr[6] >> 31) != 0;
     w.bytes = f.u64();
     get_dev(f, w.u_off, cap, s);
     get_dev(f, w.u_idx, cap, s);

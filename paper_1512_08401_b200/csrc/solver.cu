@@ -1166,11 +1166,19 @@ __device__ __forceinline__ void win_phase(const WinView& W, const uint32_t* uidx
     WinSlice<DICT> b0, b1;
     if (wib < ns) win_load<DICT>(W.rec, stab[wib], lane, pol, b0);
     // window fill (L1 lines are invalidated by the grid barrier's acquire)
-    for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
-        WBX_ASSERT(uslot[i] < W.max_win && uidx[i] < W.src_len);
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
-                     : "memory");
+    if (sizeof(X) == 4 && W.chunk) {  // chunk layout: 16-byte copies, chunk i to window floats 4 slot(i)..
+        for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
+            WBX_ASSERT(4u * uslot[i] + 3 < W.max_win && 4 * uidx[i] < W.src_len);
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + 4u * uslot[i]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(x + 4 * uidx[i]) : "memory");
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < nu; i += kWinBlock) {
+            WBX_ASSERT(uslot[i] < W.max_win && uidx[i] < W.src_len);
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(win + uslot[i]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(x + uidx[i]), "n"(sizeof(X))
+                         : "memory");
+        }
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
@@ -2415,8 +2423,13 @@ std::shared_ptr<WinPair> win_layout(const wbx_op* op, uint32_t G, cudaStream_t s
     if (it != op->win_cache.end()) return it->second;
     auto p = std::make_shared<WinPair>();
     try {
-        build_win(p->A, op->hA, G, st, 'A');
-        build_win(p->T, op->hT, G, st, 'T');
+        // window placement: chunk layout (16-byte fills, chunks in source order; default, or
+        // bank-aware chunk slots with WBX_WIN_PLACE=chunk-bank), or per-entry slots, bank-aware
+        // (=bank, round 1's default) or in source order (=sorted)
+        const char* pl = std::getenv("WBX_WIN_PLACE");
+        const bool chunk = !pl || std::string(pl).rfind("chunk", 0) == 0;
+        build_win(p->A, op->hA, G, st, 'A', chunk);
+        build_win(p->T, op->hT, G, st, 'T', chunk);
         p->A.src_len = static_cast<uint32_t>(op->nC);  // A rows gather C-space vectors
         p->T.src_len = static_cast<uint32_t>(op->nR);
         WBX_CUDA(cudaStreamSynchronize(st));  // usable from any stream of the device
@@ -2467,7 +2480,9 @@ void alloc_state(wbx_solver* s) {
             const WinView vA = view_of(s->wp->A), vT = view_of(s->wp->T);
             const unsigned mu = std::max(s->wp->A.max_win, s->wp->T.max_win);
             s->win_smem_fista = win_smem_head<4, 16>(vA, vT, lg) + mu * 4u;
-            s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64";
+            // fp64 windows (diagnostics) need per-entry window layouts (WBX_WIN_PLACE=bank)
+            s->tau_win64 = std::getenv("WBX_TAU_WINDOW") && std::string(std::getenv("WBX_TAU_WINDOW")) == "64" &&
+                           !s->wp->A.chunk;
             // tau by Lanczos + the power iteration on the tridiagonal (tau_lanczos_win_kernel);
             // WBX_TAU=power runs the literal power iteration
             // (falls back to the power iteration when its state does not fit next to the window)

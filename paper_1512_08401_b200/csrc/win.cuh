@@ -31,8 +31,10 @@ constexpr uint32_t kWinDictBudget = 16384;  // bytes of dictionary per CTA and s
 
 struct WinView {
     const uint32_t* u_off;   // [G+1] window offsets into u_idx
-    const uint32_t* u_idx;   // window entries: positions in the source vector
-    const uint16_t* u_slot;  // shared-memory slot of each window entry (bank-aware placement)
+    const uint32_t* u_idx;   // window entries: positions in the source vector (chunk layout: the
+                             // 16-byte chunk index)
+    const uint16_t* u_slot;  // shared-memory slot of each window entry (bank-aware placement;
+                             // chunk layout: chunk slot, the chunk fills window floats 4 slot ..)
     const uint32_t* s_off;   // [G+1] slice offsets of each CTA
     const uint4* s_tab;      // per slice {record offset (uint4), meta, first row, 0}
     const uint32_t* r_off;   // [G+1] first compacted row of each CTA (rows are contiguous)
@@ -45,6 +47,7 @@ struct WinView {
     uint32_t max_slices;     // most slices of any CTA
     uint32_t max_dict;       // largest dictionary of any CTA (floats; 0 = full format)
     uint32_t src_len;        // length of the vector the windows gather from (debug checks)
+    uint32_t chunk;          // 1: chunk layout (fp32 sources; one 16-byte copy per chunk)
 };
 
 // slice meta word: nq (quads per lane) | m (lane stride) << 8 | q (segments per row) << 16 |

@@ -109,7 +109,7 @@ std::vector<uint16_t> place_window(const std::vector<uint4>& rec, const std::vec
                                    bool dict_fmt, size_t nu, uint32_t* max_win) {
     std::vector<uint16_t> slot(nu);
     const char* mode = std::getenv("WBX_WIN_PLACE");
-    if (mode && std::string(mode) == "sorted") {
+    if (mode && std::string(mode) == "sorted") {  // diagnostics: source order
         for (size_t i = 0; i < nu; ++i) slot[i] = static_cast<uint16_t>(i);
         *max_win = std::max<uint32_t>(*max_win, static_cast<uint32_t>(nu));
         return slot;
@@ -168,7 +168,154 @@ std::vector<uint16_t> place_window(const std::vector<uint4>& rec, const std::vec
 
 }  // namespace
 
-void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side) {
+// Rotations of the chunks inside each 128-byte line of the (source-order) chunk layout: a
+// rotation keeps a line's chunks in that line (the fill still reads and writes contiguous
+// 512 B per warp) but moves its entries to other banks. Greedy per line (most-read lines
+// first): the rotation whose entries collide least with the entries already placed in the
+// gather groups (one gather instruction's 32 lanes) that read them.
+std::vector<uint32_t> line_rotations(const std::vector<uint4>& rec, const std::vector<uint4>& s_tab, size_t slice0,
+                                     bool dict_fmt, const std::vector<uint32_t>& u,
+                                     const std::vector<uint32_t>& chunk_of, size_t nc) {
+    const size_t nl = (nc + 7) / 8;
+    std::vector<std::vector<uint32_t>> groups_of(u.size());  // rank -> gather groups reading it
+    uint32_t ng = 0;
+    for (size_t sidx = slice0; sidx < s_tab.size(); ++sidx) {
+        const uint32_t nq = s_tab[sidx].y & 0xffu;
+        const uint16_t* cols = reinterpret_cast<const uint16_t*>(&rec[s_tab[sidx].x + (dict_fmt ? 4 : nq * 32)]);
+        for (uint32_t qd = 0; qd < nq; ++qd)
+            for (uint32_t e = 0; e < 4; ++e) {
+                std::vector<uint16_t> g;
+                for (uint32_t lane = 0; lane < 32; ++lane) g.push_back(cols[(qd * 32 + lane) * 4 + e]);
+                std::sort(g.begin(), g.end());
+                g.erase(std::unique(g.begin(), g.end()), g.end());
+                if (g.size() < 2) continue;
+                for (uint16_t r : g) groups_of[r].push_back(ng);
+                ++ng;
+            }
+    }
+    std::vector<std::vector<uint32_t>> ranks_of_line(nl);
+    std::vector<uint32_t> reads(nl, 0);
+    for (size_t r = 0; r < u.size(); ++r) {
+        ranks_of_line[chunk_of[r] >> 3].push_back(static_cast<uint32_t>(r));
+        reads[chunk_of[r] >> 3] += static_cast<uint32_t>(groups_of[r].size());
+    }
+    std::vector<uint32_t> order(nl);
+    for (uint32_t i = 0; i < nl; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return reads[a] > reads[b]; });
+    std::vector<uint8_t> used(static_cast<size_t>(ng) * 32, 0);
+    std::vector<uint32_t> rot(nl, 0);
+    for (uint32_t L : order) {
+        uint32_t best = 0, best_cost = UINT32_MAX;
+        for (uint32_t r = 0; r < 8; ++r) {
+            uint32_t cost = 0;
+            for (uint32_t rk : ranks_of_line[L]) {
+                const uint32_t bank = 4 * ((chunk_of[rk] + r) & 7u) + (u[rk] & 3u);
+                for (uint32_t g : groups_of[rk]) cost += used[static_cast<size_t>(g) * 32 + bank];
+            }
+            if (cost < best_cost) {
+                best_cost = cost;
+                best = r;
+            }
+        }
+        rot[L] = best;
+        for (uint32_t rk : ranks_of_line[L]) {
+            const uint32_t bank = 4 * ((chunk_of[rk] + best) & 7u) + (u[rk] & 3u);
+            for (uint32_t g : groups_of[rk]) {
+                uint8_t& c = used[static_cast<size_t>(g) * 32 + bank];
+                if (c < 255) ++c;
+            }
+        }
+    }
+    return rot;
+}
+
+// Chunk layout placement: window chunk c (4 consecutive source floats) goes to chunk slot
+// cs[c], its floats to window 4 cs[c] .. 4 cs[c] + 3, so entry u sits in bank
+// 4 (cs[c] mod 8) + (u mod 4). Default: cs[c] = c (source order). WBX_WIN_PLACE=chunk-bank
+// chooses the bank group cs mod 8 of each chunk greedily, as place_window does per entry, so
+// that the entries one gather instruction reads spread over the banks.
+// `rank_slot` receives each window entry's float slot (entries in rank order of u).
+std::vector<uint16_t> place_chunks(const std::vector<uint4>& rec, const std::vector<uint4>& s_tab, size_t slice0,
+                                   bool dict_fmt, const std::vector<uint32_t>& u, const std::vector<uint32_t>& chunks,
+                                   std::vector<uint16_t>& rank_slot, uint32_t* max_win) {
+    constexpr int kGroups = 8;
+    const size_t nc = chunks.size();
+    std::vector<uint32_t> chunk_of(u.size());  // rank -> chunk ordinal
+    for (size_t i = 0, c = 0; i < u.size(); ++i) {
+        while (chunks[c] != u[i] >> 2) ++c;
+        chunk_of[i] = static_cast<uint32_t>(c);
+    }
+    std::vector<int> bg(nc, -1);
+    std::vector<uint32_t> fill(kGroups, 0);
+    // default: chunks in source order, rotated inside their 128-byte lines (a warp's fill reads
+    // and writes contiguous 512 B); WBX_WIN_PLACE=chunk-plain: no rotation; =chunk-bank: chunk
+    // slots chosen per chunk (gathers conflict less, but the fills touch scattered lines: C2
+    // 2.20 vs 2.13-2.16 ms per deblur for plain)
+    const char* mode = std::getenv("WBX_WIN_PLACE");
+    const bool plain = !(mode && std::string(mode) == "chunk-bank");
+    if (!plain) {
+        std::vector<std::vector<uint16_t>> groups;  // ranks one gather reads
+        for (size_t sidx = slice0; sidx < s_tab.size(); ++sidx) {
+            const uint32_t nq = s_tab[sidx].y & 0xffu;
+            const uint16_t* cols = reinterpret_cast<const uint16_t*>(&rec[s_tab[sidx].x + (dict_fmt ? 4 : nq * 32)]);
+            for (uint32_t qd = 0; qd < nq; ++qd)
+                for (uint32_t e = 0; e < 4; ++e) {
+                    std::vector<uint16_t> g;
+                    for (uint32_t lane = 0; lane < 32; ++lane) g.push_back(cols[(qd * 32 + lane) * 4 + e]);
+                    std::sort(g.begin(), g.end());
+                    g.erase(std::unique(g.begin(), g.end()), g.end());
+                    if (g.size() > 1) groups.push_back(std::move(g));
+                }
+        }
+        std::stable_sort(groups.begin(), groups.end(),
+                         [](const std::vector<uint16_t>& x, const std::vector<uint16_t>& y) { return x.size() > y.size(); });
+        for (const auto& g : groups) {
+            int used[32] = {0};
+            for (uint16_t r : g)
+                if (bg[chunk_of[r]] >= 0) ++used[4 * bg[chunk_of[r]] + (u[r] & 3u)];
+            for (uint16_t r : g) {
+                const uint32_t c = chunk_of[r];
+                if (bg[c] >= 0) continue;
+                int best = 0;
+                for (int k = 1; k < kGroups; ++k) {
+                    const int uk = used[4 * k + (u[r] & 3u)], ub = used[4 * best + (u[r] & 3u)];
+                    if (uk < ub || (uk == ub && fill[k] < fill[best])) best = k;
+                }
+                bg[c] = best;
+                ++fill[best];
+                // the chunk's other entries of this group now occupy their banks too
+                for (uint16_t r2 : g)
+                    if (chunk_of[r2] == c) ++used[4 * best + (u[r2] & 3u)];
+            }
+        }
+    }
+    for (size_t c = 0; c < nc; ++c)
+        if (bg[c] < 0) {
+            int best = 0;
+            for (int k = 1; k < kGroups; ++k)
+                if (fill[k] < fill[best]) best = k;
+            bg[c] = plain ? static_cast<int>(c % kGroups) : best;
+            if (!plain) ++fill[best];
+        }
+    std::vector<uint16_t> cslot(nc);
+    std::vector<uint32_t> next(kGroups, 0);
+    uint32_t extent = 0;
+    std::vector<uint32_t> rot;  // default: per 128-byte line of 8 chunks, a rotation of its chunks
+    if (plain && !(mode && std::string(mode) == "chunk-plain")) rot = line_rotations(rec, s_tab, slice0, dict_fmt, u, chunk_of, nc);
+    for (size_t c = 0; c < nc; ++c) {
+        uint32_t sl = plain ? static_cast<uint32_t>(c) : static_cast<uint32_t>(bg[c]) + kGroups * next[bg[c]]++;
+        if (!rot.empty()) sl = (sl & ~7u) | ((sl + rot[sl >> 3]) & 7u);
+        if (4 * sl + 3 > 0xffffu) fail(WBX_TOO_LARGE, "CTA window exceeds 16-bit slots");
+        cslot[c] = static_cast<uint16_t>(sl);
+        extent = std::max(extent, 4 * sl + 4);
+    }
+    rank_slot.resize(u.size());
+    for (size_t i = 0; i < u.size(); ++i) rank_slot[i] = static_cast<uint16_t>(4 * cslot[chunk_of[i]] + (u[i] & 3u));
+    *max_win = std::max(*max_win, extent);
+    return cslot;
+}
+
+void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, char side, bool chunk) {
     const std::vector<uint64_t> rb = balance(M, G, side);
     // format: the dictionary when every CTA's fits the budget
     bool dict_fmt = std::getenv("WBX_WIN_FULL") == nullptr;  // diagnostics: force the full format
@@ -190,8 +337,17 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, 
         std::sort(u.begin(), u.end());
         u.erase(std::unique(u.begin(), u.end()), u.end());
         if (u.size() > 65536) fail(WBX_TOO_LARGE, "CTA window exceeds 16-bit local indices");
-        max_u = std::max<uint32_t>(max_u, static_cast<uint32_t>(u.size()));
-        u_idx.insert(u_idx.end(), u.begin(), u.end());
+        std::vector<uint32_t> chunks;  // chunk layout: the 16-byte source chunks the window covers
+        if (chunk) {
+            for (uint32_t v : u)
+                if (chunks.empty() || chunks.back() != v >> 2) chunks.push_back(v >> 2);
+            if (chunks.size() * 4 > 65536) fail(WBX_TOO_LARGE, "CTA window exceeds 16-bit slots");
+            max_u = std::max<uint32_t>(max_u, static_cast<uint32_t>(chunks.size()));
+            u_idx.insert(u_idx.end(), chunks.begin(), chunks.end());
+        } else {
+            max_u = std::max<uint32_t>(max_u, static_cast<uint32_t>(u.size()));
+            u_idx.insert(u_idx.end(), u.begin(), u.end());
+        }
         u_off[b + 1] = static_cast<uint32_t>(u_idx.size());
         auto loc = [&](uint32_t pos) {
             return static_cast<uint16_t>(std::lower_bound(u.begin(), u.end(), pos) - u.begin());
@@ -252,13 +408,27 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, 
         // bank-aware placement of the window: the entries one gather instruction reads (one
         // element position across the 32 lanes of a slice) go to distinct shared-memory
         // banks where possible; records are rewritten from ranks to slots
-        const std::vector<uint16_t> slot = place_window(rec, s_tab, slice0, dict_fmt, u.size(), &max_win);
+        std::vector<uint16_t> slot;
+        if (chunk) {  // chunk i -> window floats 4 cs .. 4 cs + 3 (a verbatim 16-byte copy)
+            const std::vector<uint16_t> cs = place_chunks(rec, s_tab, slice0, dict_fmt, u, chunks, slot, &max_win);
+            // the fill list in slot order: a warp's 16-byte copies land in consecutive smem
+            std::vector<uint32_t> ord(cs.size());
+            for (uint32_t i = 0; i < ord.size(); ++i) ord[i] = i;
+            std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return cs[x] < cs[y]; });
+            const size_t at = u_idx.size() - chunks.size();
+            for (size_t i = 0; i < ord.size(); ++i) {
+                u_idx[at + i] = chunks[ord[i]];
+                u_slot.push_back(cs[ord[i]]);
+            }
+        } else {
+            slot = place_window(rec, s_tab, slice0, dict_fmt, u.size(), &max_win);
+            u_slot.insert(u_slot.end(), slot.begin(), slot.end());
+        }
         for (size_t sidx = slice0; sidx < s_tab.size(); ++sidx) {
             const uint32_t nq = s_tab[sidx].y & 0xffu;
             uint16_t* cols = reinterpret_cast<uint16_t*>(&rec[s_tab[sidx].x + (dict_fmt ? 4 : nq * 32)]);
             for (uint32_t e = 0; e < nq * 128; ++e) cols[e] = slot[cols[e]];
         }
-        u_slot.insert(u_slot.end(), slot.begin(), slot.end());
     }
     std::vector<uint32_t> r_off(G + 1);
     uint32_t max_rows = 0;
@@ -272,6 +442,7 @@ void build_win(WinSide& out, const HostCompact& M, uint32_t G, cudaStream_t st, 
     if (rec.empty()) rec.resize(1, make_uint4(0, 0, 0, 0));
     if (d_val.empty()) d_val.push_back(0.0f);
     out.G = G;
+    out.chunk = chunk;
     out.max_u = max_u;
     out.max_win = std::max(max_win, max_u);
     out.max_rows = max_rows;
@@ -308,6 +479,7 @@ WinView view_of(const WinSide& w) {
     v.max_slices = w.max_slices;
     v.max_dict = w.max_dict;
     v.src_len = w.src_len;
+    v.chunk = w.chunk ? 1u : 0u;
     return v;
 }
 

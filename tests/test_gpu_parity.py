@@ -432,7 +432,8 @@ def test_deblurrer_c2_1024_vs_oracle(golden):
 
 
 # ----------------------------------------------------------------------------- engine / format variants
-@pytest.mark.parametrize("env", [{}, {"WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"}, {"WBX_TAU_WINDOW": "64"},
+@pytest.mark.parametrize("env", [{}, {"WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"},
+                                 {"WBX_TAU_WINDOW": "64", "WBX_WIN_PLACE": "bank"}, {"WBX_WIN_PLACE": "bank"},
                                  {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
                                  {"WBX_WIN_COST": "16,1"}, {"WBX_WIN_LISTS": "global"}])
 def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
@@ -451,7 +452,8 @@ def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
     assert np.array_equal(u, u2)  # run-to-run deterministic
 
 
-@pytest.mark.parametrize("env", [{"WBX_WIN_FULL": "1"}, {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
+@pytest.mark.parametrize("env", [{"WBX_WIN_FULL": "1"}, {"WBX_WIN_PLACE": "sorted"}, {"WBX_WIN_PLACE": "bank"}, {"WBX_WIN_PLACE": "chunk-bank"},
+                                 {"WBX_BARRIER": "master"},
                                  {"WBX_WIN_COST": "16,1"}, {"WBX_WIN_LISTS": "global"}, {"WBX_BARRIER_GROUPS": "4"},
                                  {"WBX_WIN_MODEL": "0.0186,0.0129,0.0024,0,0"}, {"WBX_GRAPH": "0"}])
 def test_window_layout_variants_leave_iterates_bitwise(golden, monkeypatch, env):

@@ -4,6 +4,8 @@ Per warp and phase of each side (A = Theta rows, T = Theta^T rows), in SM cycles
 fill, slice loop, grid barrier (incl. waiting for the slowest CTA)."""
 import ctypes as C
 import json
+
+import numpy as np
 import sys
 from pathlib import Path
 
@@ -14,7 +16,8 @@ from paper_1512_08401_b200 import waveblur as W  # noqa: E402
 
 lib = _native.lib
 lib.wbx_diag_slice_profile.argtypes = [C.POINTER(C.c_double)]
-op, basis, u0, meta = bench.make_inputs()
+op, basis, u0 = bench.make_inputs()
+meta = json.loads(bytes(np.load(bench.GOLDEN)["meta_json"]).decode())
 ctx = W.Context(0)
 P = W.spai(op, ctx)
 w = W.scale_weights(basis.layout)
