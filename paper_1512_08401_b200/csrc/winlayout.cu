@@ -15,13 +15,14 @@ namespace {
 
 uint64_t segs_of(uint64_t len) { return std::max<uint64_t>(1, (len + kSegElems - 1) / kSegElems); }
 
-// Contiguous row ranges per CTA balanced by a per-row COST. Default model (round 2, fitted by
-// least squares to per-CTA phase times measured with WBX_TRACE_FILE at C2, tools/win_fit.py):
+// Contiguous row ranges per CTA balanced by a per-row COST. Default: round 1's cost
+// 8*q + len (q = segments, len = nonzeros). WBX_WIN_MODEL[_A|_T] = "a,b,c,d,e" selects the
+// model fitted by least squares to per-CTA phase times (WBX_TRACE_FILE, tools/win_fit.py):
 //   cost(row) = (a + b*nq + c*(q - 1)) / m + d*len + e
 // with q = segments of the row, m = floor(32/q) rows per slice, nq = quads per lane (the slice
 // chain: record loads, nq gathers + fmas per lane, q - 1 shuffle folds), len = nonzeros (window
-// growth, epilogue). WBX_WIN_MODEL_A/_T = "a,b,c,d,e" overrides per side; WBX_WIN_COST[_A|_T] =
-// "wseg,wnnz" selects round 1's model cost = wseg*q + wnnz*len.
+// growth, epilogue); it evens the per-CTA times (C2 spread 1.7 -> 0.8 us) but measured no
+// faster end to end. WBX_WIN_COST[_A|_T] = "wseg,wnnz" sets round 1's weights.
 std::vector<uint64_t> balance(const HostCompact& M, uint32_t G, char side) {
     const uint64_t nrows = M.rows();
     double cm[5] = {0, 0, 0, 0, 0};
