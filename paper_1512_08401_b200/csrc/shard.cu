@@ -852,7 +852,7 @@ int wbx_shard_lz_update(wbx_shard* s, int phase, int first, int every, int gap) 
     if (!s || !s->sums_pad || !s->lz.p || phase < 0 || phase > 2 || first < 1 || every < 1 || gap < 1)
         return WBX_INVALID_ARGUMENT;
     // the single-GPU solver's agreement tolerance (WBX_LZ_TOL, solver.cu make_args)
-    const double tol = std::getenv("WBX_LZ_TOL") ? std::atof(std::getenv("WBX_LZ_TOL")) : 1e-9;
+    const double tol = std::getenv("WBX_LZ_TOL") ? std::atof(std::getenv("WBX_LZ_TOL")) : 1e-8;
     wbx::lz_update_kernel<<<1, 64, 0, s->ctx->stream>>>(wbx::args_of(s), phase, first, every, gap, tol);
     wbx::count_launch(s->ctx);
     return cudaGetLastError() == cudaSuccess ? WBX_OK : WBX_CUDA_ERROR;
@@ -980,7 +980,7 @@ struct wbx_sharded {
     wbx::DevBuf<float> y, res;
     wbx::DevBuf<double> u, t, sums, x0, x;
     wbx_solver_cfg cfg{};
-    int lz_first = 52, lz_every = 4, lz_gap = 4;
+    int lz_first = 48, lz_every = 4, lz_gap = 4;
     bool power = false;
     cudaGraphExec_t fista_exec = nullptr, lz_exec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -1196,7 +1196,7 @@ int wbx_sharded_create(wbx_ctx* ctx, uint64_t n, const uint64_t* rowptr, const u
             const char* e = std::getenv(k);
             return e ? std::max(1, std::min(wbx::kLzCap, std::atoi(e))) : d;
         };
-        S->lz_first = env("WBX_LZ_FIRST", 52);
+        S->lz_first = env("WBX_LZ_FIRST", 48);
         S->lz_every = wbx::kLzChunk;
         S->lz_gap = env("WBX_LZ_GAP", 4);
         S->power = std::getenv("WBX_TAU") && std::string(std::getenv("WBX_TAU")) == "power";
