@@ -201,7 +201,8 @@ inline void count_launch(wbx_ctx* ctx, uint64_t k = 1) { ctx->launches += k; }
 
 // dwt.cu
 void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s);
-void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s);
+// clamp: the deblur's final clamp to [0, 1] fused into the last level
+void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s, int clamp = 0);
 void make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, std::vector<wbx_band>& bands);
 void make_filters(uint32_t family, uint32_t order, double* lo, double* hi, uint32_t* len);
 

@@ -2786,8 +2786,7 @@ void deblur_rest(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp, 
     const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
     for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
     wbx::solver_iters(s, s->x0full.p, s->xfull.p);
-    for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st);
-    if (clamp) wbx::launch_clamp(s->ctx, u_dev, n * B, st);
+    for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st, clamp);
 }
 
 // capture fn's enqueues on st into an executable graph; counts the kernels it enqueued

@@ -107,16 +107,30 @@ __device__ __forceinline__ double fma_free(double acc, double a, double b) {
 
 // ---------------------------------------------------------------- forward
 // dwt_line on every row of an m0 x m1 block: dst[r][k] = lowpass, dst[r][m1/2+k] = highpass.
+// A block computes kThreads outputs of one row from a shared-memory copy of the 2 kThreads +
+// l - 2 inputs they read (one coalesced load per input instead of l/2 strided ones); the sum
+// over taps is the reference's order, so the result is bitwise the same.
 __global__ void fwd_rows_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
                                 int64_t ldd, int m0, int m1, Taps f) {
+    extern __shared__ double sh[];
     const int half = m1 >> 1;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k0 = blockIdx.x * blockDim.x;
     const int r = blockIdx.y;
-    if (k >= half || r >= m0) return;
+    if (r >= m0) return;
     const double* row = src + static_cast<int64_t>(r) * lds;
+    const int nin = 2 * static_cast<int>(blockDim.x) + f.l - 2;
+    for (int t = threadIdx.x; t < nin; t += blockDim.x) {
+        int idx = 2 * k0 + t;
+        if (idx >= m1) idx %= m1;
+        sh[t] = row[idx];
+    }
+    __syncthreads();
+    const int k = k0 + threadIdx.x;
+    if (k >= half) return;
+    const double* w = sh + 2 * threadIdx.x;
     double a = 0.0, d = 0.0;
     for (int i = 0; i < f.l; ++i) {
-        const double s = row[(2 * k + i) % m1];
+        const double s = w[i];
         a = fma_free(a, f.lo[i], s);
         d = fma_free(d, f.hi[i], s);
     }
@@ -125,26 +139,44 @@ __global__ void fwd_rows_kernel(const double* __restrict__ src, int64_t lds, dou
 }
 
 // dwt_line on every column of the rows-pass output, writing subbands directly.
-// Quadrant (row-high e0, col-high e1) -> band orientation e = 2*e0 + e1.
+// Quadrant (row-high e0, col-high e1) -> band orientation e = 2*e0 + e1. A block computes
+// kColsOut outputs down kThreads columns from a shared-memory tile of the 2 kColsOut + l - 2
+// input rows they read (each input row loaded once per block instead of l/2 times); tap
+// order as the reference's (bitwise).
+constexpr int kColsOut = 8;
 __global__ void fwd_cols_kernel(const double* __restrict__ src, int64_t lds, int m0, int m1, Taps f,
                                 double* __restrict__ ll, double* __restrict__ b1,
                                 double* __restrict__ b2, double* __restrict__ b3) {
+    extern __shared__ double sh[];
     const int h0 = m0 >> 1, h1 = m1 >> 1;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    if (c >= m1 || k >= h0) return;
-    double a = 0.0, d = 0.0;
-    for (int i = 0; i < f.l; ++i) {
-        const double s = src[static_cast<int64_t>((2 * k + i) % m0) * lds + c];
-        a = fma_free(a, f.lo[i], s);
-        d = fma_free(d, f.hi[i], s);
+    const int k0 = blockIdx.y * kColsOut;
+    const int nrows = 2 * kColsOut + f.l - 2;
+    if (c >= m1) return;  // no block-wide barrier below: each thread reads its own column
+    for (int t = 0; t < nrows; ++t) {  // all rows in flight (asynchronous copies)
+        int idx = 2 * k0 + t;
+        if (idx >= m0) idx %= m0;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sh + t * blockDim.x + threadIdx.x));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + static_cast<int64_t>(idx) * lds + c)
+                     : "memory");
     }
-    if (c < h1) {
-        ll[static_cast<int64_t>(k) * h1 + c] = a;
-        b2[static_cast<int64_t>(k) * h1 + c] = d;
-    } else {
-        b1[static_cast<int64_t>(k) * h1 + (c - h1)] = a;
-        b3[static_cast<int64_t>(k) * h1 + (c - h1)] = d;
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    for (int kk = 0; kk < kColsOut; ++kk) {
+        const int k = k0 + kk;
+        if (k >= h0) break;
+        double a = 0.0, d = 0.0;
+        for (int i = 0; i < f.l; ++i) {
+            const double s = sh[(2 * kk + i) * blockDim.x + threadIdx.x];
+            a = fma_free(a, f.lo[i], s);
+            d = fma_free(d, f.hi[i], s);
+        }
+        if (c < h1) {
+            ll[static_cast<int64_t>(k) * h1 + c] = a;
+            b2[static_cast<int64_t>(k) * h1 + c] = d;
+        } else {
+            b1[static_cast<int64_t>(k) * h1 + (c - h1)] = a;
+            b3[static_cast<int64_t>(k) * h1 + (c - h1)] = d;
+        }
     }
 }
 
@@ -220,23 +252,27 @@ __global__ void inv_cols_kernel(const double* __restrict__ ll, const double* __r
 }
 
 // Rows pass of inverse level: out[j][x] from V[j][0:h1] (lowpass) and V[j][h1:m1].
+// clamp: the deblur's final std::clamp(v, 0, 1) (waveblur.cpp:297) fused into the last level
 __global__ void inv_rows_kernel(const double* __restrict__ src, int m0, int m1, Taps f,
-                                double* __restrict__ dst, int64_t ldd) {
+                                double* __restrict__ dst, int64_t ldd, int clamp) {
     const int h1 = m1 >> 1;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
     if (x >= m1 || j >= m0) return;
     const double* row = src + static_cast<int64_t>(j) * m1;
-    const double v = idwt_point(
+    double v = idwt_point(
         x, m1, f, [&](int k) { return row[k]; }, [&](int k) { return row[h1 + k]; });
+    if (clamp) v = fmin(fmax(v, 0.0), 1.0);
     dst[static_cast<int64_t>(j) * ldd + x] = v;
 }
 
 __global__ void inv_line_kernel(const double* __restrict__ ll, const double* __restrict__ hb, int m,
-                                Taps f, double* __restrict__ dst) {
+                                Taps f, double* __restrict__ dst, int clamp) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
-    dst[j] = idwt_point(j, m, f, [&](int k) { return ll[k]; }, [&](int k) { return hb[k]; });
+    double v = idwt_point(j, m, f, [&](int k) { return ll[k]; }, [&](int k) { return hb[k]; });
+    if (clamp) v = fmin(fmax(v, 0.0), 1.0);
+    dst[j] = v;
 }
 
 inline int band_index(const wbx_basis* b, uint32_t t, uint32_t e) {
@@ -336,13 +372,14 @@ void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s) {
             const int m0 = static_cast<int>(b->dims[0] >> t), m1 = static_cast<int>(b->dims[1] >> t);
             const bool last = t + 1 == b->J;
             dim3 g1((m1 / 2 + kThreads - 1) / kThreads, m0);
-            fwd_rows_kernel<<<g1, kThreads, 0, s>>>(src, lds, tmp, m1, m0, m1, f);
+            fwd_rows_kernel<<<g1, kThreads, (2 * kThreads + f.l) * sizeof(double), s>>>(src, lds, tmp, m1, m0, m1, f);
             double* ll = last ? x + b->bands[0].offset : llbuf;
             double* b1 = x + b->bands[band_index(b, t + 1, 1)].offset;
             double* b2 = x + b->bands[band_index(b, t + 1, 2)].offset;
             double* b3 = x + b->bands[band_index(b, t + 1, 3)].offset;
-            dim3 g2((m1 + kThreads - 1) / kThreads, m0 / 2);
-            fwd_cols_kernel<<<g2, kThreads, 0, s>>>(tmp, m1, m0, m1, f, ll, b1, b2, b3);
+            dim3 g2((m1 + kThreads - 1) / kThreads, (m0 / 2 + kColsOut - 1) / kColsOut);
+            fwd_cols_kernel<<<g2, kThreads, (2 * kColsOut + f.l) * kThreads * sizeof(double), s>>>(tmp, m1, m0, m1, f, ll,
+                                                                                                  b1, b2, b3);
             count_launch(b->ctx, 2);
             src = ll;
             lds = m1 / 2;
@@ -351,7 +388,7 @@ void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s) {
     WBX_CUDA(cudaGetLastError());
 }
 
-void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s) {
+void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s, int clamp) {
     const Taps f = taps_of(b);
     double* tmp = b->work_a.p;
     double* llbufs[2] = {b->work_b.p, b->work_b.p + b->n / 2};
@@ -362,7 +399,7 @@ void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s) {
             const int m = static_cast<int>(b->dims[0] >> (t - 1));
             const double* hb = x + b->bands[band_index(b, t, 1)].offset;
             double* dst = t == 1 ? u : llbufs[which];
-            inv_line_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(ll, hb, m, f, dst);
+            inv_line_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(ll, hb, m, f, dst, t == 1 ? clamp : 0);
             count_launch(b->ctx);
             ll = dst;
             which ^= 1;
@@ -378,7 +415,7 @@ void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s) {
             dim3 g((m1 + kThreads - 1) / kThreads, m0);
             inv_cols_kernel<<<g, kThreads, 0, s>>>(ll, b1, b2, b3, m0, m1, f, tmp);
             double* dst = t == 1 ? u : llbufs[which];
-            inv_rows_kernel<<<g, kThreads, 0, s>>>(tmp, m0, m1, f, dst, m1);
+            inv_rows_kernel<<<g, kThreads, 0, s>>>(tmp, m0, m1, f, dst, m1, t == 1 ? clamp : 0);
             count_launch(b->ctx, 2);
             ll = dst;
             which ^= 1;
