@@ -16,3 +16,7 @@ P = W.spai(op, ctx)
 w = W.scale_weights(basis.layout)
 d = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=100, track_energy=False), ctx)
 print(d.kernels(), op.nnz(), op.info(ctx).nonempty_rows, op.info(ctx).nonempty_cols)
+import json  # noqa: E402
+for _ in range(3):
+    u, rep = d.deblur(np.zeros(op.n) + 0.5, clamp=True)
+print(json.dumps({"tau_ms": d.phase_ms()[0], "iters_ms": d.phase_ms()[1], "tau_stats": d.tau_stats()}))
