@@ -155,6 +155,11 @@ int wbx_spmv_compact_dev(wbx_ctx* ctx, const wbx_op* op, int transpose, int prec
 int wbx_op_set_generators(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
                           const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
                           const double* values);
+/* Attach the wavelet layout the operator acts on (SparseOperator::layout, theta.hpp:55; also set
+ * by wbx_op_set_generators). Solvers created without a basis (wbx_pgd: the reference's fista() /
+ * ista()) use it for the block-Fourier step estimate of translation-invariant operators
+ * (csrc/circ_tau.cu). make_layout's errors; WBX_SHAPE_MISMATCH when the sizes differ. */
+int wbx_op_set_layout(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J);
 /* write_operator / read_operator (theta.cpp:413-490): the reference's WTHETA01 file, same
  * bytes, same validation (WBX_IO_ERROR with the reference's messages; bad layouts raise what
  * make_layout raises). read: the arrays are allocated by the library (malloc; wbx_free);

@@ -36,6 +36,11 @@ int wbx_diag_spmv_compact_mode(struct wbx_ctx* ctx, const struct wbx_op* op, int
 int wbx_diag_stencil_apply_host(uint32_t ndim, const uint64_t* dims, uint32_t J, uint64_t n_gens,
                                 const uint32_t* blocks, const uint32_t* gen_index, const uint64_t* counts,
                                 const double* values, int phase, uint32_t G, const double* x, double* y);
+/* Block-Fourier step estimate (csrc/circ_tau.cu): does it apply to `op` on the layout
+ * (ndim, dims, J)? info[5] = {applies, row orbits, column orbits, g0, g1}; `why` gets the reason
+ * when it does not (host analysis, cached on the operator). */
+int wbx_diag_circ_info(const struct wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J, uint32_t* info,
+                       char* why, uint64_t why_len);
 struct wbx_solver;
 int wbx_diag_win_features(const struct wbx_solver* s, int side, double* out, int* G);
 #ifdef __cplusplus

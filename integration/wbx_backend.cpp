@@ -93,6 +93,8 @@ wbx_op* device_op(const SparseOperator& s) {
     mix(key, s.row_offsets.data(), s.row_offsets.size() * sizeof(uint64_t));
     mix(key, s.col_indices.data(), s.col_indices.size() * sizeof(uint32_t));
     mix(key, s.values.data(), s.values.size() * sizeof(double));
+    mix(key, s.layout.dims.data(), s.layout.dims.size() * sizeof(std::size_t));
+    mix(key, &s.layout.J, sizeof s.layout.J);
     struct Entry {
         uint64_t key;
         wbx_op* op;
@@ -105,6 +107,14 @@ wbx_op* device_op(const SparseOperator& s) {
         }
     wbx_op* op = nullptr;
     check(wbx_op_create(ctx(), s.n, s.row_offsets.data(), s.col_indices.data(), s.values.data(), &op));
+    if (!s.layout.dims.empty() && s.layout.total() == s.n) {  // SparseOperator::layout (theta.hpp:55)
+        const uint64_t d[2] = {s.layout.dims[0], s.layout.dims.size() == 2 ? s.layout.dims[1] : 1};
+        const int st = wbx_op_set_layout(op, static_cast<uint32_t>(s.layout.dims.size()), d, s.layout.J);
+        if (st != WBX_OK) {
+            wbx_op_destroy(op);
+            check(st);
+        }
+    }
     cache.push_front({key, op});
     if (cache.size() > 4) {
         wbx_op_destroy(cache.back().op);

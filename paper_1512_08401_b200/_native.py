@@ -79,6 +79,7 @@ SIGNATURES = {
     "wbx_spmv_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_spmv_compact_dev": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
     "wbx_op_set_generators": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D]),
+    "wbx_op_set_layout": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32]),
     "wbx_write_operator": (C.c_int, [C.c_char_p, C.c_uint32, _U64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                      _U64, _U32, _D]),
     "wbx_read_operator": (C.c_int, [C.c_char_p, _U32, _U64, _U32, _U32, _U32, _U64, _U64, C.POINTER(_U64),
@@ -176,6 +177,7 @@ DIAG_SIGNATURES = {
     "wbx_diag_stencil_apply_host": (C.c_int, [C.c_uint32, _U64, C.c_uint32, C.c_uint64, _U32, _U32, _U64, _D,
                                               C.c_int, C.c_uint32, _D, _D]),
     "wbx_diag_win_features": (C.c_int, [_P, C.c_int, _D, C.POINTER(C.c_int)]),
+    "wbx_diag_circ_info": (C.c_int, [_P, C.c_uint32, _U64, C.c_uint32, _U32, C.c_char_p, C.c_uint64]),
 }
 
 

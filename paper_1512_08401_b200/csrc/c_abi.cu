@@ -315,6 +315,25 @@ int wbx_op_destroy(wbx_op* op) {
     return guard([&] { delete op; });
 }
 
+int wbx_op_set_layout(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J) {
+    return guard([&] {
+        need(op, "op");
+        need(dims, "dims");
+        std::vector<wbx_band> bands;
+        wbx::make_layout(ndim, dims, J, bands);  // make_layout's own errors (wavelet.cpp:32-70)
+        if (dims[0] * (ndim == 2 ? dims[1] : 1) != op->n)
+            wbx::fail(WBX_SHAPE_MISMATCH, "layout and operator sizes differ");
+        std::lock_guard<std::mutex> g(op->win_mu);
+        op->has_layout = true;
+        op->l_ndim = ndim;
+        op->l_J = J;
+        op->l_dims[0] = dims[0];
+        op->l_dims[1] = ndim == 2 ? dims[1] : 1;
+        op->l_bands = std::move(bands);
+        op->circ_cache.clear();
+    });
+}
+
 int wbx_op_get_info(const wbx_op* op, wbx_op_info* info) {
     return guard([&] {
         need(op, "op");

@@ -83,6 +83,7 @@ struct WinSide {
     uint64_t bytes = 0;
 };
 struct StencilPlan;  // stencil_plan.cu
+struct CircPlan;     // circ_tau.cu
 
 // both sides for one grid size G; ok == false when a window exceeds 16-bit local indices
 struct WinPair {
@@ -189,6 +190,14 @@ struct wbx_op {
     std::vector<uint64_t> g_count;
     std::vector<double> g_val;
     mutable std::map<uint64_t, std::shared_ptr<wbx::StencilPlan>> st_cache;  // by (CTA warps, G)
+    // the wavelet layout the operator acts on (SparseOperator::layout, theta.hpp:55), when the
+    // caller attached it (wbx_op_set_layout / wbx_op_set_generators)
+    bool has_layout = false;
+    uint32_t l_ndim = 0, l_J = 0;
+    uint64_t l_dims[2] = {1, 1};
+    std::vector<wbx_band> l_bands;
+    // block-Fourier step-estimate plans (circ_tau.cu) per wavelet layout (ndim, dims, J)
+    mutable std::map<std::vector<uint64_t>, std::shared_ptr<wbx::CircPlan>> circ_cache;
 };
 
 namespace wbx {
@@ -248,6 +257,17 @@ struct StencilView;
 StencilView view_of(const StencilPlan& p);
 // the operator's plan for grid G (built from its generator groups, uploaded, cached on it)
 std::shared_ptr<StencilPlan> stencil_plan_for(const wbx_op* op, uint32_t G, uint32_t cta_warps, cudaStream_t st);
+
+// circ_tau.cu: the step estimate of translation-invariant operators, block-diagonal in the
+// Fourier domain of the translation group (ok == false when it does not apply)
+std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J,
+                                       const std::vector<wbx_band>& bands);
+bool circ_plan_ok(const CircPlan& p, std::string* why, uint32_t* info5);  // {ok, nRo, nCo, g0, g1}
+bool circ_check_p(const CircPlan& p, const double* p_full, std::vector<double>& isp, std::string* why);
+void circ_upload(CircPlan& p, cudaStream_t st);
+uint64_t circ_work_doubles(const CircPlan& p);
+void circ_tau_launch(wbx_ctx* ctx, const CircPlan& p, const double* isp_dev, double step_safety, double* work,
+                     double* out, cudaStream_t st);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

@@ -40,6 +40,7 @@
 #include "win.cuh"
 #include "lanczos.cuh"
 #include "stencil_engine.cuh"
+#include "rng.cuh"
 
 extern "C" void wbx_set_last_error(const char* msg);
 
@@ -132,25 +133,6 @@ struct SolveArgs {
 
 __device__ __forceinline__ bool bit_set(const uint32_t* mask, uint64_t i) {
     return (mask[i >> 5] >> (i & 31)) & 1u;
-}
-
-__device__ __forceinline__ uint64_t rng_at(uint64_t seed, uint64_t i) {
-    uint64_t z = seed + 0x9e3779b97f4a7c15ull * (i + 1);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
-__device__ __forceinline__ double rng_u01(uint64_t v) {
-    return (static_cast<double>(v >> 11) + 0.5) * 0x1p-53;
-}
-// i-th draw of CounterRng(seed).next_normal() (rng.hpp:30-43): pairs (cos, sin).
-__device__ __forceinline__ double rng_normal(uint64_t seed, uint64_t i) {
-    const uint64_t m = i >> 1;
-    const double u1 = rng_u01(rng_at(seed, 2 * m));
-    const double u2 = rng_u01(rng_at(seed, 2 * m + 1));
-    const double r = sqrt(-2.0 * log(u1));
-    const double a = 2.0 * M_PI * u2;
-    return (i & 1) ? r * sin(a) : r * cos(a);
 }
 
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -2158,6 +2140,10 @@ struct wbx_solver {
     int grid_st = 0;
     unsigned st_smem = 0;
     std::shared_ptr<wbx::StencilPlan> sp;  // owned by the operator's cache
+    // block-Fourier step estimate (circ_tau.cu) for translation-invariant operators
+    bool tau_circ = false;
+    std::shared_ptr<wbx::CircPlan> circ;  // owned by the operator's cache
+    wbx::DevBuf<double> circ_isp, circ_work;
     wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
@@ -2342,6 +2328,9 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
     // step: estimate_step on the device, or the given one
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
+    } else if (s->tau_circ) {  // translation-invariant operator: block-Fourier power iteration
+        circ_tau_launch(ctx, *s->circ, s->circ_isp.p, s->cfg.step_safety, s->circ_work.p, s->out.p, st);
+        return;
     } else if (s->win && !s->tau_stream_lz) {
         const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos, s->win_lists_global);
         launch_coop_smem(k, s->grid_win, s->win_smem_tau, a, st, kWinBlock);
@@ -2415,6 +2404,21 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
         count_launch(ctx);
     }
     WBX_CUDA(cudaGetLastError());
+}
+
+// The operator's block-Fourier step-estimate plan for the basis's layout (cached on the operator)
+// (the solver's basis, or the layout attached to the operator: the drop-in fista() has no basis)
+std::shared_ptr<CircPlan> circ_plan_for(const wbx_op* op, const wbx_basis* basis) {
+    std::lock_guard<std::mutex> g(op->win_mu);
+    const uint32_t ndim = basis ? basis->ndim : op->l_ndim, J = basis ? basis->J : op->l_J;
+    const uint64_t* dims = basis ? basis->dims : op->l_dims;
+    const std::vector<wbx_band>& bands = basis ? basis->bands : op->l_bands;
+    std::vector<uint64_t> key{ndim, dims[0], ndim == 2 ? dims[1] : 1, J};
+    auto it = op->circ_cache.find(key);
+    if (it != op->circ_cache.end()) return it->second;
+    auto p = circ_analyze(op, ndim, dims, J, bands);
+    op->circ_cache[key] = p;
+    return p;
 }
 
 // The operator's window layouts for grid size G, built on first use and cached on the operator
@@ -2615,6 +2619,26 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     else
         alloc_state<float>(s);
     s->dec_grid = 4 * s->ctx->num_sms;
+    // step estimate: block-Fourier for translation-invariant operators on the fp32 hot path
+    // (WBX_TAU=lanczos / power keep the full-operator estimates; the fp64 reference mode keeps
+    // the literal power iteration, bitwise)
+    const char* tau_env = std::getenv("WBX_TAU");
+    if (s->cfg.precision == WBX_FP32 && (s->basis || op->has_layout) &&
+        !(tau_env && (std::string(tau_env) == "lanczos" || std::string(tau_env) == "power"))) {
+        auto plan = circ_plan_for(op, s->basis);
+        std::string why;
+        std::vector<double> isp;
+        if (circ_plan_ok(*plan, &why, nullptr) && circ_check_p(*plan, p, isp, &why)) {
+            circ_upload(*plan, st);
+            s->circ = plan;
+            s->circ_isp.upload(isp, st);
+            s->circ_work.alloc(circ_work_doubles(*plan));
+            s->tau_circ = true;
+        }
+        if (std::getenv("WBX_VERBOSE"))
+            std::fprintf(stderr, "wbx: block-Fourier step estimate %s%s%s\n", s->tau_circ ? "on" : "off",
+                         s->tau_circ ? "" : ": ", s->tau_circ ? "" : why.c_str());
+    }
     s->wv.alloc(nC ? nC : 1);
     s->uC.alloc(nC ? nC : 1);
     s->t64.alloc(op->nR ? op->nR : 1);
@@ -2717,7 +2741,7 @@ void solver_report(wbx_solver* s, wbx_report* rep) {
     if (std::getenv("WBX_VERBOSE"))
         std::fprintf(stderr, "wbx tau: %.17g after %g reference iterations, %g operator product pairs (%s)\n",
                      out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_TAU_STEPS],
-                     (s->tau_lanczos || s->tau_stream_lz) ? "lanczos" : "power");
+                     s->tau_circ ? "block-Fourier" : (s->tau_lanczos || s->tau_stream_lz) ? "lanczos" : "power");
     if (rep == nullptr) return;
     rep->iters_used = static_cast<uint64_t>(out[OUT_ITERS_USED]);
     rep->tau = out[OUT_TAU];
@@ -2961,6 +2985,7 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
     const bool fp64 = s->cfg.precision == WBX_FP64;
     const bool track = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
     const char* tau = s->cfg.tau > 0.0 ? "set_tau_kernel"
+                      : s->tau_circ ? "circ_lanczos_kernel"
                       : s->tau_stream_lz ? "tau_lanczos_kernel"
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"

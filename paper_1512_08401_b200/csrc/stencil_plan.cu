@@ -739,6 +739,13 @@ int wbx_op_set_generators(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint3
         op->g_count.assign(counts, counts + n_gens);
         op->g_val.assign(values, values + n_gens);
         op->st_cache.clear();
+        op->has_layout = true;  // the generators' layout is the operator's
+        op->l_ndim = ndim;
+        op->l_J = J;
+        op->l_dims[0] = dims[0];
+        op->l_dims[1] = ndim == 2 ? dims[1] : 1;
+        op->l_bands = bands;
+        op->circ_cache.clear();
         return WBX_OK;
     } catch (const wbx::Error& e) {
         wbx_set_last_error(e.what());

@@ -344,6 +344,12 @@ class SparseOperator:
             h = C.c_void_p()
             _check(lib.wbx_op_create(ctx.handle, self.n, _u64ptr(self.row_offsets),
                                      _u32ptr(self.col_indices), _dptr(self.values), C.byref(h)))
+            if self.layout is not None:  # SparseOperator::layout (theta.hpp:55)
+                d = np.array(self.layout.dims, dtype=np.uint64)
+                st = lib.wbx_op_set_layout(h, len(self.layout.dims), _u64ptr(d), self.layout.J)
+                if st != N.WBX_OK:
+                    lib.wbx_op_destroy(h)
+                    _check(st)
             gl = getattr(self, "generators", None)
             if gl is not None:
                 d = np.array(gl.dims, dtype=np.uint64)
