@@ -51,6 +51,10 @@
 #include "rng.cuh"
 #include "wbx_diag.h"
 
+#ifndef WBX_CIRC_PROF
+#define WBX_CIRC_PROF 0
+#endif
+
 extern "C" void wbx_set_last_error(const char* msg);
 
 namespace wbx {
@@ -79,8 +83,14 @@ struct CircPlan {
     std::vector<double> h_eval;
     std::vector<double2> h_tw0, h_tw1;
     std::vector<uint32_t> h_fhalf;  // half spectrum: f << 1 | (weight 2)
+    std::vector<int> h_hidx;        // frequency -> half-spectrum index, or -1 - its conjugate's
+    std::vector<CircOrbit> h_rorb;  // row orbits, in the order of the representative rows
+    bool fista_ok = false;          // the spectral FISTA engine applies (circ_fista_kernel)
+    std::string fista_why;
     bool uploaded = false;
     DevBuf<uint32_t> fhalf;
+    DevBuf<int> hidx;
+    DevBuf<CircOrbit> rorb;
     DevBuf<CircOrbit> orb;
     DevBuf<uint32_t> eoff;  // [nRo * nCo + 1]: entries of representative row r, column orbit j
     DevBuf<uint32_t> eh;    // h0 << 16 | h1
@@ -167,20 +177,15 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 
-// Half a warp per frequency of the half spectrum (f and -f have conjugate blocks and
-// transforms, so equal moments: weight 2; self-conjugate frequencies weight 1), two
-// frequencies per warp. Lane i < nCo of a half owns row / component i. Every frequency's
-// control flow is the same (the representative rows do not depend on f), so the halves do
-// not diverge except at a Lanczos breakdown (per-half flags).
-//   1. Theta^_f row by row (lane j: column orbit j), M^_f = D Theta^_f^H Theta^_f D (lane i: row i)
-//   2. Lanczos on M^_f from v^_f with full reorthogonalisation (classical Gram-Schmidt, twice):
-//      the real tridiagonal T_f (k <= nCo) with v^H M^p v = |v|^2 e1^T T^p e1 for every p;
-//      written as {alpha[16], beta[16], |v|^2 (weight folded in), k}
-__global__ void __launch_bounds__(kCircWarps * 32) circ_lanczos_kernel(
+// Half a warp per frequency of the half spectrum, two frequencies per warp (lane i < nCo of a
+// half owns column orbit i): Theta^_f row by row from the representative rows (staged in shared
+// memory once per block), G_f = Theta^_f^H Theta^_f (lane i: row i), written to gram[hf] as
+// nCo x nCo complex fp64. G_f is the Fourier block of Theta^T Theta: the step estimate scales it
+// by D = P^-1/2, the spectral FISTA engine applies it as is.
+__global__ void __launch_bounds__(kCircWarps * 32) circ_gram_kernel(
     uint32_t nhalf, const uint32_t* __restrict__ fhalf, uint32_t g1, uint32_t g0, uint32_t nRo, uint32_t nCo,
     const uint32_t* __restrict__ eoff, const uint32_t* __restrict__ eh, const double* __restrict__ eval,
-    const double2* __restrict__ tw0, const double2* __restrict__ tw1, const double* __restrict__ isp,
-    const double2* __restrict__ vh, double* __restrict__ tri, uint32_t nent) {
+    const double2* __restrict__ tw0, const double2* __restrict__ tw1, double2* __restrict__ gram, uint32_t nent) {
     // the representative rows and twiddles, staged once per block (dynamic shared memory)
     extern __shared__ double2 circ_smem[];
     double2* s_tw0 = circ_smem;
@@ -197,10 +202,7 @@ __global__ void __launch_bounds__(kCircWarps * 32) circ_lanczos_kernel(
     for (uint32_t i = threadIdx.x; i <= nRo * nCo; i += blockDim.x) s_eoff[i] = eoff[i];
     __syncthreads();
     constexpr int kSlots = 2 * kCircWarps;
-    __shared__ double2 Ms[kSlots][kCircMaxCo][kCircMaxCo + 1];
-    __shared__ double2 Qs[kSlots][kCircMaxCo][kCircMaxCo];
-    __shared__ double2 vec[kSlots][kCircMaxCo];  // Theta^ row / current r / q broadcast
-    __shared__ double2 cof[kSlots][kCircMaxCo];  // reorthogonalisation coefficients
+    __shared__ double2 vec[kSlots][kCircMaxCo];  // Theta^ row
     const int lane = threadIdx.x & 31, li = lane & 15;
     const int slot = (threadIdx.x >> 5) * 2 + (lane >> 4);
     const uint32_t hf = blockIdx.x * kSlots + slot;
@@ -208,17 +210,11 @@ __global__ void __launch_bounds__(kCircWarps * 32) circ_lanczos_kernel(
     if (warp_first >= nhalf) return;  // whole warp
     const bool live = hf < nhalf;
     const uint32_t fw = live ? fhalf[hf] : 0u;
-    const uint32_t f = fw >> 1;  // frequency index f0 * g1 + f1; bit 0: weight 2
+    const uint32_t f = fw >> 1;
     const uint32_t f0 = f / g1, f1 = f % g1;
     const uint32_t m0 = (g0 & (g0 - 1)) == 0 ? g0 - 1 : 0, m1 = (g1 & (g1 - 1)) == 0 ? g1 - 1 : 0;
     const int nc = static_cast<int>(nCo);
     const bool own = li < nc;
-    auto half_sum = [](double v) {  // sum over the 16 lanes of this half (identical in every lane)
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        return v;
-    };
-
     // 1. M^_f
     double2 acc[kCircMaxCo];
 #pragma unroll
@@ -249,17 +245,59 @@ __global__ void __launch_bounds__(kCircWarps * 32) circ_lanczos_kernel(
         }
         __syncwarp();
     }
+    if (own && live) {
+        double2* G = gram + static_cast<uint64_t>(hf) * nCo * nCo + static_cast<uint64_t>(li) * nCo;
+#pragma unroll
+        for (int j = 0; j < kCircMaxCo; ++j)
+            if (j < nc) G[j] = acc[j];
+    }
+}
+
+
+// Half a warp per frequency of the half spectrum (f and -f have conjugate blocks and
+// transforms, so equal moments: weight 2; self-conjugate frequencies weight 1), two
+// frequencies per warp. Lane i < nCo of a half owns row / component i. Every frequency's
+// control flow is the same (the representative rows do not depend on f), so the halves do
+// not diverge except at a Lanczos breakdown (per-half flags).
+//   1. M^_f = D G_f D from circ_gram_kernel's G_f (lane i: row i), D = P^-1/2 per column orbit
+//   2. Lanczos on M^_f from v^_f with full reorthogonalisation (classical Gram-Schmidt, twice):
+//      the real tridiagonal T_f (k <= nCo) with v^H M^p v = |v|^2 e1^T T^p e1 for every p;
+//      written as {alpha[16], beta[16], |v|^2 (weight folded in), k}
+__global__ void __launch_bounds__(kCircWarps * 32) circ_lanczos_kernel(
+    uint32_t nhalf, const uint32_t* __restrict__ fhalf, uint32_t nCo, const double2* __restrict__ gram,
+    const double* __restrict__ isp, const double2* __restrict__ vh, double* __restrict__ tri) {
+    constexpr int kSlots = 2 * kCircWarps;
+    __shared__ double2 Ms[kSlots][kCircMaxCo][kCircMaxCo + 1];
+    __shared__ double2 Qs[kSlots][kCircMaxCo][kCircMaxCo];
+    __shared__ double2 vec[kSlots][kCircMaxCo];  // Theta^ row / current r / q broadcast
+    __shared__ double2 cof[kSlots][kCircMaxCo];  // reorthogonalisation coefficients
+    const int lane = threadIdx.x & 31, li = lane & 15;
+    const int slot = (threadIdx.x >> 5) * 2 + (lane >> 4);
+    const uint32_t hf = blockIdx.x * kSlots + slot;
+    const uint32_t warp_first = blockIdx.x * kSlots + (threadIdx.x >> 5) * 2;
+    if (warp_first >= nhalf) return;  // whole warp
+    const bool live = hf < nhalf;
+    const uint32_t fw = live ? fhalf[hf] : 0u;
+    const uint32_t f = fw >> 1;  // frequency index f0 * g1 + f1; bit 0: weight 2
+    const int nc = static_cast<int>(nCo);
+    const bool own = li < nc;
+    auto half_sum = [](double v) {  // sum over the 16 lanes of this half (identical in every lane)
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+
+    // 1. M^_f = D G_f D
     double fro = 0.0;
     if (own) {
         const double di = isp[li];
-#pragma unroll
-        for (int j = 0; j < kCircMaxCo; ++j) {
-            if (j < nc) {
-                const double s = di * isp[j];
-                const double2 m = make_double2(acc[j].x * s, acc[j].y * s);
-                Ms[slot][li][j] = m;
-                fro = fma(m.x, m.x, fma(m.y, m.y, fro));
-            }
+        const double2* G = gram + static_cast<uint64_t>(live ? hf : 0) * nCo * nCo + static_cast<uint64_t>(li) * nCo;
+        for (int j = 0; j < nc; ++j) {
+            const double s = di * isp[j];
+            const double2 g = G[j];
+            const double2 m = make_double2(g.x * s, g.y * s);
+            Ms[slot][li][j] = m;
+            fro = fma(m.x, m.x, fma(m.y, m.y, fro));
         }
     }
     fro = sqrt(half_sum(fro));
@@ -508,6 +546,363 @@ __global__ void __launch_bounds__(256) circ_final_kernel(uint32_t NG, const doub
     }
 }
 
+// ----------------------------------------------------------------------------- spectral FISTA
+// The iterations of run_pgd (solver.cpp:119-151) for a translation-invariant operator, with the
+// gradient Theta^T (Theta y - x0) = G y - b applied in the Fourier domain of the translation
+// group: (G y)^_f = G_f y^_f, G_f = Theta^_f^H Theta^_f (nCo x nCo, circ_gram_kernel), b = Theta^T x0
+// computed once from the representative rows. All arithmetic fp64 (the prox / momentum /
+// threshold expressions of the reference, solver.cpp:57-67,126,145).
+//
+// Grid: g spectral CTAs (g = g0 = g1) + the remaining SMs' CTAs for the decoupled coordinates
+// (empty Theta column: prox + momentum only, fp64, run concurrently). Spectral CTA c owns row
+// h0 = c of every column orbit (nCo x g coordinates: y, x_prev, p, thr, b in shared memory) and
+// column f1 = c of the spectrum (the g blocks G_(f0, c) in shared memory). Per iteration:
+//   row phase    (CTA r) inverse row DFTs of T2[.][r][.] -> G y on row r; prox + momentum;
+//                forward row DFTs of the new y -> T1[.][r][.]                      -- barrier --
+//   column phase (CTA c) column DFTs of T1[.][.][c] -> y^_(f0, c); a^ = G_f y^; inverse column
+//                DFTs -> T2[.][.][c]                                                 -- barrier --
+// Radix-2 FFTs in shared memory, twiddles e^{2 pi i k / g} from the host (long double).
+struct CircFistaArgs {
+    const double* x0_full;
+    const double* w_full;
+    const double* p_full;
+    double* x_full;
+    const uint32_t* isC;
+    uint64_t n;
+    const double* beta64;
+    double lambda;
+    int K;
+    const double* out;  // tau at out[0]
+    const double2* gram;
+    const int* hidx;  // frequency -> half-spectrum index (>= 0) or -1 - index of its conjugate
+    const CircOrbit* corb;
+    const CircOrbit* rorb;
+    const uint32_t* eoff;
+    const uint32_t* eh;
+    const double* eval;
+    const double2* tw;  // e^{+2 pi i k / g}, k < g
+    double2* T1;        // [nCo][f1][h0]: row DFTs of y
+    double2* T2;        // [nCo][h0][f1]: inverse column DFTs of G_f y^
+    unsigned* counter;
+    uint32_t g, lg, nRo, nCo, NB;
+    int diag_skip_decoupled;  // WBX_CIRC_DIAG=nodec: time the spectral CTAs alone (wrong x)
+    unsigned long long* prof;  // diagnostics build (WBX_CIRC_PROF=1): CTA 0's cycles per section
+};
+
+
+__device__ __forceinline__ void circ_barrier(unsigned* cnt, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+        } while (static_cast<int>(v - target) < 0);
+    }
+    __syncthreads();
+}
+
+// solver.cpp:61-64 (thr = tau * lambda * w / p left to right) and :145
+__device__ __forceinline__ double circ_thr(double tau, double lambda, double w, double p) {
+    return __ddiv_rn(__dmul_rn(__dmul_rn(tau, lambda), w), p);
+}
+__device__ __forceinline__ double circ_prox(double z0, double thr) {
+    const double a = __dsub_rn(fabs(z0), thr);
+    return a > 0.0 ? (z0 > 0.0 ? a : -a) : 0.0;
+}
+__device__ __forceinline__ double circ_momentum(double xn, double xp, double beta) {
+    return __dadd_rn(xn, __dmul_rn(beta, __dsub_rn(xn, xp)));
+}
+
+// Copy n complex values src(i) -> dst(i) with every load of a thread issued before its stores
+// (one memory round trip per call, not one per element)
+template <typename Src, typename Dst>
+__device__ __forceinline__ void batched_copy(uint32_t n, Src src, Dst dst) {
+    constexpr int kB = 8;
+    for (uint32_t base = 0; base < n; base += kB * blockDim.x) {
+        double2 v[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const uint32_t i = base + r * blockDim.x + threadIdx.x;
+            if (i < n) v[r] = src(i);
+        }
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const uint32_t i = base + r * blockDim.x + threadIdx.x;
+            if (i < n) dst(i, v[r]);
+        }
+    }
+}
+
+// Warp FFTs of one length-G row held in registers: lane l holds elements l + 32 q (q < PPL).
+// DIF forward (e^{-}): natural-order input, bit-reversed-order output; DIT inverse (e^{+}):
+// bit-reversed input, natural output (unnormalised). Butterflies of distance d < 32 exchange
+// with lane l ^ d by shuffles; d = 32 (G = 64) is lane-local. tw[k] = e^{+2 pi i k / G}.
+template <int G>
+struct WarpFft {
+    static constexpr int PPL = G > 32 ? G / 32 : 1;
+    __device__ static double2 shfl(double2 v, int d) {
+        return make_double2(__shfl_xor_sync(0xffffffffu, v.x, d), __shfl_xor_sync(0xffffffffu, v.y, d));
+    }
+    __device__ static void forward(double2 (&v)[PPL], const double2* tw) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int d = G / 2; d >= 1; d >>= 1) {
+            if (d >= 32) {  // lane-local: elements lane, lane + 32
+                const double2 a = v[0], b = v[1];
+                double2 w = tw[(lane % d) * (G / (2 * d))];
+                w.y = -w.y;
+                v[0] = make_double2(a.x + b.x, a.y + b.y);
+                v[1] = cmul(make_double2(a.x - b.x, a.y - b.y), w);
+            } else {
+                const bool hi = (lane & d) != 0;
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    const int e = lane + 32 * q;
+                    const double2 p = shfl(v[q], d);
+                    if (!hi) {
+                        v[q] = make_double2(v[q].x + p.x, v[q].y + p.y);
+                    } else {
+                        double2 w = tw[(e % d) * (G / (2 * d))];
+                        w.y = -w.y;
+                        v[q] = cmul(make_double2(p.x - v[q].x, p.y - v[q].y), w);
+                    }
+                }
+            }
+        }
+    }
+    __device__ static void inverse(double2 (&v)[PPL], const double2* tw) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int d = 1; d <= G / 2; d <<= 1) {
+            if (d >= 32) {
+                const double2 w = tw[(lane % d) * (G / (2 * d))];
+                const double2 a = v[0], bw = cmul(v[1], w);
+                v[0] = make_double2(a.x + bw.x, a.y + bw.y);
+                v[1] = make_double2(a.x - bw.x, a.y - bw.y);
+            } else {
+                const bool hi = (lane & d) != 0;
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    const int e = lane + 32 * q;
+                    const double2 t = hi ? cmul(v[q], tw[(e % d) * (G / (2 * d))]) : v[q];
+                    const double2 p = shfl(t, d);
+                    v[q] = hi ? make_double2(p.x - t.x, p.y - t.y) : make_double2(t.x + p.x, t.y + p.y);
+                }
+            }
+        }
+    }
+};
+
+template <int G>
+__device__ __forceinline__ int brev_g(int i) {
+    return static_cast<int>(__brev(static_cast<unsigned>(i)) >> (32 - __builtin_ctz(G)));
+}
+
+// One CTA per SM: blockIdx < g the spectral CTAs (NCP warps, warp j = orbit row j), the rest the
+// decoupled coordinates.
+template <int G, int NCP>
+__global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a) {
+    using F = WarpFft<G>;
+    constexpr int PPL = F::PPL;
+    const double tau = a.out[0];
+    if (blockIdx.x >= a.NB) {
+        if (a.diag_skip_decoupled) return;
+        // decoupled coordinates (gradient exactly 0): x' = prox(y), y = x' + beta (x' - x_prev),
+        // iterated in registers to the fixed point x' == x_prev == 0 or the iteration count
+        const uint64_t nthreads = static_cast<uint64_t>(gridDim.x - a.NB) * blockDim.x;
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x - a.NB) * blockDim.x + threadIdx.x; i < a.n; i += nthreads) {
+            if ((a.isC[i >> 5] >> (i & 31)) & 1u) continue;
+            const double thr = circ_thr(tau, a.lambda, a.w_full[i], a.p_full[i]);
+            double x = a.x0_full[i], xp = x, y = x;
+            for (int k = 1; k <= a.K; ++k) {
+                const double xn = circ_prox(y, thr);
+                const bool fixed = xn == 0.0 && xp == 0.0;
+                y = circ_momentum(xn, xp, a.beta64[k - 1]);
+                xp = xn;
+                x = xn;
+                if (fixed) break;
+            }
+            a.x_full[i] = x;
+        }
+        return;
+    }
+    const int nc = static_cast<int>(a.nCo), c = blockIdx.x, lane = threadIdx.x & 31, wj = threadIdx.x >> 5;
+    const bool row_live = wj < nc;  // warp-uniform (lanes >= G of a G = 16 row idle in the shuffles)
+    const bool lane_live = lane < G;
+    constexpr int GS = NCP + 1;  // padded G block rows
+    extern __shared__ double2 circ_smem[];
+    double2* Gs = circ_smem;                       // [pos][NCP][NCP + 1]: G_(brev(pos), c), zero padded
+    double2* X = Gs + G * NCP * GS;                // [NCP][G]: spectrum of the rows at column c (positions)
+    double2* Y = X + NCP * G;                      // [NCP][G]: G_f times it
+    double2* tw = Y + NCP * G;                     // [G]
+    double* ys = reinterpret_cast<double*>(tw + G);  // [NCP][G] y on row c
+    double* xps = ys + NCP * G;
+    double* bs = xps + NCP * G;
+    double* ps = bs + NCP * G;  // tau / p
+    double* ths = ps + NCP * G;
+    for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
+    for (int i = threadIdx.x; i < 2 * NCP * G; i += blockDim.x) X[i] = make_double2(0.0, 0.0);  // padded rows stay 0
+    batched_copy(
+        G * NCP * NCP,
+        [&](uint32_t i) {  // G_(f0, c) for f0 = brev(pos); conjugate half from its partner's block
+            const int pos = i / (NCP * NCP), e = i % (NCP * NCP), ii = e / NCP, j = e % NCP;
+            if (ii >= nc || j >= nc) return make_double2(0.0, 0.0);
+            const int h = a.hidx[brev_g<G>(pos) * G + c];
+            const double2 v = a.gram[static_cast<uint64_t>(h >= 0 ? h : -1 - h) * nc * nc + ii * nc + j];
+            return h >= 0 ? v : make_double2(v.x, -v.y);
+        },
+        [&](uint32_t i, double2 v) {
+            const int pos = i / (NCP * NCP), e = i % (NCP * NCP);
+            Gs[(pos * NCP + e / NCP) * GS + e % NCP] = v;
+        });
+    for (int i = threadIdx.x; i < NCP * G; i += blockDim.x) {  // own row: y = x_prev = x0, p, thr, b
+        const int j = i / G, h1 = i % G;
+        if (j >= nc) {
+            ys[i] = xps[i] = bs[i] = ths[i] = 0.0;
+            ps[i] = 1.0;
+            continue;
+        }
+        const CircOrbit o = a.corb[j];
+        const uint64_t fl = static_cast<uint64_t>(o.off) + static_cast<uint64_t>(o.a0 + o.s0 * c) * o.W + o.a1 + o.s1 * h1;
+        const double x0 = a.x0_full[fl], p = a.p_full[fl];
+        ys[i] = x0;
+        xps[i] = x0;
+        ps[i] = tau / p;
+        ths[i] = circ_thr(tau, a.lambda, a.w_full[fl], p);
+        // b_j[c][h1] = sum over rows o' and entries (j, e) of its representative: val x0_o'[(c, h1) - e]
+        double b = 0.0;
+        for (uint32_t r = 0; r < a.nRo; ++r) {
+            const CircOrbit ro = a.rorb[r];
+            for (uint32_t e = a.eoff[r * nc + j]; e < a.eoff[r * nc + j + 1]; ++e) {
+                const uint32_t h = a.eh[e];
+                const uint32_t t0 = (c + G - (h >> 16)) & (G - 1), t1 = (h1 + G - (h & 0xffffu)) & (G - 1);
+                const uint64_t rf = static_cast<uint64_t>(ro.off) + static_cast<uint64_t>(ro.a0 + ro.s0 * t0) * ro.W +
+                                    ro.a1 + ro.s1 * t1;
+                b = fma(a.eval[e], a.x0_full[rf], b);
+            }
+        }
+        bs[i] = b;
+    }
+    __syncthreads();
+    const double inv_ng = 1.0 / (static_cast<double>(G) * G);  // exact (power of two)
+    unsigned bar = 0;
+    // forward row DFT of this warp's row of y -> T1[j][f1][c] (f1 = brev(position))
+    auto row_forward = [&]() {
+        if (!row_live) return;
+        double2 v[PPL];
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) v[q] = make_double2(lane_live ? ys[wj * G + lane + 32 * q] : 0.0, 0.0);
+        F::forward(v, tw);
+        if (lane_live)
+#pragma unroll
+            for (int q = 0; q < PPL; ++q)
+                a.T1[(static_cast<uint64_t>(wj) * G + brev_g<G>(lane + 32 * q)) * G + c] = v[q];
+    };
+#if WBX_CIRC_PROF
+    __shared__ unsigned long long prof_acc[8];
+    if (threadIdx.x < 8) prof_acc[threadIdx.x] = 0;
+    __syncthreads();
+    long long t_prev = clock64();
+    auto mark = [&](int slot) {
+        __syncthreads();
+        const long long t = clock64();
+        if (threadIdx.x == 0) prof_acc[slot] += static_cast<unsigned long long>(t - t_prev);
+        t_prev = t;
+    };
+#else
+    auto mark = [](int) {};
+#endif
+    if (a.K > 0) row_forward();
+    for (int k = 1; k <= a.K; ++k) {
+        mark(0);
+        circ_barrier(a.counter, ++bar * a.NB);
+        mark(1);
+        // column phase: column c of the spectrum; warp j transforms orbit j along h0
+        if (row_live) {
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q)
+                v[q] = lane_live ? a.T1[(static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            F::forward(v, tw);
+            if (lane_live)
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) X[wj * G + lane + 32 * q] = v[q];
+        }
+        mark(2);
+        __syncthreads();
+        for (int t0 = threadIdx.x; t0 < G * NCP; t0 += 2 * blockDim.x) {  // Y[i][pos] = G_(f0(pos), c) X[.][pos]
+            const int t1 = t0 + blockDim.x;  // a second output, interleaved (independent chains)
+            const bool two = t1 < G * NCP;
+            const int pos0 = t0 / NCP, ii0 = t0 % NCP, pos1 = two ? t1 / NCP : pos0, ii1 = two ? t1 % NCP : ii0;
+            const double2* G0 = Gs + (pos0 * NCP + ii0) * GS;
+            const double2* G1 = Gs + (pos1 * NCP + ii1) * GS;
+            double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NCP; ++j) {
+                const double2 m = G0[j], x = X[j * G + pos0], n = G1[j], y = X[j * G + pos1];
+                r0 = fma(m.x, x.x, fma(-m.y, x.y, r0));
+                i0 = fma(m.x, x.y, fma(m.y, x.x, i0));
+                r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
+                i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
+            }
+            Y[ii0 * G + pos0] = make_double2(r0, i0);
+            if (two) Y[ii1 * G + pos1] = make_double2(r1, i1);
+        }
+        mark(3);
+        __syncthreads();
+        if (row_live) {  // inverse along h0 (bit-reversed positions in, natural h0 out) -> T2[i][h0][c]
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            F::inverse(v, tw);
+            if (lane_live)
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) a.T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+        }
+        mark(4);
+        circ_barrier(a.counter, ++bar * a.NB);
+        mark(5);
+        // row phase: row c; warp i inverts orbit i along f1 (loaded in bit-reversed order)
+        if (row_live) {
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q)
+                v[q] = lane_live ? a.T2[(static_cast<uint64_t>(wj) * G + c) * G + brev_g<G>(lane + 32 * q)]
+                                 : make_double2(0.0, 0.0);
+            F::inverse(v, tw);  // v[q].x * NG = (Theta^T Theta y)[wj][c][lane + 32 q]
+            const double beta = a.beta64[k - 1];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) {
+                if (!lane_live) break;
+                const int i = wj * G + lane + 32 * q;
+                const double grad = __dsub_rn(v[q].x * inv_ng, bs[i]);                      // Theta^T (Theta y - x0)
+                const double z0 = fma(-ps[i], grad, ys[i]);  // y - tau g / p (solver.cpp:126), tau / p once
+                const double xn = circ_prox(z0, ths[i]);
+                ys[i] = circ_momentum(xn, xps[i], beta);
+                xps[i] = xn;
+            }
+            __syncwarp();
+            if (k < a.K) row_forward();
+        }
+        mark(6);
+    }
+    __syncthreads();
+#if WBX_CIRC_PROF
+    if (c == 0 && threadIdx.x < 8) a.prof[threadIdx.x] = prof_acc[threadIdx.x];
+#endif
+    for (int i = threadIdx.x; i < nc * G; i += blockDim.x) {  // x_final on row c
+        const int j = i / G, h1 = i % G;
+        const CircOrbit o = a.corb[j];
+        a.x_full[static_cast<uint64_t>(o.off) + static_cast<uint64_t>(o.a0 + o.s0 * c) * o.W + o.a1 + o.s1 * h1] = xps[i];
+    }
+}
+
+template <int G, int NCP>
+size_t circ_fista_smem() {
+    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + 2 * NCP * G * 16 + G * 16 + 5 * NCP * G * 8;
+}
+
 // ----------------------------------------------------------------------------- host
 
 double2 twiddle(uint64_t k, uint64_t g) {
@@ -611,6 +1006,7 @@ std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const ui
         }
         // every row of the orbit
         const CircOrbit& ob = orbits[o];
+        P->h_rorb.push_back(ob);
         for (uint64_t h0 = 0; h0 < g0; ++h0)
             for (uint64_t h1 = 0; h1 < g1; ++h1) {
                 const uint64_t r = ob.off + (ob.a0 + ob.s0 * h0) * ob.W + ob.a1 + ob.s1 * h1;
@@ -638,9 +1034,25 @@ std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const ui
             const uint64_t f = f0 * g1 + f1, fc = ((g0 - f0) % g0) * g1 + (g1 - f1) % g1;
             if (f <= fc) P->h_fhalf.push_back(static_cast<uint32_t>(f << 1 | (f < fc ? 1u : 0u)));
         }
+    P->h_hidx.assign(NG, 0);
+    for (size_t i = 0; i < P->h_fhalf.size(); ++i) {
+        const uint64_t f = P->h_fhalf[i] >> 1, f0 = f / g1, f1 = f % g1;
+        const uint64_t fc = ((g0 - f0) % g0) * g1 + (g1 - f1) % g1;
+        P->h_hidx[f] = static_cast<int>(i);
+        if (fc != f) P->h_hidx[fc] = -1 - static_cast<int>(i);
+    }
     for (uint64_t k = 0; k < g0; ++k) P->h_tw0.push_back(twiddle(k, g0));
     for (uint64_t k = 0; k < g1; ++k) P->h_tw1.push_back(twiddle(k, g1));
     P->ok = true;
+    // the spectral FISTA engine: square translation group of 16, 32 or 64, its shared memory
+    const uint64_t ncp = (nCo + 3) / 4 * 4;
+    const uint64_t fista_smem = g0 * ncp * (ncp + 1) * 16 + 2 * ncp * g0 * 16 + g0 * 16 + 5 * ncp * g0 * 8;
+    if (ndim != 2 || g0 != g1 || (g0 != 8 && g0 != 16 && g0 != 32 && g0 != 64))
+        P->fista_why = "spectral FISTA needs a square translation group of 8, 16, 32 or 64";
+    else if (fista_smem > 227u * 1024u)
+        P->fista_why = "spectral FISTA blocks exceed shared memory";
+    else
+        P->fista_ok = true;
     return P;
 }
 
@@ -654,6 +1066,11 @@ bool circ_plan_ok(const CircPlan& P, std::string* why, uint32_t* info5) {
         info5[4] = P.g1;
     }
     return P.ok;
+}
+
+bool circ_fista_ok(const CircPlan& P, std::string* why) {
+    if (why) *why = P.ok ? P.fista_why : P.why;
+    return P.ok && P.fista_ok;
 }
 
 // Per-solver check of P on the column orbits; fills isp (P^-1/2 of each column orbit).
@@ -684,6 +1101,33 @@ bool circ_check_p(const CircPlan& P, const double* p, std::vector<double>& isp, 
     return true;
 }
 
+namespace {
+struct FistaKernel {
+    const void* fn = nullptr;
+    size_t smem = 0;
+    int warps = 0;
+};
+template <int G, int NCP>
+FistaKernel fista_kernel_of() {
+    return FistaKernel{reinterpret_cast<const void*>(circ_fista_kernel<G, NCP>), circ_fista_smem<G, NCP>(), NCP};
+}
+template <int G>
+FistaKernel fista_kernel_g(uint32_t nc) {
+    if (nc <= 4) return fista_kernel_of<G, 4>();
+    if (nc <= 8) return fista_kernel_of<G, 8>();
+    if (nc <= 12) return fista_kernel_of<G, 12>();
+    return fista_kernel_of<G, 16>();
+}
+// (g, nCo) -> instance: g in {8, 16, 32, 64}, nCo padded to 4, 8, 12, 16 rows (warps)
+FistaKernel fista_kernel_for(uint32_t g, uint32_t nc) {
+    if (g == 8) return fista_kernel_g<8>(nc);
+    if (g == 16) return fista_kernel_g<16>(nc);
+    if (g == 32) return fista_kernel_g<32>(nc);
+    if (g == 64) return fista_kernel_g<64>(nc);
+    return FistaKernel{};
+}
+}  // namespace
+
 void circ_upload(CircPlan& P, cudaStream_t st) {
     if (P.uploaded) return;
     P.orb.alloc(P.h_orb.size());
@@ -694,8 +1138,15 @@ void circ_upload(CircPlan& P, cudaStream_t st) {
     P.tw0.upload(P.h_tw0, st);
     P.tw1.upload(P.h_tw1, st);
     P.fhalf.upload(P.h_fhalf, st);
-    WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(circ_lanczos_kernel),
+    P.hidx.upload(P.h_hidx, st);
+    P.rorb.alloc(P.h_rorb.size());
+    P.rorb.upload(P.h_rorb.data(), P.h_rorb.size(), st);
+    WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(circ_gram_kernel),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+    if (P.fista_ok) {
+        const FistaKernel k = fista_kernel_for(P.g0, P.nCo);
+        WBX_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
+    }
     WBX_CUDA(cudaStreamSynchronize(st));
     P.uploaded = true;
 }
@@ -709,8 +1160,79 @@ uint64_t circ_work_doubles(const CircPlan& P) {
 }
 
 // Enqueue the estimate; writes out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_LAMBDA_MAX], out[OUT_TAU_STEPS].
+// G_f = Theta^_f^H Theta^_f for the half spectrum (nh x nCo x nCo complex)
+uint64_t circ_gram_doubles(const CircPlan& P) { return 2ull * P.h_fhalf.size() * P.nCo * P.nCo; }
+void circ_gram_launch(wbx_ctx* ctx, const CircPlan& P, double2* gram, cudaStream_t st) {
+    const uint32_t nh = static_cast<uint32_t>(P.h_fhalf.size());
+    const uint32_t nent = static_cast<uint32_t>(P.h_eval.size());
+    const size_t smem = (P.g0 + P.g1) * sizeof(double2) + nent * (sizeof(double) + sizeof(uint32_t)) +
+                        (P.nRo * P.nCo + 1) * sizeof(uint32_t);
+    circ_gram_kernel<<<(nh + 2 * kCircWarps - 1) / (2 * kCircWarps), kCircWarps * 32, smem, st>>>(
+        nh, P.fhalf.p, P.g1, P.g0, P.nRo, P.nCo, P.eoff.p, P.eh.p, P.eval.p, P.tw0.p, P.tw1.p, gram, nent);
+    count_launch(ctx);
+}
+
+// The spectral FISTA engine's exchange buffers T1, T2 (2 x nCo x NG complex)
+uint64_t circ_exchange_doubles(const CircPlan& P) { return 4ull * P.nCo * P.NG; }
+uint32_t circ_fista_blocks(const CircPlan& P) { return P.g0; }
+
+
+void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, const double2* gram, double2* T,
+                       unsigned* counter, cudaStream_t st) {
+    CircFistaArgs a{};
+    a.x0_full = pr.x0_full;
+    a.w_full = pr.w_full;
+    a.p_full = pr.p_full;
+    a.x_full = pr.x_full;
+    a.isC = pr.isC;
+    a.n = P.n;
+    a.beta64 = pr.beta64;
+    a.lambda = pr.lambda;
+    a.K = pr.K;
+    a.out = pr.out;
+    a.gram = gram;
+    a.hidx = P.hidx.p;
+    a.corb = P.orb.p;
+    a.rorb = P.rorb.p;
+    a.eoff = P.eoff.p;
+    a.eh = P.eh.p;
+    a.eval = P.eval.p;
+    a.tw = P.tw0.p;
+    a.T1 = T;
+    a.T2 = T + static_cast<uint64_t>(P.nCo) * P.NG;
+    a.counter = counter;
+    a.g = P.g0;
+    a.lg = static_cast<uint32_t>(__builtin_ctz(P.g0));
+    a.nRo = P.nRo;
+    a.nCo = P.nCo;
+    a.NB = P.g0;
+    a.diag_skip_decoupled = std::getenv("WBX_CIRC_DIAG") && std::string(std::getenv("WBX_CIRC_DIAG")) == "nodec";
+    const FistaKernel k = fista_kernel_for(P.g0, P.nCo);
+    if (!k.fn) fail(WBX_BAD_SPEC, "spectral FISTA: unsupported group size");
+#if WBX_CIRC_PROF
+    static unsigned long long* prof = nullptr;
+    if (!prof) WBX_CUDA(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
+    WBX_CUDA(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
+    a.prof = prof;
+#endif
+    WBX_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    void* params[] = {&a};
+    // one CTA per SM: g spectral CTAs, the rest run the decoupled coordinates
+    WBX_CUDA(cudaLaunchCooperativeKernel(k.fn, dim3(ctx->num_sms), dim3(32 * k.warps), params, k.smem, st));
+    count_launch(ctx);
+    WBX_CUDA(cudaGetLastError());
+#if WBX_CIRC_PROF
+    unsigned long long h[16];
+    WBX_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st));
+    WBX_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "circ_fista cycles per iteration (CTA 0):");
+    for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %d:%.0f", i, static_cast<double>(h[i]) / std::max(1, pr.K));
+    std::fprintf(stderr, "\n");
+#endif
+}
+
 void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, double step_safety, double* work,
-                     double* out, cudaStream_t st) {
+                     double2* gram, double* out, cudaStream_t st) {
     const uint32_t nh = static_cast<uint32_t>(P.h_fhalf.size());
     double* norm_part = work;
     double2* t1 = reinterpret_cast<double2*>(work + kCircNormBlocks);
@@ -725,11 +1247,9 @@ void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, dou
     circ_dft1_kernel<<<dim3(P.g0, P.nCo), th1, P.g1 * sizeof(double), st>>>(P.orb.p, P.g0, P.g1, P.tw1.p, t1);
     const unsigned th0 = std::min<uint32_t>(1024, ((P.g0 + 31) / 32) * 32);
     circ_dft0_kernel<<<dim3(P.g1, P.nCo), th0, P.g0 * sizeof(double2), st>>>(P.nCo, P.g0, P.g1, P.tw0.p, t1, vh);
-    const uint32_t nent = static_cast<uint32_t>(P.h_eval.size());
-    const size_t lz_smem = (P.g0 + P.g1) * sizeof(double2) + nent * (sizeof(double) + sizeof(uint32_t)) +
-                           (P.nRo * P.nCo + 1) * sizeof(uint32_t);
-    circ_lanczos_kernel<<<(nh + 2 * kCircWarps - 1) / (2 * kCircWarps), kCircWarps * 32, lz_smem, st>>>(
-        nh, P.fhalf.p, P.g1, P.g0, P.nRo, P.nCo, P.eoff.p, P.eh.p, P.eval.p, P.tw0.p, P.tw1.p, isp_dev, vh, tri, nent);
+    circ_gram_launch(ctx, P, gram, st);
+    circ_lanczos_kernel<<<(nh + 2 * kCircWarps - 1) / (2 * kCircWarps), kCircWarps * 32, 0, st>>>(
+        nh, P.fhalf.p, P.nCo, gram, isp_dev, vh, tri);
     const unsigned pb = (nh + 31) / 32;  // one warp per SM: the steps are a dependent chain
     if (P.nCo <= 4)
         circ_power_kernel<4><<<pb, 32, 0, st>>>(nh, tri, mom_m, mom_e);
@@ -741,7 +1261,7 @@ void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, dou
         circ_power_kernel<16><<<pb, 32, 0, st>>>(nh, tri, mom_m, mom_e);
     circ_reduce_kernel<<<kCircMoments, 256, 0, st>>>(nh, mom_m, mom_e, S, X);
     circ_final_kernel<<<1, 256, 0, st>>>(P.NG, S, X, norm_part, kCircNormBlocks, step_safety, out);
-    count_launch(ctx, 7);
+    count_launch(ctx, 7);  // + circ_gram_kernel
     WBX_CUDA(cudaGetLastError());
 }
 

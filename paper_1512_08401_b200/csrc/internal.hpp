@@ -267,7 +267,26 @@ bool circ_check_p(const CircPlan& p, const double* p_full, std::vector<double>& 
 void circ_upload(CircPlan& p, cudaStream_t st);
 uint64_t circ_work_doubles(const CircPlan& p);
 void circ_tau_launch(wbx_ctx* ctx, const CircPlan& p, const double* isp_dev, double step_safety, double* work,
-                     double* out, cudaStream_t st);
+                     double2* gram, double* out, cudaStream_t st);
+uint64_t circ_gram_doubles(const CircPlan& p);
+void circ_gram_launch(wbx_ctx* ctx, const CircPlan& p, double2* gram, cudaStream_t st);
+// the spectral FISTA engine (fp64 iterations, gradient in the Fourier domain of the group)
+struct CircProblem {
+    const double* x0_full;
+    const double* w_full;
+    const double* p_full;
+    double* x_full;
+    const uint32_t* isC;
+    const double* beta64;
+    double lambda;
+    int K;
+    const double* out;  // tau at out[0]
+};
+bool circ_fista_ok(const CircPlan& p, std::string* why);
+uint64_t circ_exchange_doubles(const CircPlan& p);
+uint32_t circ_fista_blocks(const CircPlan& p);
+void circ_fista_launch(wbx_ctx* ctx, const CircPlan& p, const CircProblem& pr, const double2* gram, double2* T,
+                       unsigned* counter, cudaStream_t st);
 
 // theta_build.cu (host): CSR assembly of thresholded circulant operators
 struct HostCsr {

@@ -2142,8 +2142,11 @@ struct wbx_solver {
     std::shared_ptr<wbx::StencilPlan> sp;  // owned by the operator's cache
     // block-Fourier step estimate (circ_tau.cu) for translation-invariant operators
     bool tau_circ = false;
+    bool fista_circ = false;  // spectral FISTA engine (circ_fista_kernel): fp64, untracked single images
     std::shared_ptr<wbx::CircPlan> circ;  // owned by the operator's cache
     wbx::DevBuf<double> circ_isp, circ_work;
+    wbx::DevBuf<double2> circ_gram, circ_T;
+    wbx::DevBuf<unsigned> circ_counter;
     wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
@@ -2329,7 +2332,8 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
     if (s->cfg.tau > 0.0) {
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->tau_circ) {  // translation-invariant operator: block-Fourier power iteration
-        circ_tau_launch(ctx, *s->circ, s->circ_isp.p, s->cfg.step_safety, s->circ_work.p, s->out.p, st);
+        circ_tau_launch(ctx, *s->circ, s->circ_isp.p, s->cfg.step_safety, s->circ_work.p, s->circ_gram.p, s->out.p,
+                        st);
         return;
     } else if (s->win && !s->tau_stream_lz) {
         const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos, s->win_lists_global);
@@ -2348,6 +2352,12 @@ template <typename T>
 void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
+    if (s->fista_circ && !a.track && s->batch == 1) {  // spectral engine (translation-invariant operator)
+        if (!s->tau_circ || s->cfg.tau > 0.0) circ_gram_launch(ctx, *s->circ, s->circ_gram.p, st);
+        CircProblem pr{a.x0_full, a.w_full, a.p_full, a.x_full, a.isC, a.beta64, a.lambda, a.max_iters, a.out};
+        circ_fista_launch(ctx, *s->circ, pr, s->circ_gram.p, s->circ_T.p, s->circ_counter.p, st);
+        return;
+    }
     if (s->stencil && !a.track && s->batch == 1) {
         a.isC = a.st.coupled;  // the decoupled pass: coordinates outside the Theta^T output bands
         launch_coop_smem(reinterpret_cast<const void*>(fista_stencil_kernel), s->grid_st, s->st_smem, a, st, kStBlock);
@@ -2626,18 +2636,33 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     if (s->cfg.precision == WBX_FP32 && (s->basis || op->has_layout) &&
         !(tau_env && (std::string(tau_env) == "lanczos" || std::string(tau_env) == "power"))) {
         auto plan = circ_plan_for(op, s->basis);
-        std::string why;
+        std::string why, fwhy;
         std::vector<double> isp;
-        if (circ_plan_ok(*plan, &why, nullptr) && circ_check_p(*plan, p, isp, &why)) {
-            circ_upload(*plan, st);
-            s->circ = plan;
+        const bool tau_on = !(tau_env && std::string(tau_env) == "spectral-off");
+        if (tau_on && circ_plan_ok(*plan, &why, nullptr) && circ_check_p(*plan, p, isp, &why)) {
             s->circ_isp.upload(isp, st);
             s->circ_work.alloc(circ_work_doubles(*plan));
             s->tau_circ = true;
         }
+        // the spectral FISTA engine: untracked single-image solves (tracked solves keep the window
+        // engine; WBX_ENGINE=window|stream|stencil selects the others)
+        const char* eng = std::getenv("WBX_ENGINE");
+        const bool track_cfg = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
+        if (!eng && !std::getenv("WBX_STENCIL") && s->batch == 1 && !track_cfg && circ_fista_ok(*plan, &fwhy) &&
+            static_cast<uint32_t>(s->ctx->num_sms) > circ_fista_blocks(*plan)) {
+            s->circ_T.alloc(circ_exchange_doubles(*plan) / 2);
+            s->circ_counter.alloc(1);
+            s->fista_circ = true;
+        }
+        if (s->tau_circ || s->fista_circ) {
+            circ_upload(*plan, st);
+            s->circ = plan;
+            s->circ_gram.alloc(circ_gram_doubles(*plan) / 2);
+        }
         if (std::getenv("WBX_VERBOSE"))
-            std::fprintf(stderr, "wbx: block-Fourier step estimate %s%s%s\n", s->tau_circ ? "on" : "off",
-                         s->tau_circ ? "" : ": ", s->tau_circ ? "" : why.c_str());
+            std::fprintf(stderr, "wbx: block-Fourier step estimate %s%s%s; spectral FISTA %s%s%s\n",
+                         s->tau_circ ? "on" : "off", s->tau_circ ? "" : ": ", s->tau_circ ? "" : why.c_str(),
+                         s->fista_circ ? "on" : "off", s->fista_circ ? "" : ": ", s->fista_circ ? "" : fwhy.c_str());
     }
     s->wv.alloc(nC ? nC : 1);
     s->uC.alloc(nC ? nC : 1);
@@ -2990,7 +3015,8 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
-    const char* it = (s->stencil && !track && s->batch == 1) ? "fista_stencil_kernel"
+    const char* it = (s->fista_circ && !track && s->batch == 1) ? "circ_fista_kernel"
+                     : (s->stencil && !track && s->batch == 1) ? "fista_stencil_kernel"
                      : (s->win && !track && s->batch == 1) ? "fista_win_kernel"
                      : (s->win_track && track && s->batch == 1) ? "fista_win_track_kernel"
                      : s->batch == 4                      ? "fista_batch_kernel<4>"

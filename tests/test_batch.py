@@ -59,7 +59,10 @@ def test_batch_sharding_world2_gloo():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("batch", [4, 8])
-def test_batched_deblur_bitwise_equals_single(golden, batch):
+def test_batched_deblur_bitwise_equals_single(golden, batch, monkeypatch):
+    # the fp32 single-image window engine is the batch kernel's per-image arithmetic (the default
+    # single-image engine for this invariant operator is the fp64 spectral one)
+    monkeypatch.setenv("WBX_ENGINE", "window")
     g = golden("c1_db4_256")
     op = g.operator()
     basis = W.make_basis(W.FilterFamily.Daubechies, 4, (256, 256), 4)

@@ -110,7 +110,8 @@ def test_c3_sharded_worlds_bitwise_equal_world1(world):
     del sh, probe
 
 
-def test_c5_batch8_at_1024_bitwise_equals_single(golden):
+def test_c5_batch8_at_1024_bitwise_equals_single(golden, monkeypatch):
+    monkeypatch.setenv("WBX_ENGINE", "window")  # the batch kernel's single-image counterpart (fp32)
     g = golden("c2_db4_1024")
     op = g.operator()
     ctx = W.Context(0)

@@ -432,10 +432,15 @@ def test_deblurrer_c2_1024_vs_oracle(golden):
 
 
 # ----------------------------------------------------------------------------- engine / format variants
-@pytest.mark.parametrize("env", [{}, {"WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"},
-                                 {"WBX_TAU_WINDOW": "64", "WBX_WIN_PLACE": "bank"}, {"WBX_WIN_PLACE": "bank"},
-                                 {"WBX_WIN_PLACE": "sorted"}, {"WBX_BARRIER": "master"},
-                                 {"WBX_WIN_COST": "16,1"}, {"WBX_WIN_LISTS": "global"}])
+_W = {"WBX_ENGINE": "window"}  # the window engine instead of the spectral one (invariant operators)
+
+
+@pytest.mark.parametrize("env", [{}, _W, {**_W, "WBX_WIN_FULL": "1"}, {"WBX_ENGINE": "stream"},
+                                 {**_W, "WBX_TAU": "lanczos"}, {**_W, "WBX_TAU": "power"},
+                                 {**_W, "WBX_TAU": "power", "WBX_TAU_WINDOW": "64", "WBX_WIN_PLACE": "bank"},
+                                 {**_W, "WBX_WIN_PLACE": "bank"},
+                                 {**_W, "WBX_WIN_PLACE": "sorted"}, {**_W, "WBX_BARRIER": "master"},
+                                 {**_W, "WBX_WIN_COST": "16,1"}, {**_W, "WBX_WIN_LISTS": "global"}])
 def test_deblurrer_engine_variants_vs_reference(golden, monkeypatch, env):
     """Every solver engine / window format / placement / barrier the library can select
     (environment switches read at solver creation) meets the same parity bar on C1."""
@@ -463,6 +468,7 @@ def test_window_layout_variants_leave_iterates_bitwise(golden, monkeypatch, env)
     cfg = W.SolverConfig(max_iters=50, track_energy=False, tau=g.meta["tau"])
     op = g.operator()
     P = W.spai(op)
+    monkeypatch.setenv("WBX_ENGINE", "window")
     ref = W.Deblurrer(op, basis_of(g), P, g.weights(), g.meta["lambda"], cfg).deblur(g["u0"], clamp=False)[0]
     for k, v in env.items():
         monkeypatch.setenv(k, v)

@@ -1,0 +1,108 @@
+"""Spectral FISTA engine (csrc/circ_tau.cu circ_fista_kernel) through the C ABI.
+
+For a translation-invariant Theta_K the solver applies the gradient Theta^T (Theta y - x0) as
+G y - b with G block-diagonal in the Fourier domain of the translation group (G_f =
+Theta^_f^H Theta^_f, 12 x 12 at C1/C2), in fp64, with the reference's prox / momentum /
+threshold expressions (solver.cpp:57-67, 119-151). Bar: the iterates of the reference's fp64
+run_pgd to ~1e-12 (vs 1e-5 for the fp32 window engine): restored images against the
+reference's golden outputs and the oracle's pgd on the same inputs."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1512_08401_b200 import waveblur as W
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+def setup(g):
+    op = g.operator()
+    b = W.make_basis(W.FilterFamily(g.family), g.meta["order"], g.dims, g.meta["J"])
+    return op, b, W.spai(op)
+
+
+def test_spectral_deblur_vs_reference(golden):
+    g = golden("c1_db4_256")
+    op, b, P = setup(g)
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=g.meta["iters"], track_energy=False))
+    assert d.kernels() == ("circ_lanczos_kernel", "circ_fista_kernel")
+    u, rep = d.deblur(g["u0"], clamp=False)
+    err = rel_l2(u, g["restored"])
+    print("C1 restored rel-L2 vs the reference:", err)
+    assert err <= 1e-11
+    x = W.analyze(u.reshape(g.dims), b).values
+    assert rel_l2(x, g["x_final"]) <= 1e-10
+    u2, _ = d.deblur(g["u0"], clamp=False)
+    assert np.array_equal(u, u2)  # run-to-run deterministic
+
+
+@pytest.mark.parametrize("iters", [0, 1, 2, 7])
+def test_spectral_iterates_vs_oracle_given_tau(golden, iters):
+    """Given tau (the gram blocks then come from the iteration launch): x_final vs the oracle's
+    fp64 pgd (pinned bitwise to the reference) for short runs, including K = 0."""
+    g = golden("c1_db4_256")
+    op, b, P = setup(g)
+    tau = g.meta["tau"]
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"],
+                    W.SolverConfig(max_iters=iters, track_energy=False, tau=tau))
+    assert d.kernels()[1] == "circ_fista_kernel"
+    u, _ = d.deblur(g["u0"], clamp=False)
+    A = O.Csr.of(op)
+    xr = O.pgd_tau(A, A.transpose(), g["x0"], g.weights(), g.meta["lambda"], P.p, tau, iters)
+    ur = O.synthesize(xr, g.dims, g.meta["J"], g.family, g.meta["order"])
+    assert rel_l2(u, ur) <= 1e-12, rel_l2(u, ur)
+
+
+def test_spectral_sym6_and_ista_case(golden):
+    """Another filter family and the ISTA-style identity-preconditioned invariant case."""
+    g = golden("s64_sym6_ista")
+    op, b, _ = setup(g)
+    P = W.identity_precond(op.n)
+    tau = g.meta["tau"]
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=20, track_energy=False, tau=tau))
+    assert d.kernels()[1] == "circ_fista_kernel"
+    u, _ = d.deblur(g["u0"], clamp=False)
+    A = O.Csr.of(op)
+    xr = O.pgd_tau(A, A.transpose(), g["x0"], g.weights(), g.meta["lambda"], P.p, tau, 20)
+    ur = O.synthesize(xr, g.dims, g.meta["J"], g.family, g.meta["order"])
+    assert rel_l2(u, ur) <= 1e-12, rel_l2(u, ur)
+
+
+def test_tracked_and_window_engines_still_selected(golden, monkeypatch):
+    """Tracked solves (energies / supports / ref_energy) keep the window engine; WBX_ENGINE=window
+    forces it for untracked ones."""
+    g = golden("c1_db4_256")
+    op, b, P = setup(g)
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=5, track_energy=True))
+    assert d.kernels()[1] == "fista_win_track_kernel"
+    monkeypatch.setenv("WBX_ENGINE", "window")
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=5, track_energy=False))
+    assert d.kernels()[1] == "fista_win_kernel"
+
+
+@pytest.mark.parametrize("dims,fam,order,J", [((64, 64), W.FilterFamily.Haar, 1, 1),     # g = 32, 1 column orbit
+                                              ((128, 128), W.FilterFamily.Daubechies, 2, 2),  # g = 32
+                                              ((128, 128), W.FilterFamily.Symmlet, 4, 3)])    # g = 16
+def test_spectral_other_groups_vs_oracle(dims, fam, order, J):
+    """Operators built on the device (theta_conv_topk) whose column-orbit count is not a multiple
+    of the engine's row padding, and other group sizes: the whole deblur vs the oracle's pgd."""
+    from paper_1512_08401_b200 import synthetic as S
+    basis = W.make_basis(fam, order, dims, J)
+    n = basis.layout.total()
+    op = W.theta_from_generators(W.theta_conv_topk(basis, W.gaussian_psf_kernel(dims, 2.5), 3 * n,
+                                                   W.dyadic_band_weights(basis.layout)))
+    P = W.spai(op)
+    u0 = S.add_noise(W.synthesize(W.spmv(op, W.analyze(S.synthetic_scene(dims), basis).values), basis), 5e-3, 4)
+    w = W.scale_weights(basis.layout)
+    d = W.Deblurrer(op, basis, P, w, 1e-4, W.SolverConfig(max_iters=30, track_energy=False))
+    u, rep = d.deblur(u0, clamp=False)
+    A = O.Csr.of(op)
+    ref = O.pgd(A, A.transpose(), O.analyze(u0, dims, J, int(fam), order), w, 1e-4, P.p, 30)
+    assert abs(rep.tau - ref["tau"]) <= 1e-12 * ref["tau"]
+    if d.kernels()[1] == "circ_fista_kernel":
+        ur = O.synthesize(ref["x_final"], dims, J, int(fam), order)
+        assert rel_l2(u, ur) <= 1e-12, rel_l2(u, ur)

@@ -27,6 +27,7 @@ def solve(g, monkeypatch, engine, u0, iters):
         monkeypatch.setenv("WBX_STENCIL", "1")
     else:
         monkeypatch.delenv("WBX_STENCIL", raising=False)
+        monkeypatch.setenv("WBX_ENGINE", engine)  # the fp32 window engine (not the spectral default)
     op = g.operator()
     basis = W.make_basis(W.FilterFamily(g.family), g.meta["order"], g.dims, g.meta["J"])
     P = W.spai(op)

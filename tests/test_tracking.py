@@ -37,7 +37,8 @@ def setup(g):
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_tracked_fp32_energies_and_iterates(golden, name):
+def test_tracked_fp32_energies_and_iterates(golden, name, monkeypatch):
+    monkeypatch.setenv("WBX_ENGINE", "window")  # untracked counterpart of the tracked window kernel
     g = golden(name)
     op, prob, P = setup(g)
     solve = W.ista if g.meta["method"] == "ista" else W.fista

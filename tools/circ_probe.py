@@ -22,5 +22,5 @@ d = W.Deblurrer(op, basis, P, W.scale_weights(basis.layout), 1e-4,
 ts = []
 for _ in range(8):
     u, rep = d.deblur(np.zeros(op.n) + 0.5, clamp=True)
-    ts.append(d.phase_ms()[0])
-print(json.dumps({"kernels": d.kernels(), "tau": rep.tau, "tau_iters": rep.tau_iters, "tau_ms": ts}))
+    ts.append(d.phase_ms())
+print(json.dumps({"kernels": d.kernels(), "tau": rep.tau, "tau_iters": rep.tau_iters, "tau_iters_ms": ts}))
