@@ -47,7 +47,7 @@ def num(vals, m, scale=1.0):
 traffic = {"source": f"ncu --set full --clock-control none ({Path(rep).name}); cold L2 per replay pass "
                      "(ncu flushes caches before each pass), DRAM read+write bytes per launch"}
 lines = ["# Solver kernels, `ncu --set full` (one launch each)", "",
-         f"Report: `{Path(rep).name}` (python tools/profile_case.py deblur, -k regex:\"tau_win|fista_win\" -c 2). "
+         f"Report: `{Path(rep).name}` (python tools/profile_case.py deblur). "
          "ncu flushes caches before each replay pass, so DRAM bytes include the cold read of the operator; "
          "inside a real solve the operator stays L2-resident across iterations.", "",
          "| kernel | duration ms | DRAM read MB | DRAM write MB | L2 hit % | L2 sectors (M) | SM thr % | L1 thr % | L2 thr % | regs | dyn smem KB |",
@@ -68,6 +68,12 @@ for name, launches in kern.items():
                  f"{g('lts__throughput.avg.pct_of_peak_sustained_elapsed')} | {g('launch__registers_per_thread', 0)} | "
                  f"{(num(v, 'launch__shared_mem_per_block_dynamic') or 0) / 1e3:.1f} |")
 Path(md).write_text("\n".join(lines) + "\n")
-Path(__file__).resolve().parents[1].joinpath("profiles", "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+tp = Path(__file__).resolve().parents[1].joinpath("profiles", "traffic.json")
+if len(sys.argv) > 3 and sys.argv[3] == "--merge" and tp.exists():  # add to an earlier capture's kernels
+    old = json.loads(tp.read_text())
+    old.update({k: v for k, v in traffic.items() if k != "source"})
+    old["source"] = old.get("source", "") + "; " + traffic["source"]
+    traffic = old
+tp.write_text(json.dumps(traffic, indent=1) + "\n")
 print("\n".join(lines))
 print(json.dumps(traffic))
