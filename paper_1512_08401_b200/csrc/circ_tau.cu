@@ -654,19 +654,16 @@ struct WarpFft {
                 w.y = -w.y;
                 v[0] = make_double2(a.x + b.x, a.y + b.y);
                 v[1] = cmul(make_double2(a.x - b.x, a.y - b.y), w);
-            } else {
+            } else {  // branch free: lo lanes a + b (times tw[0] = 1), hi lanes (a - b) w
                 const bool hi = (lane & d) != 0;
 #pragma unroll
                 for (int q = 0; q < PPL; ++q) {
                     const int e = lane + 32 * q;
                     const double2 p = shfl(v[q], d);
-                    if (!hi) {
-                        v[q] = make_double2(v[q].x + p.x, v[q].y + p.y);
-                    } else {
-                        double2 w = tw[(e % d) * (G / (2 * d))];
-                        w.y = -w.y;
-                        v[q] = cmul(make_double2(p.x - v[q].x, p.y - v[q].y), w);
-                    }
+                    double2 w = tw[hi ? (e % d) * (G / (2 * d)) : 0];
+                    w.y = -w.y;
+                    const double sg = hi ? -1.0 : 1.0;
+                    v[q] = cmul(make_double2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y)), w);
                 }
             }
         }
@@ -680,14 +677,15 @@ struct WarpFft {
                 const double2 a = v[0], bw = cmul(v[1], w);
                 v[0] = make_double2(a.x + bw.x, a.y + bw.y);
                 v[1] = make_double2(a.x - bw.x, a.y - bw.y);
-            } else {
+            } else {  // branch free: hi lanes pass b w, lo lanes a (times tw[0] = 1)
                 const bool hi = (lane & d) != 0;
 #pragma unroll
                 for (int q = 0; q < PPL; ++q) {
                     const int e = lane + 32 * q;
-                    const double2 t = hi ? cmul(v[q], tw[(e % d) * (G / (2 * d))]) : v[q];
+                    const double2 t = cmul(v[q], tw[hi ? (e % d) * (G / (2 * d)) : 0]);
                     const double2 p = shfl(t, d);
-                    v[q] = hi ? make_double2(p.x - t.x, p.y - t.y) : make_double2(t.x + p.x, t.y + p.y);
+                    const double sg = hi ? -1.0 : 1.0;
+                    v[q] = make_double2(fma(sg, t.x, p.x), fma(sg, t.y, p.y));
                 }
             }
         }
@@ -756,6 +754,20 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
             const int pos = i / (NCP * NCP), e = i % (NCP * NCP);
             Gs[(pos * NCP + e / NCP) * GS + e % NCP] = v;
         });
+    // this thread's block-product outputs (t0, t0 + blockDim) and their G rows, in registers
+    constexpr int kOut = (G * NCP + 32 * NCP * 2 - 1) / (32 * NCP * 2);  // rounds of two outputs
+    static_assert(kOut == 1, "one round of two block-product outputs per thread");
+    const int t0 = threadIdx.x, t1 = threadIdx.x + blockDim.x;
+    const bool one = t0 < G * NCP, two = t1 < G * NCP;  // G < 32 leaves threads without outputs
+    const int pos0 = one ? t0 / NCP : 0, ii0 = one ? t0 % NCP : 0;
+    const int pos1 = two ? t1 / NCP : pos0, ii1 = two ? t1 % NCP : ii0;
+    __syncthreads();
+    double2 g0r[NCP], g1r[NCP];
+#pragma unroll
+    for (int j = 0; j < NCP; ++j) {
+        g0r[j] = Gs[(pos0 * NCP + ii0) * GS + j];
+        g1r[j] = Gs[(pos1 * NCP + ii1) * GS + j];
+    }
     for (int i = threadIdx.x; i < NCP * G; i += blockDim.x) {  // own row: y = x_prev = x0, p, thr, b
         const int j = i / G, h1 = i % G;
         if (j >= nc) {
@@ -831,22 +843,17 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         }
         mark(2);
         __syncthreads();
-        for (int t0 = threadIdx.x; t0 < G * NCP; t0 += 2 * blockDim.x) {  // Y[i][pos] = G_(f0(pos), c) X[.][pos]
-            const int t1 = t0 + blockDim.x;  // a second output, interleaved (independent chains)
-            const bool two = t1 < G * NCP;
-            const int pos0 = t0 / NCP, ii0 = t0 % NCP, pos1 = two ? t1 / NCP : pos0, ii1 = two ? t1 % NCP : ii0;
-            const double2* G0 = Gs + (pos0 * NCP + ii0) * GS;
-            const double2* G1 = Gs + (pos1 * NCP + ii1) * GS;
+        {  // Y[i][pos] = G_(f0(pos), c) X[.][pos]: two outputs per thread, G rows in registers
             double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
 #pragma unroll
             for (int j = 0; j < NCP; ++j) {
-                const double2 m = G0[j], x = X[j * G + pos0], n = G1[j], y = X[j * G + pos1];
+                const double2 m = g0r[j], x = X[j * G + pos0], n = g1r[j], y = X[j * G + pos1];
                 r0 = fma(m.x, x.x, fma(-m.y, x.y, r0));
                 i0 = fma(m.x, x.y, fma(m.y, x.x, i0));
                 r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
                 i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
             }
-            Y[ii0 * G + pos0] = make_double2(r0, i0);
+            if (one) Y[ii0 * G + pos0] = make_double2(r0, i0);
             if (two) Y[ii1 * G + pos1] = make_double2(r1, i1);
         }
         mark(3);
