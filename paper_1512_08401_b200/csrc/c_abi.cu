@@ -15,6 +15,12 @@ struct wbx_solver;
 
 namespace wbx {
 void solver_setup(wbx_solver* s, const double* p, const double* w);
+wbx_solver* pgd_acquire(wbx_ctx* ctx, const wbx_op* op, const wbx_solver_cfg& cfg, int accelerate, double lambda,
+                        const double* p, const double* w);
+void pgd_release(wbx_solver* s);
+void pgd_purge(const wbx_ctx* ctx, const wbx_op* op);
+double* solver_x0_buf(wbx_solver* s);
+double* solver_x_buf(wbx_solver* s);
 void solver_run(wbx_solver* s, const double* x0_full_dev, double* x_full_dev);
 void solver_report(wbx_solver* s, wbx_report* rep);
 void launch_clamp(wbx_ctx* ctx, double* u, uint64_t n, cudaStream_t st);
@@ -129,6 +135,7 @@ int wbx_ctx_create(int device, wbx_ctx** out) {
 int wbx_ctx_destroy(wbx_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
+        wbx::pgd_purge(ctx, nullptr);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
@@ -312,7 +319,10 @@ int wbx_op_create(wbx_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const u
 }
 
 int wbx_op_destroy(wbx_op* op) {
-    return guard([&] { delete op; });
+    return guard([&] {
+        if (op) wbx::pgd_purge(nullptr, op);  // cached wbx_pgd solvers on it
+        delete op;
+    });
 }
 
 int wbx_op_set_layout(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J) {
@@ -323,6 +333,7 @@ int wbx_op_set_layout(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t 
         wbx::make_layout(ndim, dims, J, bands);  // make_layout's own errors (wavelet.cpp:32-70)
         if (dims[0] * (ndim == 2 ? dims[1] : 1) != op->n)
             wbx::fail(WBX_SHAPE_MISMATCH, "layout and operator sizes differ");
+        wbx::pgd_purge(nullptr, op);  // cached wbx_pgd solvers chose engines for the old layout
         std::lock_guard<std::mutex> g(op->win_mu);
         op->has_layout = true;
         op->l_ndim = ndim;
@@ -623,17 +634,20 @@ int wbx_pgd(wbx_ctx* ctx, const wbx_op* op, const double* x0, const double* w, d
         need(p, "p");
         need(cfg, "cfg");
         need(x_final, "x_final");
-        s = wbx::solver_new(ctx, op, nullptr, lambda, *cfg, accelerate);
-        wbx::solver_setup(s, p, w);
+        // a solver for (ctx, op, cfg, accelerate), reused across calls (layouts and buffers kept)
+        s = wbx::pgd_acquire(ctx, op, *cfg, accelerate, lambda, p, w);
         const uint64_t n = op->n;
-        wbx::DevBuf<double> dx0(n), dxf(n);
-        dx0.upload(x0, n, ctx->stream);
-        wbx::solver_run(s, dx0.p, dxf.p);
+        double* dx0 = wbx::solver_x0_buf(s);
+        double* dxf = wbx::solver_x_buf(s);
+        WBX_CUDA(cudaMemcpyAsync(dx0, x0, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        wbx::solver_run(s, dx0, dxf);
         wbx::solver_report(s, report);
-        WBX_CUDA(cudaMemcpyAsync(x_final, dxf.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        WBX_CUDA(cudaMemcpyAsync(x_final, dxf, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         WBX_CUDA(cudaStreamSynchronize(ctx->stream));
+        wbx::pgd_release(s);
+        s = nullptr;
     });
-    if (s) wbx::solver_free(s);
+    if (s) wbx::solver_free(s);  // an error: not returned to the cache
     return st;
 }
 

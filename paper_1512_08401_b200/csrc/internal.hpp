@@ -258,6 +258,9 @@ StencilView view_of(const StencilPlan& p);
 // the operator's plan for grid G (built from its generator groups, uploaded, cached on it)
 std::shared_ptr<StencilPlan> stencil_plan_for(const wbx_op* op, uint32_t G, uint32_t cta_warps, cudaStream_t st);
 
+// solver.cu: wbx_pgd's solver cache (drop entries of a context / an operator)
+void pgd_purge(const wbx_ctx* ctx, const wbx_op* op);
+
 // circ_tau.cu: the step estimate of translation-invariant operators, block-diagonal in the
 // Fourier domain of the translation group (ok == false when it does not apply)
 std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const uint64_t* dims, uint32_t J,

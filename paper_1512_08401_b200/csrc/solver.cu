@@ -32,6 +32,8 @@
 // with the reference's CounterRng(0x5eed) start, 200-iteration cap and 1e-6 rule.
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <list>
 
 #include "internal.hpp"
 #include "wbx_diag.h"
@@ -2156,8 +2158,10 @@ struct wbx_solver {
     float last_solve_ms = 0.f;
     // CUDA graphs of the deblur (WBX_GRAPH=0 disables): the step estimate, and analyze +
     // iterations + synthesize (+ clamp) for the last (u0, u, clamp) pointers
-    cudaGraphExec_t g_tau = nullptr, g_rest = nullptr;
-    const double* g_u0 = nullptr;
+    cudaGraphExec_t g_tau = nullptr, g_rest = nullptr, g_an = nullptr;  // g_an: analyze (side stream)
+    cudaEvent_t ev_an = nullptr;  // the analysis of the input is done (side stream -> main stream)
+    const double* g_an_u0 = nullptr;
+    uint64_t g_an_launches = 0;
     double* g_u = nullptr;
     int g_clamp = -1;
     uint64_t g_tau_launches = 0, g_rest_launches = 0;
@@ -2590,7 +2594,10 @@ void alloc_state(wbx_solver* s) {
 
 }  // namespace
 
-void solver_setup(wbx_solver* s, const double* p, const double* w) {
+// The preconditioner / weight dependent state of a solver (its layouts, engines and buffers
+// depend on the operator and the configuration only): used by setup and by a cached solver
+// that is reused with new P, w (wbx_pgd)
+void upload_pw(wbx_solver* s, const double* p, const double* w) {
     const wbx_op* op = s->op;
     const uint64_t n = op->n, nC = op->nC;
     cudaStream_t st = s->ctx->stream;
@@ -2607,10 +2614,38 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     s->pC.upload(hp, st);
     s->wC.upload(hw, st);
     s->ispC.upload(hisp, st);
-    s->p_full.alloc(n);
+    if (s->p_full.n != n) s->p_full.alloc(n);
     s->p_full.upload(p, n, st);
-    s->w_full.alloc(n);
+    if (s->w_full.n != n) s->w_full.alloc(n);
     s->w_full.upload(w, n, st);
+}
+
+// a cached solver (same operator and configuration) with a new P, w, lambda
+void solver_update(wbx_solver* s, const double* p, const double* w, double lambda) {
+    upload_pw(s, p, w);
+    s->lambda = lambda;
+    if (s->circ) {  // the block-Fourier estimate needs P constant on the column orbits
+        std::string why;
+        std::vector<double> isp;
+        const bool was = s->tau_circ;
+        s->tau_circ = circ_check_p(*s->circ, p, isp, &why);
+        if (s->tau_circ) {
+            s->circ_isp.upload(isp, s->ctx->stream);
+            if (!s->circ_work.p) s->circ_work.alloc(circ_work_doubles(*s->circ));
+        }
+        if (was != s->tau_circ && s->g_tau) {  // the step-estimate graph changes
+            cudaGraphExecDestroy(s->g_tau);
+            s->g_tau = nullptr;
+        }
+    }
+    WBX_CUDA(cudaStreamSynchronize(s->ctx->stream));
+}
+
+void solver_setup(wbx_solver* s, const double* p, const double* w) {
+    const wbx_op* op = s->op;
+    const uint64_t nC = op->nC;
+    cudaStream_t st = s->ctx->stream;
+    upload_pw(s, p, w);
     const uint64_t K = s->cfg.max_iters;
     std::vector<double> b64(K > 0 ? K : 1, 0.0);
     std::vector<float> b32(K > 0 ? K : 1, 0.f);
@@ -2639,7 +2674,13 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
         std::string why, fwhy;
         std::vector<double> isp;
         const bool tau_on = !(tau_env && std::string(tau_env) == "spectral-off");
-        if (tau_on && circ_plan_ok(*plan, &why, nullptr) && circ_check_p(*plan, p, isp, &why)) {
+        const bool plan_ok = circ_plan_ok(*plan, &why, nullptr);
+        if (plan_ok) {  // the G_f blocks serve both the estimate and the spectral engine
+            circ_upload(*plan, st);
+            s->circ = plan;
+            s->circ_gram.alloc(circ_gram_doubles(*plan) / 2);
+        }
+        if (plan_ok && tau_on && circ_check_p(*plan, p, isp, &why)) {
             s->circ_isp.upload(isp, st);
             s->circ_work.alloc(circ_work_doubles(*plan));
             s->tau_circ = true;
@@ -2653,11 +2694,6 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
             s->circ_T.alloc(circ_exchange_doubles(*plan) / 2);
             s->circ_counter.alloc(1);
             s->fista_circ = true;
-        }
-        if (s->tau_circ || s->fista_circ) {
-            circ_upload(*plan, st);
-            s->circ = plan;
-            s->circ_gram.alloc(circ_gram_doubles(*plan) / 2);
         }
         if (std::getenv("WBX_VERBOSE"))
             std::fprintf(stderr, "wbx: block-Fourier step estimate %s%s%s; spectral FISTA %s%s%s\n",
@@ -2695,6 +2731,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     WBX_CUDA(cudaEventCreate(&s->ev_mid));
     WBX_CUDA(cudaEventCreate(&s->ev_it0));
     WBX_CUDA(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+    WBX_CUDA(cudaEventCreateWithFlags(&s->ev_an, cudaEventDisableTiming));
     WBX_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     WBX_CUDA(cudaStreamSynchronize(st));
 }
@@ -2812,11 +2849,96 @@ void solver_free(wbx_solver* s) {
     if (s->ev_mid) cudaEventDestroy(s->ev_mid);
     if (s->ev_it0) cudaEventDestroy(s->ev_it0);
     if (s->ev_in) cudaEventDestroy(s->ev_in);
+    if (s->ev_an) cudaEventDestroy(s->ev_an);
+    if (s->g_an) cudaGraphExecDestroy(s->g_an);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     if (s->g_tau) cudaGraphExecDestroy(s->g_tau);
     if (s->g_rest) cudaGraphExecDestroy(s->g_rest);
     delete s;
 }
+
+// wbx_pgd's solver cache: the reference calls fista() / ista() repeatedly on one operator; a
+// solver's layouts, engines and device buffers depend on (context, operator, configuration,
+// accelerate) only, so a repeated call re-uploads P, w and x0 instead of rebuilding it. A solver
+// is taken out while in use; at most 4 are kept; entries of an operator are dropped when it is
+// destroyed or its layout changes, entries of a context when it is destroyed.
+namespace {
+struct PgdEntry {
+    wbx_ctx* ctx;
+    const wbx_op* op;
+    int accelerate;
+    wbx_solver_cfg cfg;
+    wbx_solver* s;
+};
+std::mutex g_pgd_mu;
+std::list<PgdEntry> g_pgd;  // most recent first
+constexpr size_t kPgdCache = 4;
+}  // namespace
+
+wbx_solver* pgd_acquire(wbx_ctx* ctx, const wbx_op* op, const wbx_solver_cfg& cfg, int accelerate, double lambda,
+                        const double* p, const double* w) {
+    wbx_solver* s = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_pgd_mu);
+        for (auto it = g_pgd.begin(); it != g_pgd.end(); ++it)
+            if (it->ctx == ctx && it->op == op && it->accelerate == accelerate &&
+                std::memcmp(&it->cfg, &cfg, sizeof cfg) == 0) {
+                s = it->s;
+                g_pgd.erase(it);
+                break;
+            }
+    }
+    if (s) {
+        try {
+            solver_update(s, p, w, lambda);
+        } catch (...) {
+            solver_free(s);
+            throw;
+        }
+        return s;
+    }
+    s = solver_new(ctx, op, nullptr, lambda, cfg, accelerate);
+    try {
+        solver_setup(s, p, w);
+        s->x0full.alloc(op->n);
+        s->xfull.alloc(op->n);
+    } catch (...) {
+        solver_free(s);
+        throw;
+    }
+    return s;
+}
+
+void pgd_release(wbx_solver* s) {
+    std::vector<wbx_solver*> evict;
+    {
+        std::lock_guard<std::mutex> g(g_pgd_mu);
+        g_pgd.push_front(PgdEntry{s->ctx, s->op, s->accelerate, s->cfg, s});
+        while (g_pgd.size() > kPgdCache) {
+            evict.push_back(g_pgd.back().s);
+            g_pgd.pop_back();
+        }
+    }
+    for (wbx_solver* e : evict) solver_free(e);
+}
+
+void pgd_purge(const wbx_ctx* ctx, const wbx_op* op) {
+    std::vector<wbx_solver*> evict;
+    {
+        std::lock_guard<std::mutex> g(g_pgd_mu);
+        for (auto it = g_pgd.begin(); it != g_pgd.end();)
+            if ((ctx && it->ctx == ctx) || (op && it->op == op)) {
+                evict.push_back(it->s);
+                it = g_pgd.erase(it);
+            } else {
+                ++it;
+            }
+    }
+    for (wbx_solver* e : evict) solver_free(e);
+}
+
+double* solver_x0_buf(wbx_solver* s) { return s->x0full.p; }
+double* solver_x_buf(wbx_solver* s) { return s->xfull.p; }
 
 void solver_alloc_images(wbx_solver* s) {
     const uint64_t B = static_cast<uint64_t>(s->batch);
@@ -2830,10 +2952,16 @@ void solver_alloc_images(wbx_solver* s) {
 
 namespace {
 
-// enqueue the image-dependent part of a deblur: analyze -> iterations -> synthesize (-> clamp)
-void deblur_rest(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp, cudaStream_t st) {
+// the analysis of the input (x0 = Psi^* u0): independent of the step estimate, so it runs on the
+// side stream concurrently with it
+void deblur_analyze(wbx_solver* s, const double* u0_dev, cudaStream_t side) {
     const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
-    for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, st);
+    for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, side);
+}
+
+// the rest of a deblur after the step estimate and the analysis: iterations -> synthesize (-> clamp)
+void deblur_rest(wbx_solver* s, double* u_dev, int clamp, cudaStream_t st) {
+    const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
     wbx::solver_iters(s, s->x0full.p, s->xfull.p);
     for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st, clamp);
 }
@@ -2873,18 +3001,24 @@ extern "C" {
 int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp) {
     try {
         if (!s || !u0_dev || !u_dev) wbx::fail(WBX_INVALID_ARGUMENT, "null argument to wbx_deblur_dev");
-        cudaStream_t st = s->ctx->stream;
+        cudaStream_t st = s->ctx->stream, side = s->copy_stream;
         const uint64_t before = s->ctx->launches;
         if (graphs_wanted(s)) {
-            // two graphs: the image-independent step estimate first (a pending host->device
-            // image copy overlaps it), then the image-dependent rest; ~20 launches -> 2
+            // three graphs: the image-independent step estimate on the main stream, concurrently
+            // the analysis of the input on the side stream (after a pending host->device copy of
+            // the image, queued there), then iterations + synthesis; ~25 launches -> 3
             try {
                 if (!s->g_tau) s->g_tau = capture_graph(s, st, &s->g_tau_launches, [&] { wbx::solver_tau(s); });
-                if (!s->g_rest || s->g_u0 != u0_dev || s->g_u != u_dev || s->g_clamp != clamp) {
+                if (!s->g_an || s->g_an_u0 != u0_dev) {
+                    if (s->g_an) cudaGraphExecDestroy(s->g_an);
+                    s->g_an = nullptr;
+                    s->g_an = capture_graph(s, side, &s->g_an_launches, [&] { deblur_analyze(s, u0_dev, side); });
+                    s->g_an_u0 = u0_dev;
+                }
+                if (!s->g_rest || s->g_u != u_dev || s->g_clamp != clamp) {
                     if (s->g_rest) cudaGraphExecDestroy(s->g_rest);
                     s->g_rest = nullptr;
-                    s->g_rest = capture_graph(s, st, &s->g_rest_launches, [&] { deblur_rest(s, u0_dev, u_dev, clamp, st); });
-                    s->g_u0 = u0_dev;
+                    s->g_rest = capture_graph(s, st, &s->g_rest_launches, [&] { deblur_rest(s, u_dev, clamp, st); });
                     s->g_u = u_dev;
                     s->g_clamp = clamp;
                 }
@@ -2893,21 +3027,26 @@ int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp
                 s->graphs_off = true;
             }
         }
+        // the side stream starts after everything queued so far on the main stream (which may
+        // still read x0full); a pending image copy is already queued on it
+        if (!s->input_pending) {
+            WBX_CUDA(cudaEventRecord(s->ev_in, st));
+            WBX_CUDA(cudaStreamWaitEvent(side, s->ev_in, 0));
+        }
+        s->input_pending = false;
         if (graphs_wanted(s)) {
+            WBX_CUDA(cudaGraphLaunch(s->g_an, side));
+            WBX_CUDA(cudaEventRecord(s->ev_an, side));
             WBX_CUDA(cudaGraphLaunch(s->g_tau, st));
-            if (s->input_pending) {
-                WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
-                s->input_pending = false;
-            }
+            WBX_CUDA(cudaStreamWaitEvent(st, s->ev_an, 0));
             WBX_CUDA(cudaGraphLaunch(s->g_rest, st));
-            s->ctx->launches += s->g_tau_launches + s->g_rest_launches;
+            s->ctx->launches += s->g_tau_launches + s->g_an_launches + s->g_rest_launches;
         } else {
-            wbx::solver_tau(s);  // image-independent: first, so a pending image copy overlaps it
-            if (s->input_pending) {
-                WBX_CUDA(cudaStreamWaitEvent(st, s->ev_in, 0));
-                s->input_pending = false;
-            }
-            deblur_rest(s, u0_dev, u_dev, clamp, st);
+            deblur_analyze(s, u0_dev, side);
+            WBX_CUDA(cudaEventRecord(s->ev_an, side));
+            wbx::solver_tau(s);  // image-independent: concurrently with the copy and the analysis
+            WBX_CUDA(cudaStreamWaitEvent(st, s->ev_an, 0));
+            deblur_rest(s, u_dev, clamp, st);
         }
         WBX_CUDA(cudaGetLastError());
         s->last_launches = s->ctx->launches - before;

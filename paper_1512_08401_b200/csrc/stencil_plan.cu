@@ -730,6 +730,7 @@ int wbx_op_set_generators(wbx_op* op, uint32_t ndim, const uint64_t* dims, uint3
         HostCsr csr = expand_generators(bands, ndim, n, n_gens, blocks, gen_index, counts, values);
         if (csr.rowptr != op->h_rowptr || csr.col != op->h_col || csr.val != op->h_val)
             fail(WBX_BAD_SPEC, "generator groups do not expand to the operator's CSR");
+        wbx::pgd_purge(nullptr, op);  // cached wbx_pgd solvers chose engines without the generators
         std::lock_guard<std::mutex> g(op->win_mu);
         op->has_gens = true;
         op->g_ndim = ndim;

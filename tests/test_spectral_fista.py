@@ -106,3 +106,24 @@ def test_spectral_other_groups_vs_oracle(dims, fam, order, J):
     if d.kernels()[1] == "circ_fista_kernel":
         ur = O.synthesize(ref["x_final"], dims, J, int(fam), order)
         assert rel_l2(u, ur) <= 1e-12, rel_l2(u, ur)
+
+
+def test_dropin_fista_solver_cache_reuse(golden):
+    """wbx_pgd keeps solvers across calls (same operator and configuration): new P, w, lambda
+    and x0 are taken into account every call, and a repeated call gives the same bits."""
+    g = golden("c1_db4_256")
+    op = g.operator()
+    P1 = W.spai(op)
+    rng = np.random.default_rng(5)
+    P2 = W.DiagonalPreconditioner(P1.p * rng.uniform(0.8, 1.25, op.n), W.PrecondKind.Spai)  # not orbit-constant
+    A = O.Csr.of(op)
+    cfg = W.SolverConfig(max_iters=20, precision=32, track_energy=False)
+    w = g.weights()
+    runs = []
+    for P, lam, x0 in [(P1, 1e-4, g["x0"]), (P2, 3e-4, g["x0"]), (P1, 1e-4, 0.5 * g["x0"]), (P1, 1e-4, g["x0"])]:
+        r = W.fista(W.DeblurProblem(W.SparseThetaOp(op), x0, w, lam), P, cfg)
+        ref = O.pgd(A, A.transpose(), x0, w, lam, P.p, 20)
+        assert abs(r.tau - ref["tau"]) <= 1e-6 * ref["tau"]
+        assert rel_l2(r.x_final, ref["x_final"]) <= 1e-5
+        runs.append(r.x_final)
+    assert np.array_equal(runs[0], runs[3])
