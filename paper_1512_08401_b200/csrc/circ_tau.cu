@@ -587,6 +587,18 @@ struct CircFistaArgs {
     uint32_t g, lg, nRo, nCo, NB;
     int diag_skip_decoupled;  // WBX_CIRC_DIAG=nodec: time the spectral CTAs alone (wrong x)
     unsigned long long* prof;  // diagnostics build (WBX_CIRC_PROF=1): CTA 0's cycles per section
+    double* outw;              // out (iteration count)
+    // energy / support tracking (TRACK instances): per-CTA partials of the spectral CTAs,
+    // [k][NB]: q = x_k . G x_k - 2 x_k . b (k = 0..K), r = lambda sum w |x_k|, s = support (k = 1..K);
+    // per-warp partials of the decoupled CTAs, [k - 1][nwd]: sum w |x_k| and support; [2][nwd]:
+    // sum x0^2 and sum w |x0| over all n
+    double* q_part;
+    double* r_part;
+    double* s_part;
+    double* dec_reg;
+    double* dec_sup;
+    double* e0_part;
+    uint32_t nwd;
 };
 
 
@@ -699,11 +711,73 @@ __device__ __forceinline__ int brev_g(int i) {
 
 // One CTA per SM: blockIdx < g the spectral CTAs (NCP warps, warp j = orbit row j), the rest the
 // decoupled coordinates.
-template <int G, int NCP>
+template <int G, int NCP, bool TRACK>
 __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a) {
     using F = WarpFft<G>;
     constexpr int PPL = F::PPL;
     const double tau = a.out[0];
+    if (TRACK && blockIdx.x >= a.NB) {
+        // decoupled coordinates with their per-iteration sums of w |x_k| and support (warp sums,
+        // accumulated over this warp's coordinate trips in a fixed order), and the constant parts
+        // of the energies (sum x0^2, sum w |x0| over every coordinate)
+        const uint64_t nthreads = static_cast<uint64_t>(gridDim.x - a.NB) * blockDim.x;
+        const uint64_t gthread = static_cast<uint64_t>(blockIdx.x - a.NB) * blockDim.x + threadIdx.x;
+        const uint32_t gwarp = static_cast<uint32_t>(gthread >> 5);
+        const int lane = threadIdx.x & 31;
+        double x0sq = 0.0, wx0 = 0.0;
+        const uint64_t trips = (a.n + nthreads - 1) / nthreads;  // warp-uniform
+        for (uint64_t t = 0; t < trips; ++t) {
+            const uint64_t i = t * nthreads + gthread;
+            const bool in = i < a.n;
+            const bool active = in && !((a.isC[i >> 5] >> (i & 31)) & 1u);
+            double x = 0.0, xp = 0.0, y = 0.0, thr = 0.0, w = 0.0;
+            if (in) {
+                const double x0 = a.x0_full[i];
+                w = a.w_full[i];
+                x0sq += x0 * x0;
+                wx0 += w * fabs(x0);
+                if (active) {
+                    thr = circ_thr(tau, a.lambda, w, a.p_full[i]);
+                    x = xp = y = x0;
+                }
+            }
+            bool live = active;
+            for (int k = 1; k <= a.K; ++k) {
+                double reg = 0.0, sup = 0.0;
+                if (live) {
+                    const double xn = circ_prox(y, thr);
+                    const bool fixed = xn == 0.0 && xp == 0.0;
+                    y = circ_momentum(xn, xp, a.beta64[k - 1]);
+                    xp = xn;
+                    x = xn;
+                    reg = w * fabs(xn);
+                    sup = xn != 0.0 ? 1.0 : 0.0;
+                    if (fixed) live = false;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    reg += __shfl_xor_sync(0xffffffffu, reg, o);
+                    sup += __shfl_xor_sync(0xffffffffu, sup, o);
+                }
+                if (lane == 0) {
+                    a.dec_reg[static_cast<uint64_t>(k - 1) * a.nwd + gwarp] += reg;
+                    a.dec_sup[static_cast<uint64_t>(k - 1) * a.nwd + gwarp] += sup;
+                }
+                if (!__any_sync(0xffffffffu, live)) break;
+            }
+            if (active) a.x_full[i] = x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            x0sq += __shfl_xor_sync(0xffffffffu, x0sq, o);
+            wx0 += __shfl_xor_sync(0xffffffffu, wx0, o);
+        }
+        if (lane == 0) {
+            a.e0_part[gwarp] = x0sq;
+            a.e0_part[a.nwd + gwarp] = wx0;
+        }
+        return;
+    }
     if (blockIdx.x >= a.NB) {
         if (a.diag_skip_decoupled) return;
         // decoupled coordinates (gradient exactly 0): x' = prox(y), y = x' + beta (x' - x_prev),
@@ -739,6 +813,34 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
     double* bs = xps + NCP * G;
     double* ps = bs + NCP * G;  // tau / p
     double* ths = ps + NCP * G;
+    double* gxs = ths + NCP * G;  // TRACK: G x_k-1 on row c (G x_k by linearity from G y_k+1)
+    __shared__ double tr_red[3][NCP];  // TRACK: block partials (fixed order)
+    // TRACK: this CTA's partials of x . G x - 2 x . b (energy of x_k-1, kq = k - 1) and of
+    // lambda w |x| and the support (of x_k, kr = k), summed over its coordinates in a fixed order
+    auto track_partials = [&](double q, double r, double sp, int kq, int kr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            q += __shfl_xor_sync(0xffffffffu, q, o);
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            sp += __shfl_xor_sync(0xffffffffu, sp, o);
+        }
+        if (lane == 0) {
+            tr_red[0][wj] = q;
+            tr_red[1][wj] = r;
+            tr_red[2][wj] = sp;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t[3] = {0.0, 0.0, 0.0};
+            for (int w = 0; w < NCP; ++w)
+                for (int v = 0; v < 3; ++v) t[v] += tr_red[v][w];
+            if (kq >= 0) a.q_part[static_cast<uint64_t>(kq) * a.NB + c] = t[0];
+            if (kr >= 1) {
+                a.r_part[static_cast<uint64_t>(kr - 1) * a.NB + c] = t[1];
+                a.s_part[static_cast<uint64_t>(kr - 1) * a.NB + c] = t[2];
+            }
+        }
+    };
     for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
     for (int i = threadIdx.x; i < 2 * NCP * G; i += blockDim.x) X[i] = make_double2(0.0, 0.0);  // padded rows stay 0
     batched_copy(
@@ -871,6 +973,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         circ_barrier(a.counter, ++bar * a.NB);
         mark(5);
         // row phase: row c; warp i inverts orbit i along f1 (loaded in bit-reversed order)
+        double tq = 0.0, trg = 0.0, tsp = 0.0;  // TRACK partials of this thread
         if (row_live) {
             double2 v[PPL];
 #pragma unroll
@@ -879,22 +982,91 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
                                  : make_double2(0.0, 0.0);
             F::inverse(v, tw);  // v[q].x * NG = (Theta^T Theta y)[wj][c][lane + 32 q]
             const double beta = a.beta64[k - 1];
+            const double bprev = k >= 2 ? a.beta64[k - 2] : 0.0;  // y_k = x_k-1 + bprev (x_k-1 - x_k-2)
 #pragma unroll
             for (int q = 0; q < PPL; ++q) {
                 if (!lane_live) break;
                 const int i = wj * G + lane + 32 * q;
-                const double grad = __dsub_rn(v[q].x * inv_ng, bs[i]);                      // Theta^T (Theta y - x0)
+                const double gy = v[q].x * inv_ng;                                       // (G y_k)_i
+                if constexpr (TRACK) {  // G x_k-1 = (G y_k + bprev G x_k-2) / (1 + bprev); x_k-1 = x_prev
+                    const double gx = k == 1 ? gy : (gy + bprev * gxs[i]) / (1.0 + bprev);
+                    gxs[i] = gx;
+                    tq += xps[i] * (gx - 2.0 * bs[i]);
+                }
+                const double grad = __dsub_rn(gy, bs[i]);                                 // Theta^T (Theta y - x0)
                 const double z0 = fma(-ps[i], grad, ys[i]);  // y - tau g / p (solver.cpp:126), tau / p once
                 const double xn = circ_prox(z0, ths[i]);
                 ys[i] = circ_momentum(xn, xps[i], beta);
                 xps[i] = xn;
+                if constexpr (TRACK) {
+                    trg += ths[i] / ps[i] * fabs(xn);  // lambda w |x_k|  (thr / (tau / p) = lambda w)
+                    tsp += xn != 0.0 ? 1.0 : 0.0;
+                }
             }
             __syncwarp();
-            if (k < a.K) row_forward();
+            if (TRACK || k < a.K) row_forward();
         }
+        if constexpr (TRACK) track_partials(tq, trg, tsp, k - 1, k);
         mark(6);
     }
+    if (TRACK && a.K > 0) {  // one more column / row pass: G y_K+1 -> G x_K -> the energy of x_K
+        circ_barrier(a.counter, ++bar * a.NB);
+        if (row_live) {
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q)
+                v[q] = lane_live ? a.T1[(static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            F::forward(v, tw);
+            if (lane_live)
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) X[wj * G + lane + 32 * q] = v[q];
+        }
+        __syncthreads();
+        {
+            double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NCP; ++j) {
+                const double2 m = g0r[j], x = X[j * G + pos0], n = g1r[j], y = X[j * G + pos1];
+                r0 = fma(m.x, x.x, fma(-m.y, x.y, r0));
+                i0 = fma(m.x, x.y, fma(m.y, x.x, i0));
+                r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
+                i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
+            }
+            if (one) Y[ii0 * G + pos0] = make_double2(r0, i0);
+            if (two) Y[ii1 * G + pos1] = make_double2(r1, i1);
+        }
+        __syncthreads();
+        if (row_live) {
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            F::inverse(v, tw);
+            if (lane_live)
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) a.T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+        }
+        circ_barrier(a.counter, ++bar * a.NB);
+        double tq = 0.0;
+        if (row_live) {
+            double2 v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q)
+                v[q] = lane_live ? a.T2[(static_cast<uint64_t>(wj) * G + c) * G + brev_g<G>(lane + 32 * q)]
+                                 : make_double2(0.0, 0.0);
+            F::inverse(v, tw);
+            const double bk = a.beta64[a.K - 1];
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) {
+                if (!lane_live) break;
+                const int i = wj * G + lane + 32 * q;
+                const double gx = (v[q].x * inv_ng + bk * gxs[i]) / (1.0 + bk);
+                tq += xps[i] * (gx - 2.0 * bs[i]);
+            }
+        }
+        track_partials(tq, 0.0, 0.0, a.K, 0);
+    }
     __syncthreads();
+    if (c == 0 && threadIdx.x == 0) a.outw[2] = a.K;  // OUT_ITERS_USED (tracking may lower it)
 #if WBX_CIRC_PROF
     if (c == 0 && threadIdx.x < 8) a.prof[threadIdx.x] = prof_acc[threadIdx.x];
 #endif
@@ -907,7 +1079,67 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
 
 template <int G, int NCP>
 size_t circ_fista_smem() {
-    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + 2 * NCP * G * 16 + G * 16 + 5 * NCP * G * 8;
+    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + 2 * NCP * G * 16 + G * 16 + 6 * NCP * G * 8;
+}
+
+// Energies of the tracked spectral solve (run_pgd's E(x_k), solver.cpp:44-55, 118, 130): block k
+// sums the partials in a fixed order; E_k = (q_k + |x0|^2) / 2 + lambda sum w |x_k|, with
+// |Theta x - x0|^2 = x . G x - 2 x . Theta^T x0 + |x0|^2. Block 0: the initial energy.
+__global__ void __launch_bounds__(256) circ_energy_kernel(const double* __restrict__ q_part,
+                                                          const double* __restrict__ r_part,
+                                                          const double* __restrict__ s_part,
+                                                          const double* __restrict__ dec_reg,
+                                                          const double* __restrict__ dec_sup,
+                                                          const double* __restrict__ e0_part, uint32_t NB, uint32_t nwd,
+                                                          double lambda, double* energies,
+                                                          unsigned long long* supports, double* out) {
+    __shared__ double red[4][256];
+    const int k = blockIdx.x, t = threadIdx.x;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};  // q + ... , C-part reg, decoupled reg, support
+    for (uint32_t i = t; i < NB; i += 256) {
+        v[0] += q_part[static_cast<uint64_t>(k) * NB + i];
+        if (k >= 1) {
+            v[1] += r_part[static_cast<uint64_t>(k - 1) * NB + i];
+            v[3] += s_part[static_cast<uint64_t>(k - 1) * NB + i];
+        }
+    }
+    for (uint32_t i = t; i < nwd; i += 256) {
+        v[0] += e0_part[i];  // |x0|^2
+        if (k >= 1) {
+            v[2] += dec_reg[static_cast<uint64_t>(k - 1) * nwd + i];
+            v[3] += dec_sup[static_cast<uint64_t>(k - 1) * nwd + i];
+        } else {
+            v[2] += e0_part[nwd + i];  // sum w |x0|
+        }
+    }
+    for (int j = 0; j < 4; ++j) red[j][t] = v[j];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (t < s)
+            for (int j = 0; j < 4; ++j) red[j][t] += red[j][t + s];
+        __syncthreads();
+    }
+    if (t == 0) {
+        const double e = 0.5 * red[0][0] + red[1][0] + lambda * red[2][0];
+        if (k == 0) {
+            out[3] = e;  // OUT_INITIAL_ENERGY
+        } else {
+            energies[k - 1] = e;
+            supports[k - 1] = static_cast<unsigned long long>(red[3][0]);
+        }
+    }
+}
+
+// NonFiniteEnergy (solver.cpp:131-133): the first iteration with a non-finite energy ends the
+// solve there (status 8, the host raises)
+__global__ void circ_energy_check_kernel(const double* energies, int K, double* out) {
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < K; ++k)
+        if (!isfinite(energies[k])) {
+            out[4] = 8.0;   // OUT_STATUS
+            out[2] = k + 1; // OUT_ITERS_USED
+            return;
+        }
 }
 
 // ----------------------------------------------------------------------------- host
@@ -1053,7 +1285,7 @@ std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const ui
     P->ok = true;
     // the spectral FISTA engine: square translation group of 16, 32 or 64, its shared memory
     const uint64_t ncp = (nCo + 3) / 4 * 4;
-    const uint64_t fista_smem = g0 * ncp * (ncp + 1) * 16 + 2 * ncp * g0 * 16 + g0 * 16 + 5 * ncp * g0 * 8;
+    const uint64_t fista_smem = g0 * ncp * (ncp + 1) * 16 + 2 * ncp * g0 * 16 + g0 * 16 + 6 * ncp * g0 * 8;
     if (ndim != 2 || g0 != g1 || (g0 != 8 && g0 != 16 && g0 != 32 && g0 != 64))
         P->fista_why = "spectral FISTA needs a square translation group of 8, 16, 32 or 64";
     else if (fista_smem > 227u * 1024u)
@@ -1115,22 +1347,24 @@ struct FistaKernel {
     int warps = 0;
 };
 template <int G, int NCP>
-FistaKernel fista_kernel_of() {
-    return FistaKernel{reinterpret_cast<const void*>(circ_fista_kernel<G, NCP>), circ_fista_smem<G, NCP>(), NCP};
+FistaKernel fista_kernel_of(bool track) {
+    return FistaKernel{track ? reinterpret_cast<const void*>(circ_fista_kernel<G, NCP, true>)
+                             : reinterpret_cast<const void*>(circ_fista_kernel<G, NCP, false>),
+                       circ_fista_smem<G, NCP>(), NCP};
 }
 template <int G>
-FistaKernel fista_kernel_g(uint32_t nc) {
-    if (nc <= 4) return fista_kernel_of<G, 4>();
-    if (nc <= 8) return fista_kernel_of<G, 8>();
-    if (nc <= 12) return fista_kernel_of<G, 12>();
-    return fista_kernel_of<G, 16>();
+FistaKernel fista_kernel_g(uint32_t nc, bool track) {
+    if (nc <= 4) return fista_kernel_of<G, 4>(track);
+    if (nc <= 8) return fista_kernel_of<G, 8>(track);
+    if (nc <= 12) return fista_kernel_of<G, 12>(track);
+    return fista_kernel_of<G, 16>(track);
 }
-// (g, nCo) -> instance: g in {8, 16, 32, 64}, nCo padded to 4, 8, 12, 16 rows (warps)
-FistaKernel fista_kernel_for(uint32_t g, uint32_t nc) {
-    if (g == 8) return fista_kernel_g<8>(nc);
-    if (g == 16) return fista_kernel_g<16>(nc);
-    if (g == 32) return fista_kernel_g<32>(nc);
-    if (g == 64) return fista_kernel_g<64>(nc);
+// (g, nCo, tracking) -> instance: g in {8, 16, 32, 64}, nCo padded to 4, 8, 12, 16 rows (warps)
+FistaKernel fista_kernel_for(uint32_t g, uint32_t nc, bool track = false) {
+    if (g == 8) return fista_kernel_g<8>(nc, track);
+    if (g == 16) return fista_kernel_g<16>(nc, track);
+    if (g == 32) return fista_kernel_g<32>(nc, track);
+    if (g == 64) return fista_kernel_g<64>(nc, track);
     return FistaKernel{};
 }
 }  // namespace
@@ -1150,10 +1384,11 @@ void circ_upload(CircPlan& P, cudaStream_t st) {
     P.rorb.upload(P.h_rorb.data(), P.h_rorb.size(), st);
     WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(circ_gram_kernel),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
-    if (P.fista_ok) {
-        const FistaKernel k = fista_kernel_for(P.g0, P.nCo);
-        WBX_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
-    }
+    if (P.fista_ok)
+        for (const bool track : {false, true}) {
+            const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
+            WBX_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
+        }
     WBX_CUDA(cudaStreamSynchronize(st));
     P.uploaded = true;
 }
@@ -1183,6 +1418,14 @@ void circ_gram_launch(wbx_ctx* ctx, const CircPlan& P, double2* gram, cudaStream
 uint64_t circ_exchange_doubles(const CircPlan& P) { return 4ull * P.nCo * P.NG; }
 uint32_t circ_fista_blocks(const CircPlan& P) { return P.g0; }
 
+
+// tracking work (doubles): q [K+1][NB], r and s [K][NB], decoupled sums [2][K][nwd], e0 [2][nwd]
+uint64_t circ_track_doubles(const CircPlan& P, int K, int num_sms) {
+    const uint64_t NB = P.g0, nwd = static_cast<uint64_t>(num_sms - static_cast<int>(NB)) *
+                                    static_cast<uint64_t>(fista_kernel_for(P.g0, P.nCo).warps);
+    const uint64_t Kp = static_cast<uint64_t>(K > 0 ? K : 0);
+    return (Kp + 1) * NB + 2 * Kp * NB + 2 * Kp * nwd + 2 * nwd + 16;
+}
 
 void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, const double2* gram, double2* T,
                        unsigned* counter, cudaStream_t st) {
@@ -1214,8 +1457,22 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     a.nCo = P.nCo;
     a.NB = P.g0;
     a.diag_skip_decoupled = std::getenv("WBX_CIRC_DIAG") && std::string(std::getenv("WBX_CIRC_DIAG")) == "nodec";
-    const FistaKernel k = fista_kernel_for(P.g0, P.nCo);
+    const bool track = pr.track_work != nullptr;
+    const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
     if (!k.fn) fail(WBX_BAD_SPEC, "spectral FISTA: unsupported group size");
+    a.outw = const_cast<double*>(pr.out);
+    if (track) {
+        const uint64_t NB = P.g0, nwd = static_cast<uint64_t>(ctx->num_sms - static_cast<int>(NB)) * k.warps;
+        const uint64_t Kp = static_cast<uint64_t>(pr.K > 0 ? pr.K : 0);
+        a.nwd = static_cast<uint32_t>(nwd);
+        a.q_part = pr.track_work;
+        a.r_part = a.q_part + (Kp + 1) * NB;
+        a.s_part = a.r_part + Kp * NB;
+        a.dec_reg = a.s_part + Kp * NB;
+        a.dec_sup = a.dec_reg + Kp * nwd;
+        a.e0_part = a.dec_sup + Kp * nwd;
+        WBX_CUDA(cudaMemsetAsync(a.dec_reg, 0, 2 * Kp * nwd * sizeof(double), st));
+    }
 #if WBX_CIRC_PROF
     static unsigned long long* prof = nullptr;
     if (!prof) WBX_CUDA(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
@@ -1228,6 +1485,14 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     WBX_CUDA(cudaLaunchCooperativeKernel(k.fn, dim3(ctx->num_sms), dim3(32 * k.warps), params, k.smem, st));
     count_launch(ctx);
     WBX_CUDA(cudaGetLastError());
+    if (track) {
+        circ_energy_kernel<<<pr.K + 1, 256, 0, st>>>(a.q_part, a.r_part, a.s_part, a.dec_reg, a.dec_sup, a.e0_part,
+                                                      a.NB, a.nwd, pr.lambda, pr.energies, pr.supports,
+                                                      const_cast<double*>(pr.out));
+        circ_energy_check_kernel<<<1, 32, 0, st>>>(pr.energies, pr.K, const_cast<double*>(pr.out));
+        count_launch(ctx, 2);
+        WBX_CUDA(cudaGetLastError());
+    }
 #if WBX_CIRC_PROF
     unsigned long long h[16];
     WBX_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st));

@@ -284,8 +284,13 @@ struct CircProblem {
     double lambda;
     int K;
     const double* out;  // tau at out[0]
+    // energy / support tracking (no ref_energy rule): work buffer (circ_track_doubles) and outputs
+    double* track_work = nullptr;
+    double* energies = nullptr;
+    unsigned long long* supports = nullptr;
 };
 bool circ_fista_ok(const CircPlan& p, std::string* why);
+uint64_t circ_track_doubles(const CircPlan& p, int K, int num_sms);
 uint64_t circ_exchange_doubles(const CircPlan& p);
 uint32_t circ_fista_blocks(const CircPlan& p);
 void circ_fista_launch(wbx_ctx* ctx, const CircPlan& p, const CircProblem& pr, const double2* gram, double2* T,

@@ -2148,6 +2148,7 @@ struct wbx_solver {
     std::shared_ptr<wbx::CircPlan> circ;  // owned by the operator's cache
     wbx::DevBuf<double> circ_isp, circ_work;
     wbx::DevBuf<double2> circ_gram, circ_T;
+    wbx::DevBuf<double> circ_track;  // tracked spectral solves: per-CTA / per-warp energy partials
     wbx::DevBuf<unsigned> circ_counter;
     wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
@@ -2356,9 +2357,14 @@ template <typename T>
 void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
-    if (s->fista_circ && !a.track && s->batch == 1) {  // spectral engine (translation-invariant operator)
+    if (s->fista_circ && s->batch == 1 && !a.stop_on_ref) {  // spectral engine (translation-invariant operator)
         if (!s->tau_circ || s->cfg.tau > 0.0) circ_gram_launch(ctx, *s->circ, s->circ_gram.p, st);
         CircProblem pr{a.x0_full, a.w_full, a.p_full, a.x_full, a.isC, a.beta64, a.lambda, a.max_iters, a.out};
+        if (a.track) {  // energies / supports of every iterate (solver.cpp:130-137)
+            pr.track_work = s->circ_track.p;
+            pr.energies = s->energies.p;
+            pr.supports = s->supports.p;
+        }
         circ_fista_launch(ctx, *s->circ, pr, s->circ_gram.p, s->circ_T.p, s->circ_counter.p, st);
         return;
     }
@@ -2685,14 +2691,17 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
             s->circ_work.alloc(circ_work_doubles(*plan));
             s->tau_circ = true;
         }
-        // the spectral FISTA engine: untracked single-image solves (tracked solves keep the window
-        // engine; WBX_ENGINE=window|stream|stencil selects the others)
+        // the spectral FISTA engine: single-image solves, with energy / support tracking too (solves
+        // with the ref_energy stopping rule keep the window engine; WBX_ENGINE=window|stream and
+        // WBX_STENCIL=1 select the others)
         const char* eng = std::getenv("WBX_ENGINE");
-        const bool track_cfg = s->cfg.track_energy || s->cfg.track_support || std::isfinite(s->cfg.ref_energy);
-        if (!eng && !std::getenv("WBX_STENCIL") && s->batch == 1 && !track_cfg && circ_fista_ok(*plan, &fwhy) &&
-            static_cast<uint32_t>(s->ctx->num_sms) > circ_fista_blocks(*plan)) {
+        const bool track_cfg = s->cfg.track_energy || s->cfg.track_support;
+        if (!eng && !std::getenv("WBX_STENCIL") && s->batch == 1 && !std::isfinite(s->cfg.ref_energy) &&
+            circ_fista_ok(*plan, &fwhy) && static_cast<uint32_t>(s->ctx->num_sms) > circ_fista_blocks(*plan)) {
             s->circ_T.alloc(circ_exchange_doubles(*plan) / 2);
             s->circ_counter.alloc(1);
+            if (track_cfg && s->cfg.max_iters > 0)
+                s->circ_track.alloc(circ_track_doubles(*plan, static_cast<int>(s->cfg.max_iters), s->ctx->num_sms));
             s->fista_circ = true;
         }
         if (std::getenv("WBX_VERBOSE"))
@@ -3154,7 +3163,7 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
-    const char* it = (s->fista_circ && !track && s->batch == 1) ? "circ_fista_kernel"
+    const char* it = (s->fista_circ && s->batch == 1 && !std::isfinite(s->cfg.ref_energy)) ? "circ_fista_kernel"
                      : (s->stencil && !track && s->batch == 1) ? "fista_stencil_kernel"
                      : (s->win && !track && s->batch == 1) ? "fista_win_kernel"
                      : (s->win_track && track && s->batch == 1) ? "fista_win_track_kernel"

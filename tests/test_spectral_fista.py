@@ -73,15 +73,42 @@ def test_spectral_sym6_and_ista_case(golden):
 
 
 def test_tracked_and_window_engines_still_selected(golden, monkeypatch):
-    """Tracked solves (energies / supports / ref_energy) keep the window engine; WBX_ENGINE=window
-    forces it for untracked ones."""
+    """Tracked solves without the ref_energy rule run on the spectral engine; the ref_energy rule
+    keeps the window engine; WBX_ENGINE=window forces it for the others."""
     g = golden("c1_db4_256")
     op, b, P = setup(g)
     d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=5, track_energy=True))
+    assert d.kernels()[1] == "circ_fista_kernel"
+    d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"],
+                    W.SolverConfig(max_iters=5, track_energy=True, ref_energy=1.0))
     assert d.kernels()[1] == "fista_win_track_kernel"
     monkeypatch.setenv("WBX_ENGINE", "window")
     d = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], W.SolverConfig(max_iters=5, track_energy=False))
     assert d.kernels()[1] == "fista_win_kernel"
+
+
+@pytest.mark.parametrize("name", ["c1_db4_256", "s64_sym6_ista"])
+def test_tracked_spectral_energies_vs_reference(golden, name):
+    """The reference's own fista() with its per-iteration energies and supports (the drop-in
+    binding's call) on the spectral engine: energies, the initial energy and the supports of the
+    reference's run, x_final as the untracked solve's."""
+    g = golden(name)
+    op, b, P = setup(g)
+    if g.meta["precond"] == "identity":
+        P = W.identity_precond(op.n)
+    prob = W.DeblurProblem(W.SparseThetaOp(op), g["x0"], g.weights(), g.meta["lambda"])
+    iters = g.meta["iters"]
+    solve = W.ista if g.meta.get("method") == "ista" else W.fista
+    tr = solve(prob, P, W.SolverConfig(max_iters=iters, precision=32, track_energy=True, track_support=True))
+    plain = solve(prob, P, W.SolverConfig(max_iters=iters, precision=32, track_energy=False))
+    assert tr.iters_used == iters
+    assert np.array_equal(tr.x_final, plain.x_final)  # bookkeeping does not touch the trajectory
+    e, ref = np.array(tr.energies), np.asarray(g["energies"])
+    assert e.shape == ref.shape
+    assert np.max(np.abs(e - ref) / np.abs(ref)) <= 1e-10, np.max(np.abs(e - ref) / np.abs(ref))
+    assert abs(tr.initial_energy - g.meta["initial_energy"]) <= 1e-10 * abs(g.meta["initial_energy"])
+    assert len(tr.support_sizes) == iters
+    assert tr.support_sizes[-1] == int(np.count_nonzero(tr.x_final))  # support of the last iterate
 
 
 @pytest.mark.parametrize("dims,fam,order,J", [((64, 64), W.FilterFamily.Haar, 1, 1),     # g = 32, 1 column orbit
