@@ -182,74 +182,94 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // memory once per block), G_f = Theta^_f^H Theta^_f (lane i: row i), written to gram[hf] as
 // nCo x nCo complex fp64. G_f is the Fourier block of Theta^T Theta: the step estimate scales it
 // by D = P^-1/2, the spectral FISTA engine applies it as is.
-__global__ void __launch_bounds__(kCircWarps * 32) circ_gram_kernel(
+// Copy n complex values src(i) -> dst(i) with every load of a thread issued before its stores
+// (one memory round trip per call, not one per element)
+template <typename Src, typename Dst>
+__device__ __forceinline__ void batched_copy(uint32_t n, Src src, Dst dst) {
+    constexpr int kB = 8;
+    for (uint32_t base = 0; base < n; base += kB * blockDim.x) {
+        double2 v[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const uint32_t i = base + r * blockDim.x + threadIdx.x;
+            if (i < n) v[r] = src(i);
+        }
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const uint32_t i = base + r * blockDim.x + threadIdx.x;
+            if (i < n) dst(i, v[r]);
+        }
+    }
+}
+
+constexpr int kGramWarps = 4;  // frequencies per block of circ_gram_kernel
+
+__global__ void __launch_bounds__(kGramWarps * 32) circ_gram_kernel(
     uint32_t nhalf, const uint32_t* __restrict__ fhalf, uint32_t g1, uint32_t g0, uint32_t nRo, uint32_t nCo,
     const uint32_t* __restrict__ eoff, const uint32_t* __restrict__ eh, const double* __restrict__ eval,
     const double2* __restrict__ tw0, const double2* __restrict__ tw1, double2* __restrict__ gram, uint32_t nent) {
-    // the representative rows and twiddles, staged once per block (dynamic shared memory)
+    // the representative rows and twiddles, staged once per block (loads issued before the stores)
     extern __shared__ double2 circ_smem[];
-    double2* s_tw0 = circ_smem;
+    const uint32_t nTh = nRo * nCo;  // Theta^_f entries of one frequency
+    double2* s_th = circ_smem;                                 // [kGramWarps][nRo][nCo]
+    double2* s_tw0 = s_th + kGramWarps * nTh;
     double2* s_tw1 = s_tw0 + g0;
     double* s_val = reinterpret_cast<double*>(s_tw1 + g1);
     uint32_t* s_eh = reinterpret_cast<uint32_t*>(s_val + nent);
     uint32_t* s_eoff = s_eh + nent;
-    for (uint32_t i = threadIdx.x; i < g0; i += blockDim.x) s_tw0[i] = tw0[i];
-    for (uint32_t i = threadIdx.x; i < g1; i += blockDim.x) s_tw1[i] = tw1[i];
-    for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
-        s_val[i] = eval[i];
-        s_eh[i] = eh[i];
-    }
-    for (uint32_t i = threadIdx.x; i <= nRo * nCo; i += blockDim.x) s_eoff[i] = eoff[i];
+    batched_copy(g0, [&](uint32_t i) { return tw0[i]; }, [&](uint32_t i, double2 v) { s_tw0[i] = v; });
+    batched_copy(g1, [&](uint32_t i) { return tw1[i]; }, [&](uint32_t i, double2 v) { s_tw1[i] = v; });
+    batched_copy(
+        nent, [&](uint32_t i) { return make_double2(eval[i], __longlong_as_double(static_cast<long long>(eh[i]))); },
+        [&](uint32_t i, double2 v) {
+            s_val[i] = v.x;
+            s_eh[i] = static_cast<uint32_t>(__double_as_longlong(v.y));
+        });
+    batched_copy(
+        nTh + 1, [&](uint32_t i) { return make_double2(__longlong_as_double(static_cast<long long>(eoff[i])), 0.0); },
+        [&](uint32_t i, double2 v) { s_eoff[i] = static_cast<uint32_t>(__double_as_longlong(v.x)); });
     __syncthreads();
-    constexpr int kSlots = 2 * kCircWarps;
-    __shared__ double2 vec[kSlots][kCircMaxCo];  // Theta^ row
-    const int lane = threadIdx.x & 31, li = lane & 15;
-    const int slot = (threadIdx.x >> 5) * 2 + (lane >> 4);
-    const uint32_t hf = blockIdx.x * kSlots + slot;
-    const uint32_t warp_first = blockIdx.x * kSlots + (threadIdx.x >> 5) * 2;
-    if (warp_first >= nhalf) return;  // whole warp
-    const bool live = hf < nhalf;
-    const uint32_t fw = live ? fhalf[hf] : 0u;
-    const uint32_t f = fw >> 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t hf = blockIdx.x * kGramWarps + w;
+    if (hf >= nhalf) return;  // whole warp
+    const uint32_t f = fhalf[hf] >> 1;
     const uint32_t f0 = f / g1, f1 = f % g1;
     const uint32_t m0 = (g0 & (g0 - 1)) == 0 ? g0 - 1 : 0, m1 = (g1 & (g1 - 1)) == 0 ? g1 - 1 : 0;
-    const int nc = static_cast<int>(nCo);
-    const bool own = li < nc;
-    // 1. M^_f
-    double2 acc[kCircMaxCo];
-#pragma unroll
-    for (int j = 0; j < kCircMaxCo; ++j) acc[j] = make_double2(0.0, 0.0);
-    for (uint32_t r = 0; r < nRo; ++r) {
-        if (own) {
-            double re = 0.0, im = 0.0;
-            for (uint32_t e = s_eoff[r * nCo + li]; e < s_eoff[r * nCo + li + 1]; ++e) {
-                const uint32_t h = s_eh[e];
-                const uint32_t a0 = f0 * (h >> 16), a1 = f1 * (h & 0xffffu);
-                const double2 ph = cmul(s_tw0[m0 ? (a0 & m0) : a0 % g0], s_tw1[m1 ? (a1 & m1) : a1 % g1]);
-                re = fma(s_val[e], ph.x, re);
-                im = fma(s_val[e], ph.y, im);
-            }
-            vec[slot][li] = make_double2(re, im);
+    double2* th = s_th + w * nTh;
+    // Theta^_f[r][j] = sum over the entries (j, h) of representative row r of val e^{+2 pi i f.h/g}:
+    // every (r, j) pair independently (lanes over pairs)
+    for (uint32_t p = lane; p < nTh; p += 32) {
+        double re = 0.0, im = 0.0;
+        for (uint32_t e = s_eoff[p]; e < s_eoff[p + 1]; ++e) {
+            const uint32_t h = s_eh[e];
+            const uint32_t a0 = f0 * (h >> 16), a1 = f1 * (h & 0xffffu);
+            const double2 ph = cmul(s_tw0[m0 ? (a0 & m0) : a0 % g0], s_tw1[m1 ? (a1 & m1) : a1 % g1]);
+            re = fma(s_val[e], ph.x, re);
+            im = fma(s_val[e], ph.y, im);
         }
-        __syncwarp();
-        if (own) {
-            const double2 a = vec[slot][li];  // conj(a) * b
-#pragma unroll
-            for (int j = 0; j < kCircMaxCo; ++j) {
-                if (j < nc) {
-                    const double2 b = vec[slot][j];
-                    acc[j].x = fma(a.x, b.x, fma(a.y, b.y, acc[j].x));
-                    acc[j].y = fma(a.x, b.y, fma(-a.y, b.x, acc[j].y));
-                }
-            }
-        }
-        __syncwarp();
+        th[p] = make_double2(re, im);
     }
-    if (own && live) {
-        double2* G = gram + static_cast<uint64_t>(hf) * nCo * nCo + static_cast<uint64_t>(li) * nCo;
-#pragma unroll
-        for (int j = 0; j < kCircMaxCo; ++j)
-            if (j < nc) G[j] = acc[j];
+    __syncwarp();
+    // G_f[i][j] = sum_r conj(Theta^[r][i]) Theta^[r][j]: every (i, j) independently, two chains
+    double2* G = gram + static_cast<uint64_t>(hf) * nCo * nCo;
+    for (uint32_t p = lane; p < nCo * nCo; p += 32) {
+        const uint32_t i = p / nCo, j = p % nCo;
+        double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+        uint32_t r = 0;
+        for (; r + 1 < nRo; r += 2) {
+            const double2 a = th[r * nCo + i], b = th[r * nCo + j];
+            const double2 c = th[(r + 1) * nCo + i], d = th[(r + 1) * nCo + j];
+            r0 = fma(a.x, b.x, fma(a.y, b.y, r0));
+            i0 = fma(a.x, b.y, fma(-a.y, b.x, i0));
+            r1 = fma(c.x, d.x, fma(c.y, d.y, r1));
+            i1 = fma(c.x, d.y, fma(-c.y, d.x, i1));
+        }
+        if (r < nRo) {
+            const double2 a = th[r * nCo + i], b = th[r * nCo + j];
+            r0 = fma(a.x, b.x, fma(a.y, b.y, r0));
+            i0 = fma(a.x, b.y, fma(-a.y, b.x, i0));
+        }
+        G[p] = make_double2(r0 + r1, i0 + i1);
     }
 }
 
@@ -626,25 +646,6 @@ __device__ __forceinline__ double circ_momentum(double xn, double xp, double bet
     return __dadd_rn(xn, __dmul_rn(beta, __dsub_rn(xn, xp)));
 }
 
-// Copy n complex values src(i) -> dst(i) with every load of a thread issued before its stores
-// (one memory round trip per call, not one per element)
-template <typename Src, typename Dst>
-__device__ __forceinline__ void batched_copy(uint32_t n, Src src, Dst dst) {
-    constexpr int kB = 8;
-    for (uint32_t base = 0; base < n; base += kB * blockDim.x) {
-        double2 v[kB];
-#pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const uint32_t i = base + r * blockDim.x + threadIdx.x;
-            if (i < n) v[r] = src(i);
-        }
-#pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const uint32_t i = base + r * blockDim.x + threadIdx.x;
-            if (i < n) dst(i, v[r]);
-        }
-    }
-}
 
 // Warp FFTs of one length-G row held in registers: lane l holds elements l + 32 q (q < PPL).
 // DIF forward (e^{-}): natural-order input, bit-reversed-order output; DIT inverse (e^{+}):
@@ -1263,7 +1264,7 @@ std::shared_ptr<CircPlan> circ_analyze(const wbx_op* op, uint32_t ndim, const ui
     if (covered != ci.size()) return no("nonzeros outside the representative orbits' rows");
     if (P->nRo == 0) return no("empty operator");
     // the representative rows and twiddles are staged in shared memory by circ_lanczos_kernel
-    if (eoff.size() * 4 + P->h_eval.size() * 12 + (g0 + g1) * 16 > 40u * 1024u)
+    if (eoff.size() * 4 + P->h_eval.size() * 12 + (g0 + g1) * 16 + 4 * P->nRo * nCo * 16 > 96u * 1024u)
         return no("representative rows too long for shared memory");
     P->h_eoff = std::move(eoff);
     // overflow safety of 4 unnormalised power steps: |M^_f| <= (sum |val|)^2 max(P^-1) is
@@ -1383,7 +1384,7 @@ void circ_upload(CircPlan& P, cudaStream_t st) {
     P.rorb.alloc(P.h_rorb.size());
     P.rorb.upload(P.h_rorb.data(), P.h_rorb.size(), st);
     WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(circ_gram_kernel),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     if (P.fista_ok)
         for (const bool track : {false, true}) {
             const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
@@ -1407,9 +1408,9 @@ uint64_t circ_gram_doubles(const CircPlan& P) { return 2ull * P.h_fhalf.size() *
 void circ_gram_launch(wbx_ctx* ctx, const CircPlan& P, double2* gram, cudaStream_t st) {
     const uint32_t nh = static_cast<uint32_t>(P.h_fhalf.size());
     const uint32_t nent = static_cast<uint32_t>(P.h_eval.size());
-    const size_t smem = (P.g0 + P.g1) * sizeof(double2) + nent * (sizeof(double) + sizeof(uint32_t)) +
-                        (P.nRo * P.nCo + 1) * sizeof(uint32_t);
-    circ_gram_kernel<<<(nh + 2 * kCircWarps - 1) / (2 * kCircWarps), kCircWarps * 32, smem, st>>>(
+    const size_t smem = kGramWarps * P.nRo * P.nCo * sizeof(double2) + (P.g0 + P.g1) * sizeof(double2) +
+                        nent * (sizeof(double) + sizeof(uint32_t)) + (P.nRo * P.nCo + 1) * sizeof(uint32_t);
+    circ_gram_kernel<<<(nh + kGramWarps - 1) / kGramWarps, kGramWarps * 32, smem, st>>>(
         nh, P.fhalf.p, P.g1, P.g0, P.nRo, P.nCo, P.eoff.p, P.eh.p, P.eval.p, P.tw0.p, P.tw1.p, gram, nent);
     count_launch(ctx);
 }
@@ -1504,7 +1505,8 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
 }
 
 void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, double step_safety, double* work,
-                     double2* gram, double* out, cudaStream_t st) {
+                     double2* gram, double* out, cudaStream_t st, cudaStream_t aux, cudaEvent_t ev_fork,
+                     cudaEvent_t ev_join) {
     const uint32_t nh = static_cast<uint32_t>(P.h_fhalf.size());
     double* norm_part = work;
     double2* t1 = reinterpret_cast<double2*>(work + kCircNormBlocks);
@@ -1514,12 +1516,17 @@ void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, dou
     int* mom_e = reinterpret_cast<int*>(mom_m + static_cast<uint64_t>(kCircMoments) * nh);
     double* S = reinterpret_cast<double*>(mom_e) + (static_cast<uint64_t>(kCircMoments) * nh + 1) / 2;
     int* X = reinterpret_cast<int*>(S + kCircMoments);
+    // G_f (operator only) on the aux stream, beside |v0|^2 and v0's transform (start vector only)
+    WBX_CUDA(cudaEventRecord(ev_fork, st));
+    WBX_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
+    circ_gram_launch(ctx, P, gram, aux);
+    WBX_CUDA(cudaEventRecord(ev_join, aux));
     circ_norm_kernel<<<kCircNormBlocks, 256, 0, st>>>(P.n, norm_part);
     const unsigned th1 = std::min<uint32_t>(1024, ((P.g1 + 31) / 32) * 32);
     circ_dft1_kernel<<<dim3(P.g0, P.nCo), th1, P.g1 * sizeof(double), st>>>(P.orb.p, P.g0, P.g1, P.tw1.p, t1);
     const unsigned th0 = std::min<uint32_t>(1024, ((P.g0 + 31) / 32) * 32);
     circ_dft0_kernel<<<dim3(P.g1, P.nCo), th0, P.g0 * sizeof(double2), st>>>(P.nCo, P.g0, P.g1, P.tw0.p, t1, vh);
-    circ_gram_launch(ctx, P, gram, st);
+    WBX_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
     circ_lanczos_kernel<<<(nh + 2 * kCircWarps - 1) / (2 * kCircWarps), kCircWarps * 32, 0, st>>>(
         nh, P.fhalf.p, P.nCo, gram, isp_dev, vh, tri);
     const unsigned pb = (nh + 31) / 32;  // one warp per SM: the steps are a dependent chain

@@ -270,7 +270,8 @@ bool circ_check_p(const CircPlan& p, const double* p_full, std::vector<double>& 
 void circ_upload(CircPlan& p, cudaStream_t st);
 uint64_t circ_work_doubles(const CircPlan& p);
 void circ_tau_launch(wbx_ctx* ctx, const CircPlan& p, const double* isp_dev, double step_safety, double* work,
-                     double2* gram, double* out, cudaStream_t st);
+                     double2* gram, double* out, cudaStream_t st, cudaStream_t aux, cudaEvent_t ev_fork,
+                     cudaEvent_t ev_join);
 uint64_t circ_gram_doubles(const CircPlan& p);
 void circ_gram_launch(wbx_ctx* ctx, const CircPlan& p, double2* gram, cudaStream_t st);
 // the spectral FISTA engine (fp64 iterations, gradient in the Fourier domain of the group)

@@ -2161,6 +2161,8 @@ struct wbx_solver {
     // iterations + synthesize (+ clamp) for the last (u0, u, clamp) pointers
     cudaGraphExec_t g_tau = nullptr, g_rest = nullptr, g_an = nullptr;  // g_an: analyze (side stream)
     cudaEvent_t ev_an = nullptr;  // the analysis of the input is done (side stream -> main stream)
+    cudaStream_t aux_stream = nullptr;  // fork / join inside the step estimate (G_f beside v0's transform)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     const double* g_an_u0 = nullptr;
     uint64_t g_an_launches = 0;
     double* g_u = nullptr;
@@ -2338,7 +2340,7 @@ void run_tau(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t 
         set_tau_kernel<<<1, 1, 0, st>>>(s->out.p, s->cfg.tau);
     } else if (s->tau_circ) {  // translation-invariant operator: block-Fourier power iteration
         circ_tau_launch(ctx, *s->circ, s->circ_isp.p, s->cfg.step_safety, s->circ_work.p, s->circ_gram.p, s->out.p,
-                        st);
+                        st, s->aux_stream, s->ev_fork, s->ev_join);
         return;
     } else if (s->win && !s->tau_stream_lz) {
         const void* k = tau_win_fn(s->win_dict, s->tau_win64, s->tau_lanczos, s->win_lists_global);
@@ -2741,6 +2743,9 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
     WBX_CUDA(cudaEventCreate(&s->ev_it0));
     WBX_CUDA(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
     WBX_CUDA(cudaEventCreateWithFlags(&s->ev_an, cudaEventDisableTiming));
+    WBX_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    WBX_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    WBX_CUDA(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking));
     WBX_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     WBX_CUDA(cudaStreamSynchronize(st));
 }
@@ -2859,6 +2864,9 @@ void solver_free(wbx_solver* s) {
     if (s->ev_it0) cudaEventDestroy(s->ev_it0);
     if (s->ev_in) cudaEventDestroy(s->ev_in);
     if (s->ev_an) cudaEventDestroy(s->ev_an);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->aux_stream) cudaStreamDestroy(s->aux_stream);
     if (s->g_an) cudaGraphExecDestroy(s->g_an);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     if (s->g_tau) cudaGraphExecDestroy(s->g_tau);
