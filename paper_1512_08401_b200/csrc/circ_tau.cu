@@ -33,16 +33,20 @@
 // moments: only the half spectrum is evaluated (2050 of 4096 frequencies at C2).
 //
 // Device work per estimate (7 launches, all image-independent, in the step-estimate graph):
+//   circ_gram_kernel     (forked stream) G_f = Theta^_f^H Theta^_f per frequency from the
+//                        representative rows staged in shared memory: lanes over (row, orbit) pairs
+//                        for Theta^_f, then over (i, j) for G_f (also the spectral FISTA's blocks)
 //   circ_norm_kernel     |v0|^2 over all n (one log per Box-Muller pair; block partials)
 //   circ_dft1/0_kernel   v^ on the column orbits (separable DFT, twiddle tables)
-//   circ_lanczos_kernel  half a warp per frequency: M^_f from the representative rows (staged in
-//                        shared memory); Lanczos with full reorthogonalisation -> the real
-//                        tridiagonal T_f (<= nCo steps, exact: the Krylov space is the block's)
+//   circ_lanczos_kernel  half a warp per frequency: M^_f = D G_f D; Lanczos with full
+//                        reorthogonalisation -> the real tridiagonal T_f (<= nCo steps, exact:
+//                        the Krylov space is the block's)
 //   circ_power_kernel    one thread per frequency: the 201 power steps on T_f (5 fma per row
 //                        instead of a dense complex matvec), exact power-of-two rescaling, the
 //                        402 moments
-//   circ_reduce_kernel   per moment, the sum over frequencies with a common exponent (fixed order)
-//   circ_final_kernel    lambda_it for every it in parallel, the reference's stopping rule, tau
+//   circ_reduce_kernel   per moment, the sum over frequencies with a common exponent (fixed
+//                        order); its last block evaluates lambda_it for every it in parallel, the
+//                        reference's stopping rule and tau (circ_final_body)
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -479,8 +483,14 @@ __global__ void __launch_bounds__(32) circ_power_kernel(uint32_t nhalf, const do
 
 // Moment p summed over the half spectrum (fixed order): common exponent X = max(e + ilogb(m)),
 // S = sum of m 2^(e - X); block p, threads strided over the frequencies, fixed tree.
+__device__ void circ_final_body(uint32_t NG, const double* Sg, const int* Xg, const double* norm_part,
+                                int norm_blocks, double step_safety, double* out);
+
+// (the last block to finish then evaluates the lambda sequence: circ_final_body)
 __global__ void __launch_bounds__(256) circ_reduce_kernel(uint32_t nhalf, const double* __restrict__ mom_m,
-                                                          const int* __restrict__ mom_e, double* S, int* X) {
+                                                          const int* __restrict__ mom_e, double* S, int* X,
+                                                          unsigned* done, uint32_t NG, const double* norm_part,
+                                                          int norm_blocks, double step_safety, double* out) {
     __shared__ double rs[256];
     __shared__ int rx[256];
     const int p = blockIdx.x, t = threadIdx.x;
@@ -506,16 +516,23 @@ __global__ void __launch_bounds__(256) circ_reduce_kernel(uint32_t nhalf, const 
         if (t < k) rs[t] += rs[t + k];
         __syncthreads();
     }
+    __shared__ bool last;
     if (t == 0) {
         S[p] = rs[0];
         X[p] = x == INT_MIN ? 0 : x;
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
     }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    circ_final_body(NG, S, X, norm_part, norm_blocks, step_safety, out);
+    if (t == 0) *done = 0;  // for the next estimate (graph replays)
 }
 
 // lambda_it for every it from the moments, the reference's stopping rule, tau
-__global__ void __launch_bounds__(256) circ_final_kernel(uint32_t NG, const double* __restrict__ Sg,
-                                                         const int* __restrict__ Xg, const double* norm_part,
-                                                         int norm_blocks, double step_safety, double* out) {
+__device__ void circ_final_body(uint32_t NG, const double* Sg, const int* Xg, const double* norm_part,
+                                int norm_blocks, double step_safety, double* out) {
     __shared__ double S[kCircMoments];
     __shared__ int X[kCircMoments];
     __shared__ double lam[200];
@@ -524,8 +541,8 @@ __global__ void __launch_bounds__(256) circ_final_kernel(uint32_t NG, const doub
     const int t = threadIdx.x;
     if (t == 0) first_stop = 1 << 30;
     for (int p = t; p < kCircMoments; p += 256) {
-        S[p] = Sg[p];
-        X[p] = Xg[p];
+        S[p] = __ldcg(Sg + p);
+        X[p] = __ldcg(Xg + p);
     }
     __shared__ double red[256];
     double s = 0.0;
@@ -1399,7 +1416,8 @@ uint64_t circ_work_doubles(const CircPlan& P) {
     const uint64_t nh = P.h_fhalf.size();
     return kCircNormBlocks + 4ull * P.nCo * P.NG /* t1, vh */ + (2 * kCircMaxCo + 2) * nh /* T_f */ +
            kCircMoments * nh /* mom_m */ +
-           (kCircMoments * nh + 1) / 2 /* mom_e */ + kCircMoments /* S */ + (kCircMoments + 1) / 2 /* X */ + 16;
+           (kCircMoments * nh + 1) / 2 /* mom_e */ + kCircMoments /* S */ + (kCircMoments + 1) / 2 /* X */ +
+           16 /* done counter (zeroed at allocation, reset by its last block) */;
 }
 
 // Enqueue the estimate; writes out[OUT_TAU], out[OUT_TAU_ITERS], out[OUT_LAMBDA_MAX], out[OUT_TAU_STEPS].
@@ -1538,9 +1556,10 @@ void circ_tau_launch(wbx_ctx* ctx, const CircPlan& P, const double* isp_dev, dou
         circ_power_kernel<12><<<pb, 32, 0, st>>>(nh, tri, mom_m, mom_e);
     else
         circ_power_kernel<16><<<pb, 32, 0, st>>>(nh, tri, mom_m, mom_e);
-    circ_reduce_kernel<<<kCircMoments, 256, 0, st>>>(nh, mom_m, mom_e, S, X);
-    circ_final_kernel<<<1, 256, 0, st>>>(P.NG, S, X, norm_part, kCircNormBlocks, step_safety, out);
-    count_launch(ctx, 7);  // + circ_gram_kernel
+    unsigned* done = reinterpret_cast<unsigned*>(X + kCircMoments);
+    circ_reduce_kernel<<<kCircMoments, 256, 0, st>>>(nh, mom_m, mom_e, S, X, done, P.NG, norm_part, kCircNormBlocks,
+                                                     step_safety, out);
+    count_launch(ctx, 6);  // + circ_gram_kernel
     WBX_CUDA(cudaGetLastError());
 }
 

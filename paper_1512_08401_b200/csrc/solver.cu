@@ -2639,7 +2639,10 @@ void solver_update(wbx_solver* s, const double* p, const double* w, double lambd
         s->tau_circ = circ_check_p(*s->circ, p, isp, &why);
         if (s->tau_circ) {
             s->circ_isp.upload(isp, s->ctx->stream);
-            if (!s->circ_work.p) s->circ_work.alloc(circ_work_doubles(*s->circ));
+            if (!s->circ_work.p) {
+                s->circ_work.alloc(circ_work_doubles(*s->circ));
+                WBX_CUDA(cudaMemsetAsync(s->circ_work.p, 0, s->circ_work.bytes(), s->ctx->stream));
+            }
         }
         if (was != s->tau_circ && s->g_tau) {  // the step-estimate graph changes
             cudaGraphExecDestroy(s->g_tau);
@@ -2691,6 +2694,7 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
         if (plan_ok && tau_on && circ_check_p(*plan, p, isp, &why)) {
             s->circ_isp.upload(isp, st);
             s->circ_work.alloc(circ_work_doubles(*plan));
+            WBX_CUDA(cudaMemsetAsync(s->circ_work.p, 0, s->circ_work.bytes(), st));
             s->tau_circ = true;
         }
         // the spectral FISTA engine: single-image solves, with energy / support tracking too (solves
@@ -2699,10 +2703,11 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
         const char* eng = std::getenv("WBX_ENGINE");
         const bool track_cfg = s->cfg.track_energy || s->cfg.track_support;
         if (!eng && !std::getenv("WBX_STENCIL") && s->batch == 1 && !std::isfinite(s->cfg.ref_energy) &&
+            !(track_cfg && s->cfg.max_iters == 0) &&  // (E(x0) alone: the window track kernel)
             circ_fista_ok(*plan, &fwhy) && static_cast<uint32_t>(s->ctx->num_sms) > circ_fista_blocks(*plan)) {
             s->circ_T.alloc(circ_exchange_doubles(*plan) / 2);
             s->circ_counter.alloc(1);
-            if (track_cfg && s->cfg.max_iters > 0)
+            if (track_cfg)
                 s->circ_track.alloc(circ_track_doubles(*plan, static_cast<int>(s->cfg.max_iters), s->ctx->num_sms));
             s->fista_circ = true;
         }
@@ -3171,7 +3176,7 @@ int wbx_solver_kernels(const wbx_solver* s, char* buf, uint64_t len) {
                       : s->win        ? (s->tau_lanczos ? "tau_lanczos_win_kernel" : "tau_win_kernel")
                       : (!fp64 && s->tau_lanczos) ? "tau_lanczos_kernel"
                                                    : (fp64 ? "tau_kernel<double>" : "tau_kernel<float>");
-    const char* it = (s->fista_circ && s->batch == 1 && !std::isfinite(s->cfg.ref_energy)) ? "circ_fista_kernel"
+    const char* it = s->fista_circ                                  ? "circ_fista_kernel"
                      : (s->stencil && !track && s->batch == 1) ? "fista_stencil_kernel"
                      : (s->win && !track && s->batch == 1) ? "fista_win_kernel"
                      : (s->win_track && track && s->batch == 1) ? "fista_win_track_kernel"
