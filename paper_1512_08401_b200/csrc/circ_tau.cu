@@ -622,6 +622,7 @@ struct CircFistaArgs {
     double2* T2;        // [nCo][h0][f1]: inverse column DFTs of G_f y^
     unsigned* counter;
     uint32_t g, lg, nRo, nCo, NB;
+    uint32_t nimg;  // images in this launch (C5 batches): NB spectral CTAs, T1/T2 and a counter per image
     int diag_skip_decoupled;  // WBX_CIRC_DIAG=nodec: time the spectral CTAs alone (wrong x)
     unsigned long long* prof;  // diagnostics build (WBX_CIRC_PROF=1): CTA 0's cycles per section
     double* outw;              // out (iteration count)
@@ -722,6 +723,38 @@ struct WarpFft {
     }
 };
 
+// The decoupled coordinates of a batch (empty Theta column: gradient exactly 0, so x' = prox(y),
+// y = x' + beta (x' - x_prev), solver.cpp:126-145, iterated in registers to the fixed point
+// x' == x_prev == 0 or the iteration count) for nimg images back to back, as its own
+// full-occupancy launch before the batch's spectral launches: the per-lane trip counts vary
+// (0-100 steps), so many resident warps per SM beat the few SMs a batch launch leaves beside
+// its spectral CTAs. Same expressions as the in-kernel pass: bitwise the single-image result.
+__global__ void __launch_bounds__(256) circ_decoupled_kernel(const double* __restrict__ x0_full,
+                                                             double* __restrict__ x_full,
+                                                             const double* __restrict__ w_full,
+                                                             const double* __restrict__ p_full,
+                                                             const uint32_t* __restrict__ isC, uint64_t n, uint32_t nimg,
+                                                             const double* __restrict__ beta64, double lambda, int K,
+                                                             const double* __restrict__ out) {
+    const double tau = out[0];
+    const uint64_t total = n * nimg, nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += nthreads) {
+        const uint64_t im = t / n, i = t - im * n;
+        if ((isC[i >> 5] >> (i & 31)) & 1u) continue;
+        const double thr = circ_thr(tau, lambda, w_full[i], p_full[i]);
+        double x = x0_full[t], xp = x, y = x;
+        for (int k = 1; k <= K; ++k) {
+            const double xn = circ_prox(y, thr);
+            const bool fixed = xn == 0.0 && xp == 0.0;
+            y = circ_momentum(xn, xp, beta64[k - 1]);
+            xp = xn;
+            x = xn;
+            if (fixed) break;
+        }
+        x_full[t] = x;
+    }
+}
+
 template <int G>
 __device__ __forceinline__ int brev_g(int i) {
     return static_cast<int>(__brev(static_cast<unsigned>(i)) >> (32 - __builtin_ctz(G)));
@@ -796,12 +829,13 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         }
         return;
     }
-    if (blockIdx.x >= a.NB) {
+    const uint32_t NBS = a.NB * a.nimg;  // spectral CTAs: NB per image of the launch
+    if (blockIdx.x >= NBS) {  // (single-image launches; batch launches run circ_decoupled_kernel first)
         if (a.diag_skip_decoupled) return;
         // decoupled coordinates (gradient exactly 0): x' = prox(y), y = x' + beta (x' - x_prev),
         // iterated in registers to the fixed point x' == x_prev == 0 or the iteration count
-        const uint64_t nthreads = static_cast<uint64_t>(gridDim.x - a.NB) * blockDim.x;
-        for (uint64_t i = static_cast<uint64_t>(blockIdx.x - a.NB) * blockDim.x + threadIdx.x; i < a.n; i += nthreads) {
+        const uint64_t nthreads = static_cast<uint64_t>(gridDim.x - NBS) * blockDim.x;
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x - NBS) * blockDim.x + threadIdx.x; i < a.n; i += nthreads) {
             if ((a.isC[i >> 5] >> (i & 31)) & 1u) continue;
             const double thr = circ_thr(tau, a.lambda, a.w_full[i], a.p_full[i]);
             double x = a.x0_full[i], xp = x, y = x;
@@ -817,7 +851,17 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         }
         return;
     }
-    const int nc = static_cast<int>(a.nCo), c = blockIdx.x, lane = threadIdx.x & 31, wj = threadIdx.x >> 5;
+    {  // this CTA's image: its coordinates, exchange buffers and barrier counter
+        const uint32_t im = blockIdx.x / a.NB;
+        const uint64_t ex = 2ull * a.nCo * a.g * a.g;
+        a.x0_full += static_cast<uint64_t>(im) * a.n;
+        a.x_full += static_cast<uint64_t>(im) * a.n;
+        a.T1 += im * ex;
+        a.T2 += im * ex;
+        a.counter += 32u * im;
+    }
+    const int nc = static_cast<int>(a.nCo), c = static_cast<int>(blockIdx.x % a.NB), lane = threadIdx.x & 31,
+              wj = threadIdx.x >> 5;
     const bool row_live = wj < nc;  // warp-uniform (lanes >= G of a G = 16 row idle in the shuffles)
     const bool lane_live = lane < G;
     constexpr int GS = NCP + 1;  // padded G block rows
@@ -1436,6 +1480,13 @@ void circ_gram_launch(wbx_ctx* ctx, const CircPlan& P, double2* gram, cudaStream
 // The spectral FISTA engine's exchange buffers T1, T2 (2 x nCo x NG complex)
 uint64_t circ_exchange_doubles(const CircPlan& P) { return 4ull * P.nCo * P.NG; }
 uint32_t circ_fista_blocks(const CircPlan& P) { return P.g0; }
+uint32_t circ_fista_slots(const CircPlan& P, int num_sms, uint32_t batch) {
+    // batch launches run no decoupled CTAs (circ_decoupled_kernel takes those coordinates), so
+    // every SM can hold a spectral CTA; WBX_CIRC_SLOTS caps the count
+    uint32_t slots = std::max(1u, std::min(batch, static_cast<uint32_t>(num_sms) / P.g0));
+    if (const char* e = std::getenv("WBX_CIRC_SLOTS")) slots = std::max(1u, std::min(slots, static_cast<uint32_t>(std::atoi(e))));
+    return slots;
+}
 
 
 // tracking work (doubles): q [K+1][NB], r and s [K][NB], decoupled sums [2][K][nwd], e0 [2][nwd]
@@ -1449,6 +1500,7 @@ uint64_t circ_track_doubles(const CircPlan& P, int K, int num_sms) {
 void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, const double2* gram, double2* T,
                        unsigned* counter, cudaStream_t st) {
     CircFistaArgs a{};
+    const bool track = pr.track_work != nullptr;
     a.x0_full = pr.x0_full;
     a.w_full = pr.w_full;
     a.p_full = pr.p_full;
@@ -1475,8 +1527,11 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     a.nRo = P.nRo;
     a.nCo = P.nCo;
     a.NB = P.g0;
+    a.nimg = pr.nimg;
+    if (pr.nimg < 1 || (track && pr.nimg != 1) || static_cast<uint64_t>(pr.nimg) * P.g0 > static_cast<uint64_t>(ctx->num_sms) ||
+        (pr.nimg == 1 && P.g0 >= static_cast<uint32_t>(ctx->num_sms)))
+        fail(WBX_BAD_SPEC, "spectral FISTA: images per launch exceed the grid");
     a.diag_skip_decoupled = std::getenv("WBX_CIRC_DIAG") && std::string(std::getenv("WBX_CIRC_DIAG")) == "nodec";
-    const bool track = pr.track_work != nullptr;
     const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
     if (!k.fn) fail(WBX_BAD_SPEC, "spectral FISTA: unsupported group size");
     a.outw = const_cast<double*>(pr.out);
@@ -1498,10 +1553,19 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     WBX_CUDA(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
     a.prof = prof;
 #endif
-    WBX_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    WBX_CUDA(cudaMemsetAsync(counter, 0, 32u * pr.nimg * sizeof(unsigned), st));
     void* params[] = {&a};
-    // one CTA per SM: g spectral CTAs, the rest run the decoupled coordinates
-    WBX_CUDA(cudaLaunchCooperativeKernel(k.fn, dim3(ctx->num_sms), dim3(32 * k.warps), params, k.smem, st));
+    // one CTA per SM: a single image's launch runs g spectral CTAs and, on the other SMs, its
+    // decoupled coordinates; a batch launch runs nimg x g spectral CTAs after the decoupled
+    // coordinates of its images in their own launch
+    uint32_t grid = static_cast<uint32_t>(ctx->num_sms);
+    if (pr.nimg > 1) {
+        circ_decoupled_kernel<<<8 * ctx->num_sms, 256, 0, st>>>(pr.x0_full, pr.x_full, pr.w_full, pr.p_full, pr.isC, P.n,
+                                                              pr.nimg, pr.beta64, pr.lambda, pr.K, pr.out);
+        count_launch(ctx);
+        grid = pr.nimg * P.g0;
+    }
+    WBX_CUDA(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(32 * k.warps), params, k.smem, st));
     count_launch(ctx);
     WBX_CUDA(cudaGetLastError());
     if (track) {

@@ -289,7 +289,13 @@ struct CircProblem {
     double* track_work = nullptr;
     double* energies = nullptr;
     unsigned long long* supports = nullptr;
+    // images in this launch (C5 batches, untracked): x0_full / x_full hold nimg images back to
+    // back, T nimg exchange buffers (circ_exchange_doubles each), counter 32 words per image
+    uint32_t nimg = 1;
 };
+// images of a batch the spectral engine solves in one launch (NB spectral CTAs per image, the
+// rest of the SMs for the decoupled coordinates)
+uint32_t circ_fista_slots(const CircPlan& p, int num_sms, uint32_t batch);
 bool circ_fista_ok(const CircPlan& p, std::string* why);
 uint64_t circ_track_doubles(const CircPlan& p, int K, int num_sms);
 uint64_t circ_exchange_doubles(const CircPlan& p);

@@ -2150,6 +2150,7 @@ struct wbx_solver {
     wbx::DevBuf<double2> circ_gram, circ_T;
     wbx::DevBuf<double> circ_track;  // tracked spectral solves: per-CTA / per-warp energy partials
     wbx::DevBuf<unsigned> circ_counter;
+    uint32_t circ_slots = 1;  // batch images per spectral launch (circ_fista_slots)
     wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_it0 = nullptr, ev_in = nullptr;
@@ -2359,7 +2360,7 @@ template <typename T>
 void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_t st) {
     SolveArgs a = make_args<T>(s, x0_full, x_full);
     wbx_ctx* ctx = s->ctx;
-    if (s->fista_circ && s->batch == 1 && !a.stop_on_ref) {  // spectral engine (translation-invariant operator)
+    if (s->fista_circ && !a.stop_on_ref) {  // spectral engine (translation-invariant operator)
         if (!s->tau_circ || s->cfg.tau > 0.0) circ_gram_launch(ctx, *s->circ, s->circ_gram.p, st);
         CircProblem pr{a.x0_full, a.w_full, a.p_full, a.x_full, a.isC, a.beta64, a.lambda, a.max_iters, a.out};
         if (a.track) {  // energies / supports of every iterate (solver.cpp:130-137)
@@ -2367,7 +2368,14 @@ void run_iters(wbx_solver* s, const double* x0_full, double* x_full, cudaStream_
             pr.energies = s->energies.p;
             pr.supports = s->supports.p;
         }
-        circ_fista_launch(ctx, *s->circ, pr, s->circ_gram.p, s->circ_T.p, s->circ_counter.p, st);
+        // a batch (C5): circ_slots images per launch, images back to back in x0_full / x_full
+        const uint32_t B = static_cast<uint32_t>(s->batch);
+        for (uint32_t b0 = 0; b0 < B; b0 += s->circ_slots) {
+            pr.nimg = std::min(s->circ_slots, B - b0);
+            pr.x0_full = x0_full + static_cast<uint64_t>(b0) * s->n;
+            pr.x_full = x_full + static_cast<uint64_t>(b0) * s->n;
+            circ_fista_launch(ctx, *s->circ, pr, s->circ_gram.p, s->circ_T.p, s->circ_counter.p, st);
+        }
         return;
     }
     if (s->stencil && !a.track && s->batch == 1) {
@@ -2702,11 +2710,13 @@ void solver_setup(wbx_solver* s, const double* p, const double* w) {
         // WBX_STENCIL=1 select the others)
         const char* eng = std::getenv("WBX_ENGINE");
         const bool track_cfg = s->cfg.track_energy || s->cfg.track_support;
-        if (!eng && !std::getenv("WBX_STENCIL") && s->batch == 1 && !std::isfinite(s->cfg.ref_energy) &&
+        if (!eng && !std::getenv("WBX_STENCIL") && !std::isfinite(s->cfg.ref_energy) &&
             !(track_cfg && s->cfg.max_iters == 0) &&  // (E(x0) alone: the window track kernel)
             circ_fista_ok(*plan, &fwhy) && static_cast<uint32_t>(s->ctx->num_sms) > circ_fista_blocks(*plan)) {
-            s->circ_T.alloc(circ_exchange_doubles(*plan) / 2);
-            s->circ_counter.alloc(1);
+            // batches (C5, untracked): circ_slots images per launch, launches over the batch
+            s->circ_slots = circ_fista_slots(*plan, s->ctx->num_sms, static_cast<uint32_t>(s->batch));
+            s->circ_T.alloc(circ_exchange_doubles(*plan) / 2 * s->circ_slots);
+            s->circ_counter.alloc(32 * s->circ_slots);
             if (track_cfg)
                 s->circ_track.alloc(circ_track_doubles(*plan, static_cast<int>(s->cfg.max_iters), s->ctx->num_sms));
             s->fista_circ = true;

@@ -154,3 +154,51 @@ def test_dropin_fista_solver_cache_reuse(golden):
         assert rel_l2(r.x_final, ref["x_final"]) <= 1e-5
         runs.append(r.x_final)
     assert np.array_equal(runs[0], runs[3])
+
+
+@pytest.mark.parametrize("batch,slots", [(4, None), (8, None), (8, "1"), (8, "3")])
+def test_spectral_batch_bitwise_equals_single(golden, batch, slots, monkeypatch):
+    """C5 on the spectral engine: a batch solves its images `slots` per launch (NB spectral CTAs,
+    an exchange buffer and a barrier counter per image; the decoupled CTAs take every image's
+    decoupled coordinates). Each image must equal its single-image spectral solve bitwise; the
+    golden image inside the batch matches the reference's restored image."""
+    if slots:
+        monkeypatch.setenv("WBX_CIRC_SLOTS", slots)
+    from paper_1512_08401_b200 import synthetic as S
+    g = golden("c1_db4_256")
+    op, b, P = setup(g)
+    cfg = W.SolverConfig(max_iters=g.meta["iters"], track_energy=False)
+    imgs = np.stack([g["u0"].reshape(g.dims)] +
+                    [S.degrade(g.dims, 5.0, 5e-3, seed)[1] for seed in range(1, batch)])
+    single = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], cfg)
+    ref = np.stack([single.deblur(im, clamp=False)[0] for im in imgs])
+    many = W.Deblurrer(op, b, P, g.weights(), g.meta["lambda"], cfg, batch=batch)
+    assert many.kernels() == ("circ_lanczos_kernel", "circ_fista_kernel")
+    out, rep = many.deblur(imgs, clamp=False)
+    assert out.shape == (batch,) + tuple(g.dims)
+    assert np.array_equal(out, ref)
+    assert rel_l2(out[0], g["restored"]) <= 1e-11
+    assert abs(rep.tau - g.meta["tau"]) <= 1e-12 * g.meta["tau"]
+    out2, _ = many.deblur(imgs, clamp=False)
+    assert np.array_equal(out, out2)
+
+
+def test_spectral_batch8_at_1024(golden):
+    """C5 at its real size: 8 images of the C2 operator (two per launch at 64 spectral CTAs each)
+    bitwise equal to single-image spectral solves (whose parity with the reference is pinned
+    above and in test_full_size), tau the reference's."""
+    from paper_1512_08401_b200 import synthetic as S
+    g = golden("c2_db4_1024")
+    op = g.operator()
+    ctx = W.Context(0)
+    b = W.make_basis(W.FilterFamily.Daubechies, 4, (1024, 1024), 4)
+    P = W.spai(op, ctx)
+    cfg = W.SolverConfig(max_iters=100, track_energy=False)
+    imgs = np.stack([S.degrade((1024, 1024), 5.0, 5e-3, seed)[1] for seed in range(8)])
+    single = W.Deblurrer(op, b, P, g.weights(), 1e-4, cfg, ctx)
+    ref = np.stack([single.deblur(im, clamp=True)[0] for im in imgs])
+    many = W.Deblurrer(op, b, P, g.weights(), 1e-4, cfg, ctx, batch=8)
+    assert many.kernels() == ("circ_lanczos_kernel", "circ_fista_kernel")
+    out, rep = many.deblur(imgs, clamp=True)
+    assert np.array_equal(out, ref)
+    assert abs(rep.tau - g.meta["tau"]) <= 1e-12 * g.meta["tau"]
