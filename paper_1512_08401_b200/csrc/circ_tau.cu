@@ -1144,6 +1144,235 @@ size_t circ_fista_smem() {
     return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + 2 * NCP * G * 16 + G * 16 + 6 * NCP * G * 8;
 }
 
+// M images per spectral CTA (C5 batches, untracked): the G_f block rows live in registers
+// after the prologue, so the shared memory that staged them holds the state of M images (X, Y,
+// y, x_prev, b each) and one grid barrier per phase serves all M. CTA (slot s, column c) owns
+// images s M .. s M + M - 1 of the launch; each warp's rows of all M images are fetched with
+// cp.async before the first transform, so a phase pays one L2 round trip, not M. Per image the
+// arithmetic is circ_fista_kernel's in the same order: bitwise its single-image result. The
+// decoupled coordinates run in circ_decoupled_kernel before the launch.
+template <int G, int NCP, int M>
+__host__ __device__ constexpr size_t circ_multi_image_bytes() {  // X, Y (complex) + y, x_prev, b
+    return static_cast<size_t>(NCP) * G * (2 * 16 + 3 * 8);
+}
+template <int G, int NCP, int M>
+__host__ __device__ constexpr size_t circ_multi_state_bytes() {
+    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 > M * circ_multi_image_bytes<G, NCP, M>()
+               ? static_cast<size_t>(G) * NCP * (NCP + 1) * 16
+               : M * circ_multi_image_bytes<G, NCP, M>();
+}
+template <int G, int NCP, int M>
+size_t circ_multi_smem() {  // state (aliasing the G_f staging) + twiddles + tau / p + thresholds
+    return circ_multi_state_bytes<G, NCP, M>() + G * 16 + 2 * NCP * G * 8;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int G, int NCP, int M>
+__global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFistaArgs a) {
+    using F = WarpFft<G>;
+    constexpr int PPL = F::PPL;
+    const double tau = a.out[0];
+    const uint32_t slots = a.nimg / M;
+    if (blockIdx.x >= a.NB * slots) return;
+    const uint32_t slot = blockIdx.x / a.NB;
+    const int nc = static_cast<int>(a.nCo), c = static_cast<int>(blockIdx.x % a.NB), lane = threadIdx.x & 31,
+              wj = threadIdx.x >> 5;
+    const bool row_live = wj < nc;
+    const bool lane_live = lane < G;
+    const uint64_t ex = 2ull * a.nCo * a.g * a.g;  // T1, T2 per image
+    unsigned* const counter = a.counter + 32u * slot;
+    constexpr int GS = NCP + 1;
+    constexpr size_t kImg = circ_multi_image_bytes<G, NCP, M>();
+    extern __shared__ double2 circ_smem[];
+    unsigned char* const sbase = reinterpret_cast<unsigned char*>(circ_smem);
+    double2* Gs = circ_smem;  // prologue only; then the images' state
+    double2* tw = reinterpret_cast<double2*>(sbase + circ_multi_state_bytes<G, NCP, M>());
+    double* ps = reinterpret_cast<double*>(tw + G);  // tau / p (the images share P, w, lambda, tau)
+    double* ths = ps + NCP * G;
+    auto Xm = [&](int m) { return reinterpret_cast<double2*>(sbase + m * kImg); };
+    auto Ym = [&](int m) { return Xm(m) + NCP * G; };
+    auto ysm = [&](int m) { return reinterpret_cast<double*>(Ym(m) + NCP * G); };
+    auto xpm = [&](int m) { return ysm(m) + NCP * G; };
+    auto bsm = [&](int m) { return xpm(m) + NCP * G; };
+    auto img = [&](int m) { return static_cast<uint64_t>(slot) * M + m; };
+    for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
+    batched_copy(
+        G * NCP * NCP,
+        [&](uint32_t i) {
+            const int pos = i / (NCP * NCP), e = i % (NCP * NCP), ii = e / NCP, j = e % NCP;
+            if (ii >= nc || j >= nc) return make_double2(0.0, 0.0);
+            const int h = a.hidx[brev_g<G>(pos) * G + c];
+            const double2 v = a.gram[static_cast<uint64_t>(h >= 0 ? h : -1 - h) * nc * nc + ii * nc + j];
+            return h >= 0 ? v : make_double2(v.x, -v.y);
+        },
+        [&](uint32_t i, double2 v) {
+            const int pos = i / (NCP * NCP), e = i % (NCP * NCP);
+            Gs[(pos * NCP + e / NCP) * GS + e % NCP] = v;
+        });
+    constexpr int kOut = (G * NCP + 32 * NCP * 2 - 1) / (32 * NCP * 2);
+    static_assert(kOut == 1, "one round of two block-product outputs per thread");
+    const int t0 = threadIdx.x, t1 = threadIdx.x + blockDim.x;
+    const bool one = t0 < G * NCP, two = t1 < G * NCP;
+    const int pos0 = one ? t0 / NCP : 0, ii0 = one ? t0 % NCP : 0;
+    const int pos1 = two ? t1 / NCP : pos0, ii1 = two ? t1 % NCP : ii0;
+    __syncthreads();
+    double2 g0r[NCP], g1r[NCP];
+#pragma unroll
+    for (int j = 0; j < NCP; ++j) {
+        g0r[j] = Gs[(pos0 * NCP + ii0) * GS + j];
+        g1r[j] = Gs[(pos1 * NCP + ii1) * GS + j];
+    }
+    __syncthreads();  // the staging is dead: the images' state takes its place
+    for (int m = 0; m < M; ++m)
+        for (int i = threadIdx.x; i < 2 * NCP * G; i += blockDim.x) Xm(m)[i] = make_double2(0.0, 0.0);  // X, Y
+    for (int i = threadIdx.x; i < NCP * G; i += blockDim.x) {  // own row: p, thr; per image y = x_prev = x0, b
+        const int j = i / G, h1 = i % G;
+        if (j >= nc) {
+            ths[i] = 0.0;
+            ps[i] = 1.0;
+            for (int m = 0; m < M; ++m) ysm(m)[i] = xpm(m)[i] = bsm(m)[i] = 0.0;
+            continue;
+        }
+        const CircOrbit o = a.corb[j];
+        const uint64_t fl = static_cast<uint64_t>(o.off) + static_cast<uint64_t>(o.a0 + o.s0 * c) * o.W + o.a1 + o.s1 * h1;
+        const double p = a.p_full[fl];
+        ps[i] = tau / p;
+        ths[i] = circ_thr(tau, a.lambda, a.w_full[fl], p);
+        for (int m = 0; m < M; ++m) {
+            const double* x0 = a.x0_full + img(m) * a.n;
+            ysm(m)[i] = x0[fl];
+            xpm(m)[i] = x0[fl];
+            double b = 0.0;  // b_j[c][h1], as circ_fista_kernel
+            for (uint32_t r = 0; r < a.nRo; ++r) {
+                const CircOrbit ro = a.rorb[r];
+                for (uint32_t e = a.eoff[r * nc + j]; e < a.eoff[r * nc + j + 1]; ++e) {
+                    const uint32_t h = a.eh[e];
+                    const uint32_t q0 = (c + G - (h >> 16)) & (G - 1), q1 = (h1 + G - (h & 0xffffu)) & (G - 1);
+                    const uint64_t rf = static_cast<uint64_t>(ro.off) + static_cast<uint64_t>(ro.a0 + ro.s0 * q0) * ro.W +
+                                        ro.a1 + ro.s1 * q1;
+                    b = fma(a.eval[e], x0[rf], b);
+                }
+            }
+            bsm(m)[i] = b;
+        }
+    }
+    __syncthreads();
+    const double inv_ng = 1.0 / (static_cast<double>(G) * G);
+    unsigned bar = 0;
+    auto row_forward = [&](int m) {  // row DFT of this warp's row of image m's y -> its T1[j][f1][c]
+        double2 v[PPL];
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) v[q] = make_double2(lane_live ? ysm(m)[wj * G + lane + 32 * q] : 0.0, 0.0);
+        F::forward(v, tw);
+        double2* T1 = a.T1 + img(m) * ex;
+        if (lane_live)
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) T1[(static_cast<uint64_t>(wj) * G + brev_g<G>(lane + 32 * q)) * G + c] = v[q];
+    };
+    if (a.K > 0 && row_live)
+        for (int m = 0; m < M; ++m) row_forward(m);
+    for (int k = 1; k <= a.K; ++k) {
+        circ_barrier(counter, ++bar * a.NB);
+        // column phase: each image's rows at column c, fetched into Y, transformed into X
+        if (row_live) {
+            if (lane_live)
+                for (int m = 0; m < M; ++m)
+#pragma unroll
+                    for (int q = 0; q < PPL; ++q)
+                        cp_async16(Ym(m) + wj * G + lane + 32 * q,
+                                   a.T1 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            for (int m = 0; m < M; ++m) {
+                double2 v[PPL];
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+                F::forward(v, tw);
+                if (lane_live)
+#pragma unroll
+                    for (int q = 0; q < PPL; ++q) Xm(m)[wj * G + lane + 32 * q] = v[q];
+            }
+        }
+        __syncthreads();
+        for (int m = 0; m < M; ++m) {  // Y = G_f X per image, the block rows from registers
+            const double2* X = Xm(m);
+            double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NCP; ++j) {
+                const double2 mm = g0r[j], x = X[j * G + pos0], n = g1r[j], y = X[j * G + pos1];
+                r0 = fma(mm.x, x.x, fma(-mm.y, x.y, r0));
+                i0 = fma(mm.x, x.y, fma(mm.y, x.x, i0));
+                r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
+                i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
+            }
+            if (one) Ym(m)[ii0 * G + pos0] = make_double2(r0, i0);
+            if (two) Ym(m)[ii1 * G + pos1] = make_double2(r1, i1);
+        }
+        __syncthreads();
+        if (row_live)
+            for (int m = 0; m < M; ++m) {  // inverse along h0 -> T2[i][h0][c]
+                double2 v[PPL];
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+                F::inverse(v, tw);
+                double2* T2 = a.T2 + img(m) * ex;
+                if (lane_live)
+#pragma unroll
+                    for (int q = 0; q < PPL; ++q) T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+            }
+        circ_barrier(counter, ++bar * a.NB);
+        // row phase: each image's row c of T2 fetched into X (contiguous), read in bit-reversed order
+        if (row_live) {
+            if (lane_live)
+                for (int m = 0; m < M; ++m)
+#pragma unroll
+                    for (int q = 0; q < PPL; ++q)
+                        cp_async16(Xm(m) + wj * G + lane + 32 * q,
+                                   a.T2 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            const double beta = a.beta64[k - 1];
+            for (int m = 0; m < M; ++m) {
+                double2 v[PPL];
+#pragma unroll
+                for (int q = 0; q < PPL; ++q)
+                    v[q] = lane_live ? Xm(m)[wj * G + brev_g<G>(lane + 32 * q)] : make_double2(0.0, 0.0);
+                F::inverse(v, tw);
+                double* ys = ysm(m);
+                double* xps = xpm(m);
+                const double* bs = bsm(m);
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    if (!lane_live) break;
+                    const int i = wj * G + lane + 32 * q;
+                    const double gy = v[q].x * inv_ng;
+                    const double grad = __dsub_rn(gy, bs[i]);
+                    const double z0 = fma(-ps[i], grad, ys[i]);
+                    const double xn = circ_prox(z0, ths[i]);
+                    ys[i] = circ_momentum(xn, xps[i], beta);
+                    xps[i] = xn;
+                }
+                __syncwarp();
+                if (k < a.K) row_forward(m);
+            }
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.outw[2] = a.K;  // OUT_ITERS_USED
+    for (int m = 0; m < M; ++m) {
+        double* x = a.x_full + img(m) * a.n;
+        for (int i = threadIdx.x; i < nc * G; i += blockDim.x) {
+            const int j = i / G, h1 = i % G;
+            const CircOrbit o = a.corb[j];
+            x[static_cast<uint64_t>(o.off) + static_cast<uint64_t>(o.a0 + o.s0 * c) * o.W + o.a1 + o.s1 * h1] = xpm(m)[i];
+        }
+    }
+}
+
 // Energies of the tracked spectral solve (run_pgd's E(x_k), solver.cpp:44-55, 118, 130): block k
 // sums the partials in a fixed order; E_k = (q_k + |x0|^2) / 2 + lambda sum w |x_k|, with
 // |Theta x - x0|^2 = x . G x - 2 x . Theta^T x0 + |x0|^2. Block 0: the initial energy.
@@ -1429,6 +1658,36 @@ FistaKernel fista_kernel_for(uint32_t g, uint32_t nc, bool track = false) {
     if (g == 64) return fista_kernel_g<64>(nc, track);
     return FistaKernel{};
 }
+// M images per CTA (batches, g = 32, 64: the groups whose images per launch are few); no
+// instance when the state does not fit the opt-in shared memory
+constexpr size_t kMaxSmem = 227 * 1024;
+template <int G, int NCP, int M>
+FistaKernel multi_kernel_of() {
+    if (circ_multi_smem<G, NCP, M>() > kMaxSmem) return FistaKernel{};
+    return FistaKernel{reinterpret_cast<const void*>(circ_fista_multi_kernel<G, NCP, M>), circ_multi_smem<G, NCP, M>(), NCP};
+}
+template <int G, int M>
+FistaKernel multi_kernel_g(uint32_t nc) {
+    if (nc <= 4) return multi_kernel_of<G, 4, M>();
+    if (nc <= 8) return multi_kernel_of<G, 8, M>();
+    if (nc <= 12) return multi_kernel_of<G, 12, M>();
+    return multi_kernel_of<G, 16, M>();
+}
+FistaKernel multi_kernel_for(uint32_t g, uint32_t nc, uint32_t m) {
+    if (g == 32) return m == 2 ? multi_kernel_g<32, 2>(nc) : m == 4 ? multi_kernel_g<32, 4>(nc) : FistaKernel{};
+    if (g == 64) return m == 2 ? multi_kernel_g<64, 2>(nc) : m == 4 ? multi_kernel_g<64, 4>(nc) : FistaKernel{};
+    return FistaKernel{};
+}
+// images per CTA for a launch of nimg images: 1 while one image per CTA fits the grid, else the
+// smallest M in {2, 4} that divides nimg and fits (0: none; WBX_CIRC_MULTI=0 turns them off)
+uint32_t multi_m(const CircPlan& P, int num_sms, uint32_t nimg) {
+    const uint32_t smax = static_cast<uint32_t>(num_sms) / P.g0;
+    if (nimg <= smax) return 1;
+    if (const char* e = std::getenv("WBX_CIRC_MULTI"); e && std::string(e) == "0") return 0;
+    for (const uint32_t m : {2u, 4u})
+        if (nimg % m == 0 && nimg / m <= smax && multi_kernel_for(P.g0, P.nCo, m).fn) return m;
+    return 0;
+}
 }  // namespace
 
 void circ_upload(CircPlan& P, cudaStream_t st) {
@@ -1446,11 +1705,15 @@ void circ_upload(CircPlan& P, cudaStream_t st) {
     P.rorb.upload(P.h_rorb.data(), P.h_rorb.size(), st);
     WBX_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(circ_gram_kernel),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    if (P.fista_ok)
+    if (P.fista_ok) {
         for (const bool track : {false, true}) {
             const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
             WBX_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
         }
+        for (const uint32_t m : {2u, 4u})
+            if (const FistaKernel k = multi_kernel_for(P.g0, P.nCo, m); k.fn)
+                WBX_CUDA(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
+    }
     WBX_CUDA(cudaStreamSynchronize(st));
     P.uploaded = true;
 }
@@ -1482,8 +1745,10 @@ uint64_t circ_exchange_doubles(const CircPlan& P) { return 4ull * P.nCo * P.NG; 
 uint32_t circ_fista_blocks(const CircPlan& P) { return P.g0; }
 uint32_t circ_fista_slots(const CircPlan& P, int num_sms, uint32_t batch) {
     // batch launches run no decoupled CTAs (circ_decoupled_kernel takes those coordinates), so
-    // every SM can hold a spectral CTA; WBX_CIRC_SLOTS caps the count
+    // every SM can hold a spectral CTA, and M images per CTA (circ_fista_multi_kernel) when one
+    // per CTA does not fit the grid; WBX_CIRC_SLOTS caps the count
     uint32_t slots = std::max(1u, std::min(batch, static_cast<uint32_t>(num_sms) / P.g0));
+    if (batch > slots && multi_m(P, num_sms, batch) > 1) slots = batch;
     if (const char* e = std::getenv("WBX_CIRC_SLOTS")) slots = std::max(1u, std::min(slots, static_cast<uint32_t>(std::atoi(e))));
     return slots;
 }
@@ -1528,11 +1793,11 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     a.nCo = P.nCo;
     a.NB = P.g0;
     a.nimg = pr.nimg;
-    if (pr.nimg < 1 || (track && pr.nimg != 1) || static_cast<uint64_t>(pr.nimg) * P.g0 > static_cast<uint64_t>(ctx->num_sms) ||
-        (pr.nimg == 1 && P.g0 >= static_cast<uint32_t>(ctx->num_sms)))
+    const uint32_t mimg = pr.nimg > 1 ? multi_m(P, ctx->num_sms, pr.nimg) : 1;  // images per CTA
+    if (pr.nimg < 1 || mimg == 0 || (track && pr.nimg != 1) || (pr.nimg == 1 && P.g0 >= static_cast<uint32_t>(ctx->num_sms)))
         fail(WBX_BAD_SPEC, "spectral FISTA: images per launch exceed the grid");
     a.diag_skip_decoupled = std::getenv("WBX_CIRC_DIAG") && std::string(std::getenv("WBX_CIRC_DIAG")) == "nodec";
-    const FistaKernel k = fista_kernel_for(P.g0, P.nCo, track);
+    const FistaKernel k = mimg > 1 ? multi_kernel_for(P.g0, P.nCo, mimg) : fista_kernel_for(P.g0, P.nCo, track);
     if (!k.fn) fail(WBX_BAD_SPEC, "spectral FISTA: unsupported group size");
     a.outw = const_cast<double*>(pr.out);
     if (track) {
@@ -1563,7 +1828,7 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
         circ_decoupled_kernel<<<8 * ctx->num_sms, 256, 0, st>>>(pr.x0_full, pr.x_full, pr.w_full, pr.p_full, pr.isC, P.n,
                                                               pr.nimg, pr.beta64, pr.lambda, pr.K, pr.out);
         count_launch(ctx);
-        grid = pr.nimg * P.g0;
+        grid = pr.nimg / mimg * P.g0;
     }
     WBX_CUDA(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(32 * k.warps), params, k.smem, st));
     count_launch(ctx);

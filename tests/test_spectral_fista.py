@@ -183,10 +183,12 @@ def test_spectral_batch_bitwise_equals_single(golden, batch, slots, monkeypatch)
     assert np.array_equal(out, out2)
 
 
-def test_spectral_batch8_at_1024(golden):
-    """C5 at its real size: 8 images of the C2 operator (two per launch at 64 spectral CTAs each)
-    bitwise equal to single-image spectral solves (whose parity with the reference is pinned
-    above and in test_full_size), tau the reference's."""
+@pytest.mark.parametrize("batch", [4, 8])
+def test_spectral_batch_at_1024(golden, batch):
+    """C5 at its real size: 4 / 8 images of the C2 operator in one launch (64 spectral CTAs per
+    slot, 2 / 4 images per CTA: circ_fista_multi_kernel) bitwise equal to single-image spectral
+    solves (whose parity with the reference is pinned above and in test_full_size), tau the
+    reference's."""
     from paper_1512_08401_b200 import synthetic as S
     g = golden("c2_db4_1024")
     op = g.operator()
@@ -194,11 +196,37 @@ def test_spectral_batch8_at_1024(golden):
     b = W.make_basis(W.FilterFamily.Daubechies, 4, (1024, 1024), 4)
     P = W.spai(op, ctx)
     cfg = W.SolverConfig(max_iters=100, track_energy=False)
-    imgs = np.stack([S.degrade((1024, 1024), 5.0, 5e-3, seed)[1] for seed in range(8)])
+    imgs = np.stack([S.degrade((1024, 1024), 5.0, 5e-3, seed)[1] for seed in range(batch)])
     single = W.Deblurrer(op, b, P, g.weights(), 1e-4, cfg, ctx)
     ref = np.stack([single.deblur(im, clamp=True)[0] for im in imgs])
-    many = W.Deblurrer(op, b, P, g.weights(), 1e-4, cfg, ctx, batch=8)
+    many = W.Deblurrer(op, b, P, g.weights(), 1e-4, cfg, ctx, batch=batch)
     assert many.kernels() == ("circ_lanczos_kernel", "circ_fista_kernel")
     out, rep = many.deblur(imgs, clamp=True)
     assert np.array_equal(out, ref)
     assert abs(rep.tau - g.meta["tau"]) <= 1e-12 * g.meta["tau"]
+
+
+@pytest.mark.parametrize("multi", ["1", "0"])
+def test_spectral_batch8_at_512_two_images_per_cta(multi, monkeypatch):
+    """g = 32 (512^2, J = 4): 4 CTA slots of 32 spectral CTAs, so a batch of 8 runs 2 images per
+    CTA in one launch (WBX_CIRC_MULTI=0: one image per CTA, two launches); Theta_K built on the
+    device from the Gaussian PSF (sigma 5, K = 3N, dyadic weights). Bitwise equal to single-image solves."""
+    if multi == "0":
+        monkeypatch.setenv("WBX_CIRC_MULTI", "0")
+    from paper_1512_08401_b200 import synthetic as S
+    dims = (512, 512)
+    ctx = W.Context(0)
+    b = W.make_basis(W.FilterFamily.Daubechies, 4, dims, 4)
+    n = dims[0] * dims[1]
+    gl = W.theta_conv_topk(b, W.gaussian_psf_kernel(dims, 5.0), 3 * n, W.dyadic_band_weights(b.layout), ctx)
+    op = W.theta_from_generators(gl)
+    P = W.spai(op, ctx)
+    w = W.scale_weights(b.layout)
+    cfg = W.SolverConfig(max_iters=30, track_energy=False)
+    imgs = np.stack([S.degrade(dims, 5.0, 5e-3, seed)[1] for seed in range(8)])
+    single = W.Deblurrer(op, b, P, w, 1e-4, cfg, ctx)
+    assert single.kernels() == ("circ_lanczos_kernel", "circ_fista_kernel")
+    ref = np.stack([single.deblur(im, clamp=False)[0] for im in imgs])
+    many = W.Deblurrer(op, b, P, w, 1e-4, cfg, ctx, batch=8)
+    out, _ = many.deblur(imgs, clamp=False)
+    assert np.array_equal(out, ref)
