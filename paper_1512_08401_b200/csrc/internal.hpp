@@ -210,6 +210,11 @@ inline void count_launch(wbx_ctx* ctx, uint64_t k = 1) { ctx->launches += k; }
 
 // dwt.cu
 void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s);
+// nimg images back to back (n doubles apart, work buffers n doubles per image each)
+void analyze_dev_n(wbx_basis* b, const double* u, double* x, uint32_t nimg, double* work_a, double* work_b,
+                   cudaStream_t s);
+void synthesize_dev_n(wbx_basis* b, const double* x, double* u, uint32_t nimg, double* work_a, double* work_b,
+                      cudaStream_t s, int clamp = 0);
 // clamp: the deblur's final clamp to [0, 1] fused into the last level
 void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s, int clamp = 0);
 void make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, std::vector<wbx_band>& bands);

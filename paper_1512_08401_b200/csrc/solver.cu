@@ -2150,6 +2150,7 @@ struct wbx_solver {
     wbx::DevBuf<double2> circ_gram, circ_T;
     wbx::DevBuf<double> circ_track;  // tracked spectral solves: per-CTA / per-warp energy partials
     wbx::DevBuf<unsigned> circ_counter;
+    wbx::DevBuf<double> bwork;  // batches: the DWT work buffers of every image (2 n per image)
     uint32_t circ_slots = 1;  // batch images per spectral launch (circ_fista_slots)
     wbx::DevBuf<float> yF, resF;
     int dec_grid = 0;
@@ -2978,6 +2979,7 @@ void solver_alloc_images(wbx_solver* s) {
     s->x0full.alloc(s->n * B);
     s->xfull.alloc(s->n * B);
     s->uout.alloc(s->n * B);
+    if (B > 1) s->bwork.alloc(2 * s->n * B);  // the batched DWTs' work buffers
 }
 
 }  // namespace wbx
@@ -2988,14 +2990,21 @@ namespace {
 // side stream concurrently with it
 void deblur_analyze(wbx_solver* s, const double* u0_dev, cudaStream_t side) {
     const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
-    for (uint64_t b = 0; b < B; ++b) wbx::analyze_dev(s->basis, u0_dev + b * n, s->x0full.p + b * n, side);
+    if (B > 1)  // one launch per level pass for the whole batch
+        wbx::analyze_dev_n(s->basis, u0_dev, s->x0full.p, static_cast<uint32_t>(B), s->bwork.p, s->bwork.p + B * n, side);
+    else
+        wbx::analyze_dev(s->basis, u0_dev, s->x0full.p, side);
 }
 
 // the rest of a deblur after the step estimate and the analysis: iterations -> synthesize (-> clamp)
 void deblur_rest(wbx_solver* s, double* u_dev, int clamp, cudaStream_t st) {
     const uint64_t n = s->n, B = static_cast<uint64_t>(s->batch);
     wbx::solver_iters(s, s->x0full.p, s->xfull.p);
-    for (uint64_t b = 0; b < B; ++b) wbx::synthesize_dev(s->basis, s->xfull.p + b * n, u_dev + b * n, st, clamp);
+    if (B > 1)
+        wbx::synthesize_dev_n(s->basis, s->xfull.p, u_dev, static_cast<uint32_t>(B), s->bwork.p, s->bwork.p + B * n, st,
+                              clamp);
+    else
+        wbx::synthesize_dev(s->basis, s->xfull.p, u_dev, st, clamp);
 }
 
 // capture fn's enqueues on st into an executable graph; counts the kernels it enqueued

@@ -111,8 +111,10 @@ __device__ __forceinline__ double fma_free(double acc, double a, double b) {
 // l - 2 inputs they read (one coalesced load per input instead of l/2 strided ones); the sum
 // over taps is the reference's order, so the result is bitwise the same.
 __global__ void fwd_rows_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
-                                int64_t ldd, int m0, int m1, Taps f) {
+                                int64_t ldd, int m0, int m1, Taps f, int64_t zs) {
     extern __shared__ double sh[];
+    src += blockIdx.z * zs;  // image blockIdx.z of a batch (images zs doubles apart in every buffer)
+    dst += blockIdx.z * zs;
     const int half = m1 >> 1;
     const int k0 = blockIdx.x * blockDim.x;
     const int r = blockIdx.y;
@@ -146,8 +148,13 @@ __global__ void fwd_rows_kernel(const double* __restrict__ src, int64_t lds, dou
 constexpr int kColsOut = 8;
 __global__ void fwd_cols_kernel(const double* __restrict__ src, int64_t lds, int m0, int m1, Taps f,
                                 double* __restrict__ ll, double* __restrict__ b1,
-                                double* __restrict__ b2, double* __restrict__ b3) {
+                                double* __restrict__ b2, double* __restrict__ b3, int64_t zs) {
     extern __shared__ double sh[];
+    src += blockIdx.z * zs;
+    ll += blockIdx.z * zs;
+    b1 += blockIdx.z * zs;
+    b2 += blockIdx.z * zs;
+    b3 += blockIdx.z * zs;
     const int h0 = m0 >> 1, h1 = m1 >> 1;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int k0 = blockIdx.y * kColsOut;
@@ -238,7 +245,12 @@ __device__ __forceinline__ double idwt_point(int j, int m, const Taps& f, LoadA 
 // Columns pass of inverse level: V[j][c], c < h1 from (LL, band2), else (band1, band3).
 __global__ void inv_cols_kernel(const double* __restrict__ ll, const double* __restrict__ b1,
                                 const double* __restrict__ b2, const double* __restrict__ b3,
-                                int m0, int m1, Taps f, double* __restrict__ dst) {
+                                int m0, int m1, Taps f, double* __restrict__ dst, int64_t zs) {
+    ll += blockIdx.z * zs;
+    b1 += blockIdx.z * zs;
+    b2 += blockIdx.z * zs;
+    b3 += blockIdx.z * zs;
+    dst += blockIdx.z * zs;
     const int h1 = m1 >> 1;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
@@ -254,7 +266,9 @@ __global__ void inv_cols_kernel(const double* __restrict__ ll, const double* __r
 // Rows pass of inverse level: out[j][x] from V[j][0:h1] (lowpass) and V[j][h1:m1].
 // clamp: the deblur's final std::clamp(v, 0, 1) (waveblur.cpp:297) fused into the last level
 __global__ void inv_rows_kernel(const double* __restrict__ src, int m0, int m1, Taps f,
-                                double* __restrict__ dst, int64_t ldd, int clamp) {
+                                double* __restrict__ dst, int64_t ldd, int clamp, int64_t zs) {
+    src += blockIdx.z * zs;
+    dst += blockIdx.z * zs;
     const int h1 = m1 >> 1;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
@@ -351,9 +365,21 @@ void make_layout(uint32_t ndim, const uint64_t* dims, uint32_t J, std::vector<wb
 }
 
 void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s) {
+    analyze_dev_n(b, u, x, 1, b->work_a.p, b->work_b.p, s);
+}
+
+// nimg images back to back (n doubles apart in u, x and both n-per-image work buffers): each
+// 2-D level pass is one launch over all images (blockIdx.z); 1-D bases run image by image
+void analyze_dev_n(wbx_basis* b, const double* u, double* x, uint32_t nimg, double* work_a, double* work_b,
+                   cudaStream_t s) {
     const Taps f = taps_of(b);
-    double* tmp = b->work_a.p;
-    double* llbuf = b->work_b.p;
+    double* tmp = work_a;
+    double* llbuf = work_b;
+    const int64_t zs = static_cast<int64_t>(b->n);
+    if (b->ndim == 1 && nimg > 1) {
+        for (uint32_t i = 0; i < nimg; ++i) analyze_dev_n(b, u + i * b->n, x + i * b->n, 1, work_a, work_b, s);
+        return;
+    }
     if (b->ndim == 1) {
         const double* src = u;
         for (uint32_t t = 0; t < b->J; ++t) {
@@ -371,15 +397,15 @@ void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s) {
         for (uint32_t t = 0; t < b->J; ++t) {
             const int m0 = static_cast<int>(b->dims[0] >> t), m1 = static_cast<int>(b->dims[1] >> t);
             const bool last = t + 1 == b->J;
-            dim3 g1((m1 / 2 + kThreads - 1) / kThreads, m0);
-            fwd_rows_kernel<<<g1, kThreads, (2 * kThreads + f.l) * sizeof(double), s>>>(src, lds, tmp, m1, m0, m1, f);
+            dim3 g1((m1 / 2 + kThreads - 1) / kThreads, m0, nimg);
+            fwd_rows_kernel<<<g1, kThreads, (2 * kThreads + f.l) * sizeof(double), s>>>(src, lds, tmp, m1, m0, m1, f, zs);
             double* ll = last ? x + b->bands[0].offset : llbuf;
             double* b1 = x + b->bands[band_index(b, t + 1, 1)].offset;
             double* b2 = x + b->bands[band_index(b, t + 1, 2)].offset;
             double* b3 = x + b->bands[band_index(b, t + 1, 3)].offset;
-            dim3 g2((m1 + kThreads - 1) / kThreads, (m0 / 2 + kColsOut - 1) / kColsOut);
+            dim3 g2((m1 + kThreads - 1) / kThreads, (m0 / 2 + kColsOut - 1) / kColsOut, nimg);
             fwd_cols_kernel<<<g2, kThreads, (2 * kColsOut + f.l) * kThreads * sizeof(double), s>>>(tmp, m1, m0, m1, f, ll,
-                                                                                                  b1, b2, b3);
+                                                                                                  b1, b2, b3, zs);
             count_launch(b->ctx, 2);
             src = ll;
             lds = m1 / 2;
@@ -389,9 +415,19 @@ void analyze_dev(wbx_basis* b, const double* u, double* x, cudaStream_t s) {
 }
 
 void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s, int clamp) {
+    synthesize_dev_n(b, x, u, 1, b->work_a.p, b->work_b.p, s, clamp);
+}
+
+void synthesize_dev_n(wbx_basis* b, const double* x, double* u, uint32_t nimg, double* work_a, double* work_b,
+                      cudaStream_t s, int clamp) {
     const Taps f = taps_of(b);
-    double* tmp = b->work_a.p;
-    double* llbufs[2] = {b->work_b.p, b->work_b.p + b->n / 2};
+    double* tmp = work_a;
+    double* llbufs[2] = {work_b, work_b + b->n / 2};
+    const int64_t zs = static_cast<int64_t>(b->n);
+    if (b->ndim == 1 && nimg > 1) {
+        for (uint32_t i = 0; i < nimg; ++i) synthesize_dev_n(b, x + i * b->n, u + i * b->n, 1, work_a, work_b, s, clamp);
+        return;
+    }
     if (b->ndim == 1) {
         const double* ll = x + b->bands[0].offset;
         int which = 0;
@@ -412,10 +448,10 @@ void synthesize_dev(wbx_basis* b, const double* x, double* u, cudaStream_t s, in
             const double* b1 = x + b->bands[band_index(b, t, 1)].offset;
             const double* b2 = x + b->bands[band_index(b, t, 2)].offset;
             const double* b3 = x + b->bands[band_index(b, t, 3)].offset;
-            dim3 g((m1 + kThreads - 1) / kThreads, m0);
-            inv_cols_kernel<<<g, kThreads, 0, s>>>(ll, b1, b2, b3, m0, m1, f, tmp);
+            dim3 g((m1 + kThreads - 1) / kThreads, m0, nimg);
+            inv_cols_kernel<<<g, kThreads, 0, s>>>(ll, b1, b2, b3, m0, m1, f, tmp, zs);
             double* dst = t == 1 ? u : llbufs[which];
-            inv_rows_kernel<<<g, kThreads, 0, s>>>(tmp, m0, m1, f, dst, m1, t == 1 ? clamp : 0);
+            inv_rows_kernel<<<g, kThreads, 0, s>>>(tmp, m0, m1, f, dst, m1, t == 1 ? clamp : 0, zs);
             count_launch(b->ctx, 2);
             ll = dst;
             which ^= 1;
