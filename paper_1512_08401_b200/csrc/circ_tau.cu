@@ -755,6 +755,12 @@ __global__ void __launch_bounds__(256) circ_decoupled_kernel(const double* __res
     }
 }
 
+// Shared-memory rows of complex values read in bit-reversed order: element e sits at
+// e ^ ((e >> 3) & 7), so the 8 lanes of a quarter warp (one 128-byte wavefront of 16-byte
+// accesses) reading brev(l) for 8 consecutive l hit 8 different 16-byte bank groups, and so do
+// 8 lanes storing consecutive e (a bijection on [0, G) for G >= 8)
+__device__ __forceinline__ int swz(int e) { return e ^ ((e >> 3) & 7); }
+
 template <int G>
 __device__ __forceinline__ int brev_g(int i) {
     return static_cast<int>(__brev(static_cast<unsigned>(i)) >> (32 - __builtin_ctz(G)));
@@ -868,8 +874,9 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
     extern __shared__ double2 circ_smem[];
     double2* Gs = circ_smem;                       // [pos][NCP][NCP + 1]: G_(brev(pos), c), zero padded
     double2* X = Gs + G * NCP * GS;                // [NCP][G]: spectrum of the rows at column c (positions)
-    double2* Y = X + NCP * G;                      // [NCP][G]: G_f times it
-    double2* tw = Y + NCP * G;                     // [G]
+    double2* Y = X + NCP * G;                      // [NCP][G + 1]: G_f times it (padded rows: the block
+                                                   // products' stores down a column hit distinct banks)
+    double2* tw = Y + NCP * (G + 1);               // [G]
     double* ys = reinterpret_cast<double*>(tw + G);  // [NCP][G] y on row c
     double* xps = ys + NCP * G;
     double* bs = xps + NCP * G;
@@ -904,7 +911,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         }
     };
     for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
-    for (int i = threadIdx.x; i < 2 * NCP * G; i += blockDim.x) X[i] = make_double2(0.0, 0.0);  // padded rows stay 0
+    for (int i = threadIdx.x; i < NCP * (2 * G + 1); i += blockDim.x) X[i] = make_double2(0.0, 0.0);  // padded rows stay 0
     batched_copy(
         G * NCP * NCP,
         [&](uint32_t i) {  // G_(f0, c) for f0 = brev(pos); conjugate half from its partner's block
@@ -1017,15 +1024,15 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
                 r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
                 i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
             }
-            if (one) Y[ii0 * G + pos0] = make_double2(r0, i0);
-            if (two) Y[ii1 * G + pos1] = make_double2(r1, i1);
+            if (one) Y[ii0 * (G + 1) + pos0] = make_double2(r0, i0);
+            if (two) Y[ii1 * (G + 1) + pos1] = make_double2(r1, i1);
         }
         mark(3);
         __syncthreads();
         if (row_live) {  // inverse along h0 (bit-reversed positions in, natural h0 out) -> T2[i][h0][c]
             double2 v[PPL];
 #pragma unroll
-            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
             F::inverse(v, tw);
             if (lane_live)
 #pragma unroll
@@ -1094,14 +1101,14 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
                 r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
                 i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
             }
-            if (one) Y[ii0 * G + pos0] = make_double2(r0, i0);
-            if (two) Y[ii1 * G + pos1] = make_double2(r1, i1);
+            if (one) Y[ii0 * (G + 1) + pos0] = make_double2(r0, i0);
+            if (two) Y[ii1 * (G + 1) + pos1] = make_double2(r1, i1);
         }
         __syncthreads();
         if (row_live) {
             double2 v[PPL];
 #pragma unroll
-            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+            for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Y[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
             F::inverse(v, tw);
             if (lane_live)
 #pragma unroll
@@ -1141,7 +1148,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
 
 template <int G, int NCP>
 size_t circ_fista_smem() {
-    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + 2 * NCP * G * 16 + G * 16 + 6 * NCP * G * 8;
+    return static_cast<size_t>(G) * NCP * (NCP + 1) * 16 + NCP * (2 * G + 1) * 16 + G * 16 + 6 * NCP * G * 8;
 }
 
 // M images per spectral CTA (C5 batches, untracked): the G_f block rows live in registers
@@ -1153,7 +1160,7 @@ size_t circ_fista_smem() {
 // decoupled coordinates run in circ_decoupled_kernel before the launch.
 template <int G, int NCP, int M>
 __host__ __device__ constexpr size_t circ_multi_image_bytes() {  // X, Y (complex) + y, x_prev, b
-    return static_cast<size_t>(NCP) * G * (2 * 16 + 3 * 8);
+    return static_cast<size_t>(NCP) * G * (2 * 16 + 3 * 8) + NCP * 16;  // (Y rows padded to G + 1)
 }
 template <int G, int NCP, int M>
 __host__ __device__ constexpr size_t circ_multi_state_bytes() {
@@ -1195,7 +1202,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     double* ths = ps + NCP * G;
     auto Xm = [&](int m) { return reinterpret_cast<double2*>(sbase + m * kImg); };
     auto Ym = [&](int m) { return Xm(m) + NCP * G; };
-    auto ysm = [&](int m) { return reinterpret_cast<double*>(Ym(m) + NCP * G); };
+    auto ysm = [&](int m) { return reinterpret_cast<double*>(Ym(m) + NCP * (G + 1)); };
     auto xpm = [&](int m) { return ysm(m) + NCP * G; };
     auto bsm = [&](int m) { return xpm(m) + NCP * G; };
     auto img = [&](int m) { return static_cast<uint64_t>(slot) * M + m; };
@@ -1228,7 +1235,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     }
     __syncthreads();  // the staging is dead: the images' state takes its place
     for (int m = 0; m < M; ++m)
-        for (int i = threadIdx.x; i < 2 * NCP * G; i += blockDim.x) Xm(m)[i] = make_double2(0.0, 0.0);  // X, Y
+        for (int i = threadIdx.x; i < NCP * (2 * G + 1); i += blockDim.x) Xm(m)[i] = make_double2(0.0, 0.0);  // X, Y
     for (int i = threadIdx.x; i < NCP * G; i += blockDim.x) {  // own row: p, thr; per image y = x_prev = x0, b
         const int j = i / G, h1 = i % G;
         if (j >= nc) {
@@ -1283,14 +1290,14 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                 for (int m = 0; m < M; ++m)
 #pragma unroll
                     for (int q = 0; q < PPL; ++q)
-                        cp_async16(Ym(m) + wj * G + lane + 32 * q,
+                        cp_async16(Ym(m) + wj * (G + 1) + lane + 32 * q,
                                    a.T1 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
             __syncwarp();
             for (int m = 0; m < M; ++m) {
                 double2 v[PPL];
 #pragma unroll
-                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
                 F::forward(v, tw);
                 if (lane_live)
 #pragma unroll
@@ -1309,15 +1316,15 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                 r1 = fma(n.x, y.x, fma(-n.y, y.y, r1));
                 i1 = fma(n.x, y.y, fma(n.y, y.x, i1));
             }
-            if (one) Ym(m)[ii0 * G + pos0] = make_double2(r0, i0);
-            if (two) Ym(m)[ii1 * G + pos1] = make_double2(r1, i1);
+            if (one) Ym(m)[ii0 * (G + 1) + pos0] = make_double2(r0, i0);
+            if (two) Ym(m)[ii1 * (G + 1) + pos1] = make_double2(r1, i1);
         }
         __syncthreads();
         if (row_live)
             for (int m = 0; m < M; ++m) {  // inverse along h0 -> T2[i][h0][c]
                 double2 v[PPL];
 #pragma unroll
-                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * G + lane + 32 * q] : make_double2(0.0, 0.0);
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
                 F::inverse(v, tw);
                 double2* T2 = a.T2 + img(m) * ex;
                 if (lane_live)
@@ -1325,13 +1332,13 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                     for (int q = 0; q < PPL; ++q) T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
             }
         circ_barrier(counter, ++bar * a.NB);
-        // row phase: each image's row c of T2 fetched into X (contiguous), read in bit-reversed order
+        // row phase: each image's row c of T2 fetched into X (swizzled), read in bit-reversed order
         if (row_live) {
             if (lane_live)
                 for (int m = 0; m < M; ++m)
 #pragma unroll
                     for (int q = 0; q < PPL; ++q)
-                        cp_async16(Xm(m) + wj * G + lane + 32 * q,
+                        cp_async16(Xm(m) + wj * G + swz(lane + 32 * q),
                                    a.T2 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
             __syncwarp();
@@ -1340,7 +1347,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                 double2 v[PPL];
 #pragma unroll
                 for (int q = 0; q < PPL; ++q)
-                    v[q] = lane_live ? Xm(m)[wj * G + brev_g<G>(lane + 32 * q)] : make_double2(0.0, 0.0);
+                    v[q] = lane_live ? Xm(m)[wj * G + swz(brev_g<G>(lane + 32 * q))] : make_double2(0.0, 0.0);
                 F::inverse(v, tw);
                 double* ys = ysm(m);
                 double* xps = xpm(m);
