@@ -668,7 +668,18 @@ __device__ __forceinline__ double circ_momentum(double xn, double xp, double bet
 // Warp FFTs of one length-G row held in registers: lane l holds elements l + 32 q (q < PPL).
 // DIF forward (e^{-}): natural-order input, bit-reversed-order output; DIT inverse (e^{+}):
 // bit-reversed input, natural output (unnormalised). Butterflies of distance d < 32 exchange
-// with lane l ^ d by shuffles; d = 32 (G = 64) is lane-local. tw[k] = e^{+2 pi i k / G}.
+// with lane l ^ d by shuffles; d = 32 (G = 64) is lane-local. tw is the per-stage table
+// (circ_stage_twiddles): tw[d - 1 + k] = e^{+2 pi i k / (2 d)}, k < d, so the lanes of a stage
+// read consecutive entries (no bank conflicts) and tw[d - 1] = 1.
+// the per-stage twiddle table of WarpFft from e^{+2 pi i k / G} (k < G): G - 1 entries
+template <int G>
+__device__ __forceinline__ void circ_stage_twiddles(const double2* __restrict__ twg, double2* tw) {
+    for (int i = threadIdx.x; i < G - 1; i += blockDim.x) {
+        const int d = 1 << (31 - __clz(i + 1));  // stage of entry i: d - 1 <= i < 2 d - 1
+        tw[i] = twg[(i - (d - 1)) * (G / (2 * d))];
+    }
+}
+
 template <int G>
 struct WarpFft {
     static constexpr int PPL = G > 32 ? G / 32 : 1;
@@ -681,7 +692,7 @@ struct WarpFft {
         for (int d = G / 2; d >= 1; d >>= 1) {
             if (d >= 32) {  // lane-local: elements lane, lane + 32
                 const double2 a = v[0], b = v[1];
-                double2 w = tw[(lane % d) * (G / (2 * d))];
+                double2 w = tw[d - 1 + lane % d];
                 w.y = -w.y;
                 v[0] = make_double2(a.x + b.x, a.y + b.y);
                 v[1] = cmul(make_double2(a.x - b.x, a.y - b.y), w);
@@ -691,7 +702,7 @@ struct WarpFft {
                 for (int q = 0; q < PPL; ++q) {
                     const int e = lane + 32 * q;
                     const double2 p = shfl(v[q], d);
-                    double2 w = tw[hi ? (e % d) * (G / (2 * d)) : 0];
+                    double2 w = tw[d - 1 + (hi ? e % d : 0)];
                     w.y = -w.y;
                     const double sg = hi ? -1.0 : 1.0;
                     v[q] = cmul(make_double2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y)), w);
@@ -704,7 +715,7 @@ struct WarpFft {
 #pragma unroll
         for (int d = 1; d <= G / 2; d <<= 1) {
             if (d >= 32) {
-                const double2 w = tw[(lane % d) * (G / (2 * d))];
+                const double2 w = tw[d - 1 + lane % d];
                 const double2 a = v[0], bw = cmul(v[1], w);
                 v[0] = make_double2(a.x + bw.x, a.y + bw.y);
                 v[1] = make_double2(a.x - bw.x, a.y - bw.y);
@@ -713,7 +724,7 @@ struct WarpFft {
 #pragma unroll
                 for (int q = 0; q < PPL; ++q) {
                     const int e = lane + 32 * q;
-                    const double2 t = cmul(v[q], tw[hi ? (e % d) * (G / (2 * d)) : 0]);
+                    const double2 t = cmul(v[q], tw[d - 1 + (hi ? e % d : 0)]);
                     const double2 p = shfl(t, d);
                     const double sg = hi ? -1.0 : 1.0;
                     v[q] = make_double2(fma(sg, t.x, p.x), fma(sg, t.y, p.y));
@@ -910,7 +921,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
             }
         }
     };
-    for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
+    circ_stage_twiddles<G>(a.tw, tw);
     for (int i = threadIdx.x; i < NCP * (2 * G + 1); i += blockDim.x) X[i] = make_double2(0.0, 0.0);  // padded rows stay 0
     batched_copy(
         G * NCP * NCP,
@@ -1206,7 +1217,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     auto xpm = [&](int m) { return ysm(m) + NCP * G; };
     auto bsm = [&](int m) { return xpm(m) + NCP * G; };
     auto img = [&](int m) { return static_cast<uint64_t>(slot) * M + m; };
-    for (int i = threadIdx.x; i < G; i += blockDim.x) tw[i] = a.tw[i];
+    circ_stage_twiddles<G>(a.tw, tw);
     batched_copy(
         G * NCP * NCP,
         [&](uint32_t i) {
