@@ -705,7 +705,8 @@ struct WarpFft {
                     double2 w = tw[d - 1 + (hi ? e % d : 0)];
                     w.y = -w.y;
                     const double sg = hi ? -1.0 : 1.0;
-                    v[q] = cmul(make_double2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y)), w);
+                    const double2 r = make_double2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y));
+                    v[q] = d == 1 ? r : cmul(r, w);  // the last stage's twiddles are all 1
                 }
             }
         }
@@ -724,7 +725,7 @@ struct WarpFft {
 #pragma unroll
                 for (int q = 0; q < PPL; ++q) {
                     const int e = lane + 32 * q;
-                    const double2 t = cmul(v[q], tw[d - 1 + (hi ? e % d : 0)]);
+                    const double2 t = d == 1 ? v[q] : cmul(v[q], tw[d - 1 + (hi ? e % d : 0)]);  // (stage 1: all 1)
                     const double2 p = shfl(t, d);
                     const double sg = hi ? -1.0 : 1.0;
                     v[q] = make_double2(fma(sg, t.x, p.x), fma(sg, t.y, p.y));
