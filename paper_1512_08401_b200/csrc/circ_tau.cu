@@ -645,9 +645,11 @@ __device__ __forceinline__ void circ_barrier(unsigned* cnt, unsigned target) {
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
         unsigned v;
-        do {
+        while (true) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-        } while (static_cast<int>(v - target) < 0);
+            if (static_cast<int>(v - target) >= 0) break;
+            __nanosleep(64);  // fewer polls contending with the arrivals at the counter's L2 slice
+        }
     }
     __syncthreads();
 }
