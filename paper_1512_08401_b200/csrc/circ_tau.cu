@@ -660,7 +660,12 @@ __device__ __forceinline__ double circ_thr(double tau, double lambda, double w, 
 }
 __device__ __forceinline__ double circ_prox(double z0, double thr) {
     const double a = __dsub_rn(fabs(z0), thr);
-    return a > 0.0 ? (z0 > 0.0 ? a : -a) : 0.0;
+    return a > 0.0 ? copysign(a, z0) : 0.0;  // (a > 0 needs |z0| > thr >= 0: z0 != 0, so the sign is z0's)
+}
+// x' == 0 && x_prev == 0 (either zero sign) by the bits: no fp64 compares in the decoupled loops
+__device__ __forceinline__ bool circ_both_zero(double a, double b) {
+    return ((static_cast<unsigned long long>(__double_as_longlong(a)) |
+             static_cast<unsigned long long>(__double_as_longlong(b))) << 1) == 0;
 }
 __device__ __forceinline__ double circ_momentum(double xn, double xp, double beta) {
     return __dadd_rn(xn, __dmul_rn(beta, __dsub_rn(xn, xp)));
@@ -759,7 +764,7 @@ __global__ void __launch_bounds__(256) circ_decoupled_kernel(const double* __res
         double x = x0_full[t], xp = x, y = x;
         for (int k = 1; k <= K; ++k) {
             const double xn = circ_prox(y, thr);
-            const bool fixed = xn == 0.0 && xp == 0.0;
+            const bool fixed = circ_both_zero(xn, xp);
             y = circ_momentum(xn, xp, beta64[k - 1]);
             xp = xn;
             x = xn;
@@ -817,7 +822,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
                 double reg = 0.0, sup = 0.0;
                 if (live) {
                     const double xn = circ_prox(y, thr);
-                    const bool fixed = xn == 0.0 && xp == 0.0;
+                    const bool fixed = circ_both_zero(xn, xp);
                     y = circ_momentum(xn, xp, a.beta64[k - 1]);
                     xp = xn;
                     x = xn;
@@ -861,7 +866,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
             double x = a.x0_full[i], xp = x, y = x;
             for (int k = 1; k <= a.K; ++k) {
                 const double xn = circ_prox(y, thr);
-                const bool fixed = xn == 0.0 && xp == 0.0;
+                const bool fixed = circ_both_zero(xn, xp);
                 y = circ_momentum(xn, xp, a.beta64[k - 1]);
                 xp = xn;
                 x = xn;
