@@ -623,6 +623,7 @@ struct CircFistaArgs {
     unsigned* counter;
     uint32_t g, lg, nRo, nCo, NB;
     uint32_t nimg;  // images in this launch (C5 batches): NB spectral CTAs, T1/T2 and a counter per image
+    int staged;     // untracked single-kernel solves: exchange blocks staged in shared memory (see below)
     int diag_skip_decoupled;  // WBX_CIRC_DIAG=nodec: time the spectral CTAs alone (wrong x)
     unsigned long long* prof;  // diagnostics build (WBX_CIRC_PROF=1): CTA 0's cycles per section
     double* outw;              // out (iteration count)
@@ -772,6 +773,11 @@ __global__ void __launch_bounds__(256) circ_decoupled_kernel(const double* __res
         }
         x_full[t] = x;
     }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 
 // Shared-memory rows of complex values read in bit-reversed order: element e sits at
@@ -989,7 +995,24 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
     __syncthreads();
     const double inv_ng = 1.0 / (static_cast<double>(G) * G);  // exact (power of two)
     unsigned bar = 0;
-    // forward row DFT of this warp's row of y -> T1[j][f1][c] (f1 = brev(position))
+    // Staged exchange (untracked): T1 as [f1][r][j] and T2 as [h0][c][i] blocks, so a CTA's
+    // outputs for one consumer are nc contiguous values (stored from a shared-memory stage by
+    // consecutive threads: a few line requests per warp instead of 32 scattered 16-byte
+    // sectors) and a consumer's input is one contiguous nc x G block (landed with cp.async).
+    // The stage / landing buffer L [G][NCP + 1] reuses the G_f staging (dead after the prologue);
+    // its rows are padded so the column reads of a warp (one orbit) are conflict free.
+    const bool staged = !TRACK && a.staged;
+    constexpr int LP = NCP + 1;
+    double2* const L = Gs;
+    const uint64_t ncs = a.nCo;
+    auto store_T1 = [&]() {  // all threads: L[p][i] (spectrum at f1 = brev(p), orbit i) -> T1[f1][c][i]
+        __syncthreads();
+        for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+            const int p = t / nc, i = t - p * nc;
+            a.T1[(static_cast<uint64_t>(brev_g<G>(p)) * G + c) * ncs + i] = L[p * LP + i];
+        }
+    };
+    // forward row DFT of this warp's row of y -> T1[j][f1][c] (f1 = brev(position)); staged: -> L
     auto row_forward = [&]() {
         if (!row_live) return;
         double2 v[PPL];
@@ -998,8 +1021,12 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
         F::forward(v, tw);
         if (lane_live)
 #pragma unroll
-            for (int q = 0; q < PPL; ++q)
-                a.T1[(static_cast<uint64_t>(wj) * G + brev_g<G>(lane + 32 * q)) * G + c] = v[q];
+            for (int q = 0; q < PPL; ++q) {
+                if (staged)
+                    L[(lane + 32 * q) * LP + wj] = v[q];
+                else
+                    a.T1[(static_cast<uint64_t>(wj) * G + brev_g<G>(lane + 32 * q)) * G + c] = v[q];
+            }
     };
 #if WBX_CIRC_PROF
     __shared__ unsigned long long prof_acc[8];
@@ -1015,17 +1042,30 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
 #else
     auto mark = [](int) {};
 #endif
-    if (a.K > 0) row_forward();
+    if (a.K > 0) {
+        row_forward();
+        if (staged) store_T1();
+    }
     for (int k = 1; k <= a.K; ++k) {
         mark(0);
         circ_barrier(a.counter, ++bar * a.NB);
         mark(1);
+        if (staged) {  // land T1[f1 = c][r][j] -> L[r][j]
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int r = t / nc, j = t - r * nc;
+                cp_async16(L + r * LP + j, a.T1 + (static_cast<uint64_t>(c) * G + r) * ncs + j);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
         // column phase: column c of the spectrum; warp j transforms orbit j along h0
         if (row_live) {
             double2 v[PPL];
 #pragma unroll
             for (int q = 0; q < PPL; ++q)
-                v[q] = lane_live ? a.T1[(static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q] : make_double2(0.0, 0.0);
+                v[q] = !lane_live ? make_double2(0.0, 0.0)
+                       : staged   ? L[(lane + 32 * q) * LP + wj]
+                                  : a.T1[(static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q];
             F::forward(v, tw);
             if (lane_live)
 #pragma unroll
@@ -1055,19 +1095,40 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
             F::inverse(v, tw);
             if (lane_live)
 #pragma unroll
-                for (int q = 0; q < PPL; ++q) a.T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+                for (int q = 0; q < PPL; ++q) {
+                    if (staged)
+                        L[(lane + 32 * q) * LP + wj] = v[q];
+                    else
+                        a.T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+                }
+        }
+        if (staged) {  // L[h0][i] -> T2[h0][c][i]
+            __syncthreads();
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int h0 = t / nc, i = t - h0 * nc;
+                a.T2[(static_cast<uint64_t>(h0) * G + c) * ncs + i] = L[h0 * LP + i];
+            }
         }
         mark(4);
         circ_barrier(a.counter, ++bar * a.NB);
         mark(5);
+        if (staged) {  // land T2[h0 = c][c'][i] -> L[brev(c')][i] (the bit-reversed order the inverse wants)
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int cc = t / nc, i = t - cc * nc;
+                cp_async16(L + brev_g<G>(cc) * LP + i, a.T2 + (static_cast<uint64_t>(c) * G + cc) * ncs + i);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
         // row phase: row c; warp i inverts orbit i along f1 (loaded in bit-reversed order)
         double tq = 0.0, trg = 0.0, tsp = 0.0;  // TRACK partials of this thread
         if (row_live) {
             double2 v[PPL];
 #pragma unroll
             for (int q = 0; q < PPL; ++q)
-                v[q] = lane_live ? a.T2[(static_cast<uint64_t>(wj) * G + c) * G + brev_g<G>(lane + 32 * q)]
-                                 : make_double2(0.0, 0.0);
+                v[q] = !lane_live ? make_double2(0.0, 0.0)
+                       : staged   ? L[(lane + 32 * q) * LP + wj]
+                                  : a.T2[(static_cast<uint64_t>(wj) * G + c) * G + brev_g<G>(lane + 32 * q)];
             F::inverse(v, tw);  // v[q].x * NG = (Theta^T Theta y)[wj][c][lane + 32 q]
             const double beta = a.beta64[k - 1];
             const double bprev = k >= 2 ? a.beta64[k - 2] : 0.0;  // y_k = x_k-1 + bprev (x_k-1 - x_k-2)
@@ -1094,6 +1155,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_kernel(CircFistaArgs a
             __syncwarp();
             if (TRACK || k < a.K) row_forward();
         }
+        if (staged && k < a.K) store_T1();
         if constexpr (TRACK) track_partials(tq, trg, tsp, k - 1, k);
         mark(6);
     }
@@ -1192,10 +1254,6 @@ size_t circ_multi_smem() {  // state (aliasing the G_f staging) + twiddles + tau
     return circ_multi_state_bytes<G, NCP, M>() + G * 16 + 2 * NCP * G * 8;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
 
 template <int G, int NCP, int M>
 __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFistaArgs a) {
@@ -1819,6 +1877,10 @@ void circ_fista_launch(wbx_ctx* ctx, const CircPlan& P, const CircProblem& pr, c
     a.nCo = P.nCo;
     a.NB = P.g0;
     a.nimg = pr.nimg;
+    {  // the staged exchange layout (untracked launches of circ_fista_kernel); WBX_CIRC_STAGED=0: off
+        const char* e = std::getenv("WBX_CIRC_STAGED");
+        a.staged = !(e && std::string(e) == "0");
+    }
     const uint32_t mimg = pr.nimg > 1 ? multi_m(P, ctx->num_sms, pr.nimg) : 1;  // images per CTA
     if (pr.nimg < 1 || mimg == 0 || (track && pr.nimg != 1) || (pr.nimg == 1 && P.g0 >= static_cast<uint32_t>(ctx->num_sms)))
         fail(WBX_BAD_SPEC, "spectral FISTA: images per launch exceed the grid");
