@@ -780,11 +780,6 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 
-// Shared-memory rows of complex values read in bit-reversed order: element e sits at
-// e ^ ((e >> 3) & 7), so the 8 lanes of a quarter warp (one 128-byte wavefront of 16-byte
-// accesses) reading brev(l) for 8 consecutive l hit 8 different 16-byte bank groups, and so do
-// 8 lanes storing consecutive e (a bijection on [0, G) for G >= 8)
-__device__ __forceinline__ int swz(int e) { return e ^ ((e >> 3) & 7); }
 
 template <int G>
 __device__ __forceinline__ int brev_g(int i) {
@@ -1239,9 +1234,13 @@ size_t circ_fista_smem() {
 // cp.async before the first transform, so a phase pays one L2 round trip, not M. Per image the
 // arithmetic is circ_fista_kernel's in the same order: bitwise its single-image result. The
 // decoupled coordinates run in circ_decoupled_kernel before the launch.
+template <int G, int NCP>
+__host__ __device__ constexpr int circ_multi_xb() {  // complex values of X and of Y per image
+    return NCP * (G + 1) > G * (NCP + 1) ? NCP * (G + 1) : G * (NCP + 1);
+}
 template <int G, int NCP, int M>
 __host__ __device__ constexpr size_t circ_multi_image_bytes() {  // X, Y (complex) + y, x_prev, b
-    return static_cast<size_t>(NCP) * G * (2 * 16 + 3 * 8) + NCP * 16;  // (Y rows padded to G + 1)
+    return static_cast<size_t>(circ_multi_xb<G, NCP>()) * 2 * 16 + static_cast<size_t>(NCP) * G * 3 * 8;
 }
 template <int G, int NCP, int M>
 __host__ __device__ constexpr size_t circ_multi_state_bytes() {
@@ -1277,9 +1276,14 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     double2* tw = reinterpret_cast<double2*>(sbase + circ_multi_state_bytes<G, NCP, M>());
     double* ps = reinterpret_cast<double*>(tw + G);  // tau / p (the images share P, w, lambda, tau)
     double* ths = ps + NCP * G;
+    // X, Y of an image: [NCP][G] spectra / [NCP][G + 1] block products, and (staged exchange, as
+    // circ_fista_kernel) [G][NCP + 1] landing / stage blocks: XB complex values each
+    constexpr int LP = NCP + 1;
+    constexpr int XB = circ_multi_xb<G, NCP>();
+    const uint64_t ncs = a.nCo;
     auto Xm = [&](int m) { return reinterpret_cast<double2*>(sbase + m * kImg); };
-    auto Ym = [&](int m) { return Xm(m) + NCP * G; };
-    auto ysm = [&](int m) { return reinterpret_cast<double*>(Ym(m) + NCP * (G + 1)); };
+    auto Ym = [&](int m) { return Xm(m) + XB; };
+    auto ysm = [&](int m) { return reinterpret_cast<double*>(Ym(m) + XB); };
     auto xpm = [&](int m) { return ysm(m) + NCP * G; };
     auto bsm = [&](int m) { return xpm(m) + NCP * G; };
     auto img = [&](int m) { return static_cast<uint64_t>(slot) * M + m; };
@@ -1312,7 +1316,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     }
     __syncthreads();  // the staging is dead: the images' state takes its place
     for (int m = 0; m < M; ++m)
-        for (int i = threadIdx.x; i < NCP * (2 * G + 1); i += blockDim.x) Xm(m)[i] = make_double2(0.0, 0.0);  // X, Y
+        for (int i = threadIdx.x; i < 2 * XB; i += blockDim.x) Xm(m)[i] = make_double2(0.0, 0.0);  // X, Y
     for (int i = threadIdx.x; i < NCP * G; i += blockDim.x) {  // own row: p, thr; per image y = x_prev = x0, b
         const int j = i / G, h1 = i % G;
         if (j >= nc) {
@@ -1347,34 +1351,47 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
     __syncthreads();
     const double inv_ng = 1.0 / (static_cast<double>(G) * G);
     unsigned bar = 0;
-    auto row_forward = [&](int m) {  // row DFT of this warp's row of image m's y -> its T1[j][f1][c]
+    auto row_forward = [&](int m) {  // row DFT of this warp's row of image m's y -> X_m stage [p][j]
         double2 v[PPL];
 #pragma unroll
         for (int q = 0; q < PPL; ++q) v[q] = make_double2(lane_live ? ysm(m)[wj * G + lane + 32 * q] : 0.0, 0.0);
         F::forward(v, tw);
-        double2* T1 = a.T1 + img(m) * ex;
         if (lane_live)
 #pragma unroll
-            for (int q = 0; q < PPL; ++q) T1[(static_cast<uint64_t>(wj) * G + brev_g<G>(lane + 32 * q)) * G + c] = v[q];
+            for (int q = 0; q < PPL; ++q) Xm(m)[(lane + 32 * q) * LP + wj] = v[q];
     };
-    if (a.K > 0 && row_live)
-        for (int m = 0; m < M; ++m) row_forward(m);
+    auto store_T1 = [&]() {  // all threads: X_m[p][i] (f1 = brev(p)) -> T1_m[f1][c][i], every image
+        __syncthreads();
+        for (int m = 0; m < M; ++m) {
+            double2* T1 = a.T1 + img(m) * ex;
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int p = t / nc, i = t - p * nc;
+                T1[(static_cast<uint64_t>(brev_g<G>(p)) * G + c) * ncs + i] = Xm(m)[p * LP + i];
+            }
+        }
+    };
+    if (a.K > 0) {
+        if (row_live)
+            for (int m = 0; m < M; ++m) row_forward(m);
+        store_T1();
+    }
     for (int k = 1; k <= a.K; ++k) {
         circ_barrier(counter, ++bar * a.NB);
-        // column phase: each image's rows at column c, fetched into Y, transformed into X
+        // column phase: each image's block T1[f1 = c][r][j] landed in Y [r][j], transformed into X
+        for (int m = 0; m < M; ++m) {
+            const double2* T1 = a.T1 + img(m) * ex + static_cast<uint64_t>(c) * G * ncs;
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int r = t / nc, j = t - r * nc;
+                cp_async16(Ym(m) + r * LP + j, T1 + static_cast<uint64_t>(r) * ncs + j);
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
         if (row_live) {
-            if (lane_live)
-                for (int m = 0; m < M; ++m)
-#pragma unroll
-                    for (int q = 0; q < PPL; ++q)
-                        cp_async16(Ym(m) + wj * (G + 1) + lane + 32 * q,
-                                   a.T1 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
-            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
             for (int m = 0; m < M; ++m) {
                 double2 v[PPL];
 #pragma unroll
-                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[(lane + 32 * q) * LP + wj] : make_double2(0.0, 0.0);
                 F::forward(v, tw);
                 if (lane_live)
 #pragma unroll
@@ -1402,29 +1419,36 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                 double2 v[PPL];
 #pragma unroll
                 for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Ym(m)[wj * (G + 1) + lane + 32 * q] : make_double2(0.0, 0.0);
-                F::inverse(v, tw);
-                double2* T2 = a.T2 + img(m) * ex;
+                F::inverse(v, tw);  // -> X_m stage [h0][i] (the products are done with X)
                 if (lane_live)
 #pragma unroll
-                    for (int q = 0; q < PPL; ++q) T2[(static_cast<uint64_t>(wj) * G + lane + 32 * q) * G + c] = v[q];
+                    for (int q = 0; q < PPL; ++q) Xm(m)[(lane + 32 * q) * LP + wj] = v[q];
             }
+        __syncthreads();
+        for (int m = 0; m < M; ++m) {  // X_m[h0][i] -> T2_m[h0][c][i]
+            double2* T2 = a.T2 + img(m) * ex;
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int h0 = t / nc, i = t - h0 * nc;
+                T2[(static_cast<uint64_t>(h0) * G + c) * ncs + i] = Xm(m)[h0 * LP + i];
+            }
+        }
         circ_barrier(counter, ++bar * a.NB);
-        // row phase: each image's row c of T2 fetched into X (swizzled), read in bit-reversed order
+        // row phase: each image's block T2[h0 = c][c'][i] landed in X [brev(c')][i] (bit-reversed rows)
+        for (int m = 0; m < M; ++m) {
+            const double2* T2 = a.T2 + img(m) * ex + static_cast<uint64_t>(c) * G * ncs;
+            for (int t = threadIdx.x; t < G * nc; t += blockDim.x) {
+                const int cc = t / nc, i = t - cc * nc;
+                cp_async16(Xm(m) + brev_g<G>(cc) * LP + i, T2 + static_cast<uint64_t>(cc) * ncs + i);
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
         if (row_live) {
-            if (lane_live)
-                for (int m = 0; m < M; ++m)
-#pragma unroll
-                    for (int q = 0; q < PPL; ++q)
-                        cp_async16(Xm(m) + wj * G + swz(lane + 32 * q),
-                                   a.T2 + img(m) * ex + (static_cast<uint64_t>(wj) * G + c) * G + lane + 32 * q);
-            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
             const double beta = a.beta64[k - 1];
             for (int m = 0; m < M; ++m) {
                 double2 v[PPL];
 #pragma unroll
-                for (int q = 0; q < PPL; ++q)
-                    v[q] = lane_live ? Xm(m)[wj * G + swz(brev_g<G>(lane + 32 * q))] : make_double2(0.0, 0.0);
+                for (int q = 0; q < PPL; ++q) v[q] = lane_live ? Xm(m)[(lane + 32 * q) * LP + wj] : make_double2(0.0, 0.0);
                 F::inverse(v, tw);
                 double* ys = ysm(m);
                 double* xps = xpm(m);
@@ -1444,6 +1468,7 @@ __global__ void __launch_bounds__(32 * NCP, 1) circ_fista_multi_kernel(CircFista
                 if (k < a.K) row_forward(m);
             }
         }
+        if (k < a.K) store_T1();
     }
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) a.outw[2] = a.K;  // OUT_ITERS_USED
