@@ -314,9 +314,11 @@ int wbx_deblur_dev(wbx_solver* s, const double* u0_dev, double* u_dev, int clamp
 /* host pointers: H2D copy, deblur, D2H copy, synchronise */
 int wbx_deblur(wbx_solver* s, const double* u0, double* u, int clamp, wbx_report* report);
 /* Batched deblur (BASELINE config C5): `batch` (1, 4 or 8) independent images share Theta_K,
- * P, w, lambda and tau; the operator is streamed once per batch (SpMM). Images are stored
- * back to back (batch * n doubles) for wbx_deblur / wbx_deblur_dev. fp32, fixed iteration
- * count. */
+ * P, w, lambda and tau (estimated once per batch). Images are stored back to back (batch * n
+ * doubles) for wbx_deblur / wbx_deblur_dev. Translation-invariant operators run the fp64
+ * spectral engine with the whole batch in one launch (up to 4 images per CTA); others stream
+ * the operator once per batch (fp32 SpMM). precision = WBX_FP32 (the hot-path setting), no
+ * energy tracking, fixed iteration count; every image equals its single-image solve bitwise. */
 int wbx_solver_create_batch(wbx_ctx* ctx, const wbx_op* op, const wbx_basis* basis, const double* p,
                             const double* w, double lambda, const wbx_solver_cfg* cfg, int batch,
                             wbx_solver** out);
