@@ -649,7 +649,7 @@ __device__ __forceinline__ void circ_barrier(unsigned* cnt, unsigned target) {
         while (true) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
             if (static_cast<int>(v - target) >= 0) break;
-            __nanosleep(64);  // fewer polls contending with the arrivals at the counter's L2 slice
+            __nanosleep(32);  // fewer polls contending with the arrivals at the counter's L2 slice
         }
     }
     __syncthreads();
